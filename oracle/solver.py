@@ -1,0 +1,207 @@
+"""Oracle: multilevel Newton iteration (Alg. 1), linear solves (Alg. 2), filtered line search.
+
+Test infrastructure only (see oracle/__init__.py).
+
+Passages followed:
+* Alg. 1, §3.9: full-space gradient, Hessian, subspace direction,
+  full-space correction, d = d_s + d_f, filtered backtracking line search, termination
+  ||d_s|| / (h |V|) < eps.
+* Alg. 2 L427-450 with readings R4 (exact coarse solves), R6 (right-hand side -g).
+* §3.7.2: fixed-count Jacobi-PCG refinement from d_f = 0 (reading R5).
+* L616 and SPEC S:170-184: CCD (ground plane) and inversion filters with safety 0.9,
+  backtracking by halving with strict decrease, alpha_min = 1e-8 (reading Q12).
+* R3: one freshly assembled, fully integrated H for every stage (no cubature / lagging).
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+
+from . import coarse, fem, ip
+
+LS_SHRINK = 0.5
+LS_MIN = 1e-8
+FILTER_SAFETY = 0.9
+
+
+def pcg(H, r, n_iter, Dinv=None):
+    """Exactly n_iter Jacobi-PCG iterations on H d = r from d = 0, stop early only if rho == 0
+    (P:477-484).  Returns d."""
+    r = np.array(r, dtype=np.float64).ravel()
+    if Dinv is None:
+        Dinv = 1.0 / H.diagonal()
+    d = np.zeros_like(r)
+    z = Dinv * r
+    p = z.copy()
+    rho = r @ z
+    for _ in range(n_iter):
+        if rho == 0.0:
+            break
+        q = H @ p
+        alpha = rho / (p @ q)
+        d = d + alpha * p
+        r = r - alpha * q
+        z = Dinv * r
+        rho_new = r @ z
+        p = z + (rho_new / rho) * p
+        rho = rho_new
+    return d
+
+
+def subspace_direction(H, g, Ua, Us):
+    """Alg. 2 SolveSubspaceDirection with exact coarse solves and rhs -g (R4, R6).
+
+    Returns d_s, d_a and the coarse matrices S_a, S."""
+    g = g.ravel()
+    Sa = coarse.galerkin(Ua, H)
+    qa = coarse.cho_solve(coarse.cholesky(Sa), Ua.T @ (-g))
+    da = Ua @ qa
+    r1 = -g - H @ da
+    S = coarse.galerkin(Us, H)
+    qs = coarse.cho_solve(coarse.cholesky(S), Us.T @ r1)
+    ds = da + Us @ qs
+    return ds, da, Sa, S
+
+
+def ccd_alpha(model, x, d):
+    """Ground-plane CCD: alpha = min(1, 0.9 min_{v: n.d_v < 0} dist_v / (-n.d_v))."""
+    if model.ground is None:
+        return 1.0
+    dist, nrm = ip.ground_distance(model, x)
+    vel = d @ nrm
+    f = model.free & (vel < 0.0)
+    if not np.any(f):
+        return 1.0
+    return float(min(1.0, FILTER_SAFETY * np.min(dist[f] / (-vel[f]))))
+
+
+def det_poly(A, B):
+    """Coefficients (c0, c1, c2, c3) of det(A + t B) = c0 + c1 t + c2 t^2 + c3 t^3.
+
+    Computed from the exact multilinearity of det in the columns: each coefficient is a sum
+    of determinants with columns drawn from A or B."""
+    cols = lambda M, k: M[..., :, k]
+    c = [np.zeros(A.shape[:-2]) for _ in range(4)]
+    for mask in range(8):
+        pick = [(B if (mask >> k) & 1 else A) for k in range(3)]
+        M = np.stack([cols(pick[k], k) for k in range(3)], axis=-1)
+        c[bin(mask).count("1")] = c[bin(mask).count("1")] + np.linalg.det(M)
+    return c
+
+
+def smallest_positive_root(c):
+    """Smallest real root t > 0 of c0 + c1 t + c2 t^2 + c3 t^3 (inf if none), per element,
+    via numpy.roots (companion-matrix eigenvalues) of the leading-nonzero polynomial."""
+    c0, c1, c2, c3 = c
+    out = np.full(c0.shape, np.inf)
+    for e in range(c0.size):
+        coeffs = [c3.flat[e], c2.flat[e], c1.flat[e], c0.flat[e]]
+        while len(coeffs) > 1 and coeffs[0] == 0.0:
+            coeffs = coeffs[1:]
+        if len(coeffs) <= 1:
+            continue
+        r = np.roots(coeffs)
+        r = r[(np.abs(r.imag) <= 1e-12 * np.maximum(1.0, np.abs(r.real))) & (r.real > 0.0)].real
+        if len(r):
+            out.flat[e] = r.min()
+    return out
+
+
+def inversion_alpha(model, x, d):
+    """Inversion filter: alpha = min(1, 0.9 min_e t_e), t_e = smallest positive root of
+    det(Ds_e + t dDs_e) = 0.  Elements whose cubic provably has no root in
+    (0, 1/0.9] are skipped before the (slow, per-element) root finding."""
+    t = model.tets
+    Ds = np.transpose(x[t][:, 1:] - x[t][:, :1], (0, 2, 1))
+    dD = np.transpose(d[t][:, 1:] - d[t][:, :1], (0, 2, 1))
+    c = det_poly(Ds, dD)
+    T = 1.0 / FILTER_SAFETY
+    # |c1| T + |c2| T^2 + |c3| T^3 < c0  =>  det > 0 on [0, T]: no root there
+    cand = np.abs(c[1]) * T + np.abs(c[2]) * T ** 2 + np.abs(c[3]) * T ** 3 >= c[0]
+    if not np.any(cand):
+        return 1.0
+    roots = smallest_positive_root([ci[cand] for ci in c])
+    return float(min(1.0, FILTER_SAFETY * np.min(roots)))
+
+
+@dataclasses.dataclass
+class NewtonInfo:
+    alpha: float
+    alpha0: float
+    ls_evals: int
+    ds_norm: float
+    converged: bool
+    ls_failed: bool
+    energy: float
+    d: np.ndarray
+    ds: np.ndarray
+    df: np.ndarray
+
+
+class OracleSim:
+    """Timestep driver: begin_step / newton_iteration / end_step (Alg. 1)."""
+
+    def __init__(self, scene, basis, n_cg=None):
+        self.scene = scene
+        self.model = ip.make_model(scene)
+        self.basis = basis
+        self.Us = coarse.sms_matrix(self.model.X, basis)
+        self.Ua = coarse.affine_matrix(self.model.X, basis)
+        self.n_cg = basis.n_cg if n_cg is None else n_cg
+        self.eps = scene.eps
+        self.max_newton = scene.max_newton
+        self.x = self.model.X.copy()
+        self.v = np.zeros_like(self.x)
+
+    def begin_step(self):
+        self.x_t = self.x.copy()
+        self.xhat = ip.predictor(self.model, self.x, self.v)
+
+    def direction(self, x):
+        """(g, H, d_s, d_f, d) at x: Alg. 1 L229-238."""
+        m = self.model
+        g = ip.gradient(m, x, self.xhat)
+        H = ip.hessian(m, x, self.xhat).tocsr()
+        ds, da, Sa, S = subspace_direction(H, g, self.Ua, self.Us)
+        r = -g.ravel() - H @ ds
+        df = pcg(H, r, self.n_cg)
+        return g, H, ds, df, ds + df
+
+    def newton_iteration(self):
+        m = self.model
+        x = self.x
+        g, H, ds, df, d = self.direction(x)
+        d3 = d.reshape(-1, 3)
+        a0 = min(ccd_alpha(m, x, d3), inversion_alpha(m, x, d3))
+        alpha = a0
+        evals = 0
+        failed = False
+        while True:
+            evals += 1
+            if ip.energy_difference(m, x, d3, alpha, self.xhat) < 0.0:
+                break
+            alpha *= LS_SHRINK
+            if alpha < LS_MIN:
+                failed = True
+                break
+        if not failed:
+            self.x = x + alpha * d3
+        ds_norm = float(np.linalg.norm(ds))
+        conv = ds_norm / (m.h * m.n) < self.eps
+        return NewtonInfo(alpha, a0, evals, ds_norm, conv, failed,
+                          ip.energy(m, self.x, self.xhat), d, ds, df)
+
+    def end_step(self):
+        self.v = (self.x - self.x_t) / self.model.h
+
+    def timestep(self):
+        self.begin_step()
+        infos = []
+        for _ in range(self.max_newton):
+            info = self.newton_iteration()
+            infos.append(info)
+            if info.converged or info.ls_failed:
+                break
+        self.end_step()
+        return infos

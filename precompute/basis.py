@@ -1,0 +1,408 @@
+"""SMS / affine basis construction (BOUNDARY precompute; SURVEY.md §8(b) `ms_basis_build`).
+
+The basis is an INPUT to the hot path: its output (handle origins, per-vertex
+(handle, phi) lists, affine weight, N_cg) is fed identically to the CUDA path
+(through `ms_basis_upload`) and to the oracle.  Neither the hot path's coarse
+projection B^T H B nor any solve lives here.
+
+Steps (§3.5, §3.6, §3.7.2; readings Q15-Q17):
+1. Partition tets into m clusters: seeded kmeans++ + Lloyd on volume-weighted tet
+   barycentres (Euclidean stand-in for the paper's heat geodesics, NEXT-3).
+2. Enforce face-connectivity of each cluster.
+3. Centroid vertex c_i = cluster vertex nearest to the cluster's barycentre (Q15).
+4. Subdomain T_i = cluster i + clusters sharing a vertex with it (R9/Q16).
+5. Solve K u = 0 on T_i, K = L_s M^-1 L_s (Q17), u(c_i)=1, u(c_j)=0 for neighbour
+   centroids, u=0 on the internal boundary and at DBC vertices.
+   Clip u_pos = max(u, 0).
+6. DBC weight, POU normalisation, affine weight 1-phi_DBC.
+7. Handles are relabelled in lexicographic (x, y, z) order of their centroids so
+   that the coarse matrix is banded in handle order.
+"""
+from __future__ import annotations
+
+import dataclasses
+import os
+from collections import deque
+
+import numpy as np
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+from scipy.spatial import cKDTree
+
+
+@dataclasses.dataclass
+class Basis:
+    m: int
+    origins: np.ndarray      # (m,3) handle origins c_i (rest positions of centroid vertices)
+    vptr: np.ndarray         # (n_v+1,) int64 CSR over vertices
+    handle: np.ndarray       # (nnz,) int32 handle ids (sorted within each vertex)
+    phi: np.ndarray          # (nnz,) float64 weights > 0
+    phi_dbc: np.ndarray      # (n_v,) DBC weight
+    phi_affine: np.ndarray   # (n_v,) affine weight 1 - phi_dbc
+    affine_origin: np.ndarray  # (3,) centre of mass
+    n_cg: int                # 20 or 40 (hop heuristic)
+    hop_radius: float
+    cluster: np.ndarray      # (n_t,) cluster id (relabelled)
+    centroid_vertex: np.ndarray  # (m,) int
+    n_holes: int = 0         # free vertices repaired by reading B1
+
+    def save(self, path):
+        np.savez_compressed(path, **{k: getattr(self, k) for k in self.__dataclass_fields__})
+
+    @staticmethod
+    def load(path):
+        z = np.load(path)
+        kw = {}
+        for k in Basis.__dataclass_fields__:
+            v = z[k]
+            kw[k] = v.item() if v.ndim == 0 else v
+        kw["m"] = int(kw["m"])
+        kw["n_cg"] = int(kw["n_cg"])
+        kw["n_holes"] = int(kw.get("n_holes", 0))
+        return Basis(**kw)
+
+
+# ----------------------------------------------------------------------------- geometry
+
+def tet_volumes(X, tets):
+    D = X[tets[:, 1:]] - X[tets[:, :1]]
+    return np.linalg.det(D) / 6.0
+
+
+def face_adjacency(tets):
+    """Pairs (e, f) of tets sharing a triangular face."""
+    nt = len(tets)
+    loc = np.array([[1, 2, 3], [0, 2, 3], [0, 1, 3], [0, 1, 2]])
+    faces = np.sort(tets[:, loc].reshape(-1, 3), axis=1).astype(np.int64)
+    owner = np.repeat(np.arange(nt), 4)
+    key = (faces[:, 0] * (1 << 21) + faces[:, 1]) * (1 << 21) + faces[:, 2]
+    order = np.argsort(key, kind="stable")
+    ks = key[order]
+    dup = np.nonzero(ks[1:] == ks[:-1])[0]
+    return owner[order[dup]], owner[order[dup + 1]]
+
+
+# ----------------------------------------------------------------------------- k-means
+
+def kmeans_pp(P, w, m, rng):
+    n = len(P)
+    first = int(rng.choice(n, p=w / w.sum()))
+    C = [P[first]]
+    d2 = np.sum((P - C[0]) ** 2, axis=1)
+    for _ in range(1, m):
+        p = w * d2
+        s = p.sum()
+        idx = int(rng.choice(n, p=p / s)) if s > 0 else int(rng.integers(n))
+        C.append(P[idx])
+        d2 = np.minimum(d2, np.sum((P - P[idx]) ** 2, axis=1))
+    return np.array(C)
+
+
+def lloyd(P, w, C, max_iter=100):
+    assign = None
+    for _ in range(max_iter):
+        _, a = cKDTree(C).query(P, k=1)
+        if assign is not None and np.array_equal(a, assign):
+            break
+        assign = a
+        m = len(C)
+        W = np.bincount(assign, weights=w, minlength=m)
+        newC = np.stack([np.bincount(assign, weights=w * P[:, d], minlength=m) for d in range(3)], 1)
+        nz = W > 0
+        C = C.copy()
+        C[nz] = newC[nz] / W[nz, None]
+    return assign
+
+
+def enforce_connectivity(assign, tets, adj_pairs, m):
+    """Keep the largest face-connected component of each cluster; move the rest to the
+    adjacent cluster sharing the most faces (repeat until every cluster is connected)."""
+    nt = len(tets)
+    ea, eb = adj_pairs
+    for _ in range(20):
+        same = assign[ea] == assign[eb]
+        G = sp.coo_matrix((np.ones(int(same.sum())), (ea[same], eb[same])), shape=(nt, nt))
+        ncomp, comp = sp.csgraph.connected_components(G, directed=False)
+        # largest component per cluster
+        size = np.bincount(comp, minlength=ncomp)
+        comp_cluster = np.zeros(ncomp, dtype=np.int64)
+        comp_cluster[comp] = assign
+        order = np.lexsort((-size, comp_cluster))   # by cluster, then size desc
+        keep = np.zeros(ncomp, dtype=bool)
+        seen = set()
+        for ci in order:
+            cl = comp_cluster[ci]
+            if cl not in seen:
+                keep[ci] = True
+                seen.add(cl)
+        bad = ~keep[comp]
+        if not bad.any():
+            return assign
+        # reassign tets of non-kept components: neighbour cluster with most shared faces
+        diff = ~same
+        votes = {}
+        for x, y in ((ea[diff], eb[diff]), (eb[diff], ea[diff])):
+            sel = bad[x]
+            for e, c in zip(x[sel], assign[y[sel]]):
+                key = (comp[e], int(c))
+                votes[key] = votes.get(key, 0) + 1
+        target = {}
+        for (ci, c), v in sorted(votes.items()):
+            if ci not in target or v > target[ci][1]:
+                target[ci] = (c, v)
+        for e in np.nonzero(bad)[0]:
+            if comp[e] in target:
+                assign[e] = target[comp[e]][0]
+    return assign
+
+
+# ----------------------------------------------------------------------------- operators
+
+def local_laplacians(X, tets, weight):
+    """Per-tet 4x4 P1 FEM Laplacian V*w*G G^T (G = shape-function gradients)."""
+    D = X[tets[:, 1:]] - X[tets[:, :1]]                  # (nt,3,3) rows = edges
+    vol = np.linalg.det(D) / 6.0
+    Dinv = np.linalg.inv(D)                               # (nt,3,3)
+    # gradients of barycentric coordinates 1..3 are the columns of D^-1 (rows edge vectors)
+    g123 = np.transpose(Dinv, (0, 2, 1))                   # (nt,3,3): g_k = Dinv[:,k]
+    g0 = -g123.sum(axis=1, keepdims=True)
+    G = np.concatenate([g0, g123], axis=1)                # (nt,4,3)
+    Kl = np.einsum("eik,ejk->eij", G, G) * (vol * weight)[:, None, None]
+    return Kl, vol
+
+
+def assemble_subdomain(tets_sub, Kl_sub, vol_sub, verts):
+    """L_s and lumped M (volume/4) of the sub-mesh, in local vertex numbering of `verts`."""
+    n = len(verts)
+    gmap = {}
+    loc = np.searchsorted(verts, tets_sub)
+    rows = np.repeat(loc, 4, axis=1).ravel()
+    cols = np.tile(loc, (1, 4)).ravel()
+    L = sp.csr_matrix((Kl_sub.ravel(), (rows, cols)), shape=(n, n))
+    Mdiag = np.bincount(loc.ravel(), weights=np.repeat(vol_sub / 4.0, 4), minlength=n)
+    return L, Mdiag
+
+
+def constrained_bilaplacian(L, Mdiag, one_idx, zero_idx):
+    """Solve K u = 0, K = L M^-1 L, with u = 1 on one_idx and u = 0 on zero_idx."""
+    n = L.shape[0]
+    K = (L @ sp.diags(1.0 / Mdiag) @ L).tocsr()
+    u = np.zeros(n)
+    cons = np.zeros(n, dtype=bool)
+    cons[one_idx] = True
+    cons[zero_idx] = True
+    u[one_idx] = 1.0
+    u[zero_idx] = 0.0
+    cons[one_idx] = True
+    free = np.nonzero(~cons)[0]
+    if len(free):
+        Kff = K[free][:, free].tocsc()
+        rhs = -(K[free][:, np.nonzero(cons)[0]] @ u[cons])
+        u[free] = spla.spsolve(Kff, rhs, permc_spec="MMD_AT_PLUS_A")
+    return u
+
+
+# ----------------------------------------------------------------------------- driver
+
+_G = {}
+
+
+def _solve_handle(i):
+    g = _G
+    sub_tets_mask = g["in_sub"](i)
+    tsub = g["tets"][sub_tets_mask]
+    verts = np.unique(tsub)
+    L, Md = assemble_subdomain(tsub, g["Kl"][sub_tets_mask], g["vol"][sub_tets_mask], verts)
+    # internal boundary: subdomain vertices also used by tets outside the subdomain
+    inner = g["vert_tet_count"][verts] > np.bincount(np.searchsorted(verts, tsub.ravel()),
+                                                       minlength=len(verts))
+    zero = set(np.nonzero(inner)[0].tolist())
+    for j in g["nbrs"][i]:
+        if j != i:
+            zero.add(int(np.searchsorted(verts, g["cv"][j])))
+    if g["dbc_mask"] is not None:
+        zero.update(np.nonzero(g["dbc_mask"][verts])[0].tolist())
+    one = int(np.searchsorted(verts, g["cv"][i]))
+    zero.discard(one)
+    u = constrained_bilaplacian(L, Md, [one], sorted(zero))
+    return verts, u
+
+
+def _solve_dbc():
+    g = _G
+    dbc = g["dbc"]
+    cl = np.unique(g["vert_clusters_of"](dbc))
+    sub = set()
+    for c in cl:
+        sub.update(g["nbrs"][c])
+    sub_mask = np.isin(g["assign"], np.array(sorted(sub)))
+    tsub = g["tets"][sub_mask]
+    verts = np.unique(tsub)
+    L, Md = assemble_subdomain(tsub, g["Kl"][sub_mask], g["vol"][sub_mask], verts)
+    inner = g["vert_tet_count"][verts] > np.bincount(np.searchsorted(verts, tsub.ravel()),
+                                                       minlength=len(verts))
+    one = np.searchsorted(verts, dbc)
+    zero = set(np.nonzero(inner)[0].tolist())
+    zero.update(int(np.searchsorted(verts, g["cv"][c])) for c in cl)
+    zero.difference_update(one.tolist())
+    u = constrained_bilaplacian(L, Md, one, sorted(zero))
+    out = np.zeros(len(g["X"]))
+    out[verts] = np.maximum(u, 0.0)
+    return out
+
+
+def hop_radius(assign, tets, cv, n_v, m):
+    """Mean over partitions of the max edge-hop distance from the centroid vertex to the
+    partition's vertices, BFS on mesh edges restricted to the partition (Q7)."""
+    e = np.concatenate([tets[:, [a, b]] for a in range(4) for b in range(a + 1, 4)])
+    A = sp.coo_matrix((np.ones(len(e)), (e[:, 0], e[:, 1])), shape=(n_v, n_v))
+    A = ((A + A.T) > 0).tocsr()
+    radii = []
+    for i in range(m):
+        pv = np.unique(tets[assign == i])
+        sub = A[pv][:, pv]
+        d = sp.csgraph.shortest_path(sub, unweighted=True, indices=int(np.searchsorted(pv, cv[i])))
+        radii.append(np.max(d[np.isfinite(d)]))
+    return float(np.mean(radii))
+
+
+def build_basis(scene, m=None, seed=None, workers=None, verbose=False) -> Basis:
+    import time
+    t0 = time.time()
+    X, tets = scene.X, scene.tets.astype(np.int64)
+    m = scene.m if m is None else m
+    n_v, n_t = len(X), len(tets)
+    rng = scene.rngs()[2] if seed is None else np.random.default_rng(seed)
+
+    vol = tet_volumes(X, tets)
+    bary = X[tets].mean(axis=1)
+    C0 = kmeans_pp(bary, vol, m, rng)
+    assign = lloyd(bary, vol, C0)
+    adj = face_adjacency(tets)
+    assign = enforce_connectivity(assign.copy(), tets, adj, m)
+    # drop empty clusters (cannot happen after kmeans++ in practice)
+    used = np.unique(assign)
+    remap = -np.ones(m, dtype=np.int64)
+    remap[used] = np.arange(len(used))
+    assign = remap[assign]
+    m = len(used)
+    if verbose:
+        print(f"  kmeans+connectivity {time.time()-t0:.1f}s", flush=True)
+
+    # centroid vertices
+    W = np.bincount(assign, weights=vol, minlength=m)
+    bc = np.stack([np.bincount(assign, weights=vol * bary[:, d], minlength=m) for d in range(3)], 1) / W[:, None]
+    cv = np.zeros(m, dtype=np.int64)
+    for i in range(m):
+        pv = np.unique(tets[assign == i])
+        dd = np.sum((X[pv] - bc[i]) ** 2, axis=1)
+        cv[i] = pv[np.argmin(dd)]          # argmin: ties -> lowest vertex index
+    # relabel handles in lexicographic (x, y, z) order of the centroid vertex
+    order = np.lexsort((X[cv, 2], X[cv, 1], X[cv, 0]))
+    newid = np.empty(m, dtype=np.int64)
+    newid[order] = np.arange(m)
+    assign = newid[assign]
+    cv = cv[order]
+
+    # vertex -> clusters incidence and cluster vertex-adjacency
+    VC = sp.coo_matrix((np.ones(4 * n_t), (tets.ravel(), np.repeat(assign, 4))), shape=(n_v, m)).tocsr()
+    VC.data[:] = 1.0
+    CA = (VC.T @ VC).tocsr()
+    nbrs = [np.sort(CA.indices[CA.indptr[i]:CA.indptr[i + 1]]) for i in range(m)]
+    vert_tet_count = np.bincount(tets.ravel(), minlength=n_v)
+
+    Ewt = scene.E / np.median(scene.E)
+    Kl, _ = local_laplacians(X, tets, Ewt)
+
+    dbc_mask = None
+    if len(scene.dbc):
+        dbc_mask = np.zeros(n_v, dtype=bool)
+        dbc_mask[scene.dbc] = True
+
+    _G.clear()
+    _G.update(X=X, tets=tets, assign=assign, Kl=Kl, vol=vol, cv=cv, nbrs=nbrs,
+              vert_tet_count=vert_tet_count, dbc_mask=dbc_mask, dbc=np.asarray(scene.dbc, np.int64))
+    _G["in_sub"] = lambda i: np.isin(assign, nbrs[i])
+    _G["vert_clusters_of"] = lambda vs: np.concatenate(
+        [VC.indices[VC.indptr[v]:VC.indptr[v + 1]] for v in vs])
+
+    if workers is None:
+        workers = min(os.cpu_count() or 1, 64)
+    t1 = time.time()
+    if workers > 1 and m > 8:
+        import multiprocessing as mp
+        ctx = mp.get_context("fork")
+        with ctx.Pool(workers) as pool:
+            res = pool.map(_solve_handle, range(m), chunksize=max(1, m // (4 * workers)))
+    else:
+        res = [_solve_handle(i) for i in range(m)]
+    if verbose:
+        print(f"  {m} bilaplacian solves {time.time()-t1:.1f}s ({workers} workers)", flush=True)
+
+    u_dbc = _solve_dbc() if dbc_mask is not None else np.zeros(n_v)
+
+    # POU normalisation
+    rows = np.concatenate([r[0] for r in res])
+    hid = np.concatenate([np.full(len(r[0]), i, dtype=np.int64) for i, r in enumerate(res)])
+    uraw = np.concatenate([r[1] for r in res])
+    val = np.maximum(uraw, 0.0)                      # clip
+    denom = np.bincount(rows, weights=val, minlength=n_v) + u_dbc
+    free = np.ones(n_v, dtype=bool)
+    if dbc_mask is not None:
+        free &= ~dbc_mask
+    holes = np.nonzero((denom <= 0) & free)[0]
+    if len(holes):
+        # Reading B1: the paper is silent on a free vertex where every clipped
+        # weight vanishes; such a vertex is given to the covering handle (v in T_i) with the
+        # largest unclipped u_i(v), weight 1.  POU and hence linear precision still hold.
+        hole_mask = np.zeros(n_v, dtype=bool)
+        hole_mask[holes] = True
+        sel = np.nonzero(hole_mask[rows])[0]
+        o = np.lexsort((-uraw[sel], rows[sel]))
+        srt = sel[o]
+        first = np.ones(len(srt), dtype=bool)
+        first[1:] = rows[srt][1:] != rows[srt][:-1]
+        val[srt[first]] = 1.0
+        denom = np.bincount(rows, weights=val, minlength=n_v) + u_dbc
+        if verbose:
+            print(f"  coverage holes repaired: {len(holes)}")
+    if np.any(denom[free] <= 0):
+        bad = np.nonzero((denom <= 0) & free)[0]
+        raise RuntimeError(f"basis coverage hole at {len(bad)} free vertices, e.g. {bad[:5]}")
+    keep = val > 0
+    rows, hid, val = rows[keep], hid[keep], val[keep]
+    phi = val / denom[rows]
+    o = np.lexsort((hid, rows))
+    rows, hid, phi = rows[o], hid[o], phi[o]
+    vptr = np.zeros(n_v + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=n_v), out=vptr[1:])
+    with np.errstate(invalid="ignore", divide="ignore"):
+        phi_dbc = np.where(denom > 0, u_dbc / np.where(denom > 0, denom, 1.0), 0.0)
+    if dbc_mask is not None:
+        phi_dbc[dbc_mask] = 1.0
+    phi_aff = 1.0 - phi_dbc
+
+    mass = np.bincount(tets.ravel(), weights=np.repeat(scene.rho * vol / 4.0, 4), minlength=n_v)
+    com = (mass[:, None] * X).sum(0) / mass.sum()
+
+    t2 = time.time()
+    hr = hop_radius(assign, tets, cv, n_v, m)
+    n_cg = 20 if abs(hr - 20) <= abs(hr - 40) else 40
+    if verbose:
+        print(f"  hop radius {hr:.2f} -> n_cg {n_cg} ({time.time()-t2:.1f}s); total {time.time()-t0:.1f}s")
+    return Basis(m=m, origins=X[cv].copy(), n_holes=len(holes), vptr=vptr, handle=hid.astype(np.int32), phi=phi,
+                 phi_dbc=phi_dbc, phi_affine=phi_aff, affine_origin=com, n_cg=n_cg, hop_radius=hr,
+                 cluster=assign.astype(np.int32), centroid_vertex=cv)
+
+
+def cached_basis(scene, cache_dir=None, **kw) -> Basis:
+    """Build or load the basis of a scene (cache keyed by scene name, sizes and m)."""
+    cache_dir = cache_dir or os.environ.get("MSIM_CACHE", os.path.join(os.path.dirname(__file__), "..", ".cache"))
+    os.makedirs(cache_dir, exist_ok=True)
+    key = f"{scene.name}_{scene.n_verts}_{scene.n_tets}_{scene.m}.npz"
+    path = os.path.join(cache_dir, key)
+    if os.path.exists(path):
+        return Basis.load(path)
+    b = build_basis(scene, **kw)
+    b.save(path)
+    return b
