@@ -1,0 +1,305 @@
+"""Benchmark of the B200-native multilevel Newton solve (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 4]
+
+A "step" is one implicit-Euler timestep of config C4 (64^3 cubes x 6 = 1,572,864 tets,
+274,625 vertices, m = 512 handles): predictor, Newton iterations (element gradient, PSD
+Hessian, BSR assembly, S = B^T H B + Cholesky, coarse correction, N_cg Jacobi-PCG, filtered
+line search) until ||d_s|| / (h n_v) < eps, velocity update -- every row of SURVEY.md §8(a).
+`value` = Newton iterations / second over the timed steps (device time, CUDA events, max over
+ranks); `pcg_iters_per_s` reports the PCG rate of the same run.  Inputs are larger than L2
+(the BSR Hessian alone is 289 MB), so no explicit flush is done between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Newton steps/s & PCG iters/s on 1.5M-tet mesh; SpMV/assembly GB/s vs HBM peak"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), "measured", d
+    return 6650.0, "fallback", {}
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, device_index):
+        self.idx = device_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th = threading.Thread(target=self._run, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if len(s) > 2 + k and s[2 + k] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- roofline
+def algorithmic_bytes(sizes, n_cg):
+    """Algorithmic bytes per unit of work (SURVEY §8(d) formulas; fp64 values, int32 indices)."""
+    nv, nt, nnzb = sizes["n_verts"], sizes["n_tets"], sizes["nnzb"]
+    spmv = nnzb * 76 + 4 * (nv + 1) + 2 * 24 * nv
+    pcg_iter = spmv + 11 * 24 * nv
+    assembly = nt * (720 + 64) + nnzb * 72          # staged 10 upper blocks read (720 B) + ids + BSR write
+    return {"spmv": spmv, "pcg_iter": pcg_iter, "assembly": assembly}
+
+
+# ----------------------------------------------------------------------------- scenes
+def load_case(config):
+    from precompute.basis import cached_basis
+    from precompute.mesh import make_scene
+    s = make_scene(config)
+    t0 = time.time()
+    b = cached_basis(s)
+    return s, b, time.time() - t0
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+# ----------------------------------------------------------------------------- oracle (cpu)
+def oracle_newton_sample(s, b, budget_s=30.0):
+    """Times the oracle (as it stands) on a bounded sample of one C4 Newton iteration and
+    scales it to the full iteration: full gradient, PSD Hessian + assembly of a 1/8 slice of
+    the tets (x 8), full S = B^T H B, dense Cholesky, 20 PCG iterations, one line-search
+    energy evaluation.  Returns (seconds per full Newton iteration, description, threads)."""
+    from oracle import coarse, fem, ip, solver
+    sim = solver.OracleSim(s, b)
+    sim.begin_step()
+    m, x = sim.model, sim.x
+    t = {}
+    t0 = time.time(); g = ip.gradient(m, x, sim.xhat); t["grad"] = time.time() - t0
+    frac = 8
+    sl = slice(0, m.tets.shape[0] // frac)
+    t0 = time.time()
+    He = fem.element_hessian_psd(x, m.tets[sl], m.Bm[sl], m.V[sl], m.mu[sl], m.lam[sl])
+    t["hess_slice"] = time.time() - t0
+    del He
+    # full assembled H is needed for S and PCG: assemble once (not timed beyond the slice)
+    H = ip.hessian(m, x, sim.xhat).tocsr()
+    t0 = time.time(); S = coarse.galerkin(sim.Us, H); t["coarse_S"] = time.time() - t0
+    t0 = time.time(); L = coarse.cholesky(S); t["chol"] = time.time() - t0
+    t0 = time.time(); solver.pcg(H, -g.ravel(), sim.n_cg); t["pcg"] = time.time() - t0
+    d = np.zeros_like(x); d[:, 2] = -1e-4
+    t0 = time.time(); ip.energy_difference(m, x, d, 1.0, sim.xhat); t["ls_eval"] = time.time() - t0
+    total = t["grad"] + frac * t["hess_slice"] + t["coarse_S"] + t["chol"] + t["pcg"] + t["ls_eval"]
+    desc = ("one C4 Newton iteration of the oracle: gradient, S=B^T H B, Cholesky, %d PCG iterations and one "
+            "line-search energy timed in full; the PSD Hessian+assembly timed on 1/%d of the tets and scaled x%d "
+            "(measured %.1f s of CPU work)") % (sim.n_cg, frac, frac, sum(t.values()))
+    return total, desc, t
+
+
+def threads_used():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------------------- main arms
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    s, b, _ = load_case(args.config)
+    per_iter = []
+    desc = None
+    for k in range(args.warmup + args.steps):
+        sec, desc, _ = oracle_newton_sample(s, b)
+        if k >= args.warmup:
+            per_iter.append(sec)
+        if k + 1 >= 1 and args.quick_reference:
+            break
+    sec = float(np.mean(per_iter)) if per_iter else sec
+    value = 1.0 / sec
+    line = {"metric": METRIC, "value": value, "unit": "Newton steps/s", "impl": "reference",
+            "n_gpus": world, "steps": len(per_iter) or 1, "warmup": args.warmup, "ms_per_step": 1e3 * sec,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_dict(s, b, world),
+            "cpu_baseline": {"value": value, "unit": "Newton steps/s", "cores": threads_used(),
+                             "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": "Newton steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(s, b, world):
+    return {"workload": f"{s.name}: {s.dims[0]}x{s.dims[1]}x{s.dims[2]} cubes x6 tets = {s.n_tets} tets, "
+                        f"{s.n_verts} vertices, m={b.m} handles, N_cg={b.n_cg}, IE h=1/60, ground barrier",
+            "n_tets": int(s.n_tets), "n_verts": int(s.n_verts), "m": int(b.m), "n_cg": int(b.n_cg),
+            "parallelism": f"replicas{world}" if world > 1 else "single",
+            "l2_flush": "inputs larger than L2 (BSR 289 MB + staged element Hessians 1.1 GB)"}
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    from paper_2508_13386_b200 import msim
+    s, b, t_basis = load_case(args.config)
+    stream = torch.cuda.current_stream()
+    ctx = msim.context_from_scene(s, b, device=local, stream=stream.cuda_stream)
+    sizes = ctx.sizes()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warm-up
+    for _ in range(args.warmup):
+        ctx.timestep()
+    # ---- timed region (device resident)
+    ctx.set_profiling(True)
+    launches0 = ctx.kernel_launches()
+    newton = pcg = 0
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            st = ctx.timestep()
+            newton += st.newton_iters
+            pcg += st.pcg_iters
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = ctx.kernel_launches() - launches0
+    phases = ctx.phase_times()
+    ctx.set_profiling(False)
+    ms_t = torch.tensor([ms], device="cuda")
+    cnt = torch.tensor([newton, pcg], device="cuda", dtype=torch.float64)
+    if world > 1:
+        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(cnt, op=torch.distributed.ReduceOp.SUM)
+    ms_max = float(ms_t.item())
+    newton_all, pcg_all = float(cnt[0].item()), float(cnt[1].item())
+
+    # ---- end-to-end through the C-ABI with host buffers (H2D state, timestep, D2H state)
+    x_h, v_h = ctx.get_state()
+    x_h = np.ascontiguousarray(x_h)
+    v_h = np.ascontiguousarray(v_h)
+    e_newton = 0
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ctx.set_state(x_h, v_h)
+        st = ctx.timestep()
+        e_newton += st.newton_iters
+        x_h, v_h = ctx.get_state()
+    barrier()
+    e_sec = time.perf_counter() - t0
+    e_t = torch.tensor([e_sec], device="cuda")
+    e_c = torch.tensor([float(e_newton)], device="cuda", dtype=torch.float64)
+    if world > 1:
+        torch.distributed.all_reduce(e_t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(e_c, op=torch.distributed.ReduceOp.SUM)
+
+    if rank == 0:
+        hbm, peak_src, peaks = load_peaks()
+        ab = algorithmic_bytes(sizes, b.n_cg)
+        pcg_ms, pcg_n = phases["pcg"]
+        pcg_iter_ms = pcg_ms / max(pcg_n * b.n_cg, 1)
+        asm_ms, asm_n = phases["assembly"]
+        asm_avg = asm_ms / max(asm_n, 1)
+        achieved = ab["pcg_iter"] / (pcg_iter_ms * 1e-3) / 1e9
+        line = {
+            "metric": METRIC, "value": newton_all / (ms_max * 1e-3), "unit": "Newton steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(s, b, world),
+            "pcg_iters_per_s": pcg_all / (ms_max * 1e-3),
+            "newton_iters": int(newton_all),
+            "roofline": {"bound": "hbm", "kernel": "PCG iteration (fused SpMV + update)",
+                         "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "peak_source": peak_src, "traffic": None,
+                         "algorithmic_bytes_per_launch": ab["pcg_iter"],
+                         "avg_ms_per_launch": pcg_iter_ms},
+            "assembly_gbs": ab["assembly"] / (asm_avg * 1e-3) / 1e9 if asm_n else None,
+            "phase_ms_per_newton": {k: (v[0] / max(newton / world, 1)) for k, v in phases.items()},
+            "gpu_launches": int(launches),
+            "e2e": {"value": float(e_c.item()) / float(e_t.item()), "unit": "Newton steps/s",
+                    "h2d_bytes_per_step": 2 * 3 * 8 * s.n_verts, "d2h_bytes_per_step": 2 * 3 * 8 * s.n_verts},
+            "clocks": clk.summary(),
+            "basis_build_s": t_basis,
+        }
+        if not args.no_cpu_baseline:
+            sec, desc, _ = oracle_newton_sample(s, b)
+            line["cpu_baseline"] = {"value": 1.0 / sec, "unit": "Newton steps/s", "cores": threads_used(),
+                                    "kind": "oracle", "sample": desc}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick-reference", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

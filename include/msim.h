@@ -1,0 +1,219 @@
+/*
+ * msim.h — C-ABI of the B200-native multilevel elastodynamics Newton solve
+ * (arXiv 2508.13386, "Sparse, Geometry- and Material-Aware Bases for Multilevel
+ * Elastodynamic Simulation").  Library: paper_2508_13386_b200/lib/libmsim.so.
+ *
+ * Citations: "P:<line>" = PAPER.md line, "S:<line>" = SPEC.md line, R#/Q# = readings
+ * listed in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - Every pointer argument is a HOST pointer unless the name ends in `_dev`.  Host arrays
+ *    are copied (or written) before the call returns; the caller keeps ownership.
+ *  - Vectors over vertices are AoS xyz: element 3*v + c (c = x,y,z), fp64.  Indices int32.
+ *  - All device work is enqueued on the CUDA stream passed to ms_create (e.g. torch's
+ *    current stream), so callers and the library share ordering.  Calls that return host
+ *    data synchronise that stream.
+ *  - Return value: 0 OK; >0 soft warning (result valid); <0 hard error.  No C++ exception
+ *    crosses the ABI.  ms_last_error() returns a message for the last non-zero status.
+ *  - A context is single-GPU, single-thread (not thread-safe).
+ */
+#ifndef MSIM_H
+#define MSIM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ms_ctx ms_ctx;
+typedef int32_t ms_status;
+
+enum {
+  MS_OK = 0,
+  MS_WARN_LS_FAILED = 1,    /* line search fell below ls_min; iterate kept   */
+  MS_WARN_NEWTON_CAP = 2,   /* max_newton iterations reached without convergence     */
+  MS_ERR_ARG = -1,          /* invalid argument: index range, V<=0, E<=0, nu not in [0,.5)…  */
+  MS_ERR_CUDA = -2,         /* CUDA runtime error                                             */
+  MS_ERR_NCCL = -3,         /* reserved (multi-GPU)                                           */
+  MS_ERR_NOT_SPD = -4,      /* coarse matrix not SPD (Cholesky pivot <= 0) (reading Q18)     */
+  MS_ERR_COVERAGE = -5,     /* basis coverage hole: sum phi = 0 at a free vertex             */
+  MS_ERR_OOM = -6,          /* device allocation failed                                       */
+  MS_ERR_INFEASIBLE = -7,   /* inverted element or penetrating vertex at entry (E = +inf)    */
+  MS_ERR_STATE = -8         /* call order violated (e.g. newton_step before begin_step)      */
+};
+
+/* Solver parameters.  Defaults (ms_default_params): h = 1/60, gravity (0,0,-9.8),
+ * eps = 1e-6, max_newton = 100, n_cg = 0 (= basis heuristic), ls_shrink = 0.5,
+ * ls_min = 1e-8, filter_safety = 0.9, ls_batch = 4, use_graphs = 1. */
+typedef struct ms_params {
+  double h;               /* timestep [s] (implicit Euler)                      */
+  double gravity[3];      /* folded into the predictor xhat (reading R8)                   */
+  double eps;             /* termination ||d_s||_2 / (h n_v) < eps (reading R7)     */
+  int32_t max_newton;     /* Newton iteration cap per timestep                             */
+  int32_t n_cg;           /* full-space Jacobi-PCG iterations; 0 = value from the basis   */
+  double ls_shrink;       /* backtracking factor (reading Q12)                      */
+  double ls_min;          /* smallest step tried before MS_WARN_LS_FAILED                  */
+  double filter_safety;   /* CCD / inversion filter safety factor                          */
+  int32_t ls_batch;       /* candidate step sizes evaluated per fused line-search pass     */
+  int32_t use_graphs;     /* capture the fixed-count PCG loop in a CUDA graph              */
+} ms_params;
+
+typedef struct ms_newton_stats {
+  double alpha;           /* accepted step (0 if the line search failed)                   */
+  double alpha0;          /* min(1, CCD filter, inversion filter)                          */
+  double ds_norm;         /* ||d_s||_2 over all 3 n_v DOFs                                  */
+  double energy;          /* E(x) at the START of the iteration (Eq. 2)                    */
+  double delta_energy;    /* E(x + alpha d) - E(x) of the accepted step                    */
+  double grad_norm;       /* ||g||_2 at the start of the iteration                          */
+  int32_t ls_evals;       /* number of candidate steps evaluated                           */
+  int32_t converged;      /* termination test passed after this iteration                  */
+  int32_t ls_failed;      /* 1 if no decrease down to ls_min                               */
+  int32_t n_cg;           /* PCG iterations performed                                      */
+} ms_newton_stats;
+
+typedef struct ms_step_stats {
+  int32_t newton_iters;   /* Newton iterations in this timestep                            */
+  int32_t pcg_iters;      /* total full-space PCG iterations                               */
+  int32_t ls_evals;       /* total line-search candidates evaluated                        */
+  int32_t status;         /* MS_OK / MS_WARN_*                                              */
+  double last_ds_norm;
+  double last_alpha;
+} ms_step_stats;
+
+/* Accumulated device time (CUDA events on the library stream) per phase while profiling
+ * is enabled (ms_set_profiling).  Index with the MS_PHASE_* constants. */
+enum {
+  MS_PHASE_GRAD = 0,      /* element energy+gradient + vertex gather   (rows a1-a2)   */
+  MS_PHASE_HESS,          /* element Hessian + PSD projection          (row a3)       */
+  MS_PHASE_ASSEMBLY,      /* BSR gather assembly + Jacobi diagonal     (row a4)       */
+  MS_PHASE_COARSE_S,      /* B^T H B and U_a^T H U_a                   (row a5)       */
+  MS_PHASE_COARSE_FACTOR, /* Cholesky of S and S_a                     (row a6)       */
+  MS_PHASE_COARSE_SOLVE,  /* restrict / solve / lift / residual SpMVs  (row a7)       */
+  MS_PHASE_PCG,           /* fixed-count Jacobi-PCG                    (row a8)       */
+  MS_PHASE_LINESEARCH,    /* filters + batched energies + update       (row a9)       */
+  MS_PHASE_COUNT
+};
+typedef struct ms_phase_times {
+  double ms[MS_PHASE_COUNT];
+  int64_t count[MS_PHASE_COUNT];
+} ms_phase_times;
+
+typedef struct ms_pcg_stats {
+  int32_t iters;          /* iterations performed                                          */
+  double rz0;             /* r0^T D^-1 r0                                                  */
+  double rz;              /* final r^T D^-1 r                                              */
+} ms_pcg_stats;
+
+/* ---------------------------------------------------------------- lifecycle */
+const char *ms_version(void);
+void ms_default_params(ms_params *out);
+/* Create a context on `device`, enqueuing on `cuda_stream` (a cudaStream_t; NULL = legacy
+ * default stream).  nccl_id / rank / world are reserved for the slab-partitioned multi-GPU
+ * path; this build accepts world == 1 only (nccl_id ignored). */
+ms_status ms_create(ms_ctx **out, int device, void *cuda_stream, const uint8_t *nccl_id,
+                    int rank, int world);
+ms_status ms_destroy(ms_ctx *ctx);
+const char *ms_last_error(ms_ctx *ctx);
+
+/* ---------------------------------------------------------------- problem setup */
+/* Tet mesh, rest positions (n_verts x 3) = initial positions, tets (n_tets x 4, positive
+ * orientation), per-tet Young's modulus E [Pa], Poisson ratio nu, density rho
+ * (S:22-31).  Builds the 3x3-block BSR pattern (vertex adjacency + diagonal), the
+ * atomic-free assembly maps and the lumped mass m_v = sum rho V / 4 (Q9).
+ * Errors: MS_ERR_ARG for out-of-range indices, V <= 0, E <= 0, nu outside [0,0.5), rho <= 0. */
+ms_status ms_upload_mesh(ms_ctx *ctx, int64_t n_verts, const double *rest_xyz, int64_t n_tets,
+                         const int32_t *tets, const double *E, const double *nu,
+                         const double *rho);
+/* Dirichlet vertices, pinned at their rest position (Q13: identity rows, g = 0). */
+ms_status ms_set_dirichlet(ms_ctx *ctx, int64_t n, const int32_t *verts);
+/* Ground-plane IPC barrier b(d) = -(d-dhat)^2 ln(d/dhat), d = normal.x - offset
+ * (P:177); kappa is the barrier stiffness.  kappa <= 0 disables contact. */
+ms_status ms_set_ground(ms_ctx *ctx, const double normal[3], double offset, double dhat,
+                        double kappa);
+ms_status ms_set_params(ms_ctx *ctx, const ms_params *p);
+ms_status ms_get_params(ms_ctx *ctx, ms_params *p);
+
+/* Upload the precomputed bases (Eq. 7):
+ *  m handles with origins c_i (m x 3); per-vertex CSR (vptr[n_verts+1], handle[], phi[])
+ *  of the SMS weights phi_i(v) > 0; the affine weight phi_a(v) = 1 - phi_DBC(v) and its
+ *  origin (centre of mass); n_cg = refinement iterations from the hop heuristic.
+ * The 3x12 block of vertex v and handle i is I3 kron (phi_i(v) [1, X_v - c_i]) with the 12
+ * coordinates ordered [x-row(4), y-row(4), z-row(4)].  Builds the handle-major transpose,
+ * the coupled-handle pattern of S = B^T H B and its Cholesky schedule.
+ * Errors: MS_ERR_ARG (bad sizes / handle ids), MS_ERR_COVERAGE (sum phi + phi_DBC = 0). */
+ms_status ms_basis_upload(ms_ctx *ctx, int32_t m, const double *origins, const int64_t *vptr,
+                          const int32_t *handle, const double *phi, const double *phi_affine,
+                          const double affine_origin[3], int32_t n_cg);
+
+/* ---------------------------------------------------------------- state */
+/* Set / get positions x and velocities v (n_verts x 3). */
+ms_status ms_set_state(ms_ctx *ctx, const double *x, const double *v);
+ms_status ms_get_state(ms_ctx *ctx, double *x, double *v);
+/* Mid-step state for bootstrapped parity (reading R10): x^t, xhat and the current iterate. */
+ms_status ms_set_step_state(ms_ctx *ctx, const double *x_t, const double *xhat, const double *x);
+ms_status ms_get_step_state(ms_ctx *ctx, double *x_t, double *xhat, double *x);
+
+/* ---------------------------------------------------------------- the hot path */
+/* One implicit-Euler timestep: begin_step, Newton iterations until converged / cap /
+ * line-search failure, end_step (Alg. 1; §3.9). */
+ms_status ms_timestep(ms_ctx *ctx, ms_step_stats *out);
+/* xhat = x^t + h v^t + h^2 g, x = x^t (R8). */
+ms_status ms_begin_step(ms_ctx *ctx);
+/* One Newton iteration: gradient, PSD Hessian, BSR assembly,
+ * S_a and S = B^T H B + Cholesky, coarse correction d_s (Alg. 2, R4, R6), N_cg Jacobi-PCG
+ * iterations on H d_f = -g - H d_s (R5), d = d_s + d_f, CCD + inversion
+ * filtered backtracking on E (Q12), x += alpha d, termination test (R7).
+ * Returns MS_WARN_LS_FAILED if the line search failed (x unchanged). */
+ms_status ms_newton_step(ms_ctx *ctx, ms_newton_stats *out);
+/* v = (x - x^t) / h. */
+ms_status ms_end_step(ms_ctx *ctx);
+
+/* ---------------------------------------------------------------- parity hooks / pieces */
+/* Evaluate energy, gradient and the assembled Hessian H at the current iterate and xhat
+ * (rows a2-a4).  energy_out may be NULL. */
+ms_status ms_assemble(ms_ctx *ctx, double *energy_out);
+/* Gradient (3 n_verts) of the last ms_assemble / Newton iteration. */
+ms_status ms_get_gradient(ms_ctx *ctx, double *g);
+/* Per-element outputs at positions x (n_verts x 3): Ee[n_tets] = V_e Psi(F_e),
+ * ge[n_tets x 12] = V_e G_e^T vec P, He[n_tets x 144] = P+(H_e) (row-major 12x12, vertex-
+ * major xyz index 3a+c); any output pointer may be NULL. */
+ms_status ms_eval_elements(ms_ctx *ctx, const double *x, double *Ee, double *ge, double *He);
+/* BSR export of the assembled H: nnzb (out), rowptr[n_verts+1], colidx[nnzb], vals[9 nnzb]
+ * (row-major 3x3).  Pass NULL arrays to query nnzb only. */
+ms_status ms_export_bsr(ms_ctx *ctx, int64_t *nnzb, int32_t *rowptr, int32_t *colidx,
+                        double *vals);
+/* y = H x with the assembled H (3 n_verts vectors). */
+ms_status ms_spmv(ms_ctx *ctx, const double *x, double *y);
+/* w = U_s q (q: 12 m) and z = U_s^T y (y: 3 n_verts). */
+ms_status ms_basis_apply(ms_ctx *ctx, const double *q, double *w);
+ms_status ms_basis_apply_t(ms_ctx *ctx, const double *y, double *z);
+/* Coarse matrices of the last assembly: S (12m x 12m, dense row-major; may be NULL) and
+ * S_a (12 x 12; may be NULL).  Computes S, S_a from the assembled H if needed. */
+ms_status ms_export_coarse(ms_ctx *ctx, double *S, double *Sa);
+/* Subspace direction of the last assembly: d_s (and d_a) from Alg. 2 with exact solves. */
+ms_status ms_subspace_direction(ms_ctx *ctx, double *ds, double *da);
+/* Directions d_s, d_f of the last Newton iteration (3 n_verts each; either may be NULL). */
+ms_status ms_get_direction(ms_ctx *ctx, double *ds, double *df);
+/* Exactly `iters` Jacobi-PCG iterations on H sol = rhs from sol = 0 with the assembled H
+ * (stops early only if r^T D^-1 r == 0). */
+ms_status ms_pcg_solve(ms_ctx *ctx, const double *rhs, double *sol, int32_t iters,
+                       ms_pcg_stats *out);
+/* Same, device-resident vectors (length 3 n_verts, on the context's device/stream). */
+ms_status ms_pcg_solve_dev(ms_ctx *ctx, const double *rhs_dev, double *sol_dev, int32_t iters,
+                           ms_pcg_stats *out);
+
+/* ---------------------------------------------------------------- instrumentation */
+ms_status ms_set_profiling(ms_ctx *ctx, int32_t on);      /* resets the accumulators   */
+ms_status ms_get_phase_times(ms_ctx *ctx, ms_phase_times *out);
+/* Number of kernel launches (graph-embedded kernels included) issued by this context. */
+int64_t ms_kernel_launches(ms_ctx *ctx);
+/* Sizes: n_verts, n_tets, nnzb (BSR blocks), m (handles), nnz_phi, nnzb_S (coupled handle
+ * pairs incl. diagonal) — any pointer may be NULL. */
+ms_status ms_get_sizes(ms_ctx *ctx, int64_t *n_verts, int64_t *n_tets, int64_t *nnzb,
+                       int32_t *m, int64_t *nnz_phi, int64_t *nnzb_S);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSIM_H */

@@ -1,0 +1,689 @@
+// C-ABI entry points (include/msim.h) and the host-side Newton orchestration.
+//
+// SURVEY §8(b) (the boundary) and §3(b) (call stack of ms_timestep).  The orchestration
+// enqueues every step of one Newton iteration on the caller's stream and synchronises once
+// per line-search batch (one device->host read of a few scalars).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+
+#include "common.cuh"
+
+using namespace msim;
+
+struct ms_ctx {
+  Ctx c;
+};
+
+namespace msim {
+
+void phase_begin(Ctx &c, int phase) {
+  if (!c.profiling) return;
+  if (c.ev_used + 2 > c.ev_pool.size()) {
+    for (int k = 0; k < 64; ++k) {
+      cudaEvent_t e;
+      MS_CUDA(cudaEventCreate(&e));
+      c.ev_pool.push_back(e);
+    }
+  }
+  Ctx::PhaseRec r{phase, c.ev_pool[c.ev_used], c.ev_pool[c.ev_used + 1]};
+  c.ev_used += 2;
+  MS_CUDA(cudaEventRecord(r.a, c.stream));
+  c.prec.push_back(r);
+  c.cur_phase = phase;
+}
+
+void phase_end(Ctx &c) {
+  if (!c.profiling || c.cur_phase < 0) return;
+  MS_CUDA(cudaEventRecord(c.prec.back().b, c.stream));
+  c.cur_phase = -1;
+}
+
+static void resolve_phases(Ctx &c) {
+  if (c.prec.empty()) return;
+  MS_CUDA(cudaStreamSynchronize(c.stream));
+  for (auto &r : c.prec) {
+    float ms = 0.f;
+    MS_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    c.ptimes.ms[r.phase] += ms;
+    c.ptimes.count[r.phase] += 1;
+  }
+  c.prec.clear();
+  c.ev_used = 0;
+}
+
+static void require_mesh(Ctx &c) { MS_REQUIRE(c.nv > 0, MS_ERR_STATE, "no mesh uploaded"); }
+static void require_basis(Ctx &c) { MS_REQUIRE(c.m > 0, MS_ERR_STATE, "no basis uploaded"); }
+
+static int n_cg_of(const Ctx &c) { return c.params.n_cg > 0 ? c.params.n_cg : c.n_cg_basis; }
+
+static void enqueue_assembly(Ctx &c) {
+  phase_begin(c, MS_PHASE_GRAD);
+  launch_elem_grad(c);
+  launch_vertex_grad(c);
+  phase_end(c);
+  phase_begin(c, MS_PHASE_HESS);
+  launch_elem_hess(c);
+  phase_end(c);
+  phase_begin(c, MS_PHASE_ASSEMBLY);
+  launch_assemble(c);
+  phase_end(c);
+  c.assembled = true;
+  c.coarse_ready = false;
+}
+
+static void enqueue_coarse(Ctx &c) {
+  phase_begin(c, MS_PHASE_COARSE_S);
+  launch_coarse_S(c);
+  phase_end(c);
+  phase_begin(c, MS_PHASE_COARSE_FACTOR);
+  launch_coarse_factor(c);
+  phase_end(c);
+  phase_begin(c, MS_PHASE_COARSE_SOLVE);
+  launch_coarse_direction(c);
+  phase_end(c);
+  c.coarse_ready = true;
+}
+
+static void fetch_scalars(Ctx &c, int K) {
+  double *h = c.h_pinned;
+  MS_CUDA(cudaMemcpyAsync(h, c.scal, sizeof(double) * SC_COUNT, cudaMemcpyDeviceToHost, c.stream));
+  MS_CUDA(cudaMemcpyAsync(h + SC_COUNT, c.ls_out, sizeof(double) * 2 * K, cudaMemcpyDeviceToHost, c.stream));
+  MS_CUDA(cudaMemcpyAsync(h + SC_COUNT + 2 * kMaxLS, c.flags, sizeof(int32_t) * 8, cudaMemcpyDeviceToHost,
+                          c.stream));
+  MS_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+static ms_status newton_step(Ctx &c, ms_newton_stats *st) {
+  require_mesh(c);
+  require_basis(c);
+  MS_REQUIRE(c.step_begun, MS_ERR_STATE, "ms_newton_step before ms_begin_step");
+  const int n3 = 3 * c.nv;
+  const int K = c.params.ls_batch;
+  enqueue_assembly(c);
+  enqueue_coarse(c);
+  phase_begin(c, MS_PHASE_PCG);
+  const int ncg = n_cg_of(c);
+  launch_pcg(c, c.r, c.df, ncg);
+  phase_end(c);
+  phase_begin(c, MS_PHASE_LINESEARCH);
+  MS_CUDA(cudaMemcpyAsync(c.d, c.ds, sizeof(double) * n3, cudaMemcpyDeviceToDevice, c.stream));
+  launch_axpby(c, c.d, 1.0, c.df, 1.0, n3);
+  launch_dot(c, c.ds, c.ds, n3, SC_DSNORM2);
+  launch_filters(c);
+  launch_ls_batch(c, 0, K);
+  fetch_scalars(c, K);
+  const double *h = c.h_pinned;
+  const int32_t *fl = reinterpret_cast<const int32_t *>(h + SC_COUNT + 2 * kMaxLS);
+  MS_REQUIRE(h[SC_INFEAS] == 0.0 && h[SC_INFEAS_V] == 0.0, MS_ERR_INFEASIBLE,
+             "infeasible iterate: inverted element or penetrating vertex (E = +inf)");
+  MS_REQUIRE(fl[0] == 0 && fl[1] == 0, MS_ERR_NOT_SPD, "coarse matrix not SPD (Cholesky pivot <= 0)");
+  const double h2 = c.params.h * c.params.h;
+  const double energy = h2 * h[SC_ENERGY_ELEM] + h[SC_ENERGY_VERT];
+  double alpha = 0.0, dE = 0.0;
+  int evals = 0;
+  bool failed = false, done = false;
+  int k0 = 0;
+  while (!done) {
+    for (int k = 0; k < K; ++k) {
+      const double a = h[SC_COUNT + K + k];
+      const int idx = k0 + k;
+      if (idx > 0 && a < c.params.ls_min) {
+        failed = true;
+        done = true;
+        break;
+      }
+      evals++;
+      const double de = h[SC_COUNT + k];
+      if (de < 0.0) {
+        alpha = a;
+        dE = de;
+        done = true;
+        break;
+      }
+    }
+    if (!done) {
+      k0 += K;
+      launch_ls_batch(c, k0, K);
+      fetch_scalars(c, K);
+    }
+  }
+  if (!failed) launch_update(c, alpha);
+  phase_end(c);
+  const double dsn = std::sqrt(h[SC_DSNORM2]);
+  const bool conv = dsn / (c.params.h * c.nv) < c.params.eps;
+  if (st) {
+    st->alpha = failed ? 0.0 : alpha;
+    st->alpha0 = h[SC_ALPHA0];
+    st->ds_norm = dsn;
+    st->energy = energy;
+    st->delta_energy = failed ? 0.0 : dE;
+    st->grad_norm = std::sqrt(h[SC_GNORM2]);
+    st->ls_evals = evals;
+    st->converged = conv ? 1 : 0;
+    st->ls_failed = failed ? 1 : 0;
+    st->n_cg = ncg;
+  }
+  return failed ? MS_WARN_LS_FAILED : MS_OK;
+}
+
+static void begin_step(Ctx &c) {
+  require_mesh(c);
+  launch_predictor(c);
+  c.step_begun = true;
+}
+
+static void end_step(Ctx &c) {
+  MS_REQUIRE(c.step_begun, MS_ERR_STATE, "ms_end_step before ms_begin_step");
+  launch_velocity(c);
+  c.step_begun = false;
+}
+
+}  // namespace msim
+
+// ============================================================================ C-ABI
+#define MS_TRY(ctx, ...)                                               \
+  try {                                                                \
+    __VA_ARGS__;                                                       \
+  } catch (const msim::Error &err) {                                   \
+    if (ctx) (ctx)->c.last_error = err.msg;                            \
+    return err.code;                                                   \
+  } catch (const std::bad_alloc &) {                                   \
+    if (ctx) (ctx)->c.last_error = "host out of memory";               \
+    return MS_ERR_OOM;                                                 \
+  } catch (...) {                                                      \
+    if (ctx) (ctx)->c.last_error = "unknown exception";                \
+    return MS_ERR_CUDA;                                                \
+  }
+
+extern "C" {
+
+const char *ms_version(void) { return "msim 0.1 (sm_100a, fp64)"; }
+
+void ms_default_params(ms_params *p) {
+  if (!p) return;
+  p->h = 1.0 / 60.0;
+  p->gravity[0] = 0.0;
+  p->gravity[1] = 0.0;
+  p->gravity[2] = -9.8;
+  p->eps = 1e-6;
+  p->max_newton = 100;
+  p->n_cg = 0;
+  p->ls_shrink = 0.5;
+  p->ls_min = 1e-8;
+  p->filter_safety = 0.9;
+  p->ls_batch = 4;
+  p->use_graphs = 1;
+}
+
+ms_status ms_create(ms_ctx **out, int device, void *cuda_stream, const uint8_t *nccl_id, int rank, int world) {
+  if (!out) return MS_ERR_ARG;
+  *out = nullptr;
+  if (world != 1 || rank != 0) return MS_ERR_ARG;
+  (void)nccl_id;
+  ms_ctx *ctx = new (std::nothrow) ms_ctx();
+  if (!ctx) return MS_ERR_OOM;
+  MS_TRY(ctx, {
+    MS_CUDA(cudaSetDevice(device));
+    ctx->c.device = device;
+    ctx->c.stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+    ms_default_params(&ctx->c.params);
+    MS_CUDA(cudaMallocHost((void **)&ctx->c.h_pinned, sizeof(double) * PH_COUNT));
+  });
+  *out = ctx;
+  return MS_OK;
+}
+
+ms_status ms_destroy(ms_ctx *ctx) {
+  if (!ctx) return MS_OK;
+  cudaSetDevice(ctx->c.device);
+  cudaStreamSynchronize(ctx->c.stream);
+  pcg_reset_graph(ctx->c);
+  for (auto e : ctx->c.ev_pool) cudaEventDestroy(e);
+  if (ctx->c.h_pinned) cudaFreeHost(ctx->c.h_pinned);
+  delete ctx;
+  return MS_OK;
+}
+
+const char *ms_last_error(ms_ctx *ctx) { return ctx ? ctx->c.last_error.c_str() : "null context"; }
+
+ms_status ms_upload_mesh(ms_ctx *ctx, int64_t n_verts, const double *rest_xyz, int64_t n_tets,
+                         const int32_t *tets, const double *E, const double *nu, const double *rho) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    MS_REQUIRE(n_verts > 0 && n_tets > 0 && rest_xyz && tets && E && nu && rho, MS_ERR_ARG, "bad mesh arguments");
+    MS_REQUIRE(n_verts < INT32_MAX / 3 && n_tets < INT32_MAX / 16, MS_ERR_ARG, "mesh too large for int32 indices");
+    Ctx &c = ctx->c;
+    MS_CUDA(cudaSetDevice(c.device));
+    c.nv = (int32_t)n_verts;
+    c.nt = (int32_t)n_tets;
+    c.m = 0;
+    pcg_reset_graph(c);
+    build_mesh_structures(c, rest_xyz, tets, E, nu, rho);
+  });
+  return MS_OK;
+}
+
+ms_status ms_set_dirichlet(ms_ctx *ctx, int64_t n, const int32_t *verts) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    require_mesh(c);
+    MS_REQUIRE(n == 0 || verts, MS_ERR_ARG, "null verts");
+    std::fill(c.h_fixed.begin(), c.h_fixed.end(), 0);
+    for (int64_t k = 0; k < n; ++k) {
+      MS_REQUIRE(verts[k] >= 0 && verts[k] < c.nv, MS_ERR_ARG, "Dirichlet vertex out of range");
+      c.h_fixed[verts[k]] = 1;
+    }
+    c.fixed.upload(c.h_fixed, c.stream);
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+  });
+  return MS_OK;
+}
+
+ms_status ms_set_ground(ms_ctx *ctx, const double normal[3], double offset, double dhat, double kappa) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    MS_REQUIRE(normal != nullptr, MS_ERR_ARG, "null normal");
+    const double nn = std::sqrt(normal[0] * normal[0] + normal[1] * normal[1] + normal[2] * normal[2]);
+    MS_REQUIRE(std::fabs(nn - 1.0) < 1e-12, MS_ERR_ARG, "ground normal must be a unit vector");
+    c.has_ground = kappa > 0.0;
+    MS_REQUIRE(!c.has_ground || dhat > 0.0, MS_ERR_ARG, "dhat must be > 0");
+    for (int k = 0; k < 3; ++k) c.gn[k] = normal[k];
+    c.goff = offset;
+    c.dhat = dhat;
+    c.kappa = kappa;
+  });
+  return MS_OK;
+}
+
+ms_status ms_set_params(ms_ctx *ctx, const ms_params *p) {
+  if (!ctx || !p) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    MS_REQUIRE(p->h > 0.0 && p->eps > 0.0 && p->max_newton > 0 && p->n_cg >= 0, MS_ERR_ARG, "bad params");
+    MS_REQUIRE(p->ls_shrink > 0.0 && p->ls_shrink < 1.0 && p->ls_min > 0.0, MS_ERR_ARG, "bad line-search params");
+    MS_REQUIRE(p->filter_safety > 0.0 && p->filter_safety <= 1.0, MS_ERR_ARG, "bad filter safety");
+    MS_REQUIRE(p->ls_batch == 1 || p->ls_batch == 2 || p->ls_batch == 4 || p->ls_batch == 8, MS_ERR_ARG,
+               "ls_batch must be 1, 2, 4 or 8");
+    if (p->n_cg != ctx->c.params.n_cg || p->use_graphs != ctx->c.params.use_graphs) pcg_reset_graph(ctx->c);
+    ctx->c.params = *p;
+  });
+  return MS_OK;
+}
+
+ms_status ms_get_params(ms_ctx *ctx, ms_params *p) {
+  if (!ctx || !p) return MS_ERR_ARG;
+  *p = ctx->c.params;
+  return MS_OK;
+}
+
+ms_status ms_basis_upload(ms_ctx *ctx, int32_t m, const double *origins, const int64_t *vptr,
+                          const int32_t *handle, const double *phi, const double *phi_affine,
+                          const double affine_origin[3], int32_t n_cg) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    require_mesh(c);
+    MS_REQUIRE(origins && vptr && handle && phi && phi_affine && affine_origin, MS_ERR_ARG, "null basis array");
+    MS_REQUIRE(n_cg > 0, MS_ERR_ARG, "n_cg must be > 0");
+    build_basis_structures(c, m, origins, vptr, handle, phi, phi_affine, affine_origin);
+    c.n_cg_basis = n_cg;
+    pcg_reset_graph(c);
+  });
+  return MS_OK;
+}
+
+ms_status ms_set_state(ms_ctx *ctx, const double *x, const double *v) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    require_mesh(c);
+    const size_t n3 = 3 * (size_t)c.nv;
+    if (x) MS_CUDA(cudaMemcpyAsync(c.x, x, sizeof(double) * n3, cudaMemcpyHostToDevice, c.stream));
+    if (v) MS_CUDA(cudaMemcpyAsync(c.v, v, sizeof(double) * n3, cudaMemcpyHostToDevice, c.stream));
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+    c.step_begun = false;
+    c.assembled = false;
+  });
+  return MS_OK;
+}
+
+ms_status ms_get_state(ms_ctx *ctx, double *x, double *v) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    require_mesh(c);
+    const size_t n3 = 3 * (size_t)c.nv;
+    if (x) c.x.download(x, n3, c.stream);
+    if (v) c.v.download(v, n3, c.stream);
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+  });
+  return MS_OK;
+}
+
+ms_status ms_set_step_state(ms_ctx *ctx, const double *x_t, const double *xhat, const double *x) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    require_mesh(c);
+    const size_t n3 = 3 * (size_t)c.nv;
+    MS_REQUIRE(x_t && xhat && x, MS_ERR_ARG, "null state array");
+    MS_CUDA(cudaMemcpyAsync(c.xt, x_t, sizeof(double) * n3, cudaMemcpyHostToDevice, c.stream));
+    MS_CUDA(cudaMemcpyAsync(c.xhat, xhat, sizeof(double) * n3, cudaMemcpyHostToDevice, c.stream));
+    MS_CUDA(cudaMemcpyAsync(c.x, x, sizeof(double) * n3, cudaMemcpyHostToDevice, c.stream));
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+    c.step_begun = true;
+    c.assembled = false;
+  });
+  return MS_OK;
+}
+
+ms_status ms_get_step_state(ms_ctx *ctx, double *x_t, double *xhat, double *x) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    require_mesh(c);
+    const size_t n3 = 3 * (size_t)c.nv;
+    if (x_t) c.xt.download(x_t, n3, c.stream);
+    if (xhat) c.xhat.download(xhat, n3, c.stream);
+    if (x) c.x.download(x, n3, c.stream);
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+  });
+  return MS_OK;
+}
+
+ms_status ms_begin_step(ms_ctx *ctx) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, { begin_step(ctx->c); });
+  return MS_OK;
+}
+
+ms_status ms_newton_step(ms_ctx *ctx, ms_newton_stats *out) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, { return newton_step(ctx->c, out); });
+  return MS_ERR_CUDA;
+}
+
+ms_status ms_end_step(ms_ctx *ctx) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    end_step(ctx->c);
+    MS_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+  return MS_OK;
+}
+
+ms_status ms_timestep(ms_ctx *ctx, ms_step_stats *out) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    begin_step(c);
+    ms_step_stats st{};
+    st.status = MS_WARN_NEWTON_CAP;
+    for (int it = 0; it < c.params.max_newton; ++it) {
+      ms_newton_stats ns{};
+      const ms_status s = newton_step(c, &ns);
+      st.newton_iters++;
+      st.pcg_iters += ns.n_cg;
+      st.ls_evals += ns.ls_evals;
+      st.last_ds_norm = ns.ds_norm;
+      st.last_alpha = ns.alpha;
+      if (ns.converged) {
+        st.status = MS_OK;
+        break;
+      }
+      if (s == MS_WARN_LS_FAILED) {
+        st.status = MS_WARN_LS_FAILED;
+        break;
+      }
+    }
+    end_step(c);
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+    if (out) *out = st;
+    return st.status;
+  });
+  return MS_ERR_CUDA;
+}
+
+ms_status ms_assemble(ms_ctx *ctx, double *energy_out) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    require_mesh(c);
+    enqueue_assembly(c);
+    fetch_scalars(c, 1);
+    if (energy_out) {
+      const double h2 = c.params.h * c.params.h;
+      *energy_out = (c.h_pinned[SC_INFEAS] > 0 || c.h_pinned[SC_INFEAS_V] > 0)
+                        ? INFINITY
+                        : h2 * c.h_pinned[SC_ENERGY_ELEM] + c.h_pinned[SC_ENERGY_VERT];
+    }
+  });
+  return MS_OK;
+}
+
+ms_status ms_get_gradient(ms_ctx *ctx, double *g) {
+  if (!ctx || !g) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    MS_REQUIRE(c.assembled, MS_ERR_STATE, "nothing assembled yet");
+    c.g.download(g, 3 * (size_t)c.nv, c.stream);
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+  });
+  return MS_OK;
+}
+
+ms_status ms_eval_elements(ms_ctx *ctx, const double *x, double *Ee, double *ge, double *He) {
+  if (!ctx || !x) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    require_mesh(c);
+    const size_t n3 = 3 * (size_t)c.nv, nt = c.nt;
+    DBuf<double> dx, dE, dg, dH;
+    dx.upload(x, n3, c.stream);
+    if (Ee) dE.alloc(nt);
+    if (ge) dg.alloc(12 * nt);
+    if (He) dH.alloc(144 * nt);
+    launch_eval_elements(c, dx, Ee ? dE.p : nullptr, ge ? dg.p : nullptr, He ? dH.p : nullptr);
+    if (Ee) dE.download(Ee, nt, c.stream);
+    if (ge) dg.download(ge, 12 * nt, c.stream);
+    if (He) dH.download(He, 144 * nt, c.stream);
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+    c.assembled = false;
+  });
+  return MS_OK;
+}
+
+ms_status ms_export_bsr(ms_ctx *ctx, int64_t *nnzb, int32_t *rowptr, int32_t *colidx, double *vals) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    require_mesh(c);
+    if (nnzb) *nnzb = c.nnzb;
+    if (rowptr) std::memcpy(rowptr, c.h_rowptr.data(), sizeof(int32_t) * (c.nv + 1));
+    if (colidx) std::memcpy(colidx, c.h_colidx.data(), sizeof(int32_t) * c.nnzb);
+    if (vals) {
+      MS_REQUIRE(c.assembled, MS_ERR_STATE, "nothing assembled yet");
+      std::vector<double> planes((size_t)9 * c.nnzb);
+      c.vals.download(planes.data(), planes.size(), c.stream);
+      MS_CUDA(cudaStreamSynchronize(c.stream));
+      for (int64_t s = 0; s < c.nnzb; ++s)
+        for (int q = 0; q < 9; ++q) vals[9 * s + q] = planes[(size_t)q * c.nnzb + s];
+    }
+  });
+  return MS_OK;
+}
+
+ms_status ms_spmv(ms_ctx *ctx, const double *x, double *y) {
+  if (!ctx || !x || !y) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    MS_REQUIRE(c.assembled, MS_ERR_STATE, "nothing assembled yet");
+    const size_t n3 = 3 * (size_t)c.nv;
+    MS_CUDA(cudaMemcpyAsync(c.p, x, sizeof(double) * n3, cudaMemcpyHostToDevice, c.stream));
+    launch_spmv(c, c.p, c.q, 0.0, nullptr);
+    c.q.download(y, n3, c.stream);
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+  });
+  return MS_OK;
+}
+
+ms_status ms_basis_apply(ms_ctx *ctx, const double *q, double *w) {
+  if (!ctx || !q || !w) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    require_basis(c);
+    MS_CUDA(cudaMemcpyAsync(c.qs, q, sizeof(double) * 12 * c.m, cudaMemcpyHostToDevice, c.stream));
+    launch_lift(c, c.qs, c.tmp, false);
+    c.tmp.download(w, 3 * (size_t)c.nv, c.stream);
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+  });
+  return MS_OK;
+}
+
+ms_status ms_basis_apply_t(ms_ctx *ctx, const double *y, double *z) {
+  if (!ctx || !y || !z) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    require_basis(c);
+    MS_CUDA(cudaMemcpyAsync(c.tmp, y, sizeof(double) * 3 * c.nv, cudaMemcpyHostToDevice, c.stream));
+    launch_restrict(c, c.tmp, c.zs);
+    c.zs.download(z, 12 * (size_t)c.m, c.stream);
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+  });
+  return MS_OK;
+}
+
+ms_status ms_export_coarse(ms_ctx *ctx, double *S, double *Sa) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    require_basis(c);
+    MS_REQUIRE(c.assembled, MS_ERR_STATE, "nothing assembled yet");
+    launch_coarse_S(c);
+    if (S) {
+      std::vector<double> blk((size_t)144 * c.nnzb_S);
+      c.Sblk.download(blk.data(), blk.size(), c.stream);
+      MS_CUDA(cudaStreamSynchronize(c.stream));
+      const int64_t n = 12 * (int64_t)c.m;
+      std::memset(S, 0, sizeof(double) * n * n);
+      for (int32_t i = 0; i < c.m; ++i)
+        for (int32_t k = c.h_sptr[i]; k < c.h_sptr[i + 1]; ++k) {
+          const int32_t j = c.h_scol[k];
+          for (int r = 0; r < 12; ++r)
+            for (int cc = 0; cc < 12; ++cc) S[(12 * i + r) * n + 12 * j + cc] = blk[(size_t)144 * k + 12 * r + cc];
+        }
+    }
+    if (Sa) c.Sa.download(Sa, 144, c.stream);
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+  });
+  return MS_OK;
+}
+
+ms_status ms_subspace_direction(ms_ctx *ctx, double *ds, double *da) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    require_basis(c);
+    MS_REQUIRE(c.assembled, MS_ERR_STATE, "nothing assembled yet");
+    enqueue_coarse(c);
+    fetch_scalars(c, 1);
+    const int32_t *fl = reinterpret_cast<const int32_t *>(c.h_pinned + SC_COUNT + 2 * kMaxLS);
+    MS_REQUIRE(fl[0] == 0 && fl[1] == 0, MS_ERR_NOT_SPD, "coarse matrix not SPD (Cholesky pivot <= 0)");
+    if (ds) c.ds.download(ds, 3 * (size_t)c.nv, c.stream);
+    if (da) c.da.download(da, 3 * (size_t)c.nv, c.stream);
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+  });
+  return MS_OK;
+}
+
+ms_status ms_get_direction(ms_ctx *ctx, double *ds, double *df) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    require_mesh(c);
+    if (ds) c.ds.download(ds, 3 * (size_t)c.nv, c.stream);
+    if (df) c.df.download(df, 3 * (size_t)c.nv, c.stream);
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+  });
+  return MS_OK;
+}
+
+static ms_status pcg_common(ms_ctx *ctx, int32_t iters, ms_pcg_stats *out) {
+  Ctx &c = ctx->c;
+  launch_pcg(c, c.rhs, c.df, iters);
+  fetch_scalars(c, 1);
+  if (out) {
+    out->iters = iters;
+    out->rz0 = c.h_pinned[SC_RZ0];
+    out->rz = c.h_pinned[SC_RZ];
+  }
+  return MS_OK;
+}
+
+ms_status ms_pcg_solve(ms_ctx *ctx, const double *rhs, double *sol, int32_t iters, ms_pcg_stats *out) {
+  if (!ctx || !rhs || !sol || iters < 0) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    MS_REQUIRE(c.assembled, MS_ERR_STATE, "nothing assembled yet");
+    const size_t n3 = 3 * (size_t)c.nv;
+    MS_CUDA(cudaMemcpyAsync(c.rhs, rhs, sizeof(double) * n3, cudaMemcpyHostToDevice, c.stream));
+    pcg_common(ctx, iters, out);
+    c.df.download(sol, n3, c.stream);
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+  });
+  return MS_OK;
+}
+
+ms_status ms_pcg_solve_dev(ms_ctx *ctx, const double *rhs_dev, double *sol_dev, int32_t iters, ms_pcg_stats *out) {
+  if (!ctx || !rhs_dev || !sol_dev || iters < 0) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    MS_REQUIRE(c.assembled, MS_ERR_STATE, "nothing assembled yet");
+    const size_t n3 = 3 * (size_t)c.nv;
+    MS_CUDA(cudaMemcpyAsync(c.rhs, rhs_dev, sizeof(double) * n3, cudaMemcpyDeviceToDevice, c.stream));
+    pcg_common(ctx, iters, out);
+    MS_CUDA(cudaMemcpyAsync(sol_dev, c.df, sizeof(double) * n3, cudaMemcpyDeviceToDevice, c.stream));
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+  });
+  return MS_OK;
+}
+
+ms_status ms_set_profiling(ms_ctx *ctx, int32_t on) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    resolve_phases(c);
+    c.profiling = on != 0;
+    c.ptimes = ms_phase_times{};
+  });
+  return MS_OK;
+}
+
+ms_status ms_get_phase_times(ms_ctx *ctx, ms_phase_times *out) {
+  if (!ctx || !out) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    resolve_phases(ctx->c);
+    *out = ctx->c.ptimes;
+  });
+  return MS_OK;
+}
+
+int64_t ms_kernel_launches(ms_ctx *ctx) { return ctx ? ctx->c.launches : -1; }
+
+ms_status ms_get_sizes(ms_ctx *ctx, int64_t *n_verts, int64_t *n_tets, int64_t *nnzb, int32_t *m,
+                       int64_t *nnz_phi, int64_t *nnzb_S) {
+  if (!ctx) return MS_ERR_ARG;
+  const Ctx &c = ctx->c;
+  if (n_verts) *n_verts = c.nv;
+  if (n_tets) *n_tets = c.nt;
+  if (nnzb) *nnzb = c.nnzb;
+  if (m) *m = c.m;
+  if (nnz_phi) *nnz_phi = c.nnz_phi;
+  if (nnzb_S) *nnzb_S = c.nnzb_S;
+  return MS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,608 @@
+// Subspace (coarse) levels: B lift / restrict, Galerkin products S = U_s^T H U_s and
+// S_a = U_a^T H U_a, tile-envelope Cholesky of S, triangular solves, and the two-stage
+// subspace direction of Alg. 2 with exact coarse solves.
+//
+// SURVEY §8(a) rows a5 (Galerkin projection), a6 (factorisation), a7 (coarse correction).
+// PAPER.md Eq. 7 L284-298 (LBS discretisation, P_i = I3 kron [1 x y z]), L300-302 (affine
+// level), L356-362 (U_s blocks), Alg. 2; readings R4 (exact solves), R6 (rhs -g).
+//
+// Coordinates of handle i: q_i[4c + k], c = x,y,z row, k = monomial [1, X-c_i].  The 3x12
+// block of (v, i) is I3 kron w_vi^T with w_vi = phi_i(v) [1, X_v - c_i].
+//
+// S = B^T H B is formed in two deterministic passes (no atomics):
+//   R_i(u)[(c',k'), c] = sum_{v in N(u), i in supp(v)} w_vi[k'] H_vu[c'][c]     (36 per (i,u))
+//   S_ij[(c',k'), (c,k)] = sum_{u in U_i, j in supp(u)} R_i(u)[(c',k'), c] w_uj[k]
+// with (i,u) pairs and per-S-block contribution lists precomputed at ms_basis_upload.
+#include "common.cuh"
+#include "reduce.cuh"
+
+namespace msim {
+
+// ------------------------------------------------------------------ lift / restrict
+// w_v[c] (+)= sum_{i in supp(v)} phi_i(v) (q_i[4c] + sum_d (X_v - c_i)[d] q_i[4c+1+d])
+__global__ void k_lift(int nv, const int32_t *__restrict__ vptr, const int32_t *__restrict__ handle,
+                       const double *__restrict__ phi, const double *__restrict__ X,
+                       const double *__restrict__ origins, const double *__restrict__ q,
+                       double *__restrict__ w, const double *__restrict__ base) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  double o[3] = {0.0, 0.0, 0.0};
+  const double xv0 = X[3 * v], xv1 = X[3 * v + 1], xv2 = X[3 * v + 2];
+  for (int k = vptr[v]; k < vptr[v + 1]; ++k) {
+    const int i = handle[k];
+    const double f = phi[k];
+    const double m1 = xv0 - origins[3 * i], m2 = xv1 - origins[3 * i + 1], m3 = xv2 - origins[3 * i + 2];
+    const double *qi = q + 12 * (size_t)i;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) o[c] += f * (qi[4 * c] + m1 * qi[4 * c + 1] + m2 * qi[4 * c + 2] + m3 * qi[4 * c + 3]);
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) w[3 * v + c] = (base ? base[3 * v + c] : 0.0) + o[c];
+}
+
+__global__ void k_lift_affine(int nv, const double *__restrict__ phi_a, const double *__restrict__ X,
+                              double ox, double oy, double oz, const double *__restrict__ q,
+                              double *__restrict__ w) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  const double f = phi_a[v];
+  const double m1 = X[3 * v] - ox, m2 = X[3 * v + 1] - oy, m3 = X[3 * v + 2] - oz;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) w[3 * v + c] = f * (q[4 * c] + m1 * q[4 * c + 1] + m2 * q[4 * c + 2] + m3 * q[4 * c + 3]);
+}
+
+// z_i[4c + k] = sign * sum_{v in supp(i)} phi_i(v) mono_k(v, i) y_v[c]   (one CTA per handle)
+__global__ void __launch_bounds__(256) k_restrict(const int32_t *__restrict__ hptr, const int32_t *__restrict__ hvert,
+                                                  const double *__restrict__ hphi, const double *__restrict__ X,
+                                                  const double *__restrict__ origins, const double *__restrict__ y,
+                                                  double sign, double *__restrict__ z) {
+  __shared__ double sh[12 * 32];
+  const int i = blockIdx.x;
+  const double o0 = origins[3 * i], o1 = origins[3 * i + 1], o2 = origins[3 * i + 2];
+  double acc[12];
+#pragma unroll
+  for (int k = 0; k < 12; ++k) acc[k] = 0.0;
+  for (int k = hptr[i] + threadIdx.x; k < hptr[i + 1]; k += blockDim.x) {
+    const int v = hvert[k];
+    const double f = hphi[k];
+    const double mono[4] = {f, f * (X[3 * v] - o0), f * (X[3 * v + 1] - o1), f * (X[3 * v + 2] - o2)};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double yc = y[3 * v + c];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) acc[4 * c + kk] = fma(mono[kk], yc, acc[4 * c + kk]);
+    }
+  }
+  block_sum<12>(acc, sh);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < 12; ++k) z[12 * (size_t)i + k] = sign * acc[k];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_restrict_affine(int nv, const double *__restrict__ phi_a,
+                                                         const double *__restrict__ X, double ox, double oy,
+                                                         double oz, const double *__restrict__ y, double sign,
+                                                         double *__restrict__ partial, unsigned int *counter,
+                                                         double *__restrict__ z) {
+  double acc[12];
+#pragma unroll
+  for (int k = 0; k < 12; ++k) acc[k] = 0.0;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    const double f = phi_a[v];
+    const double mono[4] = {f, f * (X[3 * v] - ox), f * (X[3 * v + 1] - oy), f * (X[3 * v + 2] - oz)};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double yc = y[3 * v + c];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) acc[4 * c + kk] = fma(mono[kk], yc, acc[4 * c + kk]);
+    }
+  }
+  double res[12];
+  if (grid_reduce<12>(acc, partial, counter, res) && threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < 12; ++k) z[k] = sign * res[k];
+  }
+}
+
+void launch_lift(Ctx &c, const double *q, double *w, bool accumulate) {
+  k_lift<<<div_up(c.nv, 256), 256, 0, c.stream>>>(c.nv, c.bvptr, c.bhandle, c.bphi, c.X, c.origins, q, w,
+                                                  accumulate ? w : nullptr);
+  c.launches++;
+  MS_CUDA(cudaGetLastError());
+}
+
+void launch_restrict(Ctx &c, const double *y, double *z) {
+  k_restrict<<<c.m, 256, 0, c.stream>>>(c.hptr, c.hvert, c.hphi, c.X, c.origins, y, 1.0, z);
+  c.launches++;
+  MS_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ Galerkin products (a5)
+struct HView {
+  int64_t nnzb;
+  const int32_t *__restrict__ rowptr;
+  const int32_t *__restrict__ colidx;
+  const double *__restrict__ vals;   // [9][nnzb]
+};
+
+// R_i(u) for every (i,u) pair: thread per pair.
+__global__ void __launch_bounds__(128) k_galerkin_R(int64_t nR, const int32_t *__restrict__ Ri,
+                                                    const int32_t *__restrict__ Ru, HView H,
+                                                    const int32_t *__restrict__ bvptr,
+                                                    const int32_t *__restrict__ bhandle,
+                                                    const double *__restrict__ bphi, const double *__restrict__ X,
+                                                    const double *__restrict__ origins, double *__restrict__ R) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nR) return;
+  const int i = Ri[r], u = Ru[r];
+  const double o0 = origins[3 * i], o1 = origins[3 * i + 1], o2 = origins[3 * i + 2];
+  double acc[36];
+#pragma unroll
+  for (int k = 0; k < 36; ++k) acc[k] = 0.0;
+  for (int s = H.rowptr[u]; s < H.rowptr[u + 1]; ++s) {
+    const int v = H.colidx[s];
+    double f = 0.0;
+    for (int k = bvptr[v]; k < bvptr[v + 1]; ++k) {
+      const int hk = bhandle[k];
+      if (hk == i) { f = bphi[k]; break; }
+      if (hk > i) break;
+    }
+    if (f == 0.0) continue;
+    const double w[4] = {f, f * (X[3 * v] - o0), f * (X[3 * v + 1] - o1), f * (X[3 * v + 2] - o2)};
+    // H_vu[c'][c] = H_uv[c][c'] = vals[(3c + c') plane][s]
+    double Hvu[3][3];
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc)
+#pragma unroll
+      for (int cp = 0; cp < 3; ++cp) Hvu[cp][cc] = H.vals[(size_t)(3 * cc + cp) * H.nnzb + s];
+#pragma unroll
+    for (int cp = 0; cp < 3; ++cp)
+#pragma unroll
+      for (int kp = 0; kp < 4; ++kp)
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) acc[(4 * cp + kp) * 3 + cc] = fma(w[kp], Hvu[cp][cc], acc[(4 * cp + kp) * 3 + cc]);
+  }
+  double *dst = R + 36 * (size_t)r;
+#pragma unroll
+  for (int k = 0; k < 36; ++k) dst[k] = acc[k];
+}
+
+// S block (i, j): warp per block, lane l owns R entries l and 32 + l (l < 4).
+__global__ void __launch_bounds__(256) k_galerkin_S(int64_t nblk, const int32_t *__restrict__ srow,
+                                                    const int32_t *__restrict__ scol,
+                                                    const int32_t *__restrict__ sc_ptr,
+                                                    const int32_t *__restrict__ sc_R,
+                                                    const int32_t *__restrict__ sc_phi,
+                                                    const int32_t *__restrict__ Ru,
+                                                    const double *__restrict__ bphi,
+                                                    const double *__restrict__ X,
+                                                    const double *__restrict__ origins,
+                                                    const double *__restrict__ R, double *__restrict__ S) {
+  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (b >= nblk) return;
+  const int j = scol[b];
+  const double o0 = origins[3 * j], o1 = origins[3 * j + 1], o2 = origins[3 * j + 2];
+  double a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0};
+  for (int k = sc_ptr[b]; k < sc_ptr[b + 1]; ++k) {
+    const int r = sc_R[k];
+    const int u = Ru[r];
+    const double f = bphi[sc_phi[k]];
+    const double w[4] = {f, f * (X[3 * u] - o0), f * (X[3 * u + 1] - o1), f * (X[3 * u + 2] - o2)};
+    const double *Rr = R + 36 * (size_t)r;
+    const double r0 = Rr[lane];
+    const double r1 = lane < 4 ? Rr[32 + lane] : 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      a0[kk] = fma(r0, w[kk], a0[kk]);
+      a1[kk] = fma(r1, w[kk], a1[kk]);
+    }
+  }
+  double *dst = S + 144 * (size_t)b;
+  {
+    const int l = lane, row = l / 3, c = l % 3;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) dst[row * 12 + 4 * c + kk] = a0[kk];
+  }
+  if (lane < 4) {
+    const int l = 32 + lane, row = l / 3, c = l % 3;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) dst[row * 12 + 4 * c + kk] = a1[kk];
+  }
+  (void)srow;
+}
+
+// Affine: Ra(u) = sum_{v in N(u)} w_a(v) kron H_vu  stored SoA [36][nv]
+__global__ void __launch_bounds__(128) k_galerkin_Ra(int nv, HView H, const double *__restrict__ phi_a,
+                                                     const double *__restrict__ X, double ox, double oy,
+                                                     double oz, double *__restrict__ Ra) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= nv) return;
+  double acc[36];
+#pragma unroll
+  for (int k = 0; k < 36; ++k) acc[k] = 0.0;
+  for (int s = H.rowptr[u]; s < H.rowptr[u + 1]; ++s) {
+    const int v = H.colidx[s];
+    const double f = phi_a[v];
+    if (f == 0.0) continue;
+    const double w[4] = {f, f * (X[3 * v] - ox), f * (X[3 * v + 1] - oy), f * (X[3 * v + 2] - oz)};
+    double Hvu[3][3];
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc)
+#pragma unroll
+      for (int cp = 0; cp < 3; ++cp) Hvu[cp][cc] = H.vals[(size_t)(3 * cc + cp) * H.nnzb + s];
+#pragma unroll
+    for (int cp = 0; cp < 3; ++cp)
+#pragma unroll
+      for (int kp = 0; kp < 4; ++kp)
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) acc[(4 * cp + kp) * 3 + cc] = fma(w[kp], Hvu[cp][cc], acc[(4 * cp + kp) * 3 + cc]);
+  }
+#pragma unroll
+  for (int k = 0; k < 36; ++k) Ra[(size_t)k * nv + u] = acc[k];
+}
+
+// S_a[(row), (4c + k)] = sum_u Ra(u)[l] w_a(u)[k], l = 3 row + c.  Grid: (36 entries) x chunks.
+__global__ void __launch_bounds__(256) k_galerkin_Sa_partial(int nv, const double *__restrict__ Ra,
+                                                             const double *__restrict__ phi_a,
+                                                             const double *__restrict__ X, double ox,
+                                                             double oy, double oz,
+                                                             double *__restrict__ part /* [36][4][chunks] */) {
+  __shared__ double sh[4 * 32];
+  const int l = blockIdx.x, chunk = blockIdx.y, nch = gridDim.y;
+  double acc[4] = {0, 0, 0, 0};
+  for (int u = chunk * blockDim.x + threadIdx.x; u < nv; u += nch * blockDim.x) {
+    const double f = phi_a[u];
+    const double rv = Ra[(size_t)l * nv + u];
+    const double w[4] = {f, f * (X[3 * u] - ox), f * (X[3 * u + 1] - oy), f * (X[3 * u + 2] - oz)};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[k] = fma(rv, w[k], acc[k]);
+  }
+  block_sum<4>(acc, sh);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) part[((size_t)l * 4 + k) * nch + chunk] = acc[k];
+  }
+}
+
+__global__ void k_galerkin_Sa_final(int nch, const double *__restrict__ part, double *__restrict__ Sa) {
+  const int t = threadIdx.x;  // 144 threads: (l, k)
+  if (t >= 144) return;
+  const int l = t / 4, k = t % 4;
+  double s = 0.0;
+  for (int ch = 0; ch < nch; ++ch) s += part[((size_t)l * 4 + k) * nch + ch];
+  const int row = l / 3, c = l % 3;
+  Sa[row * 12 + 4 * c + k] = s;
+}
+
+static HView hview(const Ctx &c) { return HView{c.nnzb, c.rowptr, c.colidx, c.vals}; }
+
+// ------------------------------------------------------------------ dense envelope S
+// Lden column-major nS_pad x nS_pad; scatter lower part of S blocks; padding -> identity.
+__global__ void k_scatter_S(int64_t nblk, const int32_t *__restrict__ srow, const int32_t *__restrict__ scol,
+                            const double *__restrict__ S, int nSp, double *__restrict__ L) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nblk * 144) return;
+  const int64_t b = t / 144;
+  const int e = (int)(t % 144), row = e / 12, col = e % 12;
+  const int i = srow[b], j = scol[b];
+  const int R = 12 * i + row, C = 12 * j + col;
+  if (R >= C) L[(size_t)C * nSp + R] = S[t];
+}
+
+__global__ void k_pad_identity(int nS, int nSp, double *__restrict__ L) {
+  const int r = nS + blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < nSp) L[(size_t)r * nSp + r] = 1.0;
+}
+
+// ------------------------------------------------------------------ tile Cholesky (a6)
+constexpr int TB = 64;
+
+// in-place Cholesky of diagonal tile k (lower), column-major with leading dim nSp
+__global__ void __launch_bounds__(256) k_potrf_tile(int k, int nSp, double *__restrict__ L, int *__restrict__ flag) {
+  __shared__ double A[TB][TB + 1];
+  const int t = threadIdx.x;
+  const size_t base = (size_t)(k * TB) * nSp + k * TB;
+  for (int e = t; e < TB * TB; e += blockDim.x) {
+    const int r = e % TB, c = e / TB;
+    A[r][c] = (r >= c) ? L[base + (size_t)c * nSp + r] : 0.0;
+  }
+  __syncthreads();
+  for (int j = 0; j < TB; ++j) {
+    if (t == 0) {
+      const double d = A[j][j];
+      if (!(d > 0.0)) *flag = 1;
+      A[j][j] = d > 0.0 ? sqrt(d) : 1.0;
+    }
+    __syncthreads();
+    const double ljj = A[j][j];
+    for (int r = j + 1 + t; r < TB; r += blockDim.x) A[r][j] /= ljj;
+    __syncthreads();
+    const int n = TB - j - 1;
+    for (int e = t; e < n * n; e += blockDim.x) {
+      const int r = j + 1 + e % n, c = j + 1 + e / n;
+      if (r >= c) A[r][c] = fma(-A[r][j], A[c][j], A[r][c]);
+    }
+    __syncthreads();
+  }
+  for (int e = t; e < TB * TB; e += blockDim.x) {
+    const int r = e % TB, c = e / TB;
+    if (r >= c) L[base + (size_t)c * nSp + r] = A[r][c];
+  }
+}
+
+// L_ik = A_ik L_kk^-T for panel tiles i (blockIdx.x indexes the panel list)
+__global__ void __launch_bounds__(256) k_trsm_tile(int k, const int32_t *__restrict__ panel, int nSp,
+                                                   double *__restrict__ L) {
+  extern __shared__ double dsm[];
+  double(*Lk)[TB + 1] = reinterpret_cast<double(*)[TB + 1]>(dsm);
+  double(*X)[TB + 1] = reinterpret_cast<double(*)[TB + 1]>(dsm + TB * (TB + 1));
+  const int i = panel[blockIdx.x], t = threadIdx.x;
+  const size_t bk = (size_t)(k * TB) * nSp + k * TB, bi = (size_t)(k * TB) * nSp + i * TB;
+  for (int e = t; e < TB * TB; e += blockDim.x) {
+    const int r = e % TB, c = e / TB;
+    Lk[r][c] = L[bk + (size_t)c * nSp + r];
+    X[r][c] = L[bi + (size_t)c * nSp + r];
+  }
+  __syncthreads();
+  // X L_kk^T = A  ->  column c: X[:,c] = (A[:,c] - sum_{c'<c} X[:,c'] L_kk[c][c']) / L_kk[c][c]
+  for (int c = 0; c < TB; ++c) {
+    const double inv = 1.0 / Lk[c][c];
+    for (int r = t; r < TB; r += blockDim.x) X[r][c] *= inv;
+    __syncthreads();
+    for (int e = t; e < TB * (TB - c - 1); e += blockDim.x) {
+      const int r = e % TB, cc = c + 1 + e / TB;
+      X[r][cc] = fma(-X[r][c], Lk[cc][c], X[r][cc]);
+    }
+    __syncthreads();
+  }
+  for (int e = t; e < TB * TB; e += blockDim.x) {
+    const int r = e % TB, c = e / TB;
+    L[bi + (size_t)c * nSp + r] = X[r][c];
+  }
+}
+
+// A_ij -= L_ik L_jk^T for task list (pairs) of step k; 256 threads, 4x4 outputs each.
+__global__ void __launch_bounds__(256) k_update_tile(int k, const int32_t *__restrict__ tasks, int nSp,
+                                                     double *__restrict__ L) {
+  extern __shared__ double dsm[];
+  double(*Li)[TB + 1] = reinterpret_cast<double(*)[TB + 1]>(dsm);
+  double(*Lj)[TB + 1] = reinterpret_cast<double(*)[TB + 1]>(dsm + TB * (TB + 1));
+  const int i = tasks[2 * blockIdx.x], j = tasks[2 * blockIdx.x + 1], t = threadIdx.x;
+  const size_t bik = (size_t)(k * TB) * nSp + i * TB, bjk = (size_t)(k * TB) * nSp + j * TB;
+  for (int e = t; e < TB * TB; e += blockDim.x) {
+    const int r = e % TB, c = e / TB;
+    Li[r][c] = L[bik + (size_t)c * nSp + r];
+    Lj[r][c] = L[bjk + (size_t)c * nSp + r];
+  }
+  __syncthreads();
+  const int tr = (t % 16) * 4, tc = (t / 16) * 4;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int kk = 0; kk < TB; ++kk) {
+    double x[4], y[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      x[a] = Li[tr + a][kk];
+      y[a] = Lj[tc + a][kk];
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = fma(x[a], y[b], acc[a][b]);
+  }
+  const size_t bij = (size_t)(j * TB) * nSp + i * TB;
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int r = tr + a, c = tc + b;
+      if (i != j || r >= c) L[bij + (size_t)c * nSp + r] -= acc[a][b];
+    }
+}
+
+// ------------------------------------------------------------------ triangular solves
+// forward step k: y_k = L_kk^-1 b_k (every CTA redundantly, warp 0); CTA 0 stores y_k;
+// CTA p >= 1 updates b_i -= L_ik y_k for i = panel[p-1].
+__global__ void __launch_bounds__(128) k_fwd_tile(int k, const int32_t *__restrict__ panel, int nSp,
+                                                  const double *__restrict__ L, double *__restrict__ b,
+                                                  double *__restrict__ y) {
+  __shared__ double yk[TB];
+  const int t = threadIdx.x, lane = t & 31;
+  const size_t bk = (size_t)(k * TB) * nSp + k * TB;
+  if (t < 32) {
+    double v0 = b[k * TB + lane], v1 = b[k * TB + 32 + lane];
+    for (int c = 0; c < TB; ++c) {
+      const double bc = __shfl_sync(0xffffffffu, c < 32 ? v0 : v1, c & 31);
+      const double yc = bc / L[bk + (size_t)c * nSp + c];
+      if (lane == (c & 31)) {
+        if (c < 32) v0 = yc; else v1 = yc;
+      }
+      if (lane > c) v0 = fma(-L[bk + (size_t)c * nSp + lane], yc, v0);
+      if (32 + lane > c) v1 = fma(-L[bk + (size_t)c * nSp + 32 + lane], yc, v1);
+    }
+    yk[lane] = v0;
+    yk[32 + lane] = v1;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) {
+    if (t < TB) y[k * TB + t] = yk[t];
+    return;
+  }
+  const int i = panel[blockIdx.x - 1];
+  const size_t bi = (size_t)(k * TB) * nSp + i * TB;
+  if (t < TB) {
+    double s = 0.0;
+    for (int c = 0; c < TB; ++c) s = fma(L[bi + (size_t)c * nSp + t], yk[c], s);
+    b[i * TB + t] -= s;
+  }
+}
+
+// backward step k: x_k = L_kk^-T y_k; CTA p >= 1 updates y_j -= L_kj^T x_k, j = rowlo(k) + p - 1
+__global__ void __launch_bounds__(128) k_bwd_tile(int k, int jlo, int nSp, const double *__restrict__ L,
+                                                  double *__restrict__ y, double *__restrict__ x) {
+  __shared__ double xk[TB];
+  const int t = threadIdx.x, lane = t & 31;
+  const size_t bk = (size_t)(k * TB) * nSp + k * TB;
+  if (t < 32) {
+    double v0 = y[k * TB + lane], v1 = y[k * TB + 32 + lane];
+    for (int c = TB - 1; c >= 0; --c) {
+      const double yc = __shfl_sync(0xffffffffu, c < 32 ? v0 : v1, c & 31);
+      const double xc = yc / L[bk + (size_t)c * nSp + c];
+      if (lane == (c & 31)) {
+        if (c < 32) v0 = xc; else v1 = xc;
+      }
+      // rows r < c: y_r -= L[c][r] x_c  (L^T)
+      if (lane < c) v0 = fma(-L[bk + (size_t)lane * nSp + c], xc, v0);
+      if (32 + lane < c) v1 = fma(-L[bk + (size_t)(32 + lane) * nSp + c], xc, v1);
+    }
+    xk[lane] = v0;
+    xk[32 + lane] = v1;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) {
+    if (t < TB) x[k * TB + t] = xk[t];
+    return;
+  }
+  const int j = jlo + blockIdx.x - 1;
+  // L_kj: rows k*TB.., cols j*TB..;  (L_kj^T x_k)[c] = sum_r L[kTB + r][jTB + c] x_k[r]
+  if (t < TB) {
+    const size_t bkj = (size_t)(j * TB + t) * nSp + k * TB;
+    double s = 0.0;
+    for (int r = 0; r < TB; ++r) s = fma(L[bkj + r], xk[r], s);
+    y[j * TB + t] -= s;
+  }
+}
+
+// ------------------------------------------------------------------ 12x12 affine solve
+__global__ void k_solve12(const double *__restrict__ Sa, const double *__restrict__ z, double *__restrict__ q,
+                          int *__restrict__ flag) {
+  if (threadIdx.x != 0) return;
+  double L[12][12];
+  for (int r = 0; r < 12; ++r)
+    for (int c = 0; c < 12; ++c) L[r][c] = Sa[r * 12 + c];
+  for (int j = 0; j < 12; ++j) {
+    double d = L[j][j];
+    for (int k = 0; k < j; ++k) d -= L[j][k] * L[j][k];
+    if (!(d > 0.0)) { *flag = 1; d = 1.0; }
+    L[j][j] = sqrt(d);
+    for (int r = j + 1; r < 12; ++r) {
+      double s = L[r][j];
+      for (int k = 0; k < j; ++k) s -= L[r][k] * L[j][k];
+      L[r][j] = s / L[j][j];
+    }
+  }
+  double y[12];
+  for (int r = 0; r < 12; ++r) {
+    double s = z[r];
+    for (int k = 0; k < r; ++k) s -= L[r][k] * y[k];
+    y[r] = s / L[r][r];
+  }
+  for (int r = 11; r >= 0; --r) {
+    double s = y[r];
+    for (int k = r + 1; k < 12; ++k) s -= L[k][r] * q[k];
+    q[r] = s / L[r][r];
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+void launch_coarse_S(Ctx &c) {
+  k_galerkin_R<<<div_up(c.n_R, 128), 128, 0, c.stream>>>(c.n_R, c.R_i, c.R_u, hview(c), c.bvptr, c.bhandle,
+                                                         c.bphi, c.X, c.origins, c.Rbuf);
+  k_galerkin_S<<<div_up(c.nnzb_S * 32, 256), 256, 0, c.stream>>>(c.nnzb_S, c.srow, c.scol, c.sc_ptr, c.sc_R,
+                                                                  c.sc_phi, c.R_u, c.bphi, c.X, c.origins,
+                                                                  c.Rbuf, c.Sblk);
+  const double *o = c.aff_origin;
+  k_galerkin_Ra<<<div_up(c.nv, 128), 128, 0, c.stream>>>(c.nv, hview(c), c.phi_aff, c.X, o[0], o[1], o[2], c.Ra);
+  const int nch = 64;
+  k_galerkin_Sa_partial<<<dim3(36, nch), 256, 0, c.stream>>>(c.nv, c.Ra, c.phi_aff, c.X, o[0], o[1], o[2],
+                                                              c.partial);
+  k_galerkin_Sa_final<<<1, 160, 0, c.stream>>>(nch, c.partial, c.Sa);
+  c.launches += 5;
+  MS_CUDA(cudaGetLastError());
+}
+
+constexpr size_t kTileSmem = sizeof(double) * 2 * TB * (TB + 1);
+
+static void enqueue_factor(Ctx &c) {
+  static bool attr = false;
+  if (!attr) {
+    MS_CUDA(cudaFuncSetAttribute(k_trsm_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
+    MS_CUDA(cudaFuncSetAttribute(k_update_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
+    attr = true;
+  }
+  const int nSp = c.nS_pad;
+  MS_CUDA(cudaMemsetAsync(c.Lden, 0, sizeof(double) * (size_t)nSp * nSp, c.stream));
+  k_scatter_S<<<div_up(c.nnzb_S * 144, 256), 256, 0, c.stream>>>(c.nnzb_S, c.srow, c.scol, c.Sblk, nSp, c.Lden);
+  if (nSp > c.nS) k_pad_identity<<<div_up(nSp - c.nS, 64), 64, 0, c.stream>>>(c.nS, nSp, c.Lden);
+  for (int k = 0; k < c.ntiles; ++k) {
+    k_potrf_tile<<<1, 256, 0, c.stream>>>(k, nSp, c.Lden, c.flags + 0);
+    const int np = (int)c.h_chol_panel[k].size();
+    if (np) {
+      k_trsm_tile<<<np, 256, kTileSmem, c.stream>>>(k, c.chol_panel + c.h_chol_panel_off[k], nSp, c.Lden);
+      const int nt = (int)(c.h_chol_task_off[k + 1] - c.h_chol_task_off[k]);
+      k_update_tile<<<nt, 256, kTileSmem, c.stream>>>(k, c.chol_tasks + 2 * c.h_chol_task_off[k], nSp, c.Lden);
+    }
+  }
+}
+
+static int64_t factor_kernel_count(const Ctx &c) {
+  int64_t n = 1 + (c.nS_pad > c.nS ? 1 : 0);
+  for (int k = 0; k < c.ntiles; ++k) n += 1 + (c.h_chol_panel[k].empty() ? 0 : 2);
+  return n;
+}
+
+void launch_coarse_factor(Ctx &c) {
+  enqueue_factor(c);
+  c.launches += factor_kernel_count(c);
+  MS_CUDA(cudaGetLastError());
+}
+
+// solve S qs = zs with the factor in Lden (zs is overwritten as work space)
+static void enqueue_solve(Ctx &c) {
+  const int nSp = c.nS_pad;
+  MS_CUDA(cudaMemsetAsync(c.zs + c.nS, 0, sizeof(double) * (nSp - c.nS), c.stream));
+  for (int k = 0; k < c.ntiles; ++k) {
+    const int np = (int)c.h_chol_panel[k].size();
+    k_fwd_tile<<<1 + np, 128, 0, c.stream>>>(k, c.chol_panel + c.h_chol_panel_off[k], nSp, c.Lden, c.zs, c.qs);
+  }
+  // qs now holds y; backward in place: y -> x (x written to zs, then copied)
+  for (int k = c.ntiles - 1; k >= 0; --k) {
+    const int jlo = c.h_tile_rowlo[k];
+    k_bwd_tile<<<1 + (k - jlo), 128, 0, c.stream>>>(k, jlo, nSp, c.Lden, c.qs, c.zs);
+  }
+}
+
+void launch_coarse_direction(Ctx &c) {
+  const int n3 = 3 * c.nv;
+  const double *o = c.aff_origin;
+  // rhs = -g
+  MS_CUDA(cudaMemsetAsync(c.rhs, 0, sizeof(double) * n3, c.stream));
+  launch_axpby(c, c.rhs, -1.0, c.g, 0.0, n3);
+  // affine stage: za = U_a^T(-g); qa = Sa^-1 za; da = U_a qa
+  k_restrict_affine<<<std::min(div_up(c.nv, 256), 592), 256, 0, c.stream>>>(
+      c.nv, c.phi_aff, c.X, o[0], o[1], o[2], c.rhs, 1.0, c.partial, c.counters + 6, c.za);
+  k_solve12<<<1, 32, 0, c.stream>>>(c.Sa, c.za, c.qa, c.flags + 1);
+  k_lift_affine<<<div_up(c.nv, 256), 256, 0, c.stream>>>(c.nv, c.phi_aff, c.X, o[0], o[1], o[2], c.qa, c.da);
+  c.launches += 3;
+  // r1 = -g - H da
+  launch_spmv(c, c.da, c.tmp, 0.0, c.rhs);
+  // SMS stage: zs = B^T r1; qs = S^-1 zs; ds = da + B qs
+  launch_restrict(c, c.tmp, c.zs);
+  enqueue_solve(c);
+  c.launches += 2 * c.ntiles;
+  MS_CUDA(cudaGetLastError());
+  // after enqueue_solve the solution x lives in zs
+  MS_CUDA(cudaMemcpyAsync(c.ds, c.da, sizeof(double) * n3, cudaMemcpyDeviceToDevice, c.stream));
+  launch_lift(c, c.zs, c.ds, true);
+  // r = -g - H ds
+  launch_spmv(c, c.ds, c.r, 0.0, c.rhs);
+  MS_CUDA(cudaGetLastError());
+}
+
+// standalone solve used by the parity hook ms_subspace_direction (same code path)
+}  // namespace msim

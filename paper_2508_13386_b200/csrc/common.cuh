@@ -1,0 +1,255 @@
+// Internal header of libmsim (B200 / sm_100a).  Not part of the C-ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "msim.h"
+
+namespace msim {
+
+// ---------------------------------------------------------------- error handling
+struct Error {
+  ms_status code;
+  std::string msg;
+};
+
+#define MS_CUDA(call)                                                                       \
+  do {                                                                                      \
+    cudaError_t _e = (call);                                                                \
+    if (_e != cudaSuccess)                                                                  \
+      throw ::msim::Error{_e == cudaErrorMemoryAllocation ? MS_ERR_OOM : MS_ERR_CUDA,       \
+                          std::string(#call) + ": " + cudaGetErrorString(_e)};              \
+  } while (0)
+
+#define MS_REQUIRE(cond, code, msg)                                                         \
+  do {                                                                                      \
+    if (!(cond)) throw ::msim::Error{(code), (msg)};                                        \
+  } while (0)
+
+// ---------------------------------------------------------------- device buffer
+template <typename T>
+struct DBuf {
+  T *p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf &) = delete;
+  DBuf &operator=(const DBuf &) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    if (count == n && p) return;
+    release();
+    if (count == 0) return;
+    MS_CUDA(cudaMalloc((void **)&p, count * sizeof(T)));
+    n = count;
+  }
+  void upload(const T *h, size_t count, cudaStream_t s) {
+    alloc(count);
+    if (count) MS_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void upload(const std::vector<T> &h, cudaStream_t s) { upload(h.data(), h.size(), s); }
+  void zero(cudaStream_t s) {
+    if (n) MS_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+  void download(T *h, size_t count, cudaStream_t s) const {
+    if (count) MS_CUDA(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+  }
+  operator T *() const { return p; }
+};
+
+// Deterministic reduction workspace: per-CTA partials + a "last CTA" counter.
+struct Reducer {
+  DBuf<double> partial;       // [slots * max_blocks]
+  DBuf<unsigned int> counter; // [n_counters]
+};
+
+// ---------------------------------------------------------------- tile Cholesky schedule
+struct CholTask {      // one trailing update A_ij -= L_ik L_jk^T (tiles)
+  int32_t i, j;
+};
+
+// ---------------------------------------------------------------- context
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+  ms_params params;
+  int64_t launches = 0;
+
+  // ---- mesh
+  int32_t nv = 0, nt = 0;
+  std::vector<double> h_X;          // rest positions (host copy)
+  std::vector<int32_t> h_tets;
+  DBuf<double> X;                   // (nv,3)
+  DBuf<int32_t> tets;               // (nt,4)
+  DBuf<double> Bm;                  // SoA [9][nt]  (Dm^-1 row-major)
+  DBuf<double> vol, mu, lam;        // [nt]
+  DBuf<double> mass;                // [nv]
+  DBuf<uint8_t> fixed;              // [nv] 1 = Dirichlet
+  std::vector<uint8_t> h_fixed;
+  DBuf<int32_t> vinc_ptr, vinc;     // vertex -> (tet*4 + corner), CSR
+  // BSR pattern (3x3 blocks)
+  int64_t nnzb = 0;
+  std::vector<int32_t> h_rowptr, h_colidx;
+  DBuf<int32_t> rowptr, colidx, diag_slot, slot_row;
+  DBuf<int32_t> cptr, contrib;      // slot -> list of (tet*16 + a*4 + b)
+  DBuf<double> vals;                // SoA [9][nnzb]
+  DBuf<double> dinv;                // [3 nv] Jacobi D^-1
+  // ground
+  bool has_ground = false;
+  double gn[3] = {0, 0, 1}, goff = 0, dhat = 1e-3, kappa = 0;
+
+  // ---- state
+  DBuf<double> x, v, xt, xhat;      // (nv,3)
+  DBuf<double> g, ds, da, df, d, r, rhs;   // 3nv
+  DBuf<double> p, q, z, tmp;               // PCG vectors
+  DBuf<double> stage_g;             // [nt*12] element gradients (unscaled by h^2)
+  DBuf<double> stage_h;             // [nt*90] 10 upper 3x3 blocks of P+(H_e)
+  bool step_begun = false;
+  bool assembled = false;
+  bool coarse_ready = false;
+
+  // ---- basis
+  int32_t m = 0;
+  int32_t n_cg_basis = 20;
+  int64_t nnz_phi = 0;
+  DBuf<double> origins;             // (m,3)
+  DBuf<int32_t> bvptr, bhandle;     // vertex-major CSR
+  DBuf<double> bphi;
+  DBuf<int32_t> hptr, hvert;        // handle-major CSR
+  DBuf<double> hphi;
+  DBuf<double> phi_aff;             // [nv]
+  double aff_origin[3] = {0, 0, 0};
+  // coarse S pattern: block CSR over handles (both triangles), 144 doubles per block
+  int64_t nnzb_S = 0;
+  std::vector<int32_t> h_sptr, h_scol;
+  DBuf<int32_t> sptr, scol, srow;
+  DBuf<double> Sblk;                // [nnzb_S * 144]
+  // R contributions: R_i(u) for (i,u) pairs; S contributions
+  int64_t n_R = 0;                  // number of (i,u) pairs
+  DBuf<int32_t> R_i, R_u;           // [n_R]
+  DBuf<double> Rbuf;                // [n_R * 36]
+  DBuf<int32_t> sc_ptr;             // [nnzb_S + 1] S block -> contributions
+  DBuf<int32_t> sc_R, sc_phi;       // [n_sc] (R index, phi index of (u, j))
+  // affine
+  DBuf<double> Sa;                  // 144
+  DBuf<double> Ra;                  // [nv * 36]
+  // dense coarse factor (tile-banded)
+  int32_t nS = 0;                   // 12 m
+  int32_t tile = 64;
+  int32_t ntiles = 0;
+  DBuf<double> Lden;                // [nS_pad * nS_pad] column-major lower factor
+  int32_t nS_pad = 0;
+  std::vector<int32_t> h_tile_first;         // first nonzero tile row per tile col (envelope)
+  std::vector<int32_t> h_tile_rowlo;         // per tile row: lowest tile column with a nonzero
+  std::vector<std::vector<CholTask>> h_chol_updates;   // per k
+  std::vector<std::vector<int32_t>> h_chol_panel;      // per k: tile rows i > k in struct
+  DBuf<int32_t> chol_tasks;         // flattened per-k task lists
+  std::vector<int64_t> h_chol_task_off;
+  DBuf<int32_t> chol_panel;
+  std::vector<int64_t> h_chol_panel_off;
+  DBuf<int32_t> band_lo;            // per DOF row: first nonzero column (envelope) [nS_pad]
+  DBuf<double> qa, qs, za, zs;      // coarse vectors
+  DBuf<int32_t> flags;              // [8]: 0 = chol not SPD (S), 1 = not SPD (Sa), 2 = infeasible
+
+  // ---- scalars / reductions
+  DBuf<double> scal;                // device scalars (see SC_* in kernels)
+  DBuf<double> partial;             // reduction partials
+  DBuf<unsigned int> counters;
+  double *h_pinned = nullptr;       // pinned host mirror of result scalars
+  int max_blocks = 0;
+
+  // ---- line search
+  DBuf<double> ls_alpha;            // [ls_batch] candidate steps
+  DBuf<double> ls_out;              // [ls_batch] energy differences
+
+  // ---- graphs
+  cudaGraphExec_t pcg_graph = nullptr;
+  int64_t pcg_graph_kernels = 0;
+  int32_t pcg_graph_iters = -1;
+
+  // ---- profiling: (phase, start, end) event triples resolved lazily (no sync in the path)
+  bool profiling = false;
+  ms_phase_times ptimes{};
+  struct PhaseRec { int phase; cudaEvent_t a, b; };
+  std::vector<PhaseRec> prec;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  int cur_phase = -1;
+};
+
+// scalar slots in ctx.scal
+enum {
+  SC_RZ = 0,      // r^T z
+  SC_RZ_OLD,
+  SC_PQ,
+  SC_ALPHA,
+  SC_BETA,
+  SC_ENERGY_ELEM, // sum V Psi
+  SC_ENERGY_VERT, // inertia + barrier   (k_vertex_grad writes 3 consecutive slots)
+  SC_GNORM2,
+  SC_INFEAS_V,    // penetrating free vertices at entry
+  SC_DSNORM2,
+  SC_ALPHA_CCD,
+  SC_ALPHA_INV,
+  SC_ALPHA0,
+  SC_RZ0,
+  SC_INFEAS,      // >0 if an element is inverted / vertex penetrates at entry
+  SC_COUNT = 32
+};
+
+// pinned host mirror layout
+enum {
+  PH_ENERGY = 0, PH_GNORM2, PH_DSNORM2, PH_ALPHA0, PH_INFEAS, PH_FLAG_S, PH_FLAG_SA,
+  PH_RZ0, PH_RZ, PH_LS = 16, PH_COUNT = 64
+};
+
+// ---------------------------------------------------------------- launch helpers
+constexpr int kMaxLS = 16;
+
+inline int div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// kernels (defined in the .cu files); every launcher increments ctx.launches
+void launch_elem_grad(Ctx &c);
+void launch_elem_hess(Ctx &c);
+void launch_eval_elements(Ctx &c, const double *x_dev, double *Ee, double *ge, double *He);
+void launch_vertex_grad(Ctx &c);
+void launch_assemble(Ctx &c);
+void launch_spmv(Ctx &c, const double *xin, double *yout, double alpha_minus_b, const double *b);
+void launch_pcg(Ctx &c, const double *rhs, double *sol, int iters);
+void pcg_reset_graph(Ctx &c);
+void launch_coarse_S(Ctx &c);
+void launch_coarse_factor(Ctx &c);
+void launch_coarse_direction(Ctx &c);
+void launch_lift(Ctx &c, const double *q, double *w, bool accumulate);
+void launch_restrict(Ctx &c, const double *y, double *z);
+void launch_filters(Ctx &c);
+void launch_ls_batch(Ctx &c, int k0, int K);
+void launch_update(Ctx &c, double alpha);
+void launch_predictor(Ctx &c);
+void launch_velocity(Ctx &c);
+void launch_axpby(Ctx &c, double *y, double a, const double *x, double b, int64_t n);
+void launch_dot(Ctx &c, const double *a, const double *b, int64_t n, int slot);
+void launch_copy_scalars_to_host(Ctx &c);
+
+// host-side symbolic setup (setup.cpp)
+void build_mesh_structures(Ctx &c, const double *X, const int32_t *tets, const double *E,
+                           const double *nu, const double *rho);
+void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int64_t *vptr,
+                            const int32_t *handle, const double *phi, const double *phi_aff,
+                            const double aff_origin[3]);
+void ensure_state_buffers(Ctx &c);
+
+// profiling helpers
+void phase_begin(Ctx &c, int phase);
+void phase_end(Ctx &c);
+
+}  // namespace msim

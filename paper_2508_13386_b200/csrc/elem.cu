@@ -1,0 +1,381 @@
+// Element kernels: stable Neo-Hookean energy, gradient and PSD-projected 12x12 Hessian.
+//
+// SURVEY §8(a) rows a2 (element energy + gradient) and a3 (element Hessian + PSD projection).
+// PAPER.md §3.1 L169-196 (IP energy, Newton system), L629 ("non-inverting Neo-Hookean");
+// readings R1 (Psi = mu/2 (I_C-3) - mu (J-1) + lam/2 (J-1)^2, +inf for J <= 0) and R2
+// (eigen-clamp of the 12x12 element Hessian).
+//
+// B200 design: one thread per tetrahedron, SoA per-tet data
+// (coalesced), vertex positions gathered through L1/L2.  The Hessian is built directly in the
+// 9-dimensional translation complement: with Q = Q4 kron I3 (Q4 = 1/2 Hadamard rows 2-4,
+// orthonormal, orthogonal to (1,1,1,1)) and C = (D_ref Bm)^T Q4,
+//     Q^T H_e Q = V [ mu (C^T C) kron I3 + lam g g^T + s HJ(F cof C) ],
+// g = vec(cof(F) C), s = lam (J-1) - mu, HJ(A)[(b,j),(b',j')] = eps_{bb'k} eps_{jj'l} A[l][k].
+// Because H_e annihilates translations, P+(H_e) = Q P+(Q^T H_e Q) Q^T exactly (pinned in
+// tests/test_oracle_fem.py::test_psd_element_reduction_equivalence).  The 9x9 symmetric
+// eigenproblem is solved in registers by cyclic Jacobi in the Brent-Luk parallel ordering
+// (9 rounds x 4 disjoint rotations per sweep -> 4 independent angle chains for ILP).
+#include "common.cuh"
+#include "reduce.cuh"
+
+namespace msim {
+
+struct MeshView {
+  int32_t nt;
+  const int4 *__restrict__ tets;
+  const double *__restrict__ Bm;  // [9][nt]
+  const double *__restrict__ vol;
+  const double *__restrict__ mu;
+  const double *__restrict__ lam;
+};
+
+static MeshView mesh_view(const Ctx &c) {
+  return MeshView{c.nt, reinterpret_cast<const int4 *>(c.tets.p), c.Bm.p, c.vol.p, c.mu.p, c.lam.p};
+}
+
+struct TetKin {
+  double F[3][3];
+  double Bm[3][3];
+  double V, mu, lam;
+  int4 t;
+};
+
+__device__ __forceinline__ void load_tet_kin(const MeshView &M, const double *__restrict__ x, int e,
+                                             TetKin &k) {
+  k.t = __ldg(&M.tets[e]);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) k.Bm[i / 3][i % 3] = __ldg(&M.Bm[(size_t)i * M.nt + e]);
+  k.V = __ldg(&M.vol[e]);
+  k.mu = __ldg(&M.mu[e]);
+  k.lam = __ldg(&M.lam[e]);
+  double x0[3], Ds[3][3];
+  const int vs[4] = {k.t.x, k.t.y, k.t.z, k.t.w};
+#pragma unroll
+  for (int i = 0; i < 3; ++i) x0[i] = x[3 * vs[0] + i];
+#pragma unroll
+  for (int a = 1; a < 4; ++a)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) Ds[i][a - 1] = x[3 * vs[a] + i] - x0[i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      k.F[i][j] = Ds[i][0] * k.Bm[0][j] + Ds[i][1] * k.Bm[1][j] + Ds[i][2] * k.Bm[2][j];
+}
+
+__device__ __forceinline__ void cofactor(const double F[3][3], double C[3][3]) {
+  // columns: c0 = f1 x f2, c1 = f2 x f0, c2 = f0 x f1 (f_k = column k of F)
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int a = (k + 1) % 3, b = (k + 2) % 3;
+    C[0][k] = F[1][a] * F[2][b] - F[2][a] * F[1][b];
+    C[1][k] = F[2][a] * F[0][b] - F[0][a] * F[2][b];
+    C[2][k] = F[0][a] * F[1][b] - F[1][a] * F[0][b];
+  }
+}
+
+__device__ __forceinline__ double det3(const double F[3][3]) {
+  return F[0][0] * (F[1][1] * F[2][2] - F[1][2] * F[2][1]) -
+         F[0][1] * (F[1][0] * F[2][2] - F[1][2] * F[2][0]) +
+         F[0][2] * (F[1][0] * F[2][1] - F[1][1] * F[2][0]);
+}
+
+__device__ __forceinline__ double psi_snh(const double F[3][3], double J, double mu, double lam) {
+  double Ic = 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) Ic += F[i][j] * F[i][j];
+  return 0.5 * mu * (Ic - 3.0) - mu * (J - 1.0) + 0.5 * lam * (J - 1.0) * (J - 1.0);
+}
+
+// ------------------------------------------------------------------ energy + gradient (a2)
+// stage_g[e*12 + 3a + i] = V_e (G_e^T vec P)_{(a,i)}; partial energy sum V_e Psi_e.
+__global__ void __launch_bounds__(256) k_elem_grad(MeshView M, const double *__restrict__ x,
+                                                   double *__restrict__ stage_g,
+                                                   double *__restrict__ partial,
+                                                   unsigned int *__restrict__ counter,
+                                                   double *__restrict__ out_energy,
+                                                   double *__restrict__ infeas,
+                                                   double *__restrict__ Ee) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  double en[2] = {0.0, 0.0};
+  if (e < M.nt) {
+    TetKin k;
+    load_tet_kin(M, x, e, k);
+    const double J = det3(k.F);
+    double cof[3][3];
+    cofactor(k.F, cof);
+    if (!(J > 0.0)) en[1] = 1.0;
+    const double s = k.lam * (J - 1.0) - k.mu;
+    double P[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) P[i][j] = k.mu * k.F[i][j] + s * cof[i][j];
+    // g_a (a = 1..3) = V * (P Bm^T)[:, a-1]; g_0 = -(g_1 + g_2 + g_3)
+    double g[4][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double v = k.V * (P[i][0] * k.Bm[a][0] + P[i][1] * k.Bm[a][1] + P[i][2] * k.Bm[a][2]);
+        g[a + 1][i] = v;
+        acc += v;
+      }
+      g[0][i] = -acc;
+    }
+    double *dst = stage_g + (size_t)e * 12;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) dst[3 * a + i] = g[a][i];
+    const double psi = psi_snh(k.F, J, k.mu, k.lam);
+    en[0] = k.V * psi;
+    if (Ee) Ee[e] = (J > 0.0) ? k.V * psi : __longlong_as_double(0x7ff0000000000000ULL);
+  }
+  double res[2];
+  if (grid_reduce<2>(en, partial, counter, res) && threadIdx.x == 0) {
+    *out_energy = res[0];
+    *infeas = res[1];
+  }
+}
+
+// ------------------------------------------------------------------ Hessian + PSD (a3)
+__host__ __device__ constexpr int sidx(int i, int j) {
+  return i <= j ? i * 9 - (i * (i - 1)) / 2 + (j - i) : j * 9 - (j * (j - 1)) / 2 + (i - j);
+}
+__host__ __device__ constexpr int blk4(int a, int b) {  // a <= b, 10 upper blocks
+  return a * 4 - (a * (a - 1)) / 2 + (b - a);
+}
+// Brent-Luk round-robin for n = 9: round r pairs ((r+k)%9, (r-k+9)%9), k = 1..4
+__host__ __device__ constexpr int rr_p(int r, int k) {
+  return ((r + k) % 9) < ((r - k + 9) % 9) ? ((r + k) % 9) : ((r - k + 9) % 9);
+}
+__host__ __device__ constexpr int rr_q(int r, int k) {
+  return ((r + k) % 9) < ((r - k + 9) % 9) ? ((r - k + 9) % 9) : ((r + k) % 9);
+}
+
+template <int R>
+__device__ __forceinline__ void jacobi_round(double (&a)[45], double (&v)[81]) {
+  double c[4], s[4], t[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    constexpr int dummy = 0;
+    (void)dummy;
+    const int p = rr_p(R, k + 1), q = rr_q(R, k + 1);
+    const double apq = a[sidx(p, q)];
+    const double dd = a[sidx(q, q)] - a[sidx(p, p)];
+    const double r = sqrt(fma(dd, dd, 4.0 * apq * apq));
+    const double den = fabs(dd) + r;
+    double tt = den > 0.0 ? (2.0 * apq) / den : 0.0;
+    tt = dd >= 0.0 ? tt : -tt;
+    t[k] = tt;
+    c[k] = rsqrt(fma(tt, tt, 1.0));
+    s[k] = tt * c[k];
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int p = rr_p(R, k + 1), q = rr_q(R, k + 1);
+    const double apq = a[sidx(p, q)];
+    a[sidx(p, p)] = fma(-t[k], apq, a[sidx(p, p)]);
+    a[sidx(q, q)] = fma(t[k], apq, a[sidx(q, q)]);
+    a[sidx(p, q)] = 0.0;
+#pragma unroll
+    for (int r = 0; r < 9; ++r) {
+      if (r == p || r == q) continue;
+      const double arp = a[sidx(r, p)], arq = a[sidx(r, q)];
+      a[sidx(r, p)] = fma(c[k], arp, -s[k] * arq);
+      a[sidx(r, q)] = fma(s[k], arp, c[k] * arq);
+    }
+#pragma unroll
+    for (int r = 0; r < 9; ++r) {
+      const double vp = v[r * 9 + p], vq = v[r * 9 + q];
+      v[r * 9 + p] = fma(c[k], vp, -s[k] * vq);
+      v[r * 9 + q] = fma(s[k], vp, c[k] * vq);
+    }
+  }
+}
+
+__device__ __forceinline__ void jacobi_sweep(double (&a)[45], double (&v)[81]) {
+  jacobi_round<0>(a, v);
+  jacobi_round<1>(a, v);
+  jacobi_round<2>(a, v);
+  jacobi_round<3>(a, v);
+  jacobi_round<4>(a, v);
+  jacobi_round<5>(a, v);
+  jacobi_round<6>(a, v);
+  jacobi_round<7>(a, v);
+  jacobi_round<8>(a, v);
+}
+
+__device__ __forceinline__ double offdiag2(const double (&a)[45]) {
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 9; ++i)
+#pragma unroll
+    for (int j = i + 1; j < 9; ++j) s = fma(a[sidx(i, j)], a[sidx(i, j)], s);
+  return s;
+}
+
+// Builds the reduced 9x9 Hessian (packed symmetric) of one tet.
+__device__ __forceinline__ void reduced_hessian(const TetKin &k, double (&a)[45]) {
+  const double J = det3(k.F);
+  double cofF[3][3];
+  cofactor(k.F, cofF);
+  const double s = k.lam * (J - 1.0) - k.mu;
+  // C = Bm^T R0, R0 = D_ref^T Q4 = [[0,-1,-1],[-1,0,-1],[-1,-1,0]]  ->  C[a][b] = Bm[b][a] - colsum_a
+  double C[3][3];
+#pragma unroll
+  for (int aa = 0; aa < 3; ++aa) {
+    const double cs = k.Bm[0][aa] + k.Bm[1][aa] + k.Bm[2][aa];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) C[aa][b] = k.Bm[b][aa] - cs;
+  }
+  double K[3][3];
+#pragma unroll
+  for (int b = 0; b < 3; ++b)
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb) K[b][bb] = C[0][b] * C[0][bb] + C[1][b] * C[1][bb] + C[2][b] * C[2][bb];
+  double cofC[3][3];
+  cofactor(C, cofC);
+  double Ft[3][3], gh[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      Ft[i][j] = k.F[i][0] * cofC[0][j] + k.F[i][1] * cofC[1][j] + k.F[i][2] * cofC[2][j];
+      gh[i][j] = cofF[i][0] * C[0][j] + cofF[i][1] * C[1][j] + cofF[i][2] * C[2][j];
+    }
+  const double Vmu = k.V * k.mu, Vlam = k.V * k.lam, Vs = k.V * s;
+#pragma unroll
+  for (int r = 0; r < 9; ++r)
+#pragma unroll
+    for (int cc = r; cc < 9; ++cc) {
+      const int b = r / 3, j = r % 3, bb = cc / 3, jj = cc % 3;
+      double val = Vlam * gh[j][b] * gh[jj][bb];
+      if (j == jj) val += Vmu * K[b][bb];
+      if (b != bb && j != jj) {
+        const int kk = 3 - b - bb, l = 3 - j - jj;
+        // eps_{b bb kk} * eps_{j jj l}
+        const int s1 = ((bb - b + 3) % 3 == 1) ? 1 : -1;
+        const int s2 = ((jj - j + 3) % 3 == 1) ? 1 : -1;
+        val += (s1 * s2) * Vs * Ft[l][kk];
+      }
+      a[sidx(r, cc)] = val;
+    }
+}
+
+// P+(Q^T H Q) in packed form (45) from the Jacobi result.
+__device__ __forceinline__ void eig_clamp(double (&a)[45], double (&p9)[45]) {
+  double v[81];
+#pragma unroll
+  for (int i = 0; i < 81; ++i) v[i] = (i / 9 == i % 9) ? 1.0 : 0.0;
+  double fro2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < 9; ++i)
+#pragma unroll
+    for (int j = i; j < 9; ++j) fro2 += (i == j ? 1.0 : 2.0) * a[sidx(i, j)] * a[sidx(i, j)];
+  const double tol2 = 1e-30 * fro2;
+  for (int sweep = 0; sweep < 12; ++sweep) {
+    if (2.0 * offdiag2(a) <= tol2) break;
+    jacobi_sweep(a, v);
+  }
+  double lp[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) lp[i] = fmax(a[sidx(i, i)], 0.0);
+#pragma unroll
+  for (int i = 0; i < 9; ++i)
+#pragma unroll
+    for (int j = i; j < 9; ++j) {
+      double acc = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 9; ++kk) acc = fma(lp[kk] * v[i * 9 + kk], v[j * 9 + kk], acc);
+      p9[sidx(i, j)] = acc;
+    }
+}
+
+// 12x12 block (a, a2) entry (i, i2) of Q P9 Q^T, Q4 = 1/2 [[1,1,1],[1,-1,-1],[-1,1,-1],[-1,-1,1]]
+__host__ __device__ constexpr int q4s(int a, int b) {  // sign of Q4[a][b]
+  return a == 0 ? 1 : (a == b + 1 ? 1 : -1);
+}
+
+__device__ __forceinline__ double lift_entry(const double (&p9)[45], int a, int a2, int i, int i2) {
+  double acc = 0.0;
+#pragma unroll
+  for (int b = 0; b < 3; ++b)
+#pragma unroll
+    for (int b2 = 0; b2 < 3; ++b2) {
+      const double pv = p9[sidx(3 * b + i, 3 * b2 + i2)];
+      acc += (q4s(a, b) * q4s(a2, b2) > 0) ? pv : -pv;
+    }
+  return 0.25 * acc;
+}
+
+// stage_h[e*90 + blk4(a,a2)*9 + 3 i + i2] = P+(H_e) block (a, a2), a <= a2 (unscaled by h^2)
+__global__ void __launch_bounds__(128) k_elem_hess(MeshView M, const double *__restrict__ x,
+                                                   double *__restrict__ stage_h) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= M.nt) return;
+  TetKin k;
+  load_tet_kin(M, x, e, k);
+  double a[45], p9[45];
+  reduced_hessian(k, a);
+  eig_clamp(a, p9);
+  double *dst = stage_h + (size_t)e * 90;
+#pragma unroll
+  for (int A = 0; A < 4; ++A)
+#pragma unroll
+    for (int A2 = A; A2 < 4; ++A2)
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int i2 = 0; i2 < 3; ++i2) dst[blk4(A, A2) * 9 + 3 * i + i2] = lift_entry(p9, A, A2, i, i2);
+}
+
+// Expand staged element data to the parity-hook layout (full 12x12 row-major).
+__global__ void k_expand_hess(int nt, const double *__restrict__ stage_h, double *__restrict__ He) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)nt * 144) return;
+  const int e = (int)(idx / 144), rc = (int)(idx % 144), r = rc / 12, cc = rc % 12;
+  const int a = r / 3, i = r % 3, a2 = cc / 3, i2 = cc % 3;
+  double v;
+  if (a <= a2) v = stage_h[(size_t)e * 90 + blk4(a, a2) * 9 + 3 * i + i2];
+  else v = stage_h[(size_t)e * 90 + blk4(a2, a) * 9 + 3 * i2 + i];
+  He[idx] = v;
+}
+
+// ------------------------------------------------------------------ launchers
+void launch_elem_grad_to(Ctx &c, const double *x, double *Ee) {
+  const int bs = 256, nb = div_up(c.nt, bs);
+  k_elem_grad<<<nb, bs, 0, c.stream>>>(mesh_view(c), x, c.stage_g, c.partial, c.counters + 0,
+                                       c.scal + SC_ENERGY_ELEM, c.scal + SC_INFEAS, Ee);
+  c.launches++;
+  MS_CUDA(cudaGetLastError());
+}
+
+void launch_elem_grad(Ctx &c) { launch_elem_grad_to(c, c.x, nullptr); }
+
+void launch_elem_hess_to(Ctx &c, const double *x) {
+  const int bs = 128, nb = div_up(c.nt, bs);
+  k_elem_hess<<<nb, bs, 0, c.stream>>>(mesh_view(c), x, c.stage_h);
+  c.launches++;
+  MS_CUDA(cudaGetLastError());
+}
+
+void launch_elem_hess(Ctx &c) { launch_elem_hess_to(c, c.x); }
+
+void launch_eval_elements(Ctx &c, const double *x_dev, double *Ee, double *ge, double *He) {
+  launch_elem_grad_to(c, x_dev, Ee);
+  if (ge) MS_CUDA(cudaMemcpyAsync(ge, c.stage_g, sizeof(double) * 12 * c.nt, cudaMemcpyDeviceToDevice, c.stream));
+  if (He) {
+    launch_elem_hess_to(c, x_dev);
+    const int64_t n = (int64_t)c.nt * 144;
+    k_expand_hess<<<div_up(n, 256), 256, 0, c.stream>>>(c.nt, c.stage_h, He);
+    c.launches++;
+    MS_CUDA(cudaGetLastError());
+  }
+}
+
+}  // namespace msim

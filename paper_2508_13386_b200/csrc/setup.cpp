@@ -1,0 +1,345 @@
+// Host-side symbolic setup: validation, per-tet rest data, BSR pattern and the atomic-free
+// assembly maps; basis CSR (vertex- and handle-major), coarse S pattern, the R_i(u) pair
+// list and the S-block contribution lists; tile-envelope schedule of the coarse Cholesky.
+//
+// SURVEY §8(a) a4 (BSR assembly into precomputed slots), a5 (Galerkin projection), a6
+// (factorisation); §8(b) ms_upload_mesh / ms_basis_upload semantics.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "common.cuh"
+
+namespace msim {
+
+static void rest_data(const double *X, const int32_t *t, double Bm[9], double &V) {
+  double Dm[3][3];
+  for (int k = 0; k < 3; ++k)
+    for (int i = 0; i < 3; ++i) Dm[i][k] = X[3 * t[k + 1] + i] - X[3 * t[0] + i];
+  const double det = Dm[0][0] * (Dm[1][1] * Dm[2][2] - Dm[1][2] * Dm[2][1]) -
+                     Dm[0][1] * (Dm[1][0] * Dm[2][2] - Dm[1][2] * Dm[2][0]) +
+                     Dm[0][2] * (Dm[1][0] * Dm[2][1] - Dm[1][1] * Dm[2][0]);
+  V = det / 6.0;
+  // inverse via adjugate
+  double A[3][3];
+  A[0][0] = Dm[1][1] * Dm[2][2] - Dm[1][2] * Dm[2][1];
+  A[0][1] = Dm[0][2] * Dm[2][1] - Dm[0][1] * Dm[2][2];
+  A[0][2] = Dm[0][1] * Dm[1][2] - Dm[0][2] * Dm[1][1];
+  A[1][0] = Dm[1][2] * Dm[2][0] - Dm[1][0] * Dm[2][2];
+  A[1][1] = Dm[0][0] * Dm[2][2] - Dm[0][2] * Dm[2][0];
+  A[1][2] = Dm[0][2] * Dm[1][0] - Dm[0][0] * Dm[1][2];
+  A[2][0] = Dm[1][0] * Dm[2][1] - Dm[1][1] * Dm[2][0];
+  A[2][1] = Dm[0][1] * Dm[2][0] - Dm[0][0] * Dm[2][1];
+  A[2][2] = Dm[0][0] * Dm[1][1] - Dm[0][1] * Dm[1][0];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) Bm[3 * i + j] = A[i][j] / det;
+}
+
+void build_mesh_structures(Ctx &c, const double *X, const int32_t *tets, const double *E,
+                           const double *nu, const double *rho) {
+  const int32_t nv = c.nv, nt = c.nt;
+  for (int64_t i = 0; i < (int64_t)nt * 4; ++i)
+    MS_REQUIRE(tets[i] >= 0 && tets[i] < nv, MS_ERR_ARG, "tet vertex index out of range");
+  for (int32_t e = 0; e < nt; ++e) {
+    MS_REQUIRE(E[e] > 0.0, MS_ERR_ARG, "Young's modulus must be > 0");
+    MS_REQUIRE(nu[e] >= 0.0 && nu[e] < 0.5, MS_ERR_ARG, "Poisson ratio must be in [0, 0.5)");
+    MS_REQUIRE(rho[e] > 0.0, MS_ERR_ARG, "density must be > 0");
+  }
+  c.h_X.assign(X, X + 3 * (size_t)nv);
+  c.h_tets.assign(tets, tets + 4 * (size_t)nt);
+
+  std::vector<double> Bm((size_t)9 * nt), vol(nt), mu(nt), lam(nt), mass(nv, 0.0);
+  for (int32_t e = 0; e < nt; ++e) {
+    double b[9], V;
+    rest_data(X, tets + 4 * (size_t)e, b, V);
+    MS_REQUIRE(V > 0.0, MS_ERR_ARG, "tet with non-positive rest volume (orientation?)");
+    for (int k = 0; k < 9; ++k) Bm[(size_t)k * nt + e] = b[k];
+    vol[e] = V;
+    mu[e] = E[e] / (2.0 * (1.0 + nu[e]));
+    lam[e] = E[e] * nu[e] / ((1.0 + nu[e]) * (1.0 - 2.0 * nu[e]));
+  }
+  // lumped mass m_v = sum_e rho_e V_e / 4 in tet order (deterministic)
+  for (int32_t e = 0; e < nt; ++e)
+    for (int a = 0; a < 4; ++a) mass[tets[4 * (size_t)e + a]] += rho[e] * vol[e] / 4.0;
+
+  // vertex -> (tet, corner) incidence, sorted by tet
+  std::vector<int32_t> vptr(nv + 1, 0), vinc((size_t)4 * nt);
+  for (int64_t i = 0; i < (int64_t)nt * 4; ++i) vptr[tets[i] + 1]++;
+  for (int32_t v = 0; v < nv; ++v) vptr[v + 1] += vptr[v];
+  {
+    std::vector<int32_t> fill(vptr.begin(), vptr.end() - 1);
+    for (int32_t e = 0; e < nt; ++e)
+      for (int a = 0; a < 4; ++a) vinc[fill[tets[4 * (size_t)e + a]]++] = 4 * e + a;
+  }
+  for (int32_t v = 0; v < nv; ++v)
+    MS_REQUIRE(vptr[v + 1] > vptr[v], MS_ERR_ARG, "vertex not referenced by any tet");
+
+  // BSR pattern: row v = sorted unique vertices of incident tets (includes v)
+  c.h_rowptr.assign(nv + 1, 0);
+  std::vector<int32_t> colidx;
+  colidx.reserve((size_t)nv * 16);
+  std::vector<int32_t> buf;
+  for (int32_t v = 0; v < nv; ++v) {
+    buf.clear();
+    for (int32_t k = vptr[v]; k < vptr[v + 1]; ++k) {
+      const int32_t e = vinc[k] >> 2;
+      for (int a = 0; a < 4; ++a) buf.push_back(tets[4 * (size_t)e + a]);
+    }
+    std::sort(buf.begin(), buf.end());
+    buf.erase(std::unique(buf.begin(), buf.end()), buf.end());
+    colidx.insert(colidx.end(), buf.begin(), buf.end());
+    MS_REQUIRE(colidx.size() < (size_t)INT32_MAX, MS_ERR_ARG, "BSR too large for int32");
+    c.h_rowptr[v + 1] = (int32_t)colidx.size();
+  }
+  c.h_colidx = colidx;
+  c.nnzb = (int64_t)colidx.size();
+  std::vector<int32_t> diag(nv), slot_row(c.nnzb);
+  for (int32_t v = 0; v < nv; ++v)
+    for (int32_t k = c.h_rowptr[v]; k < c.h_rowptr[v + 1]; ++k) slot_row[k] = v;
+  auto slot_of = [&](int32_t r, int32_t col) {
+    const int32_t *b = colidx.data() + c.h_rowptr[r], *e = colidx.data() + c.h_rowptr[r + 1];
+    return (int32_t)(std::lower_bound(b, e, col) - colidx.data());
+  };
+  for (int32_t v = 0; v < nv; ++v) diag[v] = slot_of(v, v);
+
+  // slot -> contributions (tet*16 + a*4 + b), ordered by tet (deterministic gather order)
+  std::vector<int32_t> cptr(c.nnzb + 1, 0);
+  std::vector<int32_t> cslot((size_t)16 * nt);
+  for (int32_t e = 0; e < nt; ++e)
+    for (int a = 0; a < 4; ++a)
+      for (int b = 0; b < 4; ++b) {
+        const int32_t s = slot_of(tets[4 * (size_t)e + a], tets[4 * (size_t)e + b]);
+        cslot[(size_t)16 * e + 4 * a + b] = s;
+        cptr[s + 1]++;
+      }
+  for (int64_t s = 0; s < c.nnzb; ++s) cptr[s + 1] += cptr[s];
+  std::vector<int32_t> contrib((size_t)16 * nt);
+  {
+    std::vector<int32_t> fill(cptr.begin(), cptr.end() - 1);
+    for (int64_t k = 0; k < (int64_t)16 * nt; ++k) contrib[fill[cslot[k]]++] = (int32_t)k;
+  }
+
+  cudaStream_t s = c.stream;
+  c.X.upload(X, 3 * (size_t)nv, s);
+  c.tets.upload(tets, 4 * (size_t)nt, s);
+  c.Bm.upload(Bm, s);
+  c.vol.upload(vol, s);
+  c.mu.upload(mu, s);
+  c.lam.upload(lam, s);
+  c.mass.upload(mass, s);
+  c.vinc_ptr.upload(vptr, s);
+  c.vinc.upload(vinc, s);
+  c.rowptr.upload(c.h_rowptr, s);
+  c.colidx.upload(c.h_colidx, s);
+  c.diag_slot.upload(diag, s);
+  c.slot_row.upload(slot_row, s);
+  c.cptr.upload(cptr, s);
+  c.contrib.upload(contrib, s);
+  c.vals.alloc((size_t)9 * c.nnzb);
+  c.h_fixed.assign(nv, 0);
+  c.fixed.upload(c.h_fixed, s);
+  ensure_state_buffers(c);
+  MS_CUDA(cudaStreamSynchronize(s));
+}
+
+void ensure_state_buffers(Ctx &c) {
+  const size_t n3 = 3 * (size_t)c.nv;
+  for (DBuf<double> *b : {&c.x, &c.v, &c.xt, &c.xhat, &c.g, &c.ds, &c.da, &c.df, &c.d, &c.r, &c.rhs,
+                          &c.p, &c.q, &c.z, &c.tmp, &c.dinv})
+    b->alloc(n3);
+  c.stage_g.alloc((size_t)12 * c.nt);
+  c.stage_h.alloc((size_t)90 * c.nt);
+  c.max_blocks = std::max(div_up(c.nt, 128), div_up(c.nv, 128)) + 1024;
+  c.partial.alloc((size_t)c.max_blocks * (kMaxLS + 2));
+  c.counters.alloc(64);
+  c.counters.zero(c.stream);
+  c.scal.alloc(SC_COUNT);
+  c.scal.zero(c.stream);
+  c.flags.alloc(8);
+  c.flags.zero(c.stream);
+  c.ls_alpha.alloc(kMaxLS);
+  c.ls_out.alloc(kMaxLS + 4);
+  // rest state: x = X, v = 0
+  MS_CUDA(cudaMemcpyAsync(c.x, c.X, sizeof(double) * n3, cudaMemcpyDeviceToDevice, c.stream));
+  c.v.zero(c.stream);
+  MS_CUDA(cudaMemcpyAsync(c.xt, c.X, sizeof(double) * n3, cudaMemcpyDeviceToDevice, c.stream));
+  MS_CUDA(cudaMemcpyAsync(c.xhat, c.X, sizeof(double) * n3, cudaMemcpyDeviceToDevice, c.stream));
+}
+
+// ------------------------------------------------------------------------- basis
+void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int64_t *vptr,
+                            const int32_t *handle, const double *phi, const double *phi_aff,
+                            const double aff_origin[3]) {
+  const int32_t nv = c.nv;
+  MS_REQUIRE(m > 0, MS_ERR_ARG, "m must be > 0");
+  MS_REQUIRE(vptr[0] == 0, MS_ERR_ARG, "vptr[0] must be 0");
+  const int64_t nnz = vptr[nv];
+  MS_REQUIRE(nnz < INT32_MAX, MS_ERR_ARG, "basis too large for int32 indices");
+  for (int32_t v = 0; v < nv; ++v) {
+    MS_REQUIRE(vptr[v + 1] >= vptr[v], MS_ERR_ARG, "vptr not monotone");
+    double sum = 0.0;
+    for (int64_t k = vptr[v]; k < vptr[v + 1]; ++k) {
+      MS_REQUIRE(handle[k] >= 0 && handle[k] < m, MS_ERR_ARG, "handle id out of range");
+      MS_REQUIRE(k == vptr[v] || handle[k] > handle[k - 1], MS_ERR_ARG,
+                 "handles of a vertex must be strictly increasing");
+      MS_REQUIRE(phi[k] > 0.0, MS_ERR_ARG, "phi entries must be > 0");
+      sum += phi[k];
+    }
+    MS_REQUIRE(sum > 0.0 || c.h_fixed[v], MS_ERR_COVERAGE,
+               "basis coverage hole: no handle covers a free vertex");
+  }
+  c.m = m;
+  c.nnz_phi = nnz;
+  std::vector<int32_t> bvptr(nv + 1);
+  for (int32_t v = 0; v <= nv; ++v) bvptr[v] = (int32_t)vptr[v];
+  // handle-major transpose (sorted by vertex)
+  std::vector<int32_t> hptr(m + 1, 0), hvert(nnz), hidx(nnz);
+  std::vector<double> hphi(nnz);
+  for (int64_t k = 0; k < nnz; ++k) hptr[handle[k] + 1]++;
+  for (int32_t i = 0; i < m; ++i) hptr[i + 1] += hptr[i];
+  {
+    std::vector<int32_t> fill(hptr.begin(), hptr.end() - 1);
+    for (int32_t v = 0; v < nv; ++v)
+      for (int64_t k = vptr[v]; k < vptr[v + 1]; ++k) {
+        const int32_t pos = fill[handle[k]]++;
+        hvert[pos] = v;
+        hphi[pos] = phi[k];
+        hidx[pos] = (int32_t)k;
+      }
+  }
+  for (int32_t i = 0; i < m; ++i)
+    MS_REQUIRE(hptr[i + 1] > hptr[i], MS_ERR_ARG, "handle with empty support");
+
+  // U_i = vertices adjacent (BSR) to supp(i); R pairs (i,u); J_i = handles of U_i;
+  // S block (i,j) contributions (R index, phi index of (u,j)).
+  std::vector<int32_t> mark(nv, -1), hmark(m, -1), jslot(m, -1);
+  std::vector<int32_t> Ri, Ru;
+  std::vector<int32_t> sptr(1, 0), scol;
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> lists;
+  std::vector<int32_t> sc_ptr(1, 0), sc_R, sc_phi;
+  const int32_t *rp = c.h_rowptr.data(), *ci = c.h_colidx.data();
+  std::vector<int32_t> U, Jl;
+  for (int32_t i = 0; i < m; ++i) {
+    U.clear();
+    for (int32_t k = hptr[i]; k < hptr[i + 1]; ++k) {
+      const int32_t v = hvert[k];
+      for (int32_t s = rp[v]; s < rp[v + 1]; ++s) {
+        const int32_t u = ci[s];
+        if (mark[u] != i) {
+          mark[u] = i;
+          U.push_back(u);
+        }
+      }
+    }
+    std::sort(U.begin(), U.end());
+    Jl.clear();
+    for (int32_t u : U)
+      for (int64_t k = vptr[u]; k < vptr[u + 1]; ++k)
+        if (hmark[handle[k]] != i) {
+          hmark[handle[k]] = i;
+          Jl.push_back(handle[k]);
+        }
+    std::sort(Jl.begin(), Jl.end());
+    for (size_t q = 0; q < Jl.size(); ++q) jslot[Jl[q]] = (int32_t)q;
+    lists.assign(Jl.size(), {});
+    for (int32_t u : U) {
+      const int32_t r = (int32_t)Ri.size();
+      Ri.push_back(i);
+      Ru.push_back(u);
+      for (int64_t k = vptr[u]; k < vptr[u + 1]; ++k) lists[jslot[handle[k]]].push_back({r, (int32_t)k});
+    }
+    for (size_t q = 0; q < Jl.size(); ++q) {
+      scol.push_back(Jl[q]);
+      for (auto &pr : lists[q]) {
+        sc_R.push_back(pr.first);
+        sc_phi.push_back(pr.second);
+      }
+      MS_REQUIRE(sc_R.size() < (size_t)INT32_MAX, MS_ERR_ARG, "coarse contribution list too large");
+      sc_ptr.push_back((int32_t)sc_R.size());
+    }
+    sptr.push_back((int32_t)scol.size());
+  }
+  c.h_sptr = sptr;
+  c.h_scol = scol;
+  c.nnzb_S = (int64_t)scol.size();
+  c.n_R = (int64_t)Ri.size();
+
+  // ---- tile envelope of S (symmetric; handles ordered by x so the profile is banded)
+  c.nS = 12 * m;
+  c.tile = 64;
+  c.ntiles = div_up(c.nS, c.tile);
+  c.nS_pad = c.ntiles * c.tile;
+  std::vector<int32_t> band_lo(c.nS_pad);
+  for (int32_t i = 0; i < m; ++i) {
+    int32_t jmin = i;
+    for (int32_t k = sptr[i]; k < sptr[i + 1]; ++k) jmin = std::min(jmin, scol[k]);
+    for (int r = 0; r < 12; ++r) band_lo[12 * i + r] = 12 * jmin;
+  }
+  for (int32_t r = c.nS; r < c.nS_pad; ++r) band_lo[r] = r;   // padding: identity rows
+  const int T = c.tile, NT = c.ntiles;
+  c.h_tile_rowlo.assign(NT, 0);
+  for (int32_t ti = 0; ti < NT; ++ti) {
+    int32_t lo = ti;
+    for (int r = ti * T; r < (ti + 1) * T; ++r) lo = std::min(lo, band_lo[r] / T);
+    c.h_tile_rowlo[ti] = lo;
+  }
+  // fill stays inside the envelope: L_ik != 0 iff rowlo(i) <= k
+  c.h_chol_panel.assign(NT, {});
+  c.h_chol_updates.assign(NT, {});
+  std::vector<int32_t> panel_flat, task_flat;
+  c.h_chol_panel_off.assign(NT + 1, 0);
+  c.h_chol_task_off.assign(NT + 1, 0);
+  for (int32_t k = 0; k < NT; ++k) {
+    auto &P = c.h_chol_panel[k];
+    for (int32_t i = k + 1; i < NT; ++i)
+      if (c.h_tile_rowlo[i] <= k) P.push_back(i);
+    for (size_t a = 0; a < P.size(); ++a)
+      for (size_t b = 0; b <= a; ++b) {
+        task_flat.push_back(P[a]);
+        task_flat.push_back(P[b]);
+      }
+    panel_flat.insert(panel_flat.end(), P.begin(), P.end());
+    c.h_chol_panel_off[k + 1] = (int64_t)panel_flat.size();
+    c.h_chol_task_off[k + 1] = (int64_t)task_flat.size() / 2;
+  }
+
+  cudaStream_t s = c.stream;
+  c.origins.upload(origins, 3 * (size_t)m, s);
+  c.bvptr.upload(bvptr, s);
+  c.bhandle.upload(handle, nnz, s);
+  c.bphi.upload(phi, nnz, s);
+  c.hptr.upload(hptr, s);
+  c.hvert.upload(hvert, s);
+  c.hphi.upload(hphi, s);
+  c.phi_aff.upload(phi_aff, nv, s);
+  for (int k = 0; k < 3; ++k) c.aff_origin[k] = aff_origin[k];
+  c.sptr.upload(sptr, s);
+  c.scol.upload(scol, s);
+  {
+    std::vector<int32_t> srow(scol.size());
+    for (int32_t i = 0; i < m; ++i)
+      for (int32_t k = sptr[i]; k < sptr[i + 1]; ++k) srow[k] = i;
+    c.srow.upload(srow, s);
+  }
+  c.Sblk.alloc((size_t)144 * c.nnzb_S);
+  c.R_i.upload(Ri, s);
+  c.R_u.upload(Ru, s);
+  c.Rbuf.alloc((size_t)36 * c.n_R);
+  c.sc_ptr.upload(sc_ptr, s);
+  c.sc_R.upload(sc_R, s);
+  c.sc_phi.upload(sc_phi, s);
+  c.Sa.alloc(144);
+  c.Ra.alloc((size_t)36 * nv);
+  c.Lden.alloc((size_t)c.nS_pad * c.nS_pad);
+  c.band_lo.upload(band_lo, s);
+  c.chol_panel.upload(panel_flat.empty() ? std::vector<int32_t>{0} : panel_flat, s);
+  c.chol_tasks.upload(task_flat.empty() ? std::vector<int32_t>{0, 0} : task_flat, s);
+  c.qa.alloc(12);
+  c.za.alloc(12);
+  c.qs.alloc(c.nS_pad);
+  c.zs.alloc(c.nS_pad);
+  MS_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace msim

@@ -1,0 +1,441 @@
+// Vertex gradient gather, atomic-free BSR assembly, 3x3-block SpMV and the fused Jacobi-PCG.
+//
+// SURVEY §8(a) rows a2 (g = M(x - xhat) + h^2 [sum_e g_e + kappa b'(d) n], g_DBC = 0),
+// a4 (H = M + h^2 (sum_e P+(H_e) + kappa b''(d) n n^T), DBC rows/cols -> identity),
+// a8 (exactly N_cg Jacobi-PCG iterations from d_f = 0, reading R5).
+//
+// B200 design: BSR values are stored as 9 planes [q][nnzb] so that a half-warp reading 16
+// consecutive blocks of one row issues fully coalesced 128-byte loads per plane; the PCG
+// direction update is fused into the SpMV (q = H z + beta q, p = z + beta p), the dot
+// products are deterministic grid reductions, and the whole fixed-count loop is captured in a
+// CUDA graph (no host synchronisation inside the loop).
+#include "common.cuh"
+#include "reduce.cuh"
+
+namespace msim {
+
+// ------------------------------------------------------------------ barrier helpers
+__device__ __forceinline__ double bar_b(double d, double dh) {
+  if (d >= dh) return 0.0;
+  const double t = d - dh;
+  return -t * t * log(d / dh);
+}
+__device__ __forceinline__ double bar_d1(double d, double dh) {
+  if (d >= dh) return 0.0;
+  const double t = d - dh;
+  return -2.0 * t * log(d / dh) - t * t / d;
+}
+__device__ __forceinline__ double bar_d2(double d, double dh) {
+  if (d >= dh) return 0.0;
+  const double t = d - dh;
+  return -2.0 * log(d / dh) - 4.0 * t / d + (t * t) / (d * d);
+}
+
+struct Ground {
+  int on;
+  double n0, n1, n2, off, dhat, kappa;
+};
+static Ground ground_of(const Ctx &c) {
+  return Ground{c.has_ground ? 1 : 0, c.gn[0], c.gn[1], c.gn[2], c.goff, c.dhat, c.kappa};
+}
+
+// ------------------------------------------------------------------ vertex gradient (a2)
+// g_v = h^2 sum_{(e,a) in inc(v)} g_e[a] + m_v (x_v - xhat_v) + h^2 kappa b'(d_v) n ; 0 at DBC.
+// Also accumulates the vertex energy terms (inertia + h^2 kappa b) over free vertices, |g|^2.
+__global__ void __launch_bounds__(256) k_vertex_grad(
+    int nv, const int32_t *__restrict__ vptr, const int32_t *__restrict__ vinc,
+    const double *__restrict__ stage_g, const double *__restrict__ x, const double *__restrict__ xhat,
+    const double *__restrict__ mass, const uint8_t *__restrict__ fixed, Ground G, double h2,
+    double *__restrict__ g, double *__restrict__ partial, unsigned int *__restrict__ counter,
+    double *__restrict__ out /* [energy, |g|^2, infeasible] */) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  double acc[3] = {0.0, 0.0, 0.0};
+  if (v < nv) {
+    double ge[3] = {0.0, 0.0, 0.0};
+    for (int k = vptr[v]; k < vptr[v + 1]; ++k) {
+      const int code = vinc[k];
+      const double *src = stage_g + (size_t)(code >> 2) * 12 + 3 * (code & 3);
+      ge[0] += src[0];
+      ge[1] += src[1];
+      ge[2] += src[2];
+    }
+    double out3[3];
+    const double m = mass[v];
+    double r[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      r[i] = x[3 * v + i] - xhat[3 * v + i];
+      out3[i] = h2 * ge[i] + m * r[i];
+    }
+    double e = 0.0;
+    if (!fixed[v]) {
+      e = 0.5 * m * (r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+      if (G.on) {
+        const double d = G.n0 * x[3 * v] + G.n1 * x[3 * v + 1] + G.n2 * x[3 * v + 2] - G.off;
+        if (!(d > 0.0)) acc[2] = 1.0;
+        const double b1 = h2 * G.kappa * bar_d1(d, G.dhat);
+        out3[0] += b1 * G.n0;
+        out3[1] += b1 * G.n1;
+        out3[2] += b1 * G.n2;
+        e += h2 * G.kappa * bar_b(d, G.dhat);
+      }
+    } else {
+      out3[0] = out3[1] = out3[2] = 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) g[3 * v + i] = out3[i];
+    acc[0] = e;
+    acc[1] = out3[0] * out3[0] + out3[1] * out3[1] + out3[2] * out3[2];
+  }
+  double res[3];
+  if (grid_reduce<3>(acc, partial, counter, res) && threadIdx.x == 0) {
+    out[0] = res[0];
+    out[1] = res[1];
+    out[2] = res[2];
+  }
+}
+
+void launch_vertex_grad(Ctx &c) {
+  const int bs = 256, nb = div_up(c.nv, bs);
+  const double h2 = c.params.h * c.params.h;
+  k_vertex_grad<<<nb, bs, 0, c.stream>>>(c.nv, c.vinc_ptr, c.vinc, c.stage_g, c.x, c.xhat, c.mass,
+                                         c.fixed, ground_of(c), h2, c.g, c.partial, c.counters + 1,
+                                         c.scal + SC_ENERGY_VERT);
+  c.launches++;
+  MS_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ assembly (a4)
+__host__ __device__ constexpr int blk4s(int a, int b) { return a * 4 - (a * (a - 1)) / 2 + (b - a); }
+
+__global__ void __launch_bounds__(256) k_assemble(
+    int64_t nnzb, int nv, const int32_t *__restrict__ rowptr, const int32_t *__restrict__ colidx,
+    const int32_t *__restrict__ cptr, const int32_t *__restrict__ contrib,
+    const double *__restrict__ stage_h, const double *__restrict__ x, const double *__restrict__ mass,
+    const uint8_t *__restrict__ fixed, const int32_t *__restrict__ slot_row, Ground G, double h2,
+    double *__restrict__ vals, double *__restrict__ dinv) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nnzb) return;
+  double acc[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) acc[q] = 0.0;
+  for (int k = cptr[s]; k < cptr[s + 1]; ++k) {
+    const int code = contrib[k];
+    const int e = code >> 4, a = (code >> 2) & 3, b = code & 3;
+    if (a <= b) {
+      const double *src = stage_h + (size_t)e * 90 + blk4s(a, b) * 9;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) acc[q] += src[q];
+    } else {
+      const double *src = stage_h + (size_t)e * 90 + blk4s(b, a) * 9;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) acc[q] += src[(q % 3) * 3 + q / 3];
+    }
+  }
+  const int row = slot_row[s], col = colidx[s];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) acc[q] *= h2;
+  if (row == col) {
+    const double m = mass[row];
+    acc[0] += m;
+    acc[4] += m;
+    acc[8] += m;
+    if (G.on) {
+      const double d = G.n0 * x[3 * row] + G.n1 * x[3 * row + 1] + G.n2 * x[3 * row + 2] - G.off;
+      const double kb = h2 * G.kappa * bar_d2(d, G.dhat);
+      const double n[3] = {G.n0, G.n1, G.n2};
+#pragma unroll
+      for (int q = 0; q < 9; ++q) acc[q] += kb * n[q / 3] * n[q % 3];
+    }
+  }
+  if (fixed[row] || fixed[col]) {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc[q] = (row == col && (q % 4 == 0)) ? 1.0 : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < 9; ++q) vals[(size_t)q * nnzb + s] = acc[q];
+  if (row == col) {
+    dinv[3 * row + 0] = 1.0 / acc[0];
+    dinv[3 * row + 1] = 1.0 / acc[4];
+    dinv[3 * row + 2] = 1.0 / acc[8];
+  }
+}
+
+void launch_assemble(Ctx &c) {
+  const int bs = 256;
+  const double h2 = c.params.h * c.params.h;
+  k_assemble<<<div_up(c.nnzb, bs), bs, 0, c.stream>>>(c.nnzb, c.nv, c.rowptr, c.colidx, c.cptr,
+                                                      c.contrib, c.stage_h, c.x, c.mass, c.fixed,
+                                                      c.slot_row, ground_of(c), h2, c.vals, c.dinv);
+  c.launches++;
+  MS_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ SpMV
+// Half-warp per block row; lane k handles blocks rowptr[i] + k, k += 16.
+// y = H x               (mode 0)
+// y = b - H x           (mode 1)
+struct BSRView {
+  int nv;
+  int64_t nnzb;
+  const int32_t *__restrict__ rowptr;
+  const int32_t *__restrict__ colidx;
+  const double *__restrict__ vals;
+};
+static BSRView bsr_view(const Ctx &c) { return BSRView{c.nv, c.nnzb, c.rowptr, c.colidx, c.vals}; }
+
+__device__ __forceinline__ void row_product(const BSRView &H, int row, int sub,
+                                            const double *__restrict__ xin, double out[3]) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  const bool ok = row < H.nv;
+  const int beg = ok ? H.rowptr[row] : 0, end = ok ? H.rowptr[row + 1] : 0;
+  for (int s = beg + sub; s < end; s += 16) {
+    const int col = H.colidx[s];
+    const double x0 = xin[3 * col], x1 = xin[3 * col + 1], x2 = xin[3 * col + 2];
+    const double *v = H.vals + s;
+    const size_t P = (size_t)H.nnzb;
+    a0 = fma(v[0 * P], x0, fma(v[1 * P], x1, fma(v[2 * P], x2, a0)));
+    a1 = fma(v[3 * P], x0, fma(v[4 * P], x1, fma(v[5 * P], x2, a1)));
+    a2 = fma(v[6 * P], x0, fma(v[7 * P], x1, fma(v[8 * P], x2, a2)));
+  }
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) {
+    a0 += __shfl_down_sync(0xffffffffu, a0, o, 16);
+    a1 += __shfl_down_sync(0xffffffffu, a1, o, 16);
+    a2 += __shfl_down_sync(0xffffffffu, a2, o, 16);
+  }
+  out[0] = a0;
+  out[1] = a1;
+  out[2] = a2;
+}
+
+__global__ void __launch_bounds__(256) k_spmv(BSRView H, const double *__restrict__ xin,
+                                              double *__restrict__ yout, const double *__restrict__ b) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
+  const int sub = threadIdx.x & 15;
+  double o[3] = {0.0, 0.0, 0.0};
+  row_product(H, row, sub, xin, o);
+  if (row < H.nv && sub == 0) {
+    if (b) {
+      yout[3 * row] = b[3 * row] - o[0];
+      yout[3 * row + 1] = b[3 * row + 1] - o[1];
+      yout[3 * row + 2] = b[3 * row + 2] - o[2];
+    } else {
+      yout[3 * row] = o[0];
+      yout[3 * row + 1] = o[1];
+      yout[3 * row + 2] = o[2];
+    }
+  }
+}
+
+void launch_spmv(Ctx &c, const double *xin, double *yout, double /*unused*/, const double *b) {
+  const int bs = 256, rows_per_block = bs / 16;
+  k_spmv<<<div_up(c.nv, rows_per_block), bs, 0, c.stream>>>(bsr_view(c), xin, yout, b);
+  c.launches++;
+  MS_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ PCG (a8)
+// Scalars in scal: SC_RZ (rho), SC_PQ, SC_ALPHA, SC_BETA, SC_RZ0.
+// init:   x = 0, r = rhs, z = D^-1 r, p = 0, q = 0, beta = 0, rho = r.z
+// iter:   K1: p = z + beta p ; q = H z + beta q ; pq = p.q ; alpha = rho / pq
+//         K2: x += alpha p ; r -= alpha q ; z = D^-1 r ; rho' = r.z ; beta = rho'/rho ; rho = rho'
+// (q = H(z + beta p_old) = H z + beta H p_old, so the direction update needs no extra pass.)
+__global__ void __launch_bounds__(256) k_pcg_init(int n3, const double *__restrict__ rhs,
+                                                  const double *__restrict__ dinv, double *__restrict__ x,
+                                                  double *__restrict__ r, double *__restrict__ z,
+                                                  double *__restrict__ p, double *__restrict__ q,
+                                                  double *__restrict__ partial, unsigned int *counter,
+                                                  double *__restrict__ scal) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double acc[1] = {0.0};
+  if (i < n3) {
+    const double ri = rhs[i], zi = dinv[i] * ri;
+    x[i] = 0.0;
+    r[i] = ri;
+    z[i] = zi;
+    p[i] = 0.0;
+    q[i] = 0.0;
+    acc[0] = ri * zi;
+  }
+  double res[1];
+  if (grid_reduce<1>(acc, partial, counter, res) && threadIdx.x == 0) {
+    scal[SC_RZ] = res[0];
+    scal[SC_RZ0] = res[0];
+    scal[SC_BETA] = 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_pcg_spmv(BSRView H, const double *__restrict__ z,
+                                                  double *__restrict__ p, double *__restrict__ q,
+                                                  double *__restrict__ partial, unsigned int *counter,
+                                                  double *__restrict__ scal) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
+  const int sub = threadIdx.x & 15;
+  const double beta = scal[SC_BETA];
+  double o[3] = {0.0, 0.0, 0.0};
+  double acc[1] = {0.0};
+  row_product(H, row, sub, z, o);
+  if (row < H.nv) {
+    if (sub == 0) {
+      double pq = 0.0;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double pn = fma(beta, p[3 * row + i], z[3 * row + i]);
+        const double qn = fma(beta, q[3 * row + i], o[i]);
+        p[3 * row + i] = pn;
+        q[3 * row + i] = qn;
+        pq = fma(pn, qn, pq);
+      }
+      acc[0] = pq;
+    }
+  }
+  double res[1];
+  if (grid_reduce<1>(acc, partial, counter, res) && threadIdx.x == 0) {
+    const double rho = scal[SC_RZ];
+    scal[SC_PQ] = res[0];
+    scal[SC_ALPHA] = (res[0] != 0.0 && rho != 0.0) ? rho / res[0] : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_pcg_update(int n3, const double *__restrict__ dinv,
+                                                    const double *__restrict__ p, const double *__restrict__ q,
+                                                    double *__restrict__ x, double *__restrict__ r,
+                                                    double *__restrict__ z, double *__restrict__ partial,
+                                                    unsigned int *counter, double *__restrict__ scal) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const double alpha = scal[SC_ALPHA];
+  double acc[1] = {0.0};
+  if (i < n3) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, q[i], r[i]);
+    const double zi = dinv[i] * ri;
+    r[i] = ri;
+    z[i] = zi;
+    acc[0] = ri * zi;
+  }
+  double res[1];
+  if (grid_reduce<1>(acc, partial, counter, res) && threadIdx.x == 0) {
+    const double rho = scal[SC_RZ];
+    scal[SC_BETA] = rho != 0.0 ? res[0] / rho : 0.0;
+    scal[SC_RZ] = res[0];
+  }
+}
+
+static void enqueue_pcg_iters(Ctx &c, double *sol, int iters) {
+  const int n3 = 3 * c.nv, bs = 256;
+  const int nb_rows = div_up(c.nv, bs / 16), nb_vec = div_up(n3, bs);
+  for (int it = 0; it < iters; ++it) {
+    k_pcg_spmv<<<nb_rows, bs, 0, c.stream>>>(bsr_view(c), c.z, c.p, c.q, c.partial, c.counters + 3, c.scal);
+    k_pcg_update<<<nb_vec, bs, 0, c.stream>>>(n3, c.dinv, c.p, c.q, sol, c.r, c.z, c.partial,
+                                              c.counters + 4, c.scal);
+  }
+}
+
+void pcg_reset_graph(Ctx &c) {
+  if (c.pcg_graph) cudaGraphExecDestroy(c.pcg_graph);
+  c.pcg_graph = nullptr;
+  c.pcg_graph_iters = -1;
+}
+
+// Runs exactly `iters` PCG iterations on H sol = rhs (sol, rhs device vectors; sol must be c.df
+// when graphs are used, since the captured graph bakes in the pointer).
+void launch_pcg(Ctx &c, const double *rhs, double *sol, int iters) {
+  const int n3 = 3 * c.nv, bs = 256;
+  k_pcg_init<<<div_up(n3, bs), bs, 0, c.stream>>>(n3, rhs, c.dinv, sol, c.r, c.z, c.p, c.q, c.partial,
+                                                  c.counters + 2, c.scal);
+  c.launches++;
+  MS_CUDA(cudaGetLastError());
+  if (iters <= 0) return;
+  const bool graphs = c.params.use_graphs && sol == c.df.p;
+  if (!graphs) {
+    enqueue_pcg_iters(c, sol, iters);
+    c.launches += 2 * (int64_t)iters;
+    MS_CUDA(cudaGetLastError());
+    return;
+  }
+  if (c.pcg_graph_iters != iters || !c.pcg_graph) {
+    pcg_reset_graph(c);
+    cudaStream_t cap;
+    MS_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    cudaStream_t saved = c.stream;
+    c.stream = cap;
+    cudaGraph_t graph;
+    MS_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    enqueue_pcg_iters(c, sol, iters);
+    MS_CUDA(cudaStreamEndCapture(cap, &graph));
+    c.stream = saved;
+    MS_CUDA(cudaGraphInstantiate(&c.pcg_graph, graph, 0));
+    cudaGraphDestroy(graph);
+    cudaStreamDestroy(cap);
+    c.pcg_graph_iters = iters;
+    c.pcg_graph_kernels = 2 * (int64_t)iters;
+  }
+  MS_CUDA(cudaGraphLaunch(c.pcg_graph, c.stream));
+  c.launches += c.pcg_graph_kernels;
+}
+
+// ------------------------------------------------------------------ small vector kernels
+__global__ void k_axpby(int64_t n, double *__restrict__ y, double a, const double *__restrict__ x, double b) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = a * x[i] + b * y[i];
+}
+void launch_axpby(Ctx &c, double *y, double a, const double *x, double b, int64_t n) {
+  k_axpby<<<div_up(n, 256), 256, 0, c.stream>>>(n, y, a, x, b);
+  c.launches++;
+  MS_CUDA(cudaGetLastError());
+}
+
+__global__ void __launch_bounds__(256) k_dot(int64_t n, const double *__restrict__ a,
+                                             const double *__restrict__ b, double *__restrict__ partial,
+                                             unsigned int *counter, double *__restrict__ out) {
+  double acc[1] = {0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc[0] = fma(a[i], b[i], acc[0]);
+  double res[1];
+  if (grid_reduce<1>(acc, partial, counter, res) && threadIdx.x == 0) *out = res[0];
+}
+void launch_dot(Ctx &c, const double *a, const double *b, int64_t n, int slot) {
+  k_dot<<<std::min(div_up(n, 256), 1184), 256, 0, c.stream>>>(n, a, b, c.partial, c.counters + 5, c.scal + slot);
+  c.launches++;
+  MS_CUDA(cudaGetLastError());
+}
+
+// xhat = x^t + h v^t + h^2 g (R8); x^t = x; DBC vertices pinned at rest
+__global__ void k_predictor(int nv, const double *__restrict__ X, const uint8_t *__restrict__ fixed,
+                            double *__restrict__ x, const double *__restrict__ v, double *__restrict__ xt,
+                            double *__restrict__ xhat, double h, double g0, double g1, double g2) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nv) return;
+  const double gg[3] = {g0, g1, g2};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double xi = x[3 * i + k];
+    if (fixed[i]) xi = X[3 * i + k];
+    x[3 * i + k] = xi;
+    xt[3 * i + k] = xi;
+    xhat[3 * i + k] = xi + h * v[3 * i + k] + h * h * gg[k];
+  }
+}
+void launch_predictor(Ctx &c) {
+  k_predictor<<<div_up(c.nv, 256), 256, 0, c.stream>>>(c.nv, c.X, c.fixed, c.x, c.v, c.xt, c.xhat,
+                                                       c.params.h, c.params.gravity[0],
+                                                       c.params.gravity[1], c.params.gravity[2]);
+  c.launches++;
+  MS_CUDA(cudaGetLastError());
+}
+
+// v = (x - x^t) / h
+__global__ void k_velocity(int n3, const double *__restrict__ x, const double *__restrict__ xt,
+                           double *__restrict__ v, double inv_h) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n3) v[i] = (x[i] - xt[i]) * inv_h;
+}
+void launch_velocity(Ctx &c) {
+  const int n3 = 3 * c.nv;
+  k_velocity<<<div_up(n3, 256), 256, 0, c.stream>>>(n3, c.x, c.xt, c.v, 1.0 / c.params.h);
+  c.launches++;
+  MS_CUDA(cudaGetLastError());
+}
+
+}  // namespace msim
