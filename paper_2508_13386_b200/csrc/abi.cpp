@@ -240,6 +240,7 @@ ms_status ms_destroy(ms_ctx *ctx) {
   cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
   pcg_reset_graph(ctx->c);
+  coarse_reset_graphs(ctx->c);
   for (auto e : ctx->c.ev_pool) cudaEventDestroy(e);
   if (ctx->c.h_pinned) cudaFreeHost(ctx->c.h_pinned);
   delete ctx;
@@ -307,7 +308,10 @@ ms_status ms_set_params(ms_ctx *ctx, const ms_params *p) {
     MS_REQUIRE(p->filter_safety > 0.0 && p->filter_safety <= 1.0, MS_ERR_ARG, "bad filter safety");
     MS_REQUIRE(p->ls_batch == 1 || p->ls_batch == 2 || p->ls_batch == 4 || p->ls_batch == 8, MS_ERR_ARG,
                "ls_batch must be 1, 2, 4 or 8");
-    if (p->n_cg != ctx->c.params.n_cg || p->use_graphs != ctx->c.params.use_graphs) pcg_reset_graph(ctx->c);
+    if (p->n_cg != ctx->c.params.n_cg || p->use_graphs != ctx->c.params.use_graphs) {
+      pcg_reset_graph(ctx->c);
+      coarse_reset_graphs(ctx->c);
+    }
     ctx->c.params = *p;
   });
   return MS_OK;

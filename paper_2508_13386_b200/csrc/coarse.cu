@@ -281,14 +281,25 @@ static HView hview(const Ctx &c) { return HView{c.nnzb, c.rowptr, c.colidx, c.va
 // ------------------------------------------------------------------ dense envelope S
 // Lden column-major nS_pad x nS_pad; scatter lower part of S blocks; padding -> identity.
 __global__ void k_scatter_S(int64_t nblk, const int32_t *__restrict__ srow, const int32_t *__restrict__ scol,
-                            const double *__restrict__ S, int nSp, double *__restrict__ L) {
+                            const int32_t *__restrict__ perm, const double *__restrict__ S, int nSp,
+                            double *__restrict__ L) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nblk * 144) return;
   const int64_t b = t / 144;
   const int e = (int)(t % 144), row = e / 12, col = e % 12;
-  const int i = srow[b], j = scol[b];
+  const int i = perm[srow[b]], j = perm[scol[b]];
   const int R = 12 * i + row, C = 12 * j + col;
   if (R >= C) L[(size_t)C * nSp + R] = S[t];
+}
+
+// z_perm[12 perm[i] + r] = z[12 i + r]  (dir = 0);  z[12 i + r] = z_perm[12 perm[i] + r]  (dir = 1)
+__global__ void k_permute(int m, const int32_t *__restrict__ perm, const double *__restrict__ src,
+                          double *__restrict__ dst, int dir) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 12 * m) return;
+  const int i = t / 12, r = t % 12;
+  if (dir == 0) dst[12 * perm[i] + r] = src[t];
+  else dst[t] = src[12 * perm[i] + r];
 }
 
 __global__ void k_pad_identity(int nS, int nSp, double *__restrict__ L) {
@@ -442,9 +453,10 @@ __global__ void __launch_bounds__(128) k_fwd_tile(int k, const int32_t *__restri
   }
 }
 
-// backward step k: x_k = L_kk^-T y_k; CTA p >= 1 updates y_j -= L_kj^T x_k, j = rowlo(k) + p - 1
-__global__ void __launch_bounds__(128) k_bwd_tile(int k, int jlo, int nSp, const double *__restrict__ L,
-                                                  double *__restrict__ y, double *__restrict__ x) {
+// backward step k: x_k = L_kk^-T y_k; CTA p >= 1 updates y_j -= L_kj^T x_k, j = rows[p-1]
+__global__ void __launch_bounds__(128) k_bwd_tile(int k, const int32_t *__restrict__ rows, int nSp,
+                                                  const double *__restrict__ L, double *__restrict__ y,
+                                                  double *__restrict__ x) {
   __shared__ double xk[TB];
   const int t = threadIdx.x, lane = t & 31;
   const size_t bk = (size_t)(k * TB) * nSp + k * TB;
@@ -468,7 +480,7 @@ __global__ void __launch_bounds__(128) k_bwd_tile(int k, int jlo, int nSp, const
     if (t < TB) x[k * TB + t] = xk[t];
     return;
   }
-  const int j = jlo + blockIdx.x - 1;
+  const int j = rows[blockIdx.x - 1];
   // L_kj: rows k*TB.., cols j*TB..;  (L_kj^T x_k)[c] = sum_r L[kTB + r][jTB + c] x_k[r]
   if (t < TB) {
     const size_t bkj = (size_t)(j * TB + t) * nSp + k * TB;
@@ -529,15 +541,10 @@ void launch_coarse_S(Ctx &c) {
 constexpr size_t kTileSmem = sizeof(double) * 2 * TB * (TB + 1);
 
 static void enqueue_factor(Ctx &c) {
-  static bool attr = false;
-  if (!attr) {
-    MS_CUDA(cudaFuncSetAttribute(k_trsm_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
-    MS_CUDA(cudaFuncSetAttribute(k_update_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
-    attr = true;
-  }
   const int nSp = c.nS_pad;
   MS_CUDA(cudaMemsetAsync(c.Lden, 0, sizeof(double) * (size_t)nSp * nSp, c.stream));
-  k_scatter_S<<<div_up(c.nnzb_S * 144, 256), 256, 0, c.stream>>>(c.nnzb_S, c.srow, c.scol, c.Sblk, nSp, c.Lden);
+  k_scatter_S<<<div_up(c.nnzb_S * 144, 256), 256, 0, c.stream>>>(c.nnzb_S, c.srow, c.scol, c.perm, c.Sblk, nSp,
+                                                                  c.Lden);
   if (nSp > c.nS) k_pad_identity<<<div_up(nSp - c.nS, 64), 64, 0, c.stream>>>(c.nS, nSp, c.Lden);
   for (int k = 0; k < c.ntiles; ++k) {
     k_potrf_tile<<<1, 256, 0, c.stream>>>(k, nSp, c.Lden, c.flags + 0);
@@ -556,32 +563,82 @@ static int64_t factor_kernel_count(const Ctx &c) {
   return n;
 }
 
+// solve S q = z: z (handle order, c.zs) -> permuted (c.qs as b) -> forward (y in c.tmp2)
+// -> backward (x in c.qs) -> unpermute into c.zs.
+static void enqueue_solve(Ctx &c) {
+  const int nSp = c.nS_pad;
+  double *b = c.qs, *y = c.yp;
+  MS_CUDA(cudaMemsetAsync(b, 0, sizeof(double) * nSp, c.stream));
+  k_permute<<<div_up(12 * c.m, 256), 256, 0, c.stream>>>(c.m, c.perm, c.zs, b, 0);
+  for (int k = 0; k < c.ntiles; ++k) {
+    const int np = (int)c.h_chol_panel[k].size();
+    k_fwd_tile<<<1 + np, 128, 0, c.stream>>>(k, c.chol_panel + c.h_chol_panel_off[k], nSp, c.Lden, b, y);
+  }
+  for (int k = c.ntiles - 1; k >= 0; --k) {
+    const int nr = (int)(c.h_chol_rows_off[k + 1] - c.h_chol_rows_off[k]);
+    k_bwd_tile<<<1 + nr, 128, 0, c.stream>>>(k, c.chol_rows + c.h_chol_rows_off[k], nSp, c.Lden, y, b);
+  }
+  k_permute<<<div_up(12 * c.m, 256), 256, 0, c.stream>>>(c.m, c.perm, b, c.zs, 1);
+}
+
+static int64_t solve_kernel_count(const Ctx &c) { return 2 + 2 * (int64_t)c.ntiles; }
+
+static void ensure_attrs() {
+  static bool attr = false;
+  if (!attr) {
+    MS_CUDA(cudaFuncSetAttribute(k_trsm_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
+    MS_CUDA(cudaFuncSetAttribute(k_update_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
+    attr = true;
+  }
+}
+
+// Capture a fixed launch sequence once (pointers are fixed per basis) and replay it.
+template <typename F>
+static void run_captured(Ctx &c, cudaGraphExec_t &exec, F enqueue) {
+  if (!c.params.use_graphs) {
+    enqueue(c);
+    return;
+  }
+  if (!exec) {
+    cudaStream_t cap;
+    MS_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    cudaStream_t saved = c.stream;
+    c.stream = cap;
+    cudaGraph_t graph;
+    MS_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    enqueue(c);
+    MS_CUDA(cudaStreamEndCapture(cap, &graph));
+    c.stream = saved;
+    MS_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    cudaGraphDestroy(graph);
+    cudaStreamDestroy(cap);
+  }
+  MS_CUDA(cudaGraphLaunch(exec, c.stream));
+}
+
+void coarse_reset_graphs(Ctx &c) {
+  if (c.factor_graph) cudaGraphExecDestroy(c.factor_graph);
+  if (c.solve_graph) cudaGraphExecDestroy(c.solve_graph);
+  c.factor_graph = c.solve_graph = nullptr;
+}
+
 void launch_coarse_factor(Ctx &c) {
-  enqueue_factor(c);
+  ensure_attrs();
+  run_captured(c, c.factor_graph, enqueue_factor);
   c.launches += factor_kernel_count(c);
   MS_CUDA(cudaGetLastError());
 }
 
-// solve S qs = zs with the factor in Lden (zs is overwritten as work space)
-static void enqueue_solve(Ctx &c) {
-  const int nSp = c.nS_pad;
-  MS_CUDA(cudaMemsetAsync(c.zs + c.nS, 0, sizeof(double) * (nSp - c.nS), c.stream));
-  for (int k = 0; k < c.ntiles; ++k) {
-    const int np = (int)c.h_chol_panel[k].size();
-    k_fwd_tile<<<1 + np, 128, 0, c.stream>>>(k, c.chol_panel + c.h_chol_panel_off[k], nSp, c.Lden, c.zs, c.qs);
-  }
-  // qs now holds y; backward in place: y -> x (x written to zs, then copied)
-  for (int k = c.ntiles - 1; k >= 0; --k) {
-    const int jlo = c.h_tile_rowlo[k];
-    k_bwd_tile<<<1 + (k - jlo), 128, 0, c.stream>>>(k, jlo, nSp, c.Lden, c.qs, c.zs);
-  }
+void launch_coarse_solve(Ctx &c) {
+  run_captured(c, c.solve_graph, enqueue_solve);
+  c.launches += solve_kernel_count(c);
+  MS_CUDA(cudaGetLastError());
 }
 
 void launch_coarse_direction(Ctx &c) {
   const int n3 = 3 * c.nv;
   const double *o = c.aff_origin;
   // rhs = -g
-  MS_CUDA(cudaMemsetAsync(c.rhs, 0, sizeof(double) * n3, c.stream));
   launch_axpby(c, c.rhs, -1.0, c.g, 0.0, n3);
   // affine stage: za = U_a^T(-g); qa = Sa^-1 za; da = U_a qa
   k_restrict_affine<<<std::min(div_up(c.nv, 256), 592), 256, 0, c.stream>>>(
@@ -591,12 +648,9 @@ void launch_coarse_direction(Ctx &c) {
   c.launches += 3;
   // r1 = -g - H da
   launch_spmv(c, c.da, c.tmp, 0.0, c.rhs);
-  // SMS stage: zs = B^T r1; qs = S^-1 zs; ds = da + B qs
+  // SMS stage: zs = B^T r1; zs <- S^-1 zs; ds = da + B zs
   launch_restrict(c, c.tmp, c.zs);
-  enqueue_solve(c);
-  c.launches += 2 * c.ntiles;
-  MS_CUDA(cudaGetLastError());
-  // after enqueue_solve the solution x lives in zs
+  launch_coarse_solve(c);
   MS_CUDA(cudaMemcpyAsync(c.ds, c.da, sizeof(double) * n3, cudaMemcpyDeviceToDevice, c.stream));
   launch_lift(c, c.zs, c.ds, true);
   // r = -g - H ds

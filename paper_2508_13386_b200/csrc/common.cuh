@@ -148,16 +148,19 @@ struct Ctx {
   int32_t ntiles = 0;
   DBuf<double> Lden;                // [nS_pad * nS_pad] column-major lower factor
   int32_t nS_pad = 0;
-  std::vector<int32_t> h_tile_first;         // first nonzero tile row per tile col (envelope)
-  std::vector<int32_t> h_tile_rowlo;         // per tile row: lowest tile column with a nonzero
-  std::vector<std::vector<CholTask>> h_chol_updates;   // per k
   std::vector<std::vector<int32_t>> h_chol_panel;      // per k: tile rows i > k in struct
   DBuf<int32_t> chol_tasks;         // flattened per-k task lists
   std::vector<int64_t> h_chol_task_off;
   DBuf<int32_t> chol_panel;
   std::vector<int64_t> h_chol_panel_off;
-  DBuf<int32_t> band_lo;            // per DOF row: first nonzero column (envelope) [nS_pad]
-  DBuf<double> qa, qs, za, zs;      // coarse vectors
+  std::vector<int32_t> h_perm;      // handle -> position in the nested-dissection order
+  DBuf<int32_t> perm;
+  DBuf<int32_t> chol_rows;          // per tile k: tile columns j < k with L_kj != 0 (flattened)
+  std::vector<int64_t> h_chol_rows_off;
+  double chol_flops = 0.0;          // flops of one factorisation (tile granularity)
+  cudaGraphExec_t factor_graph = nullptr, solve_graph = nullptr;
+  int64_t factor_graph_kernels = 0, solve_graph_kernels = 0;
+  DBuf<double> qa, qs, za, zs, yp;  // coarse vectors (qs/yp: permuted work space)
   DBuf<int32_t> flags;              // [8]: 0 = chol not SPD (S), 1 = not SPD (Sa), 2 = infeasible
 
   // ---- scalars / reductions
@@ -209,7 +212,7 @@ enum {
 // pinned host mirror layout
 enum {
   PH_ENERGY = 0, PH_GNORM2, PH_DSNORM2, PH_ALPHA0, PH_INFEAS, PH_FLAG_S, PH_FLAG_SA,
-  PH_RZ0, PH_RZ, PH_LS = 16, PH_COUNT = 64
+  PH_RZ0, PH_RZ, PH_LS = 16, PH_COUNT = 128
 };
 
 // ---------------------------------------------------------------- launch helpers
@@ -229,6 +232,8 @@ void pcg_reset_graph(Ctx &c);
 void launch_coarse_S(Ctx &c);
 void launch_coarse_factor(Ctx &c);
 void launch_coarse_direction(Ctx &c);
+void launch_coarse_solve(Ctx &c);
+void coarse_reset_graphs(Ctx &c);
 void launch_lift(Ctx &c, const double *q, double *w, bool accumulate);
 void launch_restrict(Ctx &c, const double *y, double *z);
 void launch_filters(Ctx &c);

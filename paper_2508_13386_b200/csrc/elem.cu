@@ -98,9 +98,8 @@ __global__ void __launch_bounds__(256) k_elem_grad(MeshView M, const double *__r
                                                    double *__restrict__ out_energy,
                                                    double *__restrict__ infeas,
                                                    double *__restrict__ Ee) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
   double en[2] = {0.0, 0.0};
-  if (e < M.nt) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < M.nt; e += gridDim.x * blockDim.x) {
     TetKin k;
     load_tet_kin(M, x, e, k);
     const double J = det3(k.F);
@@ -132,7 +131,7 @@ __global__ void __launch_bounds__(256) k_elem_grad(MeshView M, const double *__r
 #pragma unroll
       for (int i = 0; i < 3; ++i) dst[3 * a + i] = g[a][i];
     const double psi = psi_snh(k.F, J, k.mu, k.lam);
-    en[0] = k.V * psi;
+    en[0] += k.V * psi;
     if (Ee) Ee[e] = (J > 0.0) ? k.V * psi : __longlong_as_double(0x7ff0000000000000ULL);
   }
   double res[2];
@@ -348,7 +347,7 @@ __global__ void k_expand_hess(int nt, const double *__restrict__ stage_h, double
 
 // ------------------------------------------------------------------ launchers
 void launch_elem_grad_to(Ctx &c, const double *x, double *Ee) {
-  const int bs = 256, nb = div_up(c.nt, bs);
+  const int bs = 256, nb = std::min(div_up(c.nt, bs), 148 * 8);
   k_elem_grad<<<nb, bs, 0, c.stream>>>(mesh_view(c), x, c.stage_g, c.partial, c.counters + 0,
                                        c.scal + SC_ENERGY_ELEM, c.scal + SC_INFEAS, Ee);
   c.launches++;

@@ -68,14 +68,27 @@ __device__ __forceinline__ bool grid_reduce(double (&v)[NV], double *partial, un
   __syncthreads();
   if (!last) return false;
   __threadfence();
-  // last block: fixed-order strided accumulation + fixed tree
+  // last block: fixed-order strided accumulation (4 independent chains for memory-level
+  // parallelism) + fixed tree
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    double s = OP == 0 ? 0.0 : 1e300;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
-      double pv = __ldcg(&partial[(size_t)k * gridDim.x + b]);
-      s = OP == 0 ? s + pv : fmin(s, pv);
+    const double init = OP == 0 ? 0.0 : 1e300;
+    double s4[4] = {init, init, init, init};
+    const double *pk = partial + (size_t)k * gridDim.x;
+    const int G = (int)gridDim.x, step = blockDim.x;
+    int b = threadIdx.x;
+    for (; b + 3 * step < G; b += 4 * step) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double pv = __ldcg(&pk[b + u * step]);
+        s4[u] = OP == 0 ? s4[u] + pv : fmin(s4[u], pv);
+      }
     }
+    for (; b < G; b += step) {
+      const double pv = __ldcg(&pk[b]);
+      s4[0] = OP == 0 ? s4[0] + pv : fmin(s4[0], pv);
+    }
+    double s = OP == 0 ? (s4[0] + s4[1]) + (s4[2] + s4[3]) : fmin(fmin(s4[0], s4[1]), fmin(s4[2], s4[3]));
     s = OP == 0 ? warp_sum(s) : warp_min(s);
     if (lane == 0) sh[k * 32 + wid] = s;
   }

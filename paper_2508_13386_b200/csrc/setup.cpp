@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <numeric>
 
 #include "common.cuh"
@@ -186,7 +187,8 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
       MS_REQUIRE(phi[k] > 0.0, MS_ERR_ARG, "phi entries must be > 0");
       sum += phi[k];
     }
-    MS_REQUIRE(sum > 0.0 || c.h_fixed[v], MS_ERR_COVERAGE,
+    // POU: sum phi + phi_DBC = 1 with phi_DBC = 1 - phi_affine; a hole is sum phi = phi_DBC = 0
+    MS_REQUIRE(sum > 0.0 || c.h_fixed[v] || phi_aff[v] < 1.0, MS_ERR_COVERAGE,
                "basis coverage hole: no handle covers a free vertex");
   }
   c.m = m;
@@ -265,43 +267,100 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   c.nnzb_S = (int64_t)scol.size();
   c.n_R = (int64_t)Ri.size();
 
-  // ---- tile envelope of S (symmetric; handles ordered by x so the profile is banded)
+  // ---- fill-reducing order of the handles: geometric nested dissection on the coupling graph
+  // (one-sided vertex separators from recursive median bisection of the handle origins).
+  std::vector<int32_t> order;
+  order.reserve(m);
+  {
+    std::vector<char> side(m, 0);
+    std::vector<int32_t> all(m);
+    std::iota(all.begin(), all.end(), 0);
+    struct Rec { std::vector<int32_t> h; };
+    std::function<void(std::vector<int32_t> &)> nd = [&](std::vector<int32_t> &H) {
+      if (H.size() <= 8) {
+        order.insert(order.end(), H.begin(), H.end());
+        return;
+      }
+      double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+      for (int32_t h : H)
+        for (int d = 0; d < 3; ++d) {
+          lo[d] = std::min(lo[d], origins[3 * h + d]);
+          hi[d] = std::max(hi[d], origins[3 * h + d]);
+        }
+      int ax = 0;
+      for (int d = 1; d < 3; ++d)
+        if (hi[d] - lo[d] > hi[ax] - lo[ax]) ax = d;
+      std::stable_sort(H.begin(), H.end(), [&](int32_t a, int32_t b) {
+        return origins[3 * a + ax] < origins[3 * b + ax];
+      });
+      const size_t half = H.size() / 2;
+      for (size_t q = 0; q < H.size(); ++q) side[H[q]] = q < half ? 1 : 2;
+      std::vector<int32_t> A(H.begin(), H.begin() + half), B, Sep;
+      for (size_t q = half; q < H.size(); ++q) {
+        const int32_t b = H[q];
+        bool touches = false;
+        for (int32_t k = sptr[b]; k < sptr[b + 1] && !touches; ++k) touches = side[scol[k]] == 1;
+        (touches ? Sep : B).push_back(b);
+      }
+      for (int32_t h : H) side[h] = 0;
+      if (B.empty()) {   // no separation possible: keep as one dense block
+        order.insert(order.end(), H.begin(), H.end());
+        return;
+      }
+      nd(A);
+      nd(B);
+      order.insert(order.end(), Sep.begin(), Sep.end());
+    };
+    nd(all);
+  }
+  c.h_perm.assign(m, 0);
+  for (int32_t p = 0; p < m; ++p) c.h_perm[order[p]] = p;
+
+  // ---- tile-level symbolic Cholesky of S in the permuted order
   c.nS = 12 * m;
   c.tile = 64;
   c.ntiles = div_up(c.nS, c.tile);
   c.nS_pad = c.ntiles * c.tile;
-  std::vector<int32_t> band_lo(c.nS_pad);
-  for (int32_t i = 0; i < m; ++i) {
-    int32_t jmin = i;
-    for (int32_t k = sptr[i]; k < sptr[i + 1]; ++k) jmin = std::min(jmin, scol[k]);
-    for (int r = 0; r < 12; ++r) band_lo[12 * i + r] = 12 * jmin;
-  }
-  for (int32_t r = c.nS; r < c.nS_pad; ++r) band_lo[r] = r;   // padding: identity rows
   const int T = c.tile, NT = c.ntiles;
-  c.h_tile_rowlo.assign(NT, 0);
-  for (int32_t ti = 0; ti < NT; ++ti) {
-    int32_t lo = ti;
-    for (int r = ti * T; r < (ti + 1) * T; ++r) lo = std::min(lo, band_lo[r] / T);
-    c.h_tile_rowlo[ti] = lo;
-  }
-  // fill stays inside the envelope: L_ik != 0 iff rowlo(i) <= k
+  std::vector<std::vector<char>> nz(NT, std::vector<char>(NT, 0));
+  for (int32_t t = 0; t < NT; ++t) nz[t][t] = 1;
+  for (int32_t i = 0; i < m; ++i)
+    for (int32_t k = sptr[i]; k < sptr[i + 1]; ++k) {
+      const int32_t pi = c.h_perm[i], pj = c.h_perm[scol[k]];
+      const int32_t r0 = 12 * pi / T, r1 = (12 * pi + 11) / T, c0 = 12 * pj / T, c1 = (12 * pj + 11) / T;
+      for (int32_t a = r0; a <= r1; ++a)
+        for (int32_t b = c0; b <= c1; ++b)
+          if (a >= b) nz[a][b] = 1;
+    }
   c.h_chol_panel.assign(NT, {});
-  c.h_chol_updates.assign(NT, {});
-  std::vector<int32_t> panel_flat, task_flat;
-  c.h_chol_panel_off.assign(NT + 1, 0);
-  c.h_chol_task_off.assign(NT + 1, 0);
+  std::vector<std::vector<int32_t>> rows(NT);
   for (int32_t k = 0; k < NT; ++k) {
     auto &P = c.h_chol_panel[k];
     for (int32_t i = k + 1; i < NT; ++i)
-      if (c.h_tile_rowlo[i] <= k) P.push_back(i);
+      if (nz[i][k]) P.push_back(i);
+    for (size_t a = 0; a < P.size(); ++a)       // fill: (P[a], P[b]) becomes nonzero
+      for (size_t b = 0; b <= a; ++b) nz[P[a]][P[b]] = 1;
+    for (int32_t i : P) rows[i].push_back(k);
+  }
+  std::vector<int32_t> panel_flat, task_flat, rows_flat;
+  c.h_chol_panel_off.assign(NT + 1, 0);
+  c.h_chol_task_off.assign(NT + 1, 0);
+  c.h_chol_rows_off.assign(NT + 1, 0);
+  c.chol_flops = 0.0;
+  for (int32_t k = 0; k < NT; ++k) {
+    const auto &P = c.h_chol_panel[k];
     for (size_t a = 0; a < P.size(); ++a)
       for (size_t b = 0; b <= a; ++b) {
         task_flat.push_back(P[a]);
         task_flat.push_back(P[b]);
       }
     panel_flat.insert(panel_flat.end(), P.begin(), P.end());
+    rows_flat.insert(rows_flat.end(), rows[k].begin(), rows[k].end());
     c.h_chol_panel_off[k + 1] = (int64_t)panel_flat.size();
     c.h_chol_task_off[k + 1] = (int64_t)task_flat.size() / 2;
+    c.h_chol_rows_off[k + 1] = (int64_t)rows_flat.size();
+    const double np = (double)P.size();
+    c.chol_flops += (double)T * T * T / 3.0 + np * T * T * T + np * (np + 1) / 2 * 2.0 * T * T * T;
   }
 
   cudaStream_t s = c.stream;
@@ -332,13 +391,16 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   c.Sa.alloc(144);
   c.Ra.alloc((size_t)36 * nv);
   c.Lden.alloc((size_t)c.nS_pad * c.nS_pad);
-  c.band_lo.upload(band_lo, s);
+  c.perm.upload(c.h_perm, s);
+  c.chol_rows.upload(rows_flat.empty() ? std::vector<int32_t>{0} : rows_flat, s);
   c.chol_panel.upload(panel_flat.empty() ? std::vector<int32_t>{0} : panel_flat, s);
   c.chol_tasks.upload(task_flat.empty() ? std::vector<int32_t>{0, 0} : task_flat, s);
   c.qa.alloc(12);
   c.za.alloc(12);
   c.qs.alloc(c.nS_pad);
   c.zs.alloc(c.nS_pad);
+  c.yp.alloc(c.nS_pad);
+  coarse_reset_graphs(c);
   MS_CUDA(cudaStreamSynchronize(s));
 }
 

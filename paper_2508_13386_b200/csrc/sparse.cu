@@ -48,9 +48,8 @@ __global__ void __launch_bounds__(256) k_vertex_grad(
     const double *__restrict__ mass, const uint8_t *__restrict__ fixed, Ground G, double h2,
     double *__restrict__ g, double *__restrict__ partial, unsigned int *__restrict__ counter,
     double *__restrict__ out /* [energy, |g|^2, infeasible] */) {
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
   double acc[3] = {0.0, 0.0, 0.0};
-  if (v < nv) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
     double ge[3] = {0.0, 0.0, 0.0};
     for (int k = vptr[v]; k < vptr[v + 1]; ++k) {
       const int code = vinc[k];
@@ -72,7 +71,7 @@ __global__ void __launch_bounds__(256) k_vertex_grad(
       e = 0.5 * m * (r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
       if (G.on) {
         const double d = G.n0 * x[3 * v] + G.n1 * x[3 * v + 1] + G.n2 * x[3 * v + 2] - G.off;
-        if (!(d > 0.0)) acc[2] = 1.0;
+        if (!(d > 0.0)) acc[2] += 1.0;
         const double b1 = h2 * G.kappa * bar_d1(d, G.dhat);
         out3[0] += b1 * G.n0;
         out3[1] += b1 * G.n1;
@@ -84,8 +83,8 @@ __global__ void __launch_bounds__(256) k_vertex_grad(
     }
 #pragma unroll
     for (int i = 0; i < 3; ++i) g[3 * v + i] = out3[i];
-    acc[0] = e;
-    acc[1] = out3[0] * out3[0] + out3[1] * out3[1] + out3[2] * out3[2];
+    acc[0] += e;
+    acc[1] += out3[0] * out3[0] + out3[1] * out3[1] + out3[2] * out3[2];
   }
   double res[3];
   if (grid_reduce<3>(acc, partial, counter, res) && threadIdx.x == 0) {
@@ -96,7 +95,7 @@ __global__ void __launch_bounds__(256) k_vertex_grad(
 }
 
 void launch_vertex_grad(Ctx &c) {
-  const int bs = 256, nb = div_up(c.nv, bs);
+  const int bs = 256, nb = std::min(div_up(c.nv, bs), 148 * 8);
   const double h2 = c.params.h * c.params.h;
   k_vertex_grad<<<nb, bs, 0, c.stream>>>(c.nv, c.vinc_ptr, c.vinc, c.stage_g, c.x, c.xhat, c.mass,
                                          c.fixed, ground_of(c), h2, c.g, c.partial, c.counters + 1,
@@ -241,22 +240,23 @@ void launch_spmv(Ctx &c, const double *xin, double *yout, double /*unused*/, con
 // iter:   K1: p = z + beta p ; q = H z + beta q ; pq = p.q ; alpha = rho / pq
 //         K2: x += alpha p ; r -= alpha q ; z = D^-1 r ; rho' = r.z ; beta = rho'/rho ; rho = rho'
 // (q = H(z + beta p_old) = H z + beta H p_old, so the direction update needs no extra pass.)
+constexpr int kGridCap = 148 * 8;   // persistent-style grids: a few CTAs per SM, grid-stride loops
+
 __global__ void __launch_bounds__(256) k_pcg_init(int n3, const double *__restrict__ rhs,
                                                   const double *__restrict__ dinv, double *__restrict__ x,
                                                   double *__restrict__ r, double *__restrict__ z,
                                                   double *__restrict__ p, double *__restrict__ q,
                                                   double *__restrict__ partial, unsigned int *counter,
                                                   double *__restrict__ scal) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   double acc[1] = {0.0};
-  if (i < n3) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n3; i += gridDim.x * blockDim.x) {
     const double ri = rhs[i], zi = dinv[i] * ri;
     x[i] = 0.0;
     r[i] = ri;
     z[i] = zi;
     p[i] = 0.0;
     q[i] = 0.0;
-    acc[0] = ri * zi;
+    acc[0] = fma(ri, zi, acc[0]);
   }
   double res[1];
   if (grid_reduce<1>(acc, partial, counter, res) && threadIdx.x == 0) {
@@ -266,28 +266,30 @@ __global__ void __launch_bounds__(256) k_pcg_init(int n3, const double *__restri
   }
 }
 
+// half-warp per row, grid-stride over rows; both half-warps of a warp run the same trip count
+// (the shuffles in row_product need the full warp)
 __global__ void __launch_bounds__(256) k_pcg_spmv(BSRView H, const double *__restrict__ z,
                                                   double *__restrict__ p, double *__restrict__ q,
                                                   double *__restrict__ partial, unsigned int *counter,
                                                   double *__restrict__ scal) {
-  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
   const int sub = threadIdx.x & 15;
+  const int hw = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
+  const int hw_stride = (gridDim.x * blockDim.x) >> 4;
   const double beta = scal[SC_BETA];
-  double o[3] = {0.0, 0.0, 0.0};
   double acc[1] = {0.0};
-  row_product(H, row, sub, z, o);
-  if (row < H.nv) {
-    if (sub == 0) {
-      double pq = 0.0;
+  for (int base = hw & ~1; base < H.nv; base += hw_stride) {
+    const int row = base + (hw & 1);
+    double o[3] = {0.0, 0.0, 0.0};
+    row_product(H, row, sub, z, o);
+    if (row < H.nv && sub == 0) {
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
         const double pn = fma(beta, p[3 * row + i], z[3 * row + i]);
         const double qn = fma(beta, q[3 * row + i], o[i]);
         p[3 * row + i] = pn;
         q[3 * row + i] = qn;
-        pq = fma(pn, qn, pq);
+        acc[0] = fma(pn, qn, acc[0]);
       }
-      acc[0] = pq;
     }
   }
   double res[1];
@@ -303,16 +305,15 @@ __global__ void __launch_bounds__(256) k_pcg_update(int n3, const double *__rest
                                                     double *__restrict__ x, double *__restrict__ r,
                                                     double *__restrict__ z, double *__restrict__ partial,
                                                     unsigned int *counter, double *__restrict__ scal) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const double alpha = scal[SC_ALPHA];
   double acc[1] = {0.0};
-  if (i < n3) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n3; i += gridDim.x * blockDim.x) {
     x[i] = fma(alpha, p[i], x[i]);
     const double ri = fma(-alpha, q[i], r[i]);
     const double zi = dinv[i] * ri;
     r[i] = ri;
     z[i] = zi;
-    acc[0] = ri * zi;
+    acc[0] = fma(ri, zi, acc[0]);
   }
   double res[1];
   if (grid_reduce<1>(acc, partial, counter, res) && threadIdx.x == 0) {
@@ -322,13 +323,15 @@ __global__ void __launch_bounds__(256) k_pcg_update(int n3, const double *__rest
   }
 }
 
+static int grid_rows(const Ctx &c) { return std::min(div_up(c.nv, 16), kGridCap); }
+static int grid_vec(int64_t n) { return std::min(div_up(n, 256), kGridCap); }
+
 static void enqueue_pcg_iters(Ctx &c, double *sol, int iters) {
   const int n3 = 3 * c.nv, bs = 256;
-  const int nb_rows = div_up(c.nv, bs / 16), nb_vec = div_up(n3, bs);
   for (int it = 0; it < iters; ++it) {
-    k_pcg_spmv<<<nb_rows, bs, 0, c.stream>>>(bsr_view(c), c.z, c.p, c.q, c.partial, c.counters + 3, c.scal);
-    k_pcg_update<<<nb_vec, bs, 0, c.stream>>>(n3, c.dinv, c.p, c.q, sol, c.r, c.z, c.partial,
-                                              c.counters + 4, c.scal);
+    k_pcg_spmv<<<grid_rows(c), bs, 0, c.stream>>>(bsr_view(c), c.z, c.p, c.q, c.partial, c.counters + 3, c.scal);
+    k_pcg_update<<<grid_vec(n3), bs, 0, c.stream>>>(n3, c.dinv, c.p, c.q, sol, c.r, c.z, c.partial,
+                                                    c.counters + 4, c.scal);
   }
 }
 
@@ -342,7 +345,7 @@ void pcg_reset_graph(Ctx &c) {
 // when graphs are used, since the captured graph bakes in the pointer).
 void launch_pcg(Ctx &c, const double *rhs, double *sol, int iters) {
   const int n3 = 3 * c.nv, bs = 256;
-  k_pcg_init<<<div_up(n3, bs), bs, 0, c.stream>>>(n3, rhs, c.dinv, sol, c.r, c.z, c.p, c.q, c.partial,
+  k_pcg_init<<<grid_vec(n3), bs, 0, c.stream>>>(n3, rhs, c.dinv, sol, c.r, c.z, c.p, c.q, c.partial,
                                                   c.counters + 2, c.scal);
   c.launches++;
   MS_CUDA(cudaGetLastError());
