@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libmsim.so")
-SOURCES = ["elem.cu", "sparse.cu", "coarse.cu", "ls.cu", "setup.cpp", "abi.cpp"]
+SOURCES = ["elem.cu", "sparse.cu", "coarse.cu", "chol.cu", "ls.cu", "setup.cpp", "abi.cpp"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC,-O2", "-shared"]
 

@@ -1,0 +1,416 @@
+// Coarse factorisation S = L L^T and the triangular solves (
+// reading R4: exact coarse solves).
+//
+// Layout: S (12m x 12m, handles in the cheaper of x-sorted / nested-dissection order, chosen at
+// ms_basis_upload) is held in a padded dense column-major array; only the tiles of the
+// symbolic factor (64 x 64 tiles) are touched.  Right-looking tile algorithm, three launches per
+// tile column k (captured once in a CUDA graph and replayed):
+//   D(k): one CTA factorises the diagonal tile (blocked, 16-column panels: warp-level panel
+//         factorisation in registers + block-wide trailing update) and inverts it, storing L_kk
+//         and U_kk = L_kk^-T;
+//   P(k): one CTA per panel tile: L_ik = A_ik U_kk (64^3 GEMM, cp.async staging, 4x4 registers);
+//   U(k): one CTA per trailing tile: A_ij -= L_ik L_jk^T.
+// The forward / backward solves are single cooperative launches: each CTA owns tile rows, waits
+// on per-tile ready flags of the tiles it depends on and applies U_kk as a GEMV.
+#include <cooperative_groups.h>
+#include <cuda_pipeline.h>
+
+#include "common.cuh"
+
+namespace msim {
+
+constexpr int TB = 64;
+constexpr int LD = TB + 1;
+
+__device__ __forceinline__ size_t tile_off(int ti, int tj, int nSp) {
+  return (size_t)(tj * TB) * nSp + (size_t)ti * TB;
+}
+
+// ------------------------------------------------------------------ D(k): potrf + inverse
+__global__ void __launch_bounds__(256) k_chol_diag(int k, int nSp, double *__restrict__ L,
+                                                   double *__restrict__ U, int *__restrict__ flag) {
+  extern __shared__ double sm[];
+  double *A = sm;              // row-major [64][LD]: the factor
+  double *Li = sm + TB * LD;   // row-major [64][LD]: its inverse
+  const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+  const size_t okk = tile_off(k, k, nSp);
+  {
+    double v[16];
+#pragma unroll
+    for (int it = 0; it < 16; ++it) {
+      const int e = t + it * 256;
+      v[it] = L[okk + (size_t)(e >> 6) * nSp + (e & 63)];
+    }
+#pragma unroll
+    for (int it = 0; it < 16; ++it) {
+      const int e = t + it * 256, r = e & 63, c = e >> 6;
+      A[r * LD + c] = r >= c ? v[it] : 0.0;
+      Li[r * LD + c] = 0.0;
+    }
+  }
+  __syncthreads();
+  bool bad = false;
+  for (int p = 0; p < 4; ++p) {
+    const int j0 = 16 * p;
+    if (w == 0) {
+      // panel rows j0 + lane and j0 + 32 + lane, columns j0 .. j0+15
+      const int ra = j0 + lane, rb = j0 + 32 + lane;
+      const bool va = ra < TB, vb = rb < TB;
+      double a[16], b[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        a[c] = va ? A[ra * LD + j0 + c] : 0.0;
+        b[c] = vb ? A[rb * LD + j0 + c] : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const double d = __shfl_sync(0xffffffffu, a[j], j);
+        if (!(d > 0.0)) bad = true;
+        const double ljj = d > 0.0 ? sqrt(d) : 1.0;
+        const double inv = 1.0 / ljj;
+        a[j] = lane == j ? ljj : (lane > j ? a[j] * inv : a[j]);
+        b[j] *= inv;
+#pragma unroll
+        for (int c = j + 1; c < 16; ++c) {
+          const double lc = __shfl_sync(0xffffffffu, a[j], c);
+          a[c] = fma(-a[j], lc, a[c]);
+          b[c] = fma(-b[j], lc, b[c]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        if (va && ra >= j0 + c) A[ra * LD + j0 + c] = a[c];
+        if (vb) A[rb * LD + j0 + c] = b[c];
+      }
+    }
+    __syncthreads();
+    // trailing update of rows/cols >= j0 + 16
+    const int s0 = j0 + 16;
+    for (int r = s0 + (t >> 2); r < TB; r += 64) {
+      for (int c = s0 + (t & 3); c <= r; c += 4) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) s = fma(A[r * LD + j0 + j], A[c * LD + j0 + j], s);
+        A[r * LD + c] -= s;
+      }
+    }
+    __syncthreads();
+  }
+  if (w == 0 && lane == 0 && bad && flag) *flag = 1;
+  // inverse: diagonal 16x16 blocks (warp p, lane l < 16 solves column l)
+  if (w < 4 && lane < 16) {
+    const int o = 16 * w;
+    double x[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      double s = r == lane ? 1.0 : 0.0;
+#pragma unroll
+      for (int q = 0; q < r; ++q) s = fma(-A[(o + r) * LD + o + q], x[q], s);
+      x[r] = s / A[(o + r) * LD + o + r];
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) Li[(o + r) * LD + o + lane] = x[r];
+  }
+  __syncthreads();
+  // off-diagonal blocks: Li_pq = -Li_pp sum_{s=q}^{p-1} L_ps Li_sq, p = 1..3
+  __shared__ double Tb[3][16][17];
+  for (int p = 1; p < 4; ++p) {
+    for (int e = t; e < p * 256; e += 256) {
+      const int q = e >> 8, r = (e >> 4) & 15, cc = e & 15;
+      double s = 0.0;
+      for (int m = 16 * q; m < 16 * p; ++m) s = fma(A[(16 * p + r) * LD + m], Li[m * LD + 16 * q + cc], s);
+      Tb[q][r][cc] = s;
+    }
+    __syncthreads();
+    for (int e = t; e < p * 256; e += 256) {
+      const int q = e >> 8, r = (e >> 4) & 15, cc = e & 15;
+      double s = 0.0;
+#pragma unroll
+      for (int m = 0; m < 16; ++m) s = fma(Li[(16 * p + r) * LD + 16 * p + m], Tb[q][m][cc], s);
+      Li[(16 * p + r) * LD + 16 * q + cc] = -s;
+    }
+    __syncthreads();
+  }
+  // store L_kk (lower, column-major) and U_kk = Li^T (row-major: U[r][c] at r*64 + c = Li[c][r])
+  double *Uk = U + (size_t)k * TB * TB;
+#pragma unroll 4
+  for (int it = 0; it < 16; ++it) {
+    const int e = t + it * 256, r = e & 63, c = e >> 6;
+    if (r >= c) L[okk + (size_t)c * nSp + r] = A[r * LD + c];
+    Uk[(size_t)c * TB + r] = Li[r * LD + c];   // U[c][r] = Li[r][c]
+  }
+}
+
+// ------------------------------------------------------------------ 64^3 tile GEMM core
+// acc[a][b] = sum_kk S1[kk*64 + tr + a] * S2[kk*64 + tc + b]
+__device__ __forceinline__ void gemm64(const double *S1, const double *S2, double (&acc)[4][4], int tr, int tc) {
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+#pragma unroll 4
+  for (int kk = 0; kk < TB; ++kk) {
+    const double2 x01 = *reinterpret_cast<const double2 *>(&S1[kk * TB + tr]);
+    const double2 x23 = *reinterpret_cast<const double2 *>(&S1[kk * TB + tr + 2]);
+    const double2 y01 = *reinterpret_cast<const double2 *>(&S2[kk * TB + tc]);
+    const double2 y23 = *reinterpret_cast<const double2 *>(&S2[kk * TB + tc + 2]);
+    const double x[4] = {x01.x, x01.y, x23.x, x23.y}, y[4] = {y01.x, y01.y, y23.x, y23.y};
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = fma(x[a], y[b], acc[a][b]);
+  }
+}
+
+// stage a column-major global tile (leading dim nSp) into k-major smem S[kk*64 + r] (cp.async)
+__device__ __forceinline__ void stage_colmajor(double *S, const double *__restrict__ G, int ld) {
+#pragma unroll
+  for (int it = 0; it < (TB * TB / 2) / 256; ++it) {
+    const int e2 = threadIdx.x + it * 256, kk = e2 >> 5, r2 = (e2 & 31) * 2;
+    __pipeline_memcpy_async(&S[kk * TB + r2], &G[(size_t)kk * ld + r2], 16);
+  }
+}
+
+// ------------------------------------------------------------------ P(k): L_ik = A_ik U_kk
+__global__ void __launch_bounds__(256) k_chol_trsm(int k, const int32_t *__restrict__ panel, int nSp,
+                                                   double *__restrict__ L, const double *__restrict__ U) {
+  extern __shared__ double sm[];
+  double *SA = sm, *SU = sm + TB * TB;   // SA[kk*64 + r] = A_ik[r][kk]; SU[kk*64 + c] = U[kk][c]
+  const int i = panel[blockIdx.x], t = threadIdx.x;
+  const size_t oik = tile_off(i, k, nSp);
+  stage_colmajor(SA, L + oik, nSp);
+  stage_colmajor(SU, U + (size_t)k * TB * TB, TB);   // row-major U == k-major operand
+  __pipeline_commit();
+  __pipeline_wait_prior(0);
+  __syncthreads();
+  const int tr = (t & 15) * 4, tc = (t >> 4) * 4;
+  double acc[4][4];
+  gemm64(SA, SU, acc, tr, tc);
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+#pragma unroll
+    for (int a = 0; a < 4; ++a) L[oik + (size_t)(tc + b) * nSp + tr + a] = acc[a][b];
+}
+
+// ------------------------------------------------------------------ U(k): A_ij -= L_ik L_jk^T
+__global__ void __launch_bounds__(256) k_chol_update(int k, const int32_t *__restrict__ tasks, int nSp,
+                                                     double *__restrict__ L) {
+  extern __shared__ double sm[];
+  double *Si = sm, *Sj = sm + TB * TB;
+  const int i = tasks[2 * blockIdx.x], j = tasks[2 * blockIdx.x + 1], t = threadIdx.x;
+  stage_colmajor(Si, L + tile_off(i, k, nSp), nSp);
+  stage_colmajor(Sj, L + tile_off(j, k, nSp), nSp);
+  __pipeline_commit();
+  const int tr = (t & 15) * 4, tc = (t >> 4) * 4;
+  const size_t oij = tile_off(i, j, nSp);
+  double old[4][4];
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+#pragma unroll
+    for (int a = 0; a < 4; ++a) old[a][b] = L[oij + (size_t)(tc + b) * nSp + tr + a];
+  __pipeline_wait_prior(0);
+  __syncthreads();
+  double acc[4][4];
+  gemm64(Si, Sj, acc, tr, tc);
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int r = tr + a, c = tc + b;
+      if (i != j || r >= c) L[oij + (size_t)c * nSp + r] = old[a][b] - acc[a][b];
+    }
+}
+
+__global__ void __launch_bounds__(256) k_zero_tiles(const int32_t *__restrict__ tiles, int nSp, double *__restrict__ L) {
+  const int ti = tiles[2 * blockIdx.x], tj = tiles[2 * blockIdx.x + 1];
+  const size_t off = tile_off(ti, tj, nSp);
+#pragma unroll
+  for (int it = 0; it < 16; ++it) {
+    const int e = threadIdx.x + it * 256;
+    L[off + (size_t)(e >> 6) * nSp + (e & 63)] = 0.0;
+  }
+}
+
+__global__ void k_pad_identity2(int nS, int nSp, double *__restrict__ L) {
+  const int r = nS + blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < nSp) L[(size_t)r * nSp + r] = 1.0;
+}
+
+// z_perm[12 perm[i] + r] = z[12 i + r]  (dir = 0);  z[12 i + r] = z_perm[12 perm[i] + r]  (dir = 1)
+__global__ void k_permute2(int m, const int32_t *__restrict__ perm, const double *__restrict__ src,
+                           double *__restrict__ dst, int dir) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 12 * m) return;
+  const int i = t / 12, r = t % 12;
+  if (dir == 0) dst[12 * perm[i] + r] = src[t];
+  else dst[t] = src[12 * perm[i] + r];
+}
+
+// ------------------------------------------------------------------ cooperative solves
+__device__ __forceinline__ void wait_flag(const int *flags, int idx) {
+  if (threadIdx.x == 0) {
+    const volatile int *f = flags + idx;
+    while (*f == 0) __nanosleep(32);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void set_flag(int *flags, int idx) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicExch(flags + idx, 1);
+  }
+}
+
+// forward: y_k = L_kk^-1 (b_k - sum_{j in rows(k)} L_kj y_j); tiles owned round-robin by CTAs
+__global__ void __launch_bounds__(256) k_chol_fwd(int NT, const int32_t *__restrict__ rows_ptr,
+                                                  const int32_t *__restrict__ rows, int nSp,
+                                                  const double *__restrict__ L, const double *__restrict__ U,
+                                                  const double *__restrict__ b, double *__restrict__ y,
+                                                  int *__restrict__ flags) {
+  __shared__ double yj[TB];
+  __shared__ double part[4][TB];
+  const int t = threadIdx.x, r = t & 63, q = t >> 6;
+  for (int k = blockIdx.x; k < NT; k += gridDim.x) {
+    double acc = 0.0;
+    for (int p = rows_ptr[k]; p < rows_ptr[k + 1]; ++p) {
+      const int j = rows[p];
+      const double *Lkj = L + tile_off(k, j, nSp) + (size_t)(q * 16) * nSp + r;
+      double lv[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) lv[c] = Lkj[(size_t)c * nSp];   // prefetch before the wait
+      wait_flag(flags, j);
+      if (t < TB) yj[t] = __ldcg(&y[j * TB + t]);
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < 16; ++c) acc = fma(lv[c], yj[q * 16 + c], acc);
+      __syncthreads();
+    }
+    part[q][r] = acc;
+    __syncthreads();
+    if (t < TB) yj[t] = b[k * TB + t] - ((part[0][t] + part[1][t]) + (part[2][t] + part[3][t]));
+    __syncthreads();
+    // y_k[r] = sum_c Linv[r][c] v[c] = sum_c U[c][r] v[c]  (U row-major: U[c][r] at c*64 + r)
+    const double *Uk = U + (size_t)k * TB * TB;
+    double s = 0.0;
+#pragma unroll
+    for (int c = q * 16; c < q * 16 + 16; ++c) s = fma(Uk[(size_t)c * TB + r], yj[c], s);
+    part[q][r] = s;
+    __syncthreads();
+    if (t < TB) y[k * TB + t] = (part[0][t] + part[1][t]) + (part[2][t] + part[3][t]);
+    set_flag(flags, k);
+  }
+}
+
+// backward: x_k = U_kk (y_k - sum_{i in panel(k)} L_ik^T x_i), tiles owned round-robin from the end
+__global__ void __launch_bounds__(256) k_chol_bwd(int NT, const int32_t *__restrict__ pan_ptr,
+                                                  const int32_t *__restrict__ panel, int nSp,
+                                                  const double *__restrict__ L, const double *__restrict__ U,
+                                                  const double *__restrict__ y, double *__restrict__ x,
+                                                  int *__restrict__ flags) {
+  __shared__ double xi[TB];
+  __shared__ double part[4][TB];
+  const int t = threadIdx.x, cidx = t >> 2, q = t & 3;
+  for (int s = blockIdx.x; s < NT; s += gridDim.x) {
+    const int k = NT - 1 - s;
+    double acc = 0.0;   // thread (c = cidx, q): rows 16q..16q+15 of column c
+    // largest i first (ready first in the backward sweep); operand prefetched before the wait
+    for (int p = pan_ptr[k + 1] - 1; p >= pan_ptr[k]; --p) {
+      const int i = panel[p];
+      const double *Lik = L + tile_off(i, k, nSp) + (size_t)cidx * nSp + q * 16;
+      double lv[16];
+#pragma unroll
+      for (int rr = 0; rr < 16; ++rr) lv[rr] = Lik[rr];
+      wait_flag(flags, i);
+      if (t < TB) xi[t] = __ldcg(&x[i * TB + t]);
+      __syncthreads();
+#pragma unroll
+      for (int rr = 0; rr < 16; ++rr) acc = fma(lv[rr], xi[q * 16 + rr], acc);
+      __syncthreads();
+    }
+    part[q][cidx] = acc;
+    __syncthreads();
+    if (t < TB) xi[t] = y[k * TB + t] - ((part[0][t] + part[1][t]) + (part[2][t] + part[3][t]));
+    __syncthreads();
+    // x_k[r] = sum_c U[r][c] v[c]  (U row-major: U[r][c] at r*64 + c); thread (r = cidx, q)
+    const double *Uk = U + (size_t)k * TB * TB + (size_t)cidx * TB;
+    double sacc = 0.0;
+#pragma unroll
+    for (int c = q * 16; c < q * 16 + 16; ++c) sacc = fma(Uk[c], xi[c], sacc);
+    part[q][cidx] = sacc;
+    __syncthreads();
+    if (t < TB) x[k * TB + t] = (part[0][t] + part[1][t]) + (part[2][t] + part[3][t]);
+    set_flag(flags, k);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+constexpr size_t kDiagSmem = sizeof(double) * 2 * TB * LD;
+constexpr size_t kGemmSmem = sizeof(double) * 2 * TB * TB;
+
+void chol_set_attrs() {
+  static bool done = false;
+  if (done) return;
+  MS_CUDA(cudaFuncSetAttribute(k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDiagSmem));
+  MS_CUDA(cudaFuncSetAttribute(k_chol_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem));
+  MS_CUDA(cudaFuncSetAttribute(k_chol_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem));
+  done = true;
+}
+
+void launch_scatter_S(Ctx &c);
+
+void enqueue_chol_factor(Ctx &c) {
+  const int nSp = c.nS_pad;
+  k_zero_tiles<<<(int)c.n_sym_tiles, 256, 0, c.stream>>>(c.sym_tiles, nSp, c.Lden);
+  launch_scatter_S(c);
+  if (nSp > c.nS) k_pad_identity2<<<div_up(nSp - c.nS, 64), 64, 0, c.stream>>>(c.nS, nSp, c.Lden);
+  for (int k = 0; k < c.ntiles; ++k) {
+    k_chol_diag<<<1, 256, kDiagSmem, c.stream>>>(k, nSp, c.Lden, c.Uinv, c.flags + 0);
+    const int np = (int)c.h_chol_panel[k].size();
+    if (np) k_chol_trsm<<<np, 256, kGemmSmem, c.stream>>>(k, c.chol_panel + c.h_chol_panel_off[k], nSp, c.Lden, c.Uinv);
+    const int nt = (int)(c.h_chol_task_off[k + 1] - c.h_chol_task_off[k]);
+    if (nt) k_chol_update<<<nt, 256, kGemmSmem, c.stream>>>(k, c.chol_tasks + 2 * c.h_chol_task_off[k], nSp, c.Lden);
+  }
+}
+
+int64_t chol_factor_kernels(const Ctx &c) {
+  int64_t n = 2 + (c.nS_pad > c.nS ? 1 : 0);
+  for (int k = 0; k < c.ntiles; ++k)
+    n += 1 + (c.h_chol_panel[k].empty() ? 0 : 1) + ((c.h_chol_task_off[k + 1] - c.h_chol_task_off[k]) ? 1 : 0);
+  return n;
+}
+
+// solve S q = z in place on c.zs (handle order)
+void enqueue_chol_solve(Ctx &c) {
+  const int nSp = c.nS_pad, NT = c.ntiles;
+  double *b = c.qs, *y = c.yp;
+  MS_CUDA(cudaMemsetAsync(b, 0, sizeof(double) * nSp, c.stream));
+  MS_CUDA(cudaMemsetAsync(c.solve_flags, 0, sizeof(int) * 2 * NT, c.stream));
+  k_permute2<<<div_up(12 * c.m, 256), 256, 0, c.stream>>>(c.m, c.perm, c.zs, b, 0);
+  const int G = std::min(NT, c.coop_grid);
+  {
+    int NTv = NT, nSpv = nSp;
+    const int32_t *rp = c.chol_rows_ptr, *rw = c.chol_rows;
+    const double *Lp = c.Lden, *Up = c.Uinv, *bp = b;
+    double *yv = y;
+    int *fl = c.solve_flags;
+    void *args[] = {&NTv, &rp, &rw, &nSpv, &Lp, &Up, &bp, &yv, &fl};
+    MS_CUDA(cudaLaunchCooperativeKernel((const void *)k_chol_fwd, dim3(G), dim3(256), args, 0, c.stream));
+  }
+  {
+    int NTv = NT, nSpv = nSp;
+    const int32_t *pp = c.chol_panel_ptr, *pw = c.chol_panel;
+    const double *Lp = c.Lden, *Up = c.Uinv, *yp = y;
+    double *xv = b;
+    int *fl = c.solve_flags + NT;
+    void *args[] = {&NTv, &pp, &pw, &nSpv, &Lp, &Up, &yp, &xv, &fl};
+    MS_CUDA(cudaLaunchCooperativeKernel((const void *)k_chol_bwd, dim3(G), dim3(256), args, 0, c.stream));
+  }
+  k_permute2<<<div_up(12 * c.m, 256), 256, 0, c.stream>>>(c.m, c.perm, b, c.zs, 1);
+}
+
+int64_t chol_solve_kernels(const Ctx &) { return 4; }
+
+}  // namespace msim

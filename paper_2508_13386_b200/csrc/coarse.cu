@@ -307,189 +307,6 @@ __global__ void k_pad_identity(int nS, int nSp, double *__restrict__ L) {
   if (r < nSp) L[(size_t)r * nSp + r] = 1.0;
 }
 
-// ------------------------------------------------------------------ tile Cholesky (a6)
-constexpr int TB = 64;
-
-// in-place Cholesky of diagonal tile k (lower), column-major with leading dim nSp
-__global__ void __launch_bounds__(256) k_potrf_tile(int k, int nSp, double *__restrict__ L, int *__restrict__ flag) {
-  __shared__ double A[TB][TB + 1];
-  const int t = threadIdx.x;
-  const size_t base = (size_t)(k * TB) * nSp + k * TB;
-  for (int e = t; e < TB * TB; e += blockDim.x) {
-    const int r = e % TB, c = e / TB;
-    A[r][c] = (r >= c) ? L[base + (size_t)c * nSp + r] : 0.0;
-  }
-  __syncthreads();
-  for (int j = 0; j < TB; ++j) {
-    if (t == 0) {
-      const double d = A[j][j];
-      if (!(d > 0.0)) *flag = 1;
-      A[j][j] = d > 0.0 ? sqrt(d) : 1.0;
-    }
-    __syncthreads();
-    const double ljj = A[j][j];
-    for (int r = j + 1 + t; r < TB; r += blockDim.x) A[r][j] /= ljj;
-    __syncthreads();
-    const int n = TB - j - 1;
-    for (int e = t; e < n * n; e += blockDim.x) {
-      const int r = j + 1 + e % n, c = j + 1 + e / n;
-      if (r >= c) A[r][c] = fma(-A[r][j], A[c][j], A[r][c]);
-    }
-    __syncthreads();
-  }
-  for (int e = t; e < TB * TB; e += blockDim.x) {
-    const int r = e % TB, c = e / TB;
-    if (r >= c) L[base + (size_t)c * nSp + r] = A[r][c];
-  }
-}
-
-// L_ik = A_ik L_kk^-T for panel tiles i (blockIdx.x indexes the panel list)
-__global__ void __launch_bounds__(256) k_trsm_tile(int k, const int32_t *__restrict__ panel, int nSp,
-                                                   double *__restrict__ L) {
-  extern __shared__ double dsm[];
-  double(*Lk)[TB + 1] = reinterpret_cast<double(*)[TB + 1]>(dsm);
-  double(*X)[TB + 1] = reinterpret_cast<double(*)[TB + 1]>(dsm + TB * (TB + 1));
-  const int i = panel[blockIdx.x], t = threadIdx.x;
-  const size_t bk = (size_t)(k * TB) * nSp + k * TB, bi = (size_t)(k * TB) * nSp + i * TB;
-  for (int e = t; e < TB * TB; e += blockDim.x) {
-    const int r = e % TB, c = e / TB;
-    Lk[r][c] = L[bk + (size_t)c * nSp + r];
-    X[r][c] = L[bi + (size_t)c * nSp + r];
-  }
-  __syncthreads();
-  // X L_kk^T = A  ->  column c: X[:,c] = (A[:,c] - sum_{c'<c} X[:,c'] L_kk[c][c']) / L_kk[c][c]
-  for (int c = 0; c < TB; ++c) {
-    const double inv = 1.0 / Lk[c][c];
-    for (int r = t; r < TB; r += blockDim.x) X[r][c] *= inv;
-    __syncthreads();
-    for (int e = t; e < TB * (TB - c - 1); e += blockDim.x) {
-      const int r = e % TB, cc = c + 1 + e / TB;
-      X[r][cc] = fma(-X[r][c], Lk[cc][c], X[r][cc]);
-    }
-    __syncthreads();
-  }
-  for (int e = t; e < TB * TB; e += blockDim.x) {
-    const int r = e % TB, c = e / TB;
-    L[bi + (size_t)c * nSp + r] = X[r][c];
-  }
-}
-
-// A_ij -= L_ik L_jk^T for task list (pairs) of step k; 256 threads, 4x4 outputs each.
-__global__ void __launch_bounds__(256) k_update_tile(int k, const int32_t *__restrict__ tasks, int nSp,
-                                                     double *__restrict__ L) {
-  extern __shared__ double dsm[];
-  double(*Li)[TB + 1] = reinterpret_cast<double(*)[TB + 1]>(dsm);
-  double(*Lj)[TB + 1] = reinterpret_cast<double(*)[TB + 1]>(dsm + TB * (TB + 1));
-  const int i = tasks[2 * blockIdx.x], j = tasks[2 * blockIdx.x + 1], t = threadIdx.x;
-  const size_t bik = (size_t)(k * TB) * nSp + i * TB, bjk = (size_t)(k * TB) * nSp + j * TB;
-  for (int e = t; e < TB * TB; e += blockDim.x) {
-    const int r = e % TB, c = e / TB;
-    Li[r][c] = L[bik + (size_t)c * nSp + r];
-    Lj[r][c] = L[bjk + (size_t)c * nSp + r];
-  }
-  __syncthreads();
-  const int tr = (t % 16) * 4, tc = (t / 16) * 4;
-  double acc[4][4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  for (int kk = 0; kk < TB; ++kk) {
-    double x[4], y[4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      x[a] = Li[tr + a][kk];
-      y[a] = Lj[tc + a][kk];
-    }
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = fma(x[a], y[b], acc[a][b]);
-  }
-  const size_t bij = (size_t)(j * TB) * nSp + i * TB;
-#pragma unroll
-  for (int b = 0; b < 4; ++b)
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int r = tr + a, c = tc + b;
-      if (i != j || r >= c) L[bij + (size_t)c * nSp + r] -= acc[a][b];
-    }
-}
-
-// ------------------------------------------------------------------ triangular solves
-// forward step k: y_k = L_kk^-1 b_k (every CTA redundantly, warp 0); CTA 0 stores y_k;
-// CTA p >= 1 updates b_i -= L_ik y_k for i = panel[p-1].
-__global__ void __launch_bounds__(128) k_fwd_tile(int k, const int32_t *__restrict__ panel, int nSp,
-                                                  const double *__restrict__ L, double *__restrict__ b,
-                                                  double *__restrict__ y) {
-  __shared__ double yk[TB];
-  const int t = threadIdx.x, lane = t & 31;
-  const size_t bk = (size_t)(k * TB) * nSp + k * TB;
-  if (t < 32) {
-    double v0 = b[k * TB + lane], v1 = b[k * TB + 32 + lane];
-    for (int c = 0; c < TB; ++c) {
-      const double bc = __shfl_sync(0xffffffffu, c < 32 ? v0 : v1, c & 31);
-      const double yc = bc / L[bk + (size_t)c * nSp + c];
-      if (lane == (c & 31)) {
-        if (c < 32) v0 = yc; else v1 = yc;
-      }
-      if (lane > c) v0 = fma(-L[bk + (size_t)c * nSp + lane], yc, v0);
-      if (32 + lane > c) v1 = fma(-L[bk + (size_t)c * nSp + 32 + lane], yc, v1);
-    }
-    yk[lane] = v0;
-    yk[32 + lane] = v1;
-  }
-  __syncthreads();
-  if (blockIdx.x == 0) {
-    if (t < TB) y[k * TB + t] = yk[t];
-    return;
-  }
-  const int i = panel[blockIdx.x - 1];
-  const size_t bi = (size_t)(k * TB) * nSp + i * TB;
-  if (t < TB) {
-    double s = 0.0;
-    for (int c = 0; c < TB; ++c) s = fma(L[bi + (size_t)c * nSp + t], yk[c], s);
-    b[i * TB + t] -= s;
-  }
-}
-
-// backward step k: x_k = L_kk^-T y_k; CTA p >= 1 updates y_j -= L_kj^T x_k, j = rows[p-1]
-__global__ void __launch_bounds__(128) k_bwd_tile(int k, const int32_t *__restrict__ rows, int nSp,
-                                                  const double *__restrict__ L, double *__restrict__ y,
-                                                  double *__restrict__ x) {
-  __shared__ double xk[TB];
-  const int t = threadIdx.x, lane = t & 31;
-  const size_t bk = (size_t)(k * TB) * nSp + k * TB;
-  if (t < 32) {
-    double v0 = y[k * TB + lane], v1 = y[k * TB + 32 + lane];
-    for (int c = TB - 1; c >= 0; --c) {
-      const double yc = __shfl_sync(0xffffffffu, c < 32 ? v0 : v1, c & 31);
-      const double xc = yc / L[bk + (size_t)c * nSp + c];
-      if (lane == (c & 31)) {
-        if (c < 32) v0 = xc; else v1 = xc;
-      }
-      // rows r < c: y_r -= L[c][r] x_c  (L^T)
-      if (lane < c) v0 = fma(-L[bk + (size_t)lane * nSp + c], xc, v0);
-      if (32 + lane < c) v1 = fma(-L[bk + (size_t)(32 + lane) * nSp + c], xc, v1);
-    }
-    xk[lane] = v0;
-    xk[32 + lane] = v1;
-  }
-  __syncthreads();
-  if (blockIdx.x == 0) {
-    if (t < TB) x[k * TB + t] = xk[t];
-    return;
-  }
-  const int j = rows[blockIdx.x - 1];
-  // L_kj: rows k*TB.., cols j*TB..;  (L_kj^T x_k)[c] = sum_r L[kTB + r][jTB + c] x_k[r]
-  if (t < TB) {
-    const size_t bkj = (size_t)(j * TB + t) * nSp + k * TB;
-    double s = 0.0;
-    for (int r = 0; r < TB; ++r) s = fma(L[bkj + r], xk[r], s);
-    y[j * TB + t] -= s;
-  }
-}
-
 // ------------------------------------------------------------------ 12x12 affine solve
 __global__ void k_solve12(const double *__restrict__ Sa, const double *__restrict__ z, double *__restrict__ q,
                           int *__restrict__ flag) {
@@ -521,13 +338,87 @@ __global__ void k_solve12(const double *__restrict__ Sa, const double *__restric
   }
 }
 
+// W[p] = phi_p [1, X_u - c_j] for every (vertex u, handle j) basis entry p (static per basis)
+__global__ void k_basis_W(int nv, const int32_t *__restrict__ vptr, const int32_t *__restrict__ handle,
+                          const double *__restrict__ phi, const double *__restrict__ X,
+                          const double *__restrict__ origins, double *__restrict__ W) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= nv) return;
+  for (int p = vptr[u]; p < vptr[u + 1]; ++p) {
+    const int j = handle[p];
+    const double f = phi[p];
+    W[4 * (size_t)p] = f;
+    W[4 * (size_t)p + 1] = f * (X[3 * u] - origins[3 * j]);
+    W[4 * (size_t)p + 2] = f * (X[3 * u + 1] - origins[3 * j + 1]);
+    W[4 * (size_t)p + 3] = f * (X[3 * u + 2] - origins[3 * j + 2]);
+  }
+}
+
+void launch_basis_W(Ctx &c) {
+  c.Wphi.alloc(4 * (size_t)c.nnz_phi);
+  k_basis_W<<<div_up(c.nv, 256), 256, 0, c.stream>>>(c.nv, c.bvptr, c.bhandle, c.bphi, c.X, c.origins, c.Wphi);
+  c.launches++;
+  MS_CUDA(cudaGetLastError());
+}
+
+// S block b: warp per block; 8 lane groups of 4 stride over the contributions, lane `sub` of a
+// group owns the 9 R entries 9 sub .. 9 sub + 8 (x 4 monomials); groups reduced by shuffles.
+__global__ void __launch_bounds__(256) k_galerkin_S2(int64_t nblk, const int32_t *__restrict__ sc_ptr,
+                                                     const int32_t *__restrict__ sc_R,
+                                                     const int32_t *__restrict__ sc_phi,
+                                                     const double *__restrict__ W, const double *__restrict__ R,
+                                                     double *__restrict__ S) {
+  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31, grp = lane >> 2, sub = lane & 3;
+  if (b >= nblk) return;
+  double acc[9][4];
+#pragma unroll
+  for (int q = 0; q < 9; ++q)
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) acc[q][kk] = 0.0;
+  const int k1 = sc_ptr[b + 1];
+#pragma unroll 2
+  for (int k = sc_ptr[b] + grp; k < k1; k += 8) {
+    const int r = __ldg(&sc_R[k]), p = __ldg(&sc_phi[k]);
+    const double2 w01 = __ldg(reinterpret_cast<const double2 *>(W + 4 * (size_t)p));
+    const double2 w23 = __ldg(reinterpret_cast<const double2 *>(W + 4 * (size_t)p + 2));
+    const double w[4] = {w01.x, w01.y, w23.x, w23.y};
+    const double *Rr = R + 36 * (size_t)r + 9 * sub;
+    double rv[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) rv[q] = __ldg(&Rr[q]);
+#pragma unroll
+    for (int q = 0; q < 9; ++q)
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) acc[q][kk] = fma(rv[q], w[kk], acc[q][kk]);
+  }
+#pragma unroll
+  for (int q = 0; q < 9; ++q)
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      double v = acc[q][kk];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      acc[q][kk] = v;
+    }
+  if (grp == 0) {
+    double *dst = S + 144 * (size_t)b;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      const int l = 9 * sub + q, row = l / 3, cc = l % 3;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) dst[row * 12 + 4 * cc + kk] = acc[q][kk];
+    }
+  }
+}
+
 // ------------------------------------------------------------------ launchers
 void launch_coarse_S(Ctx &c) {
   k_galerkin_R<<<div_up(c.n_R, 128), 128, 0, c.stream>>>(c.n_R, c.R_i, c.R_u, hview(c), c.bvptr, c.bhandle,
                                                          c.bphi, c.X, c.origins, c.Rbuf);
-  k_galerkin_S<<<div_up(c.nnzb_S * 32, 256), 256, 0, c.stream>>>(c.nnzb_S, c.srow, c.scol, c.sc_ptr, c.sc_R,
-                                                                  c.sc_phi, c.R_u, c.bphi, c.X, c.origins,
-                                                                  c.Rbuf, c.Sblk);
+  k_galerkin_S2<<<div_up(c.nnzb_S * 32, 256), 256, 0, c.stream>>>(c.nnzb_S, c.sc_ptr, c.sc_R, c.sc_phi, c.Wphi,
+                                                                   c.Rbuf, c.Sblk);
   const double *o = c.aff_origin;
   k_galerkin_Ra<<<div_up(c.nv, 128), 128, 0, c.stream>>>(c.nv, hview(c), c.phi_aff, c.X, o[0], o[1], o[2], c.Ra);
   const int nch = 64;
@@ -538,58 +429,9 @@ void launch_coarse_S(Ctx &c) {
   MS_CUDA(cudaGetLastError());
 }
 
-constexpr size_t kTileSmem = sizeof(double) * 2 * TB * (TB + 1);
-
-static void enqueue_factor(Ctx &c) {
-  const int nSp = c.nS_pad;
-  MS_CUDA(cudaMemsetAsync(c.Lden, 0, sizeof(double) * (size_t)nSp * nSp, c.stream));
-  k_scatter_S<<<div_up(c.nnzb_S * 144, 256), 256, 0, c.stream>>>(c.nnzb_S, c.srow, c.scol, c.perm, c.Sblk, nSp,
-                                                                  c.Lden);
-  if (nSp > c.nS) k_pad_identity<<<div_up(nSp - c.nS, 64), 64, 0, c.stream>>>(c.nS, nSp, c.Lden);
-  for (int k = 0; k < c.ntiles; ++k) {
-    k_potrf_tile<<<1, 256, 0, c.stream>>>(k, nSp, c.Lden, c.flags + 0);
-    const int np = (int)c.h_chol_panel[k].size();
-    if (np) {
-      k_trsm_tile<<<np, 256, kTileSmem, c.stream>>>(k, c.chol_panel + c.h_chol_panel_off[k], nSp, c.Lden);
-      const int nt = (int)(c.h_chol_task_off[k + 1] - c.h_chol_task_off[k]);
-      k_update_tile<<<nt, 256, kTileSmem, c.stream>>>(k, c.chol_tasks + 2 * c.h_chol_task_off[k], nSp, c.Lden);
-    }
-  }
-}
-
-static int64_t factor_kernel_count(const Ctx &c) {
-  int64_t n = 1 + (c.nS_pad > c.nS ? 1 : 0);
-  for (int k = 0; k < c.ntiles; ++k) n += 1 + (c.h_chol_panel[k].empty() ? 0 : 2);
-  return n;
-}
-
-// solve S q = z: z (handle order, c.zs) -> permuted (c.qs as b) -> forward (y in c.tmp2)
-// -> backward (x in c.qs) -> unpermute into c.zs.
-static void enqueue_solve(Ctx &c) {
-  const int nSp = c.nS_pad;
-  double *b = c.qs, *y = c.yp;
-  MS_CUDA(cudaMemsetAsync(b, 0, sizeof(double) * nSp, c.stream));
-  k_permute<<<div_up(12 * c.m, 256), 256, 0, c.stream>>>(c.m, c.perm, c.zs, b, 0);
-  for (int k = 0; k < c.ntiles; ++k) {
-    const int np = (int)c.h_chol_panel[k].size();
-    k_fwd_tile<<<1 + np, 128, 0, c.stream>>>(k, c.chol_panel + c.h_chol_panel_off[k], nSp, c.Lden, b, y);
-  }
-  for (int k = c.ntiles - 1; k >= 0; --k) {
-    const int nr = (int)(c.h_chol_rows_off[k + 1] - c.h_chol_rows_off[k]);
-    k_bwd_tile<<<1 + nr, 128, 0, c.stream>>>(k, c.chol_rows + c.h_chol_rows_off[k], nSp, c.Lden, y, b);
-  }
-  k_permute<<<div_up(12 * c.m, 256), 256, 0, c.stream>>>(c.m, c.perm, b, c.zs, 1);
-}
-
-static int64_t solve_kernel_count(const Ctx &c) { return 2 + 2 * (int64_t)c.ntiles; }
-
-static void ensure_attrs() {
-  static bool attr = false;
-  if (!attr) {
-    MS_CUDA(cudaFuncSetAttribute(k_trsm_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
-    MS_CUDA(cudaFuncSetAttribute(k_update_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
-    attr = true;
-  }
+void launch_scatter_S(Ctx &c) {
+  k_scatter_S<<<div_up(c.nnzb_S * 144, 256), 256, 0, c.stream>>>(c.nnzb_S, c.srow, c.scol, c.perm, c.Sblk,
+                                                                  c.nS_pad, c.Lden);
 }
 
 // Capture a fixed launch sequence once (pointers are fixed per basis) and replay it.
@@ -623,15 +465,15 @@ void coarse_reset_graphs(Ctx &c) {
 }
 
 void launch_coarse_factor(Ctx &c) {
-  ensure_attrs();
-  run_captured(c, c.factor_graph, enqueue_factor);
-  c.launches += factor_kernel_count(c);
+  chol_set_attrs();
+  run_captured(c, c.factor_graph, enqueue_chol_factor);
+  c.launches += chol_factor_kernels(c);
   MS_CUDA(cudaGetLastError());
 }
 
 void launch_coarse_solve(Ctx &c) {
-  run_captured(c, c.solve_graph, enqueue_solve);
-  c.launches += solve_kernel_count(c);
+  run_captured(c, c.solve_graph, enqueue_chol_solve);
+  c.launches += chol_solve_kernels(c);
   MS_CUDA(cudaGetLastError());
 }
 

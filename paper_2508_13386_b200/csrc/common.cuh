@@ -133,6 +133,7 @@ struct Ctx {
   std::vector<int32_t> h_sptr, h_scol;
   DBuf<int32_t> sptr, scol, srow;
   DBuf<double> Sblk;                // [nnzb_S * 144]
+  DBuf<double> Wphi;                // [nnz_phi * 4] phi [1, X - c] per basis entry
   // R contributions: R_i(u) for (i,u) pairs; S contributions
   int64_t n_R = 0;                  // number of (i,u) pairs
   DBuf<int32_t> R_i, R_u;           // [n_R]
@@ -158,6 +159,11 @@ struct Ctx {
   DBuf<int32_t> chol_rows;          // per tile k: tile columns j < k with L_kj != 0 (flattened)
   std::vector<int64_t> h_chol_rows_off;
   double chol_flops = 0.0;          // flops of one factorisation (tile granularity)
+  DBuf<int32_t> chol_rows_ptr, chol_panel_ptr, sym_tiles;
+  int64_t n_sym_tiles = 0;
+  DBuf<double> Uinv;                // [ntiles][64*64] U_kk = L_kk^-T (column-major)
+  DBuf<int> solve_flags;            // [2 ntiles] tile-ready flags of the cooperative solves
+  int coop_grid = 148;
   cudaGraphExec_t factor_graph = nullptr, solve_graph = nullptr;
   int64_t factor_graph_kernels = 0, solve_graph_kernels = 0;
   DBuf<double> qa, qs, za, zs, yp;  // coarse vectors (qs/yp: permuted work space)
@@ -233,6 +239,12 @@ void launch_coarse_S(Ctx &c);
 void launch_coarse_factor(Ctx &c);
 void launch_coarse_direction(Ctx &c);
 void launch_coarse_solve(Ctx &c);
+void launch_basis_W(Ctx &c);
+void enqueue_chol_factor(Ctx &c);
+void enqueue_chol_solve(Ctx &c);
+int64_t chol_factor_kernels(const Ctx &c);
+int64_t chol_solve_kernels(const Ctx &c);
+void chol_set_attrs();
 void coarse_reset_graphs(Ctx &c);
 void launch_lift(Ctx &c, const double *q, double *w, bool accumulate);
 void launch_restrict(Ctx &c, const double *y, double *z);

@@ -149,11 +149,37 @@ __host__ __device__ constexpr int blk4(int a, int b) {  // a <= b, 10 upper bloc
   return a * 4 - (a * (a - 1)) / 2 + (b - a);
 }
 // Brent-Luk round-robin for n = 9: round r pairs ((r+k)%9, (r-k+9)%9), k = 1..4
+// r < 0: the fixed positions (0,7),(1,6),(2,5),(3,4) of the circle method (index 8 idles); the
+// matrix is relabelled by a cyclic shift i -> i+1 (mod 9) after every round, so 9 rounds meet
+// every pair once with ONE round of code (small I-cache footprint).
 __host__ __device__ constexpr int rr_p(int r, int k) {
-  return ((r + k) % 9) < ((r - k + 9) % 9) ? ((r + k) % 9) : ((r - k + 9) % 9);
+  return r < 0 ? k - 1 : (((r + k) % 9) < ((r - k + 9) % 9) ? ((r + k) % 9) : ((r - k + 9) % 9));
 }
 __host__ __device__ constexpr int rr_q(int r, int k) {
-  return ((r + k) % 9) < ((r - k + 9) % 9) ? ((r - k + 9) % 9) : ((r + k) % 9);
+  return r < 0 ? 8 - k : (((r + k) % 9) < ((r - k + 9) % 9) ? ((r - k + 9) % 9) : ((r + k) % 9));
+}
+
+// Branch-free fp64 reciprocal / reciprocal square root: MUFU seed + Newton steps (no slow-path
+// subroutine calls, no divergence).  Relative error ~1 ulp for normal inputs.
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double h = 0.5 * x * y;
+    y = fma(y, fma(-h, y, 0.5), y);   // y += y (0.5 - 0.5 x y^2)
+  }
+  return y;
 }
 
 template <int R>
@@ -161,17 +187,17 @@ __device__ __forceinline__ void jacobi_round(double (&a)[45], double (&v)[81]) {
   double c[4], s[4], t[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    constexpr int dummy = 0;
-    (void)dummy;
     const int p = rr_p(R, k + 1), q = rr_q(R, k + 1);
     const double apq = a[sidx(p, q)];
     const double dd = a[sidx(q, q)] - a[sidx(p, p)];
-    const double r = sqrt(fma(dd, dd, 4.0 * apq * apq));
+    // t = sgn(dd) 2 apq / (|dd| + sqrt(dd^2 + 4 apq^2))  (NR 11.1; tan of the Jacobi angle)
+    const double r2 = fma(dd, dd, 4.0 * apq * apq);
+    const double r = r2 > 1e-290 ? r2 * rsqrt_nr(r2) : 0.0;
     const double den = fabs(dd) + r;
-    double tt = den > 0.0 ? (2.0 * apq) / den : 0.0;
+    double tt = den > 0.0 ? (2.0 * apq) * rcp_nr(den) : 0.0;
     tt = dd >= 0.0 ? tt : -tt;
     t[k] = tt;
-    c[k] = rsqrt(fma(tt, tt, 1.0));
+    c[k] = rsqrt_nr(fma(tt, tt, 1.0));
     s[k] = tt * c[k];
   }
 #pragma unroll
@@ -197,6 +223,32 @@ __device__ __forceinline__ void jacobi_round(double (&a)[45], double (&v)[81]) {
   }
 }
 
+__device__ __forceinline__ void cyclic_relabel(double (&a)[45], double (&v)[81]) {
+  double na[45];
+#pragma unroll
+  for (int i = 0; i < 9; ++i)
+#pragma unroll
+    for (int j = i; j < 9; ++j) na[sidx((i + 1) % 9, (j + 1) % 9)] = a[sidx(i, j)];
+#pragma unroll
+  for (int k = 0; k < 45; ++k) a[k] = na[k];
+#pragma unroll
+  for (int r = 0; r < 9; ++r) {
+    const double last = v[r * 9 + 8];
+#pragma unroll
+    for (int k = 8; k > 0; --k) v[r * 9 + k] = v[r * 9 + k - 1];
+    v[r * 9] = last;
+  }
+}
+
+#ifndef MSIM_JACOBI_UNROLLED
+__device__ __forceinline__ void jacobi_sweep(double (&a)[45], double (&v)[81]) {
+#pragma unroll 1
+  for (int rd = 0; rd < 9; ++rd) {
+    jacobi_round<-1>(a, v);
+    cyclic_relabel(a, v);
+  }
+}
+#else
 __device__ __forceinline__ void jacobi_sweep(double (&a)[45], double (&v)[81]) {
   jacobi_round<0>(a, v);
   jacobi_round<1>(a, v);
@@ -208,6 +260,7 @@ __device__ __forceinline__ void jacobi_sweep(double (&a)[45], double (&v)[81]) {
   jacobi_round<7>(a, v);
   jacobi_round<8>(a, v);
 }
+#endif
 
 __device__ __forceinline__ double offdiag2(const double (&a)[45]) {
   double s = 0.0;

@@ -313,55 +313,79 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
     };
     nd(all);
   }
-  c.h_perm.assign(m, 0);
-  for (int32_t p = 0; p < m; ++p) c.h_perm[order[p]] = p;
-
-  // ---- tile-level symbolic Cholesky of S in the permuted order
+  // ---- tile-level symbolic Cholesky for a handle order; the cheaper of the x-sorted order
+  // (handles arrive sorted by centroid) and the nested-dissection order is kept.
   c.nS = 12 * m;
   c.tile = 64;
   c.ntiles = div_up(c.nS, c.tile);
   c.nS_pad = c.ntiles * c.tile;
   const int T = c.tile, NT = c.ntiles;
-  std::vector<std::vector<char>> nz(NT, std::vector<char>(NT, 0));
-  for (int32_t t = 0; t < NT; ++t) nz[t][t] = 1;
-  for (int32_t i = 0; i < m; ++i)
-    for (int32_t k = sptr[i]; k < sptr[i + 1]; ++k) {
-      const int32_t pi = c.h_perm[i], pj = c.h_perm[scol[k]];
-      const int32_t r0 = 12 * pi / T, r1 = (12 * pi + 11) / T, c0 = 12 * pj / T, c1 = (12 * pj + 11) / T;
-      for (int32_t a = r0; a <= r1; ++a)
-        for (int32_t b = c0; b <= c1; ++b)
-          if (a >= b) nz[a][b] = 1;
+  struct Sym {
+    std::vector<int32_t> perm;
+    std::vector<std::vector<int32_t>> panel, rows;
+    std::vector<std::vector<char>> nz;
+    double flops = 0.0;
+  };
+  auto symbolic = [&](const std::vector<int32_t> &ord) {
+    Sym y;
+    y.perm.assign(m, 0);
+    for (int32_t p = 0; p < m; ++p) y.perm[ord[p]] = p;
+    y.nz.assign(NT, std::vector<char>(NT, 0));
+    for (int32_t t = 0; t < NT; ++t) y.nz[t][t] = 1;
+    for (int32_t i = 0; i < m; ++i)
+      for (int32_t k = sptr[i]; k < sptr[i + 1]; ++k) {
+        const int32_t pi = y.perm[i], pj = y.perm[scol[k]];
+        for (int32_t a = 12 * pi / T; a <= (12 * pi + 11) / T; ++a)
+          for (int32_t b = 12 * pj / T; b <= (12 * pj + 11) / T; ++b)
+            if (a >= b) y.nz[a][b] = 1;
+      }
+    y.panel.assign(NT, {});
+    y.rows.assign(NT, {});
+    for (int32_t k = 0; k < NT; ++k) {
+      auto &P = y.panel[k];
+      for (int32_t i = k + 1; i < NT; ++i)
+        if (y.nz[i][k]) P.push_back(i);
+      for (size_t a = 0; a < P.size(); ++a)
+        for (size_t b = 0; b <= a; ++b) y.nz[P[a]][P[b]] = 1;
+      for (int32_t i : P) y.rows[i].push_back(k);
+      const double np = (double)P.size();
+      y.flops += (double)T * T * T / 3.0 + np * T * T * T + np * (np + 1) * T * T * T;
     }
-  c.h_chol_panel.assign(NT, {});
-  std::vector<std::vector<int32_t>> rows(NT);
-  for (int32_t k = 0; k < NT; ++k) {
-    auto &P = c.h_chol_panel[k];
-    for (int32_t i = k + 1; i < NT; ++i)
-      if (nz[i][k]) P.push_back(i);
-    for (size_t a = 0; a < P.size(); ++a)       // fill: (P[a], P[b]) becomes nonzero
-      for (size_t b = 0; b <= a; ++b) nz[P[a]][P[b]] = 1;
-    for (int32_t i : P) rows[i].push_back(k);
-  }
-  std::vector<int32_t> panel_flat, task_flat, rows_flat;
+    return y;
+  };
+  std::vector<int32_t> ident(m);
+  std::iota(ident.begin(), ident.end(), 0);
+  Sym sx = symbolic(ident), snd = symbolic(order);
+  Sym &best = snd.flops < sx.flops ? snd : sx;
+  c.h_perm = best.perm;
+  c.chol_flops = best.flops;
+  c.h_chol_panel = best.panel;
+  std::vector<int32_t> panel_flat, task_flat, rows_flat, sym_tiles;
+  std::vector<int32_t> panel_ptr(NT + 1, 0), rows_ptr(NT + 1, 0);
   c.h_chol_panel_off.assign(NT + 1, 0);
   c.h_chol_task_off.assign(NT + 1, 0);
   c.h_chol_rows_off.assign(NT + 1, 0);
-  c.chol_flops = 0.0;
   for (int32_t k = 0; k < NT; ++k) {
-    const auto &P = c.h_chol_panel[k];
+    const auto &P = best.panel[k];
     for (size_t a = 0; a < P.size(); ++a)
       for (size_t b = 0; b <= a; ++b) {
         task_flat.push_back(P[a]);
         task_flat.push_back(P[b]);
       }
     panel_flat.insert(panel_flat.end(), P.begin(), P.end());
-    rows_flat.insert(rows_flat.end(), rows[k].begin(), rows[k].end());
+    rows_flat.insert(rows_flat.end(), best.rows[k].begin(), best.rows[k].end());
     c.h_chol_panel_off[k + 1] = (int64_t)panel_flat.size();
     c.h_chol_task_off[k + 1] = (int64_t)task_flat.size() / 2;
     c.h_chol_rows_off[k + 1] = (int64_t)rows_flat.size();
-    const double np = (double)P.size();
-    c.chol_flops += (double)T * T * T / 3.0 + np * T * T * T + np * (np + 1) / 2 * 2.0 * T * T * T;
+    panel_ptr[k + 1] = (int32_t)panel_flat.size();
+    rows_ptr[k + 1] = (int32_t)rows_flat.size();
+    for (int32_t i = k; i < NT; ++i)
+      if (best.nz[i][k]) {
+        sym_tiles.push_back(i);
+        sym_tiles.push_back(k);
+      }
   }
+  c.n_sym_tiles = (int64_t)sym_tiles.size() / 2;
 
   cudaStream_t s = c.stream;
   c.origins.upload(origins, 3 * (size_t)m, s);
@@ -393,6 +417,16 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   c.Lden.alloc((size_t)c.nS_pad * c.nS_pad);
   c.perm.upload(c.h_perm, s);
   c.chol_rows.upload(rows_flat.empty() ? std::vector<int32_t>{0} : rows_flat, s);
+  c.chol_rows_ptr.upload(rows_ptr, s);
+  c.chol_panel_ptr.upload(panel_ptr, s);
+  c.sym_tiles.upload(sym_tiles, s);
+  c.Uinv.alloc((size_t)NT * T * T);
+  c.solve_flags.alloc(2 * (size_t)NT);
+  {
+    int nsm = 0;
+    MS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));
+    c.coop_grid = std::max(1, nsm);
+  }
   c.chol_panel.upload(panel_flat.empty() ? std::vector<int32_t>{0} : panel_flat, s);
   c.chol_tasks.upload(task_flat.empty() ? std::vector<int32_t>{0, 0} : task_flat, s);
   c.qa.alloc(12);
@@ -401,6 +435,7 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   c.zs.alloc(c.nS_pad);
   c.yp.alloc(c.nS_pad);
   coarse_reset_graphs(c);
+  launch_basis_W(c);
   MS_CUDA(cudaStreamSynchronize(s));
 }
 
