@@ -510,11 +510,13 @@ ms_status ms_export_bsr(ms_ctx *ctx, int64_t *nnzb, int32_t *rowptr, int32_t *co
     if (colidx) std::memcpy(colidx, c.h_colidx.data(), sizeof(int32_t) * c.nnzb);
     if (vals) {
       MS_REQUIRE(c.assembled, MS_ERR_STATE, "nothing assembled yet");
-      std::vector<double> planes((size_t)9 * c.nnzb);
-      c.vals.download(planes.data(), planes.size(), c.stream);
+      std::vector<double> sell((size_t)9 * c.npos);   // SELL-32 layout (sell.cuh)
+      c.vals.download(sell.data(), sell.size(), c.stream);
       MS_CUDA(cudaStreamSynchronize(c.stream));
-      for (int64_t s = 0; s < c.nnzb; ++s)
-        for (int q = 0; q < 9; ++q) vals[9 * s + q] = planes[(size_t)q * c.nnzb + s];
+      for (int64_t s = 0; s < c.nnzb; ++s) {
+        const int64_t pos = c.h_sell_pos[s], cc = pos >> 5, lane = pos & 31;
+        for (int q = 0; q < 9; ++q) vals[9 * s + q] = sell[((size_t)cc * 9 + q) * 32 + lane];
+      }
     }
   });
   return MS_OK;

@@ -16,6 +16,7 @@
 #include <cuda_pipeline.h>
 
 #include "common.cuh"
+#include "fastmath.cuh"
 
 namespace msim {
 
@@ -27,11 +28,15 @@ __device__ __forceinline__ size_t tile_off(int ti, int tj, int nSp) {
 }
 
 // ------------------------------------------------------------------ D(k): potrf + inverse
-__global__ void __launch_bounds__(256) k_chol_diag(int k, int nSp, double *__restrict__ L,
-                                                   double *__restrict__ U, int *__restrict__ flag) {
-  extern __shared__ double sm[];
+// smem: A [64][LD], Li [64][LD], Tb [3*16*17], invd [64]
+constexpr int kDiagSmemDoubles = 2 * TB * LD + 3 * 16 * 17 + TB;
+
+__device__ void diag_factor(int k, int nSp, double *__restrict__ L, double *__restrict__ U,
+                            int *__restrict__ flag, double *sm) {
   double *A = sm;              // row-major [64][LD]: the factor
   double *Li = sm + TB * LD;   // row-major [64][LD]: its inverse
+  double(*Tb)[16][17] = reinterpret_cast<double(*)[16][17]>(sm + 2 * TB * LD);
+  double *invd = sm + 2 * TB * LD + 3 * 16 * 17;
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
   const size_t okk = tile_off(k, k, nSp);
   {
@@ -39,7 +44,7 @@ __global__ void __launch_bounds__(256) k_chol_diag(int k, int nSp, double *__res
 #pragma unroll
     for (int it = 0; it < 16; ++it) {
       const int e = t + it * 256;
-      v[it] = L[okk + (size_t)(e >> 6) * nSp + (e & 63)];
+      v[it] = __ldcg(&L[okk + (size_t)(e >> 6) * nSp + (e & 63)]);
     }
 #pragma unroll
     for (int it = 0; it < 16; ++it) {
@@ -66,8 +71,9 @@ __global__ void __launch_bounds__(256) k_chol_diag(int k, int nSp, double *__res
       for (int j = 0; j < 16; ++j) {
         const double d = __shfl_sync(0xffffffffu, a[j], j);
         if (!(d > 0.0)) bad = true;
-        const double ljj = d > 0.0 ? sqrt(d) : 1.0;
-        const double inv = 1.0 / ljj;
+        const double inv = d > 0.0 ? rsqrt_nr(d) : 1.0;   // 1 / sqrt(d)
+        const double ljj = d > 0.0 ? d * inv : 1.0;
+        if (lane == 0) invd[j0 + j] = inv;
         a[j] = lane == j ? ljj : (lane > j ? a[j] * inv : a[j]);
         b[j] *= inv;
 #pragma unroll
@@ -106,14 +112,13 @@ __global__ void __launch_bounds__(256) k_chol_diag(int k, int nSp, double *__res
       double s = r == lane ? 1.0 : 0.0;
 #pragma unroll
       for (int q = 0; q < r; ++q) s = fma(-A[(o + r) * LD + o + q], x[q], s);
-      x[r] = s / A[(o + r) * LD + o + r];
+      x[r] = s * invd[o + r];
     }
 #pragma unroll
     for (int r = 0; r < 16; ++r) Li[(o + r) * LD + o + lane] = x[r];
   }
   __syncthreads();
   // off-diagonal blocks: Li_pq = -Li_pp sum_{s=q}^{p-1} L_ps Li_sq, p = 1..3
-  __shared__ double Tb[3][16][17];
   for (int p = 1; p < 4; ++p) {
     for (int e = t; e < p * 256; e += 256) {
       const int q = e >> 8, r = (e >> 4) & 15, cc = e & 15;
@@ -139,6 +144,12 @@ __global__ void __launch_bounds__(256) k_chol_diag(int k, int nSp, double *__res
     if (r >= c) L[okk + (size_t)c * nSp + r] = A[r * LD + c];
     Uk[(size_t)c * TB + r] = Li[r * LD + c];   // U[c][r] = Li[r][c]
   }
+}
+
+__global__ void __launch_bounds__(256) k_chol_diag(int k, int nSp, double *__restrict__ L,
+                                                   double *__restrict__ U, int *__restrict__ flag) {
+  extern __shared__ double sm[];
+  diag_factor(k, nSp, L, U, flag, sm);
 }
 
 // ------------------------------------------------------------------ 64^3 tile GEMM core
@@ -193,9 +204,16 @@ __global__ void __launch_bounds__(256) k_chol_trsm(int k, const int32_t *__restr
 }
 
 // ------------------------------------------------------------------ U(k): A_ij -= L_ik L_jk^T
-__global__ void __launch_bounds__(256) k_chol_update(int k, const int32_t *__restrict__ tasks, int nSp,
-                                                     double *__restrict__ L) {
+// Look-ahead: the CTA updating tile (la, la) (la = k + 1) -- or an extra CTA if that tile gets no
+// update in this step -- factorises it right away (D(k+1) runs inside U(k)).
+__global__ void __launch_bounds__(256) k_chol_update(int k, const int32_t *__restrict__ tasks, int ntasks,
+                                                     int la, int nSp, double *__restrict__ L,
+                                                     double *__restrict__ U, int *__restrict__ flag) {
   extern __shared__ double sm[];
+  if ((int)blockIdx.x >= ntasks) {
+    diag_factor(la, nSp, L, U, flag, sm);
+    return;
+  }
   double *Si = sm, *Sj = sm + TB * TB;
   const int i = tasks[2 * blockIdx.x], j = tasks[2 * blockIdx.x + 1], t = threadIdx.x;
   stage_colmajor(Si, L + tile_off(i, k, nSp), nSp);
@@ -219,6 +237,10 @@ __global__ void __launch_bounds__(256) k_chol_update(int k, const int32_t *__res
       const int r = tr + a, c = tc + b;
       if (i != j || r >= c) L[oij + (size_t)c * nSp + r] = old[a][b] - acc[a][b];
     }
+  if (i == la && j == la) {
+    __syncthreads();
+    diag_factor(la, nSp, L, U, flag, sm);
+  }
 }
 
 __global__ void __launch_bounds__(256) k_zero_tiles(const int32_t *__restrict__ tiles, int nSp, double *__restrict__ L) {
@@ -347,38 +369,52 @@ __global__ void __launch_bounds__(256) k_chol_bwd(int NT, const int32_t *__restr
 }
 
 // ------------------------------------------------------------------ host side
-constexpr size_t kDiagSmem = sizeof(double) * 2 * TB * LD;
+constexpr size_t kDiagSmem = sizeof(double) * kDiagSmemDoubles;
 constexpr size_t kGemmSmem = sizeof(double) * 2 * TB * TB;
+constexpr size_t kUpdSmem = kDiagSmem > kGemmSmem ? kDiagSmem : kGemmSmem;
 
 void chol_set_attrs() {
   static bool done = false;
   if (done) return;
   MS_CUDA(cudaFuncSetAttribute(k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDiagSmem));
   MS_CUDA(cudaFuncSetAttribute(k_chol_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem));
-  MS_CUDA(cudaFuncSetAttribute(k_chol_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem));
+  MS_CUDA(cudaFuncSetAttribute(k_chol_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem));
   done = true;
 }
 
 void launch_scatter_S(Ctx &c);
 
+static bool step_updates_diag(const Ctx &c, int k) {   // is tile (k+1, k+1) among the tasks of step k?
+  const auto &P = c.h_chol_panel[k];
+  return !P.empty() && P.front() == k + 1;
+}
+
+// D(0); then for each k: P(k), U(k) with D(k+1) fused (look-ahead)
 void enqueue_chol_factor(Ctx &c) {
   const int nSp = c.nS_pad;
   k_zero_tiles<<<(int)c.n_sym_tiles, 256, 0, c.stream>>>(c.sym_tiles, nSp, c.Lden);
   launch_scatter_S(c);
   if (nSp > c.nS) k_pad_identity2<<<div_up(nSp - c.nS, 64), 64, 0, c.stream>>>(c.nS, nSp, c.Lden);
+  k_chol_diag<<<1, 256, kDiagSmem, c.stream>>>(0, nSp, c.Lden, c.Uinv, c.flags + 0);
   for (int k = 0; k < c.ntiles; ++k) {
-    k_chol_diag<<<1, 256, kDiagSmem, c.stream>>>(k, nSp, c.Lden, c.Uinv, c.flags + 0);
     const int np = (int)c.h_chol_panel[k].size();
     if (np) k_chol_trsm<<<np, 256, kGemmSmem, c.stream>>>(k, c.chol_panel + c.h_chol_panel_off[k], nSp, c.Lden, c.Uinv);
     const int nt = (int)(c.h_chol_task_off[k + 1] - c.h_chol_task_off[k]);
-    if (nt) k_chol_update<<<nt, 256, kGemmSmem, c.stream>>>(k, c.chol_tasks + 2 * c.h_chol_task_off[k], nSp, c.Lden);
+    const int la = k + 1 < c.ntiles ? k + 1 : -1;
+    const int extra = (la >= 0 && !step_updates_diag(c, k)) ? 1 : 0;
+    if (nt + extra)
+      k_chol_update<<<nt + extra, 256, kUpdSmem, c.stream>>>(k, c.chol_tasks + 2 * c.h_chol_task_off[k], nt, la,
+                                                             nSp, c.Lden, c.Uinv, c.flags + 0);
   }
 }
 
 int64_t chol_factor_kernels(const Ctx &c) {
-  int64_t n = 2 + (c.nS_pad > c.nS ? 1 : 0);
-  for (int k = 0; k < c.ntiles; ++k)
-    n += 1 + (c.h_chol_panel[k].empty() ? 0 : 1) + ((c.h_chol_task_off[k + 1] - c.h_chol_task_off[k]) ? 1 : 0);
+  int64_t n = 3 + (c.nS_pad > c.nS ? 1 : 0);
+  for (int k = 0; k < c.ntiles; ++k) {
+    const int nt = (int)(c.h_chol_task_off[k + 1] - c.h_chol_task_off[k]);
+    const int extra = (k + 1 < c.ntiles && !step_updates_diag(c, k)) ? 1 : 0;
+    n += (c.h_chol_panel[k].empty() ? 0 : 1) + ((nt + extra) ? 1 : 0);
+  }
   return n;
 }
 

@@ -119,11 +119,10 @@ void launch_restrict(Ctx &c, const double *y, double *z) {
 }
 
 // ------------------------------------------------------------------ Galerkin products (a5)
-struct HView {
-  int64_t nnzb;
-  const int32_t *__restrict__ rowptr;
-  const int32_t *__restrict__ colidx;
-  const double *__restrict__ vals;   // [9][nnzb]
+struct HView {                      // SELL-32 Hessian (sell.cuh)
+  const int32_t *__restrict__ sl_ptr;
+  const int32_t *__restrict__ col;
+  const double *__restrict__ vals;
 };
 
 // R_i(u) for every (i,u) pair: thread per pair.
@@ -140,8 +139,9 @@ __global__ void __launch_bounds__(128) k_galerkin_R(int64_t nR, const int32_t *_
   double acc[36];
 #pragma unroll
   for (int k = 0; k < 36; ++k) acc[k] = 0.0;
-  for (int s = H.rowptr[u]; s < H.rowptr[u + 1]; ++s) {
-    const int v = H.colidx[s];
+  const int sl_ = u >> 5, ln_ = u & 31;
+  for (int cs = H.sl_ptr[sl_]; cs < H.sl_ptr[sl_ + 1]; ++cs) {
+    const int v = H.col[(size_t)cs * 32 + ln_];
     double f = 0.0;
     for (int k = bvptr[v]; k < bvptr[v + 1]; ++k) {
       const int hk = bhandle[k];
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(128) k_galerkin_R(int64_t nR, const int32_t *_
 #pragma unroll
     for (int cc = 0; cc < 3; ++cc)
 #pragma unroll
-      for (int cp = 0; cp < 3; ++cp) Hvu[cp][cc] = H.vals[(size_t)(3 * cc + cp) * H.nnzb + s];
+      for (int cp = 0; cp < 3; ++cp) Hvu[cp][cc] = H.vals[((size_t)cs * 9 + 3 * cc + cp) * 32 + ln_];
 #pragma unroll
     for (int cp = 0; cp < 3; ++cp)
 #pragma unroll
@@ -222,8 +222,9 @@ __global__ void __launch_bounds__(128) k_galerkin_Ra(int nv, HView H, const doub
   double acc[36];
 #pragma unroll
   for (int k = 0; k < 36; ++k) acc[k] = 0.0;
-  for (int s = H.rowptr[u]; s < H.rowptr[u + 1]; ++s) {
-    const int v = H.colidx[s];
+  const int sl_ = u >> 5, ln_ = u & 31;
+  for (int cs = H.sl_ptr[sl_]; cs < H.sl_ptr[sl_ + 1]; ++cs) {
+    const int v = H.col[(size_t)cs * 32 + ln_];
     const double f = phi_a[v];
     if (f == 0.0) continue;
     const double w[4] = {f, f * (X[3 * v] - ox), f * (X[3 * v + 1] - oy), f * (X[3 * v + 2] - oz)};
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(128) k_galerkin_Ra(int nv, HView H, const doub
 #pragma unroll
     for (int cc = 0; cc < 3; ++cc)
 #pragma unroll
-      for (int cp = 0; cp < 3; ++cp) Hvu[cp][cc] = H.vals[(size_t)(3 * cc + cp) * H.nnzb + s];
+      for (int cp = 0; cp < 3; ++cp) Hvu[cp][cc] = H.vals[((size_t)cs * 9 + 3 * cc + cp) * 32 + ln_];
 #pragma unroll
     for (int cp = 0; cp < 3; ++cp)
 #pragma unroll
@@ -276,7 +277,7 @@ __global__ void k_galerkin_Sa_final(int nch, const double *__restrict__ part, do
   Sa[row * 12 + 4 * c + k] = s;
 }
 
-static HView hview(const Ctx &c) { return HView{c.nnzb, c.rowptr, c.colidx, c.vals}; }
+static HView hview(const Ctx &c) { return HView{c.sl_ptr, c.sell_col, c.vals}; }
 
 // ------------------------------------------------------------------ dense envelope S
 // Lden column-major nS_pad x nS_pad; scatter lower part of S blocks; padding -> identity.

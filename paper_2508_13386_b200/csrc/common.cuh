@@ -101,7 +101,10 @@ struct Ctx {
   std::vector<int32_t> h_rowptr, h_colidx;
   DBuf<int32_t> rowptr, colidx, diag_slot, slot_row;
   DBuf<int32_t> cptr, contrib;      // slot -> list of (tet*16 + a*4 + b)
-  DBuf<double> vals;                // SoA [9][nnzb]
+  DBuf<double> vals;                // SELL-32 values [npos/32][9][32] (sell.cuh)
+  int64_t npos = 0;                 // SELL positions (nnzb + padding)
+  DBuf<int32_t> sl_ptr, sell_col, sell_slot;
+  std::vector<int64_t> h_sell_pos;  // CSR slot -> SELL position
   DBuf<double> dinv;                // [3 nv] Jacobi D^-1
   // ground
   bool has_ground = false;

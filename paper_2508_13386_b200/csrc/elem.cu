@@ -16,6 +16,7 @@
 // eigenproblem is solved in registers by cyclic Jacobi in the Brent-Luk parallel ordering
 // (9 rounds x 4 disjoint rotations per sweep -> 4 independent angle chains for ILP).
 #include "common.cuh"
+#include "fastmath.cuh"
 #include "reduce.cuh"
 
 namespace msim {
@@ -157,29 +158,6 @@ __host__ __device__ constexpr int rr_p(int r, int k) {
 }
 __host__ __device__ constexpr int rr_q(int r, int k) {
   return r < 0 ? 8 - k : (((r + k) % 9) < ((r - k + 9) % 9) ? ((r - k + 9) % 9) : ((r + k) % 9));
-}
-
-// Branch-free fp64 reciprocal / reciprocal square root: MUFU seed + Newton steps (no slow-path
-// subroutine calls, no divergence).  Relative error ~1 ulp for normal inputs.
-__device__ __forceinline__ double rcp_nr(double x) {
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  return fma(y, e, y);
-}
-__device__ __forceinline__ double rsqrt_nr(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const double h = 0.5 * x * y;
-    y = fma(y, fma(-h, y, 0.5), y);   // y += y (0.5 - 0.5 x y^2)
-  }
-  return y;
 }
 
 template <int R>

@@ -121,7 +121,35 @@ void build_mesh_structures(Ctx &c, const double *X, const int32_t *tets, const d
     for (int64_t k = 0; k < (int64_t)16 * nt; ++k) contrib[fill[cslot[k]]++] = (int32_t)k;
   }
 
+  // SELL-32 layout (sell.cuh): slice pointers, per-position column and slot
+  const int32_t nslice = div_up(nv, 32);
+  std::vector<int32_t> sl_ptr(nslice + 1, 0);
+  for (int32_t sl = 0; sl < nslice; ++sl) {
+    int32_t Ls = 0;
+    for (int32_t r = 32 * sl; r < std::min(nv, 32 * sl + 32); ++r) Ls = std::max(Ls, c.h_rowptr[r + 1] - c.h_rowptr[r]);
+    sl_ptr[sl + 1] = sl_ptr[sl] + Ls;
+  }
+  c.npos = (int64_t)sl_ptr[nslice] * 32;
+  std::vector<int32_t> sell_col(c.npos), sell_slot(c.npos, -1);
+  c.h_sell_pos.assign(c.nnzb, 0);
+  for (int32_t sl = 0; sl < nslice; ++sl)
+    for (int32_t l = 0; l < 32; ++l) {
+      const int32_t r = 32 * sl + l;
+      for (int32_t j = 0; j < sl_ptr[sl + 1] - sl_ptr[sl]; ++j) {
+        const int64_t pos = (int64_t)(sl_ptr[sl] + j) * 32 + l;
+        const bool real = r < nv && j < c.h_rowptr[r + 1] - c.h_rowptr[r];
+        sell_col[pos] = real ? colidx[c.h_rowptr[r] + j] : std::min(r, nv - 1);
+        if (real) {
+          sell_slot[pos] = c.h_rowptr[r] + j;
+          c.h_sell_pos[c.h_rowptr[r] + j] = pos;
+        }
+      }
+    }
+
   cudaStream_t s = c.stream;
+  c.sl_ptr.upload(sl_ptr, s);
+  c.sell_col.upload(sell_col, s);
+  c.sell_slot.upload(sell_slot, s);
   c.X.upload(X, 3 * (size_t)nv, s);
   c.tets.upload(tets, 4 * (size_t)nt, s);
   c.Bm.upload(Bm, s);
@@ -137,7 +165,7 @@ void build_mesh_structures(Ctx &c, const double *X, const int32_t *tets, const d
   c.slot_row.upload(slot_row, s);
   c.cptr.upload(cptr, s);
   c.contrib.upload(contrib, s);
-  c.vals.alloc((size_t)9 * c.nnzb);
+  c.vals.alloc((size_t)9 * c.npos);
   c.h_fixed.assign(nv, 0);
   c.fixed.upload(c.h_fixed, s);
   ensure_state_buffers(c);

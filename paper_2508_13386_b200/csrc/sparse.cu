@@ -11,6 +11,7 @@
 // CUDA graph (no host synchronisation inside the loop).
 #include "common.cuh"
 #include "reduce.cuh"
+#include "sell.cuh"
 
 namespace msim {
 
@@ -107,129 +108,108 @@ void launch_vertex_grad(Ctx &c) {
 // ------------------------------------------------------------------ assembly (a4)
 __host__ __device__ constexpr int blk4s(int a, int b) { return a * 4 - (a * (a - 1)) / 2 + (b - a); }
 
+// thread per SELL position (coalesced value writes); slot s = sell_slot[pos] (-1: padding)
 __global__ void __launch_bounds__(256) k_assemble(
-    int64_t nnzb, int nv, const int32_t *__restrict__ rowptr, const int32_t *__restrict__ colidx,
+    int64_t npos, const int32_t *__restrict__ sell_slot, const int32_t *__restrict__ sell_col,
     const int32_t *__restrict__ cptr, const int32_t *__restrict__ contrib,
     const double *__restrict__ stage_h, const double *__restrict__ x, const double *__restrict__ mass,
     const uint8_t *__restrict__ fixed, const int32_t *__restrict__ slot_row, Ground G, double h2,
     double *__restrict__ vals, double *__restrict__ dinv) {
-  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= nnzb) return;
+  const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= npos) return;
+  const int cidx = (int)(pos >> 5), lane = (int)(pos & 31);
+  const int s = sell_slot[pos];
   double acc[9];
 #pragma unroll
   for (int q = 0; q < 9; ++q) acc[q] = 0.0;
-  for (int k = cptr[s]; k < cptr[s + 1]; ++k) {
-    const int code = contrib[k];
-    const int e = code >> 4, a = (code >> 2) & 3, b = code & 3;
-    if (a <= b) {
-      const double *src = stage_h + (size_t)e * 90 + blk4s(a, b) * 9;
+  if (s >= 0) {
+    for (int k = cptr[s]; k < cptr[s + 1]; ++k) {
+      const int code = contrib[k];
+      const int e = code >> 4, a = (code >> 2) & 3, b = code & 3;
+      if (a <= b) {
+        const double *src = stage_h + (size_t)e * 90 + blk4s(a, b) * 9;
 #pragma unroll
-      for (int q = 0; q < 9; ++q) acc[q] += src[q];
-    } else {
-      const double *src = stage_h + (size_t)e * 90 + blk4s(b, a) * 9;
+        for (int q = 0; q < 9; ++q) acc[q] += src[q];
+      } else {
+        const double *src = stage_h + (size_t)e * 90 + blk4s(b, a) * 9;
 #pragma unroll
-      for (int q = 0; q < 9; ++q) acc[q] += src[(q % 3) * 3 + q / 3];
+        for (int q = 0; q < 9; ++q) acc[q] += src[(q % 3) * 3 + q / 3];
+      }
+    }
+    const int row = slot_row[s], col = sell_col[pos];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc[q] *= h2;
+    if (row == col) {
+      const double m = mass[row];
+      acc[0] += m;
+      acc[4] += m;
+      acc[8] += m;
+      if (G.on) {
+        const double d = G.n0 * x[3 * row] + G.n1 * x[3 * row + 1] + G.n2 * x[3 * row + 2] - G.off;
+        const double kb = h2 * G.kappa * bar_d2(d, G.dhat);
+        const double n[3] = {G.n0, G.n1, G.n2};
+#pragma unroll
+        for (int q = 0; q < 9; ++q) acc[q] += kb * n[q / 3] * n[q % 3];
+      }
+    }
+    if (fixed[row] || fixed[col]) {
+#pragma unroll
+      for (int q = 0; q < 9; ++q) acc[q] = (row == col && (q % 4 == 0)) ? 1.0 : 0.0;
+    }
+    if (row == col) {
+      dinv[3 * row + 0] = 1.0 / acc[0];
+      dinv[3 * row + 1] = 1.0 / acc[4];
+      dinv[3 * row + 2] = 1.0 / acc[8];
     }
   }
-  const int row = slot_row[s], col = colidx[s];
 #pragma unroll
-  for (int q = 0; q < 9; ++q) acc[q] *= h2;
-  if (row == col) {
-    const double m = mass[row];
-    acc[0] += m;
-    acc[4] += m;
-    acc[8] += m;
-    if (G.on) {
-      const double d = G.n0 * x[3 * row] + G.n1 * x[3 * row + 1] + G.n2 * x[3 * row + 2] - G.off;
-      const double kb = h2 * G.kappa * bar_d2(d, G.dhat);
-      const double n[3] = {G.n0, G.n1, G.n2};
-#pragma unroll
-      for (int q = 0; q < 9; ++q) acc[q] += kb * n[q / 3] * n[q % 3];
-    }
-  }
-  if (fixed[row] || fixed[col]) {
-#pragma unroll
-    for (int q = 0; q < 9; ++q) acc[q] = (row == col && (q % 4 == 0)) ? 1.0 : 0.0;
-  }
-#pragma unroll
-  for (int q = 0; q < 9; ++q) vals[(size_t)q * nnzb + s] = acc[q];
-  if (row == col) {
-    dinv[3 * row + 0] = 1.0 / acc[0];
-    dinv[3 * row + 1] = 1.0 / acc[4];
-    dinv[3 * row + 2] = 1.0 / acc[8];
-  }
+  for (int q = 0; q < 9; ++q) vals[sell_val_index(cidx, q, lane)] = acc[q];
 }
 
 void launch_assemble(Ctx &c) {
   const int bs = 256;
   const double h2 = c.params.h * c.params.h;
-  k_assemble<<<div_up(c.nnzb, bs), bs, 0, c.stream>>>(c.nnzb, c.nv, c.rowptr, c.colidx, c.cptr,
-                                                      c.contrib, c.stage_h, c.x, c.mass, c.fixed,
-                                                      c.slot_row, ground_of(c), h2, c.vals, c.dinv);
+  k_assemble<<<div_up(c.npos, bs), bs, 0, c.stream>>>(c.npos, c.sell_slot, c.sell_col, c.cptr, c.contrib,
+                                                      c.stage_h, c.x, c.mass, c.fixed, c.slot_row,
+                                                      ground_of(c), h2, c.vals, c.dinv);
   c.launches++;
   MS_CUDA(cudaGetLastError());
 }
 
-// ------------------------------------------------------------------ SpMV
-// Half-warp per block row; lane k handles blocks rowptr[i] + k, k += 16.
-// y = H x               (mode 0)
-// y = b - H x           (mode 1)
-struct BSRView {
-  int nv;
-  int64_t nnzb;
-  const int32_t *__restrict__ rowptr;
-  const int32_t *__restrict__ colidx;
-  const double *__restrict__ vals;
-};
-static BSRView bsr_view(const Ctx &c) { return BSRView{c.nv, c.nnzb, c.rowptr, c.colidx, c.vals}; }
+// ------------------------------------------------------------------ SpMV (SELL-32, thread per row)
+static SellView sell_view(const Ctx &c) { return SellView{c.nv, c.sl_ptr, c.sell_col, c.vals}; }
 
-__device__ __forceinline__ void row_product(const BSRView &H, int row, int sub,
-                                            const double *__restrict__ xin, double out[3]) {
+__device__ __forceinline__ void sell_row_product(const SellView &H, int row, const double *__restrict__ xin,
+                                                 double o[3]) {
+  const int sl = row >> 5, lane = row & 31;
+  const int c0 = __ldg(&H.sl_ptr[sl]), c1 = __ldg(&H.sl_ptr[sl + 1]);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  const bool ok = row < H.nv;
-  const int beg = ok ? H.rowptr[row] : 0, end = ok ? H.rowptr[row + 1] : 0;
-  for (int s = beg + sub; s < end; s += 16) {
-    const int col = H.colidx[s];
+#pragma unroll 4
+  for (int cc = c0; cc < c1; ++cc) {
+    const int col = __ldg(&H.col[(size_t)cc * 32 + lane]);
+    const double *v = H.vals + (size_t)cc * 288 + lane;
     const double x0 = xin[3 * col], x1 = xin[3 * col + 1], x2 = xin[3 * col + 2];
-    const double *v = H.vals + s;
-    const size_t P = (size_t)H.nnzb;
-    a0 = fma(v[0 * P], x0, fma(v[1 * P], x1, fma(v[2 * P], x2, a0)));
-    a1 = fma(v[3 * P], x0, fma(v[4 * P], x1, fma(v[5 * P], x2, a1)));
-    a2 = fma(v[6 * P], x0, fma(v[7 * P], x1, fma(v[8 * P], x2, a2)));
+    a0 = fma(__ldg(v), x0, fma(__ldg(v + 32), x1, fma(__ldg(v + 64), x2, a0)));
+    a1 = fma(__ldg(v + 96), x0, fma(__ldg(v + 128), x1, fma(__ldg(v + 160), x2, a1)));
+    a2 = fma(__ldg(v + 192), x0, fma(__ldg(v + 224), x1, fma(__ldg(v + 256), x2, a2)));
   }
-#pragma unroll
-  for (int o = 8; o > 0; o >>= 1) {
-    a0 += __shfl_down_sync(0xffffffffu, a0, o, 16);
-    a1 += __shfl_down_sync(0xffffffffu, a1, o, 16);
-    a2 += __shfl_down_sync(0xffffffffu, a2, o, 16);
-  }
-  out[0] = a0;
-  out[1] = a1;
-  out[2] = a2;
+  o[0] = a0;
+  o[1] = a1;
+  o[2] = a2;
 }
 
-__global__ void __launch_bounds__(256) k_spmv(BSRView H, const double *__restrict__ xin,
+__global__ void __launch_bounds__(256) k_spmv(SellView H, const double *__restrict__ xin,
                                               double *__restrict__ yout, const double *__restrict__ b) {
-  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
-  const int sub = threadIdx.x & 15;
-  double o[3] = {0.0, 0.0, 0.0};
-  row_product(H, row, sub, xin, o);
-  if (row < H.nv && sub == 0) {
-    if (b) {
-      yout[3 * row] = b[3 * row] - o[0];
-      yout[3 * row + 1] = b[3 * row + 1] - o[1];
-      yout[3 * row + 2] = b[3 * row + 2] - o[2];
-    } else {
-      yout[3 * row] = o[0];
-      yout[3 * row + 1] = o[1];
-      yout[3 * row + 2] = o[2];
-    }
-  }
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= H.nv) return;
+  double o[3];
+  sell_row_product(H, row, xin, o);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) yout[3 * row + i] = b ? b[3 * row + i] - o[i] : o[i];
 }
 
 void launch_spmv(Ctx &c, const double *xin, double *yout, double /*unused*/, const double *b) {
-  const int bs = 256, rows_per_block = bs / 16;
-  k_spmv<<<div_up(c.nv, rows_per_block), bs, 0, c.stream>>>(bsr_view(c), xin, yout, b);
+  k_spmv<<<div_up(c.nv, 256), 256, 0, c.stream>>>(sell_view(c), xin, yout, b);
   c.launches++;
   MS_CUDA(cudaGetLastError());
 }
@@ -266,30 +246,24 @@ __global__ void __launch_bounds__(256) k_pcg_init(int n3, const double *__restri
   }
 }
 
-// half-warp per row, grid-stride over rows; both half-warps of a warp run the same trip count
-// (the shuffles in row_product need the full warp)
-__global__ void __launch_bounds__(256) k_pcg_spmv(BSRView H, const double *__restrict__ z,
+// thread per row (SELL-32); fused direction update and p.q partial
+__global__ void __launch_bounds__(256) k_pcg_spmv(SellView H, const double *__restrict__ z,
                                                   double *__restrict__ p, double *__restrict__ q,
                                                   double *__restrict__ partial, unsigned int *counter,
                                                   double *__restrict__ scal) {
-  const int sub = threadIdx.x & 15;
-  const int hw = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
-  const int hw_stride = (gridDim.x * blockDim.x) >> 4;
   const double beta = scal[SC_BETA];
   double acc[1] = {0.0};
-  for (int base = hw & ~1; base < H.nv; base += hw_stride) {
-    const int row = base + (hw & 1);
-    double o[3] = {0.0, 0.0, 0.0};
-    row_product(H, row, sub, z, o);
-    if (row < H.nv && sub == 0) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row < H.nv) {
+    double o[3];
+    sell_row_product(H, row, z, o);
 #pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const double pn = fma(beta, p[3 * row + i], z[3 * row + i]);
-        const double qn = fma(beta, q[3 * row + i], o[i]);
-        p[3 * row + i] = pn;
-        q[3 * row + i] = qn;
-        acc[0] = fma(pn, qn, acc[0]);
-      }
+    for (int i = 0; i < 3; ++i) {
+      const double pn = fma(beta, p[3 * row + i], z[3 * row + i]);
+      const double qn = fma(beta, q[3 * row + i], o[i]);
+      p[3 * row + i] = pn;
+      q[3 * row + i] = qn;
+      acc[0] = fma(pn, qn, acc[0]);
     }
   }
   double res[1];
@@ -323,13 +297,12 @@ __global__ void __launch_bounds__(256) k_pcg_update(int n3, const double *__rest
   }
 }
 
-static int grid_rows(const Ctx &c) { return std::min(div_up(c.nv, 16), kGridCap); }
 static int grid_vec(int64_t n) { return std::min(div_up(n, 256), kGridCap); }
 
 static void enqueue_pcg_iters(Ctx &c, double *sol, int iters) {
   const int n3 = 3 * c.nv, bs = 256;
   for (int it = 0; it < iters; ++it) {
-    k_pcg_spmv<<<grid_rows(c), bs, 0, c.stream>>>(bsr_view(c), c.z, c.p, c.q, c.partial, c.counters + 3, c.scal);
+    k_pcg_spmv<<<div_up(c.nv, bs), bs, 0, c.stream>>>(sell_view(c), c.z, c.p, c.q, c.partial, c.counters + 3, c.scal);
     k_pcg_update<<<grid_vec(n3), bs, 0, c.stream>>>(n3, c.dinv, c.p, c.q, sol, c.r, c.z, c.partial,
                                                     c.counters + 4, c.scal);
   }
