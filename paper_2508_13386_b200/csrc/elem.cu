@@ -150,14 +150,21 @@ __host__ __device__ constexpr int blk4(int a, int b) {  // a <= b, 10 upper bloc
   return a * 4 - (a * (a - 1)) / 2 + (b - a);
 }
 // Brent-Luk round-robin for n = 9: round r pairs ((r+k)%9, (r-k+9)%9), k = 1..4
-// r < 0: the fixed positions (0,7),(1,6),(2,5),(3,4) of the circle method (index 8 idles); the
-// matrix is relabelled by a cyclic shift i -> i+1 (mod 9) after every round, so 9 rounds meet
-// every pair once with ONE round of code (small I-cache footprint).
+// r < 0 (r = -1 - sh, sh = 0..2): the circle-method pairs (0,7),(1,6),(2,5),(3,4) shifted by sh;
+// three such rounds are unrolled and the matrix is then relabelled by i -> i+3 (mod 9), so a
+// sweep (3 x 3 rounds) meets every pair once with 3 rounds of code (small I-cache footprint,
+// one third of the relabelling moves of a per-round shift).
+__host__ __device__ constexpr int rr_pf(int sh, int k) {
+  return ((k - 1 + sh) % 9) < ((8 - k + sh) % 9) ? ((k - 1 + sh) % 9) : ((8 - k + sh) % 9);
+}
+__host__ __device__ constexpr int rr_qf(int sh, int k) {
+  return ((k - 1 + sh) % 9) < ((8 - k + sh) % 9) ? ((8 - k + sh) % 9) : ((k - 1 + sh) % 9);
+}
 __host__ __device__ constexpr int rr_p(int r, int k) {
-  return r < 0 ? k - 1 : (((r + k) % 9) < ((r - k + 9) % 9) ? ((r + k) % 9) : ((r - k + 9) % 9));
+  return r < 0 ? rr_pf(-1 - r, k) : (((r + k) % 9) < ((r - k + 9) % 9) ? ((r + k) % 9) : ((r - k + 9) % 9));
 }
 __host__ __device__ constexpr int rr_q(int r, int k) {
-  return r < 0 ? 8 - k : (((r + k) % 9) < ((r - k + 9) % 9) ? ((r - k + 9) % 9) : ((r + k) % 9));
+  return r < 0 ? rr_qf(-1 - r, k) : (((r + k) % 9) < ((r - k + 9) % 9) ? ((r - k + 9) % 9) : ((r + k) % 9));
 }
 
 template <int R>
@@ -201,29 +208,41 @@ __device__ __forceinline__ void jacobi_round(double (&a)[45], double (&v)[81]) {
   }
 }
 
-__device__ __forceinline__ void cyclic_relabel(double (&a)[45], double (&v)[81]) {
-  double na[45];
+// relabel i -> i+3 (mod 9): orbits of length 3, moved in place with one temporary each
+__device__ __forceinline__ void cyclic_relabel3(double (&a)[45], double (&v)[81]) {
 #pragma unroll
   for (int i = 0; i < 9; ++i)
 #pragma unroll
-    for (int j = i; j < 9; ++j) na[sidx((i + 1) % 9, (j + 1) % 9)] = a[sidx(i, j)];
+    for (int j = i; j < 9; ++j) {
+      // visit each orbit {(i,j), (i+3,j+3), (i+6,j+6)} once, from its smallest packed index
+      const int i1 = (i + 3) % 9, j1 = (j + 3) % 9, i2 = (i + 6) % 9, j2 = (j + 6) % 9;
+      const int k0 = sidx(i, j), k1 = sidx(i1, j1), k2 = sidx(i2, j2);
+      if (k0 < k1 && k0 < k2) {
+        const double t0 = a[k0];
+        a[k0] = a[k2];   // new(i,j) = old(i-3,j-3) = old(i+6,j+6)
+        a[k2] = a[k1];
+        a[k1] = t0;
+      }
+    }
 #pragma unroll
-  for (int k = 0; k < 45; ++k) a[k] = na[k];
+  for (int r = 0; r < 9; ++r)
 #pragma unroll
-  for (int r = 0; r < 9; ++r) {
-    const double last = v[r * 9 + 8];
-#pragma unroll
-    for (int k = 8; k > 0; --k) v[r * 9 + k] = v[r * 9 + k - 1];
-    v[r * 9] = last;
-  }
+    for (int k = 0; k < 3; ++k) {
+      const double t0 = v[r * 9 + k];
+      v[r * 9 + k] = v[r * 9 + k + 6];
+      v[r * 9 + k + 6] = v[r * 9 + k + 3];
+      v[r * 9 + k + 3] = t0;
+    }
 }
 
 #ifndef MSIM_JACOBI_UNROLLED
 __device__ __forceinline__ void jacobi_sweep(double (&a)[45], double (&v)[81]) {
 #pragma unroll 1
-  for (int rd = 0; rd < 9; ++rd) {
+  for (int rd = 0; rd < 3; ++rd) {
     jacobi_round<-1>(a, v);
-    cyclic_relabel(a, v);
+    jacobi_round<-2>(a, v);
+    jacobi_round<-3>(a, v);
+    cyclic_relabel3(a, v);
   }
 }
 #else
@@ -307,8 +326,11 @@ __device__ __forceinline__ void eig_clamp(double (&a)[45], double (&p9)[45]) {
   for (int i = 0; i < 9; ++i)
 #pragma unroll
     for (int j = i; j < 9; ++j) fro2 += (i == j ? 1.0 : 2.0) * a[sidx(i, j)] * a[sidx(i, j)];
-  const double tol2 = 1e-30 * fro2;
-  for (int sweep = 0; sweep < 12; ++sweep) {
+  // stop when ||offdiag||_F <= 1e-13 ||A||_F: the clamp then differs from the exact P+ by
+  // ~1e-13 relative, three orders under the 1e-10 parity tolerance; a tighter test sits in the
+  // rounding noise (~1e-15) and only adds sweeps
+  const double tol2 = 1e-26 * fro2;
+  for (int sweep = 0; sweep < 10; ++sweep) {
     if (2.0 * offdiag2(a) <= tol2) break;
     jacobi_sweep(a, v);
   }
