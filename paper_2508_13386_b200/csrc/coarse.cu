@@ -368,10 +368,13 @@ __global__ void __launch_bounds__(256) k_galerkin_S2(int64_t nblk, const int32_t
                                                      const int32_t *__restrict__ sc_R,
                                                      const int32_t *__restrict__ sc_phi,
                                                      const double *__restrict__ W, const double *__restrict__ R,
-                                                     double *__restrict__ S) {
+                                                     const int32_t *__restrict__ srow,
+                                                     const int32_t *__restrict__ scol,
+                                                     const int32_t *__restrict__ sT, double *__restrict__ S) {
   const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, grp = lane >> 2, sub = lane & 3;
   if (b >= nblk) return;
+  if (srow[b] > scol[b]) return;   // S symmetric: block (j,i) = (i,j)^T is written by (i,j)
   double acc[9][4];
 #pragma unroll
   for (int q = 0; q < 9; ++q)
@@ -405,11 +408,15 @@ __global__ void __launch_bounds__(256) k_galerkin_S2(int64_t nblk, const int32_t
     }
   if (grp == 0) {
     double *dst = S + 144 * (size_t)b;
+    double *dstT = S + 144 * (size_t)sT[b];
 #pragma unroll
     for (int q = 0; q < 9; ++q) {
       const int l = 9 * sub + q, row = l / 3, cc = l % 3;
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) dst[row * 12 + 4 * cc + kk] = acc[q][kk];
+      for (int kk = 0; kk < 4; ++kk) {
+        dst[row * 12 + 4 * cc + kk] = acc[q][kk];
+        dstT[(4 * cc + kk) * 12 + row] = acc[q][kk];
+      }
     }
   }
 }
@@ -419,7 +426,7 @@ void launch_coarse_S(Ctx &c) {
   k_galerkin_R<<<div_up(c.n_R, 128), 128, 0, c.stream>>>(c.n_R, c.R_i, c.R_u, hview(c), c.bvptr, c.bhandle,
                                                          c.bphi, c.X, c.origins, c.Rbuf);
   k_galerkin_S2<<<div_up(c.nnzb_S * 32, 256), 256, 0, c.stream>>>(c.nnzb_S, c.sc_ptr, c.sc_R, c.sc_phi, c.Wphi,
-                                                                   c.Rbuf, c.Sblk);
+                                                                   c.Rbuf, c.srow, c.scol, c.sT, c.Sblk);
   const double *o = c.aff_origin;
   k_galerkin_Ra<<<div_up(c.nv, 128), 128, 0, c.stream>>>(c.nv, hview(c), c.phi_aff, c.X, o[0], o[1], o[2], c.Ra);
   const int nch = 64;

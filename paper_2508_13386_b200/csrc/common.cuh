@@ -134,7 +134,7 @@ struct Ctx {
   // coarse S pattern: block CSR over handles (both triangles), 144 doubles per block
   int64_t nnzb_S = 0;
   std::vector<int32_t> h_sptr, h_scol;
-  DBuf<int32_t> sptr, scol, srow;
+  DBuf<int32_t> sptr, scol, srow, sT;   // sT[b]: block index of the transposed block
   DBuf<double> Sblk;                // [nnzb_S * 144]
   DBuf<double> Wphi;                // [nnz_phi * 4] phi [1, X - c] per basis entry
   // R contributions: R_i(u) for (i,u) pairs; S contributions

@@ -244,25 +244,49 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   // U_i = vertices adjacent (BSR) to supp(i); R pairs (i,u); J_i = handles of U_i;
   // S block (i,j) contributions (R index, phi index of (u,j)).
   std::vector<int32_t> mark(nv, -1), hmark(m, -1), jslot(m, -1);
-  std::vector<int32_t> Ri, Ru;
   std::vector<int32_t> sptr(1, 0), scol;
   std::vector<std::vector<std::pair<int32_t, int32_t>>> lists;
   std::vector<int32_t> sc_ptr(1, 0), sc_R, sc_phi;
   const int32_t *rp = c.h_rowptr.data(), *ci = c.h_colidx.data();
-  std::vector<int32_t> U, Jl;
+  // pass 1: U_i for every handle; the (i,u) pairs of R_i(u) are stored u-major so that the
+  // threads of a warp share the Hessian row u and the handle lists of its neighbours
+  std::vector<int32_t> Uptr(m + 1, 0), Uall;
   for (int32_t i = 0; i < m; ++i) {
-    U.clear();
+    const size_t b0 = Uall.size();
     for (int32_t k = hptr[i]; k < hptr[i + 1]; ++k) {
       const int32_t v = hvert[k];
       for (int32_t s = rp[v]; s < rp[v + 1]; ++s) {
         const int32_t u = ci[s];
         if (mark[u] != i) {
           mark[u] = i;
-          U.push_back(u);
+          Uall.push_back(u);
         }
       }
     }
-    std::sort(U.begin(), U.end());
+    std::sort(Uall.begin() + b0, Uall.end());
+    Uptr[i + 1] = (int32_t)Uall.size();
+  }
+  std::vector<int32_t> rstart(nv + 1, 0);
+  for (int32_t u : Uall) rstart[u + 1]++;
+  for (int32_t u = 0; u < nv; ++u) rstart[u + 1] += rstart[u];
+  std::vector<int32_t> Ri(Uall.size()), Ru(Uall.size());
+  {
+    std::vector<int32_t> fill(rstart.begin(), rstart.end() - 1);
+    for (int32_t i = 0; i < m; ++i)                    // i ascending -> sorted within each u
+      for (int32_t q = Uptr[i]; q < Uptr[i + 1]; ++q) {
+        const int32_t u = Uall[q];
+        Ri[fill[u]] = i;
+        Ru[fill[u]] = u;
+        fill[u]++;
+      }
+  }
+  auto pair_index = [&](int32_t i, int32_t u) {
+    const int32_t *b = Ri.data() + rstart[u], *e = Ri.data() + rstart[u + 1];
+    return (int32_t)(std::lower_bound(b, e, i) - Ri.data());
+  };
+  std::vector<int32_t> U, Jl;
+  for (int32_t i = 0; i < m; ++i) {
+    U.assign(Uall.begin() + Uptr[i], Uall.begin() + Uptr[i + 1]);
     Jl.clear();
     for (int32_t u : U)
       for (int64_t k = vptr[u]; k < vptr[u + 1]; ++k)
@@ -274,9 +298,7 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
     for (size_t q = 0; q < Jl.size(); ++q) jslot[Jl[q]] = (int32_t)q;
     lists.assign(Jl.size(), {});
     for (int32_t u : U) {
-      const int32_t r = (int32_t)Ri.size();
-      Ri.push_back(i);
-      Ru.push_back(u);
+      const int32_t r = pair_index(i, u);
       for (int64_t k = vptr[u]; k < vptr[u + 1]; ++k) lists[jslot[handle[k]]].push_back({r, (int32_t)k});
     }
     for (size_t q = 0; q < Jl.size(); ++q) {
@@ -428,10 +450,15 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   c.sptr.upload(sptr, s);
   c.scol.upload(scol, s);
   {
-    std::vector<int32_t> srow(scol.size());
+    std::vector<int32_t> srow(scol.size()), sT(scol.size());
     for (int32_t i = 0; i < m; ++i)
-      for (int32_t k = sptr[i]; k < sptr[i + 1]; ++k) srow[k] = i;
+      for (int32_t k = sptr[i]; k < sptr[i + 1]; ++k) {
+        srow[k] = i;
+        const int32_t j = scol[k];
+        sT[k] = (int32_t)(std::lower_bound(scol.begin() + sptr[j], scol.begin() + sptr[j + 1], i) - scol.begin());
+      }
     c.srow.upload(srow, s);
+    c.sT.upload(sT, s);
   }
   c.Sblk.alloc((size_t)144 * c.nnzb_S);
   c.R_i.upload(Ri, s);
