@@ -71,7 +71,7 @@ __device__ void diag_factor(int k, int nSp, double *__restrict__ L, double *__re
       for (int j = 0; j < 16; ++j) {
         const double d = __shfl_sync(0xffffffffu, a[j], j);
         if (!(d > 0.0)) bad = true;
-        const double inv = d > 0.0 ? rsqrt_nr(d) : 1.0;   // 1 / sqrt(d)
+        const double inv = d > 0.0 ? rsqrt_nr2(d) : 1.0;   // 1 / sqrt(d)
         const double ljj = d > 0.0 ? d * inv : 1.0;
         if (lane == 0) invd[j0 + j] = inv;
         a[j] = lane == j ? ljj : (lane > j ? a[j] * inv : a[j]);
@@ -93,11 +93,21 @@ __device__ void diag_factor(int k, int nSp, double *__restrict__ L, double *__re
     // trailing update of rows/cols >= j0 + 16
     const int s0 = j0 + 16;
     for (int r = s0 + (t >> 2); r < TB; r += 64) {
-      for (int c = s0 + (t & 3); c <= r; c += 4) {
-        double s = 0.0;
+      for (int c = s0 + (t & 3); c <= r; c += 8) {   // two columns, four partial sums each
+        const bool two = c + 4 <= r;
+        double s0a = 0.0, s1a = 0.0, s0b = 0.0, s1b = 0.0;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) s = fma(A[r * LD + j0 + j], A[c * LD + j0 + j], s);
-        A[r * LD + c] -= s;
+        for (int j = 0; j < 16; j += 2) {
+          const double x0 = A[r * LD + j0 + j], x1 = A[r * LD + j0 + j + 1];
+          s0a = fma(x0, A[c * LD + j0 + j], s0a);
+          s1a = fma(x1, A[c * LD + j0 + j + 1], s1a);
+          if (two) {
+            s0b = fma(x0, A[(c + 4) * LD + j0 + j], s0b);
+            s1b = fma(x1, A[(c + 4) * LD + j0 + j + 1], s1b);
+          }
+        }
+        A[r * LD + c] -= s0a + s1a;
+        if (two) A[r * LD + c + 4] -= s0b + s1b;
       }
     }
     __syncthreads();
@@ -109,10 +119,13 @@ __device__ void diag_factor(int k, int nSp, double *__restrict__ L, double *__re
     double x[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      double s = r == lane ? 1.0 : 0.0;
+      double s = r == lane ? 1.0 : 0.0, s2 = 0.0;
 #pragma unroll
-      for (int q = 0; q < r; ++q) s = fma(-A[(o + r) * LD + o + q], x[q], s);
-      x[r] = s * invd[o + r];
+      for (int q = 0; q < r; q += 2) {
+        s = fma(-A[(o + r) * LD + o + q], x[q], s);
+        if (q + 1 < r) s2 = fma(-A[(o + r) * LD + o + q + 1], x[q + 1], s2);
+      }
+      x[r] = (s + s2) * invd[o + r];
     }
 #pragma unroll
     for (int r = 0; r < 16; ++r) Li[(o + r) * LD + o + lane] = x[r];
@@ -122,17 +135,20 @@ __device__ void diag_factor(int k, int nSp, double *__restrict__ L, double *__re
   for (int p = 1; p < 4; ++p) {
     for (int e = t; e < p * 256; e += 256) {
       const int q = e >> 8, r = (e >> 4) & 15, cc = e & 15;
-      double s = 0.0;
-      for (int m = 16 * q; m < 16 * p; ++m) s = fma(A[(16 * p + r) * LD + m], Li[m * LD + 16 * q + cc], s);
-      Tb[q][r][cc] = s;
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int m = 16 * q; m < 16 * p; m += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s4[u] = fma(A[(16 * p + r) * LD + m + u], Li[(m + u) * LD + 16 * q + cc], s4[u]);
+      }
+      Tb[q][r][cc] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
     }
     __syncthreads();
     for (int e = t; e < p * 256; e += 256) {
       const int q = e >> 8, r = (e >> 4) & 15, cc = e & 15;
-      double s = 0.0;
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int m = 0; m < 16; ++m) s = fma(Li[(16 * p + r) * LD + 16 * p + m], Tb[q][m][cc], s);
-      Li[(16 * p + r) * LD + 16 * q + cc] = -s;
+      for (int m = 0; m < 16; ++m) s4[m & 3] = fma(Li[(16 * p + r) * LD + 16 * p + m], Tb[q][m][cc], s4[m & 3]);
+      Li[(16 * p + r) * LD + 16 * q + cc] = -((s4[0] + s4[1]) + (s4[2] + s4[3]));
     }
     __syncthreads();
   }
@@ -141,8 +157,8 @@ __device__ void diag_factor(int k, int nSp, double *__restrict__ L, double *__re
 #pragma unroll 4
   for (int it = 0; it < 16; ++it) {
     const int e = t + it * 256, r = e & 63, c = e >> 6;
-    if (r >= c) L[okk + (size_t)c * nSp + r] = A[r * LD + c];
-    Uk[(size_t)c * TB + r] = Li[r * LD + c];   // U[c][r] = Li[r][c]
+    if (r >= c) __stcg(&L[okk + (size_t)c * nSp + r], A[r * LD + c]);
+    __stcg(&Uk[(size_t)c * TB + r], Li[r * LD + c]);   // U[c][r] = Li[r][c]
   }
 }
 
@@ -159,13 +175,17 @@ __device__ __forceinline__ void gemm64(const double *S1, const double *S2, doubl
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  // thread (tr, tc) = (t & 15, t >> 4) owns rows tr + 16a and columns tc + 16b: for each a the
+  // 16 lanes of a half-warp read 16 consecutive doubles (one conflict-free wavefront) and the
+  // other half-warp the same addresses (broadcast); the column operand is a 2-address broadcast.
 #pragma unroll 4
   for (int kk = 0; kk < TB; ++kk) {
-    const double2 x01 = *reinterpret_cast<const double2 *>(&S1[kk * TB + tr]);
-    const double2 x23 = *reinterpret_cast<const double2 *>(&S1[kk * TB + tr + 2]);
-    const double2 y01 = *reinterpret_cast<const double2 *>(&S2[kk * TB + tc]);
-    const double2 y23 = *reinterpret_cast<const double2 *>(&S2[kk * TB + tc + 2]);
-    const double x[4] = {x01.x, x01.y, x23.x, x23.y}, y[4] = {y01.x, y01.y, y23.x, y23.y};
+    double x[4], y[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      x[a] = S1[kk * TB + tr + 16 * a];
+      y[a] = S2[kk * TB + tc + 16 * a];
+    }
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -174,11 +194,22 @@ __device__ __forceinline__ void gemm64(const double *S1, const double *S2, doubl
 }
 
 // stage a column-major global tile (leading dim nSp) into k-major smem S[kk*64 + r] (cp.async)
+// cp.async.cg: 16-byte global -> shared copy through L2 only (L1 is not coherent across SMs, and
+// the dataflow kernel reads tiles other CTAs wrote during the same launch)
+__device__ __forceinline__ void cp_async_cg16(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit_wait() {
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void stage_colmajor(double *S, const double *__restrict__ G, int ld) {
 #pragma unroll
   for (int it = 0; it < (TB * TB / 2) / 256; ++it) {
     const int e2 = threadIdx.x + it * 256, kk = e2 >> 5, r2 = (e2 & 31) * 2;
-    __pipeline_memcpy_async(&S[kk * TB + r2], &G[(size_t)kk * ld + r2], 16);
+    cp_async_cg16(&S[kk * TB + r2], &G[(size_t)kk * ld + r2]);
   }
 }
 
@@ -194,13 +225,13 @@ __global__ void __launch_bounds__(256) k_chol_trsm(int k, const int32_t *__restr
   __pipeline_commit();
   __pipeline_wait_prior(0);
   __syncthreads();
-  const int tr = (t & 15) * 4, tc = (t >> 4) * 4;
+  const int tr = t & 15, tc = t >> 4;
   double acc[4][4];
   gemm64(SA, SU, acc, tr, tc);
 #pragma unroll
   for (int b = 0; b < 4; ++b)
 #pragma unroll
-    for (int a = 0; a < 4; ++a) L[oik + (size_t)(tc + b) * nSp + tr + a] = acc[a][b];
+    for (int a = 0; a < 4; ++a) L[oik + (size_t)(tc + 16 * b) * nSp + tr + 16 * a] = acc[a][b];
 }
 
 // ------------------------------------------------------------------ U(k): A_ij -= L_ik L_jk^T
@@ -219,13 +250,13 @@ __global__ void __launch_bounds__(256) k_chol_update(int k, const int32_t *__res
   stage_colmajor(Si, L + tile_off(i, k, nSp), nSp);
   stage_colmajor(Sj, L + tile_off(j, k, nSp), nSp);
   __pipeline_commit();
-  const int tr = (t & 15) * 4, tc = (t >> 4) * 4;
+  const int tr = t & 15, tc = t >> 4;
   const size_t oij = tile_off(i, j, nSp);
   double old[4][4];
 #pragma unroll
   for (int b = 0; b < 4; ++b)
 #pragma unroll
-    for (int a = 0; a < 4; ++a) old[a][b] = L[oij + (size_t)(tc + b) * nSp + tr + a];
+    for (int a = 0; a < 4; ++a) old[a][b] = L[oij + (size_t)(tc + 16 * b) * nSp + tr + 16 * a];
   __pipeline_wait_prior(0);
   __syncthreads();
   double acc[4][4];
@@ -234,12 +265,102 @@ __global__ void __launch_bounds__(256) k_chol_update(int k, const int32_t *__res
   for (int b = 0; b < 4; ++b)
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-      const int r = tr + a, c = tc + b;
+      const int r = tr + 16 * a, c = tc + 16 * b;
       if (i != j || r >= c) L[oij + (size_t)c * nSp + r] = old[a][b] - acc[a][b];
     }
   if (i == la && j == la) {
     __syncthreads();
     diag_factor(la, nSp, L, U, flag, sm);
+  }
+}
+
+// ------------------------------------------------------------------ dataflow factorisation
+// One cooperative launch runs the whole tile DAG: task t is executed by CTA t mod G in task
+// order; a task waits only on tasks that precede it in the (topological) task order, so the
+// earliest unfinished task is always runnable (all CTAs are co-resident).  Tasks:
+//   D(k):     wait upd[k][k] == need;         factor + invert the diagonal tile;   dfl[k] = 1
+//   P(i,k):   wait dfl[k], upd[i][k] == need; L_ik = A_ik U_kk;                     pfl[i][k] = 1
+//   U(i,j,k): wait pfl[i][k], pfl[j][k], upd[i][j] == rank (updates of a tile are applied in
+//             step order -> deterministic);  A_ij -= L_ik L_jk^T;               upd[i][j] = rank + 1
+// Tile data produced by other CTAs is read through L2 only (cp.async.cg / ld.global.cg).
+__device__ __forceinline__ void df_wait(const int *p, int val) {
+  if (threadIdx.x == 0) {
+    const volatile int *f = p;
+    while (*f != val) __nanosleep(20);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void df_signal(int *p, int val) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicExch(p, val);
+  }
+}
+
+__global__ void __launch_bounds__(256, 2) k_chol_dataflow(int ntask, const int4 *__restrict__ tasks, int NT, int nSp,
+                                                       double *__restrict__ L, double *__restrict__ U,
+                                                       int *__restrict__ upd, int *__restrict__ dfl,
+                                                       int *__restrict__ pfl, int *__restrict__ flag) {
+  extern __shared__ double sm[];
+  const int t = threadIdx.x, tr = t & 15, tc = t >> 4;
+  for (int id = blockIdx.x; id < ntask; id += gridDim.x) {
+    const int4 tk = tasks[id];
+    const int type = tk.x, i = tk.y, j = tk.z & 0xffff, k = tk.z >> 16, cnt = tk.w;
+    if (type == 0) {
+      df_wait(&upd[k * NT + k], cnt);
+      diag_factor(k, nSp, L, U, flag, sm);
+      df_signal(&dfl[k], 1);
+    } else if (type == 1) {
+      df_wait(&dfl[k], 1);
+      df_wait(&upd[i * NT + k], cnt);
+      double *SA = sm, *SU = sm + TB * TB;
+      const size_t oik = tile_off(i, k, nSp);
+      stage_colmajor(SA, L + oik, nSp);
+      stage_colmajor(SU, U + (size_t)k * TB * TB, TB);
+      cp_async_commit_wait();
+      __syncthreads();
+      double acc[4][4];
+      gemm64(SA, SU, acc, tr, tc);
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) __stcg(&L[oik + (size_t)(tc + 16 * b) * nSp + tr + 16 * a], acc[a][b]);
+      df_signal(&pfl[i * NT + k], 1);
+    } else {
+      df_wait(&pfl[i * NT + k], 1);
+      df_wait(&pfl[j * NT + k], 1);
+      double *Si = sm, *Sj = sm + TB * TB;
+      stage_colmajor(Si, L + tile_off(i, k, nSp), nSp);
+      stage_colmajor(Sj, L + tile_off(j, k, nSp), nSp);
+      df_wait(&upd[i * NT + j], cnt);
+      const size_t oij = tile_off(i, j, nSp);
+      double old[4][4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) old[a][b] = __ldcg(&L[oij + (size_t)(tc + 16 * b) * nSp + tr + 16 * a]);
+      cp_async_commit_wait();
+      __syncthreads();
+      double acc[4][4];
+      gemm64(Si, Sj, acc, tr, tc);
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const int r = tr + 16 * a, c = tc + 16 * b;
+          if (i != j || r >= c) __stcg(&L[oij + (size_t)c * nSp + r], old[a][b] - acc[a][b]);
+        }
+      if (type == 3) {   // fused U(k+1,k+1,k) + D(k+1): the updated diagonal tile is factorised at once
+        __syncthreads();
+        diag_factor(i, nSp, L, U, flag, sm);
+        df_signal(&dfl[i], 1);
+      }
+      df_signal(&upd[i * NT + j], cnt + 1);
+    }
+    __syncthreads();
   }
 }
 
@@ -389,12 +510,36 @@ static bool step_updates_diag(const Ctx &c, int k) {   // is tile (k+1, k+1) amo
   return !P.empty() && P.front() == k + 1;
 }
 
-// D(0); then for each k: P(k), U(k) with D(k+1) fused (look-ahead)
+static int dataflow_grid(const Ctx &c) {
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    MS_CUDA(cudaFuncSetAttribute(k_chol_dataflow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem));
+    MS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chol_dataflow, 256, kUpdSmem));
+    per_sm = std::max(per_sm, 1);
+  }
+  return (int)std::min<int64_t>(c.n_dag, (int64_t)per_sm * c.coop_grid);
+}
+
+// D(0); then for each k: P(k), U(k) with D(k+1) fused (look-ahead) -- or the single-launch
+// dataflow version (default)
 void enqueue_chol_factor(Ctx &c) {
   const int nSp = c.nS_pad;
   k_zero_tiles<<<(int)c.n_sym_tiles, 256, 0, c.stream>>>(c.sym_tiles, nSp, c.Lden);
   launch_scatter_S(c);
   if (nSp > c.nS) k_pad_identity2<<<div_up(nSp - c.nS, 64), 64, 0, c.stream>>>(c.nS, nSp, c.Lden);
+  if (c.chol_dataflow) {
+    const int NT = c.ntiles;
+    MS_CUDA(cudaMemsetAsync(c.df_flags, 0, sizeof(int) * ((size_t)2 * NT * NT + NT), c.stream));
+    int ntask = (int)c.n_dag, NTv = NT, nSpv = nSp;
+    const int4 *tk = reinterpret_cast<const int4 *>(c.chol_dag.p);
+    double *Lp = c.Lden, *Up = c.Uinv;
+    int *upd = c.df_flags, *pfl = c.df_flags + (size_t)NT * NT, *dfl = c.df_flags + (size_t)2 * NT * NT;
+    int *fl = c.flags + 0;
+    void *args[] = {&ntask, &tk, &NTv, &nSpv, &Lp, &Up, &upd, &dfl, &pfl, &fl};
+    MS_CUDA(cudaLaunchCooperativeKernel((const void *)k_chol_dataflow, dim3(dataflow_grid(c)), dim3(256), args,
+                                        kUpdSmem, c.stream));
+    return;
+  }
   k_chol_diag<<<1, 256, kDiagSmem, c.stream>>>(0, nSp, c.Lden, c.Uinv, c.flags + 0);
   for (int k = 0; k < c.ntiles; ++k) {
     const int np = (int)c.h_chol_panel[k].size();
@@ -409,6 +554,7 @@ void enqueue_chol_factor(Ctx &c) {
 }
 
 int64_t chol_factor_kernels(const Ctx &c) {
+  if (c.chol_dataflow) return 3 + (c.nS_pad > c.nS ? 1 : 0);
   int64_t n = 3 + (c.nS_pad > c.nS ? 1 : 0);
   for (int k = 0; k < c.ntiles; ++k) {
     const int nt = (int)(c.h_chol_task_off[k + 1] - c.h_chol_task_off[k]);

@@ -166,6 +166,10 @@ struct Ctx {
   int64_t n_sym_tiles = 0;
   DBuf<double> Uinv;                // [ntiles][64*64] U_kk = L_kk^-T (column-major)
   DBuf<int> solve_flags;            // [2 ntiles] tile-ready flags of the cooperative solves
+  DBuf<int32_t> chol_dag;           // dataflow factorisation tasks (int4 each)
+  int64_t n_dag = 0;
+  DBuf<int> df_flags;               // upd[NT*NT], pfl[NT*NT], dfl[NT]
+  bool chol_dataflow = true;
   int coop_grid = 148;
   cudaGraphExec_t factor_graph = nullptr, solve_graph = nullptr;
   int64_t factor_graph_kernels = 0, solve_graph_kernels = 0;

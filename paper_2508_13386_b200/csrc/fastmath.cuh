@@ -26,4 +26,16 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   return y;
 }
 
+// two Newton steps: enough from the MUFU seed for ~1-2 ulp
+__device__ __forceinline__ double rsqrt_nr2(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double h = 0.5 * x * y;
+    y = fma(y, fma(-h, y, 0.5), y);
+  }
+  return y;
+}
+
 }  // namespace msim

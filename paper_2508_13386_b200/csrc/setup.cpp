@@ -437,6 +437,39 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   }
   c.n_sym_tiles = (int64_t)sym_tiles.size() / 2;
 
+  // dataflow task list (chol.cu k_chol_dataflow): D(0); per k: P(.,k); U(.,k+1,k); D(k+1); U(rest,k)
+  std::vector<int32_t> dag;
+  {
+    std::vector<int32_t> nupd((size_t)NT * NT, 0);
+    auto emit = [&](int type, int i, int j, int k, int cnt) {
+      dag.push_back(type);
+      dag.push_back(i);
+      dag.push_back(j | (k << 16));
+      dag.push_back(cnt);
+    };
+    MS_REQUIRE(NT < 32768, MS_ERR_ARG, "coarse matrix too large for the tile DAG encoding");
+    emit(0, 0, 0, 0, 0);
+    for (int32_t k = 0; k < NT; ++k) {
+      const auto &P = best.panel[k];
+      for (int32_t i : P) emit(1, i, 0, k, nupd[(size_t)i * NT + k]);
+      const bool next_in = !P.empty() && P.front() == k + 1;
+      if (next_in)
+        for (size_t a = 0; a < P.size(); ++a) {       // column k+1: (P[a], k+1); the diagonal tile
+          const int32_t i = P[a];                      // update is fused with D(k+1) (type 3)
+          emit(a == 0 ? 3 : 2, i, k + 1, k, nupd[(size_t)i * NT + k + 1]++);
+        }
+      else if (k + 1 < NT)
+        emit(0, 0, 0, k + 1, nupd[(size_t)(k + 1) * NT + k + 1]);
+      for (size_t a = 0; a < P.size(); ++a)
+        for (size_t b = 0; b <= a; ++b) {
+          const int32_t i = P[a], j = P[b];
+          if (next_in && j == k + 1) continue;
+          emit(2, i, j, k, nupd[(size_t)i * NT + j]++);
+        }
+    }
+  }
+  c.n_dag = (int64_t)dag.size() / 4;
+
   cudaStream_t s = c.stream;
   c.origins.upload(origins, 3 * (size_t)m, s);
   c.bvptr.upload(bvptr, s);
@@ -475,6 +508,8 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   c.chol_rows_ptr.upload(rows_ptr, s);
   c.chol_panel_ptr.upload(panel_ptr, s);
   c.sym_tiles.upload(sym_tiles, s);
+  c.chol_dag.upload(dag, s);
+  c.df_flags.alloc((size_t)2 * NT * NT + NT);
   c.Uinv.alloc((size_t)NT * T * T);
   c.solve_flags.alloc(2 * (size_t)NT);
   {
