@@ -31,6 +31,108 @@ __device__ __forceinline__ size_t tile_off(int ti, int tj, int nSp) {
 // smem: A [64][LD], Li [64][LD], Tb [3*16*17], invd [64]
 constexpr int kDiagSmemDoubles = 2 * TB * LD + 3 * 16 * 17 + TB;
 
+// Register-blocked right-looking Cholesky of the 64x64 diagonal tile with the inverse built in
+// the same sweep (Gauss-Jordan on [L | I]): L = L_0 ... L_63 with L_j the identity whose column j
+// is l_j, so L^-1 = L_63^-1 ... L_0^-1 and applying L_j^-1 from the left is
+//   Z_j <- Z_j / l_jj,   Z_r <- Z_r - (l_rj / l_jj) Z_j^old  (r > j).
+// Thread t = rb + 16 cb owns the 4x4 blocks (rows 4rb.., cols 4cb..) of A and of Z; the 16
+// owners of column j form one half-warp, so the pivot is a shuffle and each step needs ONE
+// barrier (the pivot column and row j of Z are double-buffered in shared memory).
+__device__ void diag_factor_gj(int k, int nSp, double *__restrict__ L, double *__restrict__ U,
+                               int *__restrict__ flag, double *sm) {
+  double *colL = sm;          // [2][64] pivot column l_.j (zero above the diagonal)
+  double *rowZ = sm + 128;    // [2][64] row j of Z before scaling
+  double *sinv = sm + 256;    // [2]     1 / l_jj
+  const int t = threadIdx.x, rb = t & 15, cb = t >> 4, lane = t & 31;
+  const int r0 = 4 * rb, c0 = 4 * cb;
+  const size_t okk = tile_off(k, k, nSp);
+  double a[4][4], z[4][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int r = r0 + p, c = c0 + q;
+      a[p][q] = r >= c ? __ldcg(&L[okk + (size_t)c * nSp + r]) : 0.0;
+      z[p][q] = r == c ? 1.0 : 0.0;
+    }
+  if (rb == 0) {   // row 0 of Z = e_0
+#pragma unroll
+    for (int q = 0; q < 4; ++q) rowZ[c0 + q] = (c0 + q == 0) ? 1.0 : 0.0;
+  }
+  bool bad = false;
+#pragma unroll 1
+  for (int j = 0; j < TB; ++j) {
+    const int buf = j & 1, jb = j >> 2, jq = j & 3;
+    // phase A: the half-warp owning column j (cb == jb) forms l_.j
+    if (cb == jb) {
+      double mine = 0.0;
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q == jq && p == jq) mine = a[p][q];
+      const double d = __shfl_sync(0xffffu << (lane & 16), mine, (lane & 16) + jb, 32);
+      const bool ok = d > 0.0;
+      if (!ok) bad = true;
+      const double inv = ok ? rsqrt_nr2(d) : 1.0;
+      const double ljj = ok ? d * inv : 1.0;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const int r = r0 + p;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q == jq) {
+            const double l = r > j ? a[p][q] * inv : (r == j ? ljj : 0.0);
+            a[p][q] = l;
+            colL[buf * 64 + r] = l;
+          }
+      }
+      if (rb == 0) sinv[buf] = inv;
+    }
+    __syncthreads();
+    // phase B: trailing update of A and Z
+    const double inv = sinv[buf];
+    double lr[4], lc[4], zj[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      lr[p] = colL[buf * 64 + r0 + p];
+      lc[p] = (c0 + p > j) ? colL[buf * 64 + c0 + p] : 0.0;
+      zj[p] = rowZ[buf * 64 + c0 + p];
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int r = r0 + p;
+      const double fz = r > j ? lr[p] * inv : 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a[p][q] = fma(-lr[p], lc[q], a[p][q]);   // lc = 0 for c <= j; lr = 0 for r < j
+        z[p][q] = fma(-fz, zj[q], z[p][q]);
+        if (r == j) z[p][q] *= inv;
+      }
+    }
+    // row j+1 of Z is final now: publish it for the next step
+    if (j + 1 < TB && rb == ((j + 1) >> 2)) {
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+        if (r0 + p == j + 1)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) rowZ[(buf ^ 1) * 64 + c0 + q] = z[p][q];
+    }
+  }
+  if (bad && flag) *flag = 1;
+  // store L_kk (lower, column-major) and U_kk = Z^T (row-major: U[c][r] at c*64 + r = Z[r][c])
+  double *Uk = U + (size_t)k * TB * TB;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int r = r0 + p, c = c0 + q;
+      if (r >= c) __stcg(&L[okk + (size_t)c * nSp + r], a[p][q]);
+      __stcg(&Uk[(size_t)c * TB + r], z[p][q]);
+    }
+  __syncthreads();
+}
+
 __device__ void diag_factor(int k, int nSp, double *__restrict__ L, double *__restrict__ U,
                             int *__restrict__ flag, double *sm) {
   double *A = sm;              // row-major [64][LD]: the factor
@@ -313,6 +415,50 @@ __global__ void __launch_bounds__(256, 2) k_chol_dataflow(int ntask, const int4 
       df_wait(&upd[k * NT + k], cnt);
       diag_factor(k, nSp, L, U, flag, sm);
       df_signal(&dfl[k], 1);
+    } else if (type == 4) {
+      // critical-path task of step k (i = k+1): P(i,k), U(i,i,k) and D(i) in one CTA.
+      // cnt = updates tile (i,k) must have seen; tk.w >> 16 unused; rank of (i,i) is upd order
+      df_wait(&dfl[k], 1);
+      df_wait(&upd[i * NT + k], cnt & 0xffff);
+      double *SA = sm, *SU = sm + TB * TB;
+      const size_t oik = tile_off(i, k, nSp);
+      stage_colmajor(SA, L + oik, nSp);
+      stage_colmajor(SU, U + (size_t)k * TB * TB, TB);
+      cp_async_commit_wait();
+      __syncthreads();
+      double acc[4][4];
+      gemm64(SA, SU, acc, tr, tc);
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) __stcg(&L[oik + (size_t)(tc + 16 * b) * nSp + tr + 16 * a], acc[a][b]);
+      df_signal(&pfl[i * NT + k], 1);             // panel tile published early for the other updates
+      // X = L_ik into k-major smem: SX[c*64 + r] = X[r][c]
+      double *SX = sm;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) SX[(tc + 16 * b) * TB + tr + 16 * a] = acc[a][b];
+      df_wait(&upd[i * NT + i], cnt >> 16);
+      const size_t oii = tile_off(i, i, nSp);
+      double old[4][4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) old[a][b] = __ldcg(&L[oii + (size_t)(tc + 16 * b) * nSp + tr + 16 * a]);
+      __syncthreads();
+      gemm64(SX, SX, acc, tr, tc);
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const int r = tr + 16 * a, c = tc + 16 * b;
+          if (r >= c) __stcg(&L[oii + (size_t)c * nSp + r], old[a][b] - acc[a][b]);
+        }
+      __syncthreads();
+      diag_factor(i, nSp, L, U, flag, sm);
+      df_signal(&dfl[i], 1);
+      df_signal(&upd[i * NT + i], (cnt >> 16) + 1);
     } else if (type == 1) {
       df_wait(&dfl[k], 1);
       df_wait(&upd[i * NT + k], cnt);

@@ -451,12 +451,19 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
     emit(0, 0, 0, 0, 0);
     for (int32_t k = 0; k < NT; ++k) {
       const auto &P = best.panel[k];
-      for (int32_t i : P) emit(1, i, 0, k, nupd[(size_t)i * NT + k]);
       const bool next_in = !P.empty() && P.front() == k + 1;
+      if (next_in) {   // critical path first: P(k+1,k) + U(k+1,k+1,k) + D(k+1) in one task (type 4)
+        const int32_t need = nupd[(size_t)(k + 1) * NT + k];
+        const int32_t rank = nupd[(size_t)(k + 1) * NT + k + 1]++;
+        MS_REQUIRE(need < 65536 && rank < 65536, MS_ERR_ARG, "tile DAG counter overflow");
+        emit(4, k + 1, k + 1, k, need | (rank << 16));
+      }
+      for (int32_t i : P)
+        if (!(next_in && i == k + 1)) emit(1, i, 0, k, nupd[(size_t)i * NT + k]);
       if (next_in)
-        for (size_t a = 0; a < P.size(); ++a) {       // column k+1: (P[a], k+1); the diagonal tile
-          const int32_t i = P[a];                      // update is fused with D(k+1) (type 3)
-          emit(a == 0 ? 3 : 2, i, k + 1, k, nupd[(size_t)i * NT + k + 1]++);
+        for (size_t a = 1; a < P.size(); ++a) {       // rest of column k+1
+          const int32_t i = P[a];
+          emit(2, i, k + 1, k, nupd[(size_t)i * NT + k + 1]++);
         }
       else if (k + 1 < NT)
         emit(0, 0, 0, k + 1, nupd[(size_t)(k + 1) * NT + k + 1]);
@@ -509,6 +516,10 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   c.chol_panel_ptr.upload(panel_ptr, s);
   c.sym_tiles.upload(sym_tiles, s);
   c.chol_dag.upload(dag, s);
+  {
+    const char *e = std::getenv("MSIM_CHOL_DATAFLOW");   // 0: per-step launches (diagnostics)
+    c.chol_dataflow = !(e && e[0] == '0');
+  }
   c.df_flags.alloc((size_t)2 * NT * NT + NT);
   c.Uinv.alloc((size_t)NT * T * T);
   c.solve_flags.alloc(2 * (size_t)NT);
