@@ -9,10 +9,10 @@
 // Coordinates of handle i: q_i[4c + k], c = x,y,z row, k = monomial [1, X-c_i].  The 3x12
 // block of (v, i) is I3 kron w_vi^T with w_vi = phi_i(v) [1, X_v - c_i].
 //
-// S = B^T H B is formed in two deterministic passes (no atomics):
+// S = B^T H B is formed by one fused kernel (one CTA per handle i, no atomics):
 //   R_i(u)[(c',k'), c] = sum_{v in N(u), i in supp(v)} w_vi[k'] H_vu[c'][c]     (36 per (i,u))
-//   S_ij[(c',k'), (c,k)] = sum_{u in U_i, j in supp(u)} R_i(u)[(c',k'), c] w_uj[k]
-// with (i,u) pairs and per-S-block contribution lists precomputed at ms_basis_upload.
+//   S_ij[(c',k'), (c,k)] = sum_{u in U_i, j in supp(u)} R_i(u)[(c',k'), c] w_uj[k]   (j >= i)
+// with R_i(u) held in shared memory chunk by chunk; the lists are precomputed at ms_basis_upload.
 #include "common.cuh"
 #include "reduce.cuh"
 
@@ -125,92 +125,155 @@ struct HView {                      // SELL-32 Hessian (sell.cuh)
   const double *__restrict__ vals;
 };
 
-// R_i(u) for every (i,u) pair: thread per pair.
-__global__ void __launch_bounds__(128) k_galerkin_R(int64_t nR, const int32_t *__restrict__ Ri,
-                                                    const int32_t *__restrict__ Ru, HView H,
-                                                    const int32_t *__restrict__ bvptr,
-                                                    const int32_t *__restrict__ bhandle,
-                                                    const double *__restrict__ bphi, const double *__restrict__ X,
-                                                    const double *__restrict__ origins, double *__restrict__ R) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= nR) return;
-  const int i = Ri[r], u = Ru[r];
-  const double o0 = origins[3 * i], o1 = origins[3 * i + 1], o2 = origins[3 * i + 2];
-  double acc[36];
-#pragma unroll
-  for (int k = 0; k < 36; ++k) acc[k] = 0.0;
-  const int sl_ = u >> 5, ln_ = u & 31;
-  for (int cs = H.sl_ptr[sl_]; cs < H.sl_ptr[sl_ + 1]; ++cs) {
-    const int v = H.col[(size_t)cs * 32 + ln_];
-    double f = 0.0;
-    for (int k = bvptr[v]; k < bvptr[v + 1]; ++k) {
-      const int hk = bhandle[k];
-      if (hk == i) { f = bphi[k]; break; }
-      if (hk > i) break;
-    }
-    if (f == 0.0) continue;
-    const double w[4] = {f, f * (X[3 * v] - o0), f * (X[3 * v + 1] - o1), f * (X[3 * v + 2] - o2)};
-    // H_vu[c'][c] = H_uv[c][c'] = vals[(3c + c') plane][s]
-    double Hvu[3][3];
-#pragma unroll
-    for (int cc = 0; cc < 3; ++cc)
-#pragma unroll
-      for (int cp = 0; cp < 3; ++cp) Hvu[cp][cc] = H.vals[((size_t)cs * 9 + 3 * cc + cp) * 32 + ln_];
-#pragma unroll
-    for (int cp = 0; cp < 3; ++cp)
-#pragma unroll
-      for (int kp = 0; kp < 4; ++kp)
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) acc[(4 * cp + kp) * 3 + cc] = fma(w[kp], Hvu[cp][cc], acc[(4 * cp + kp) * 3 + cc]);
-  }
-  double *dst = R + 36 * (size_t)r;
-#pragma unroll
-  for (int k = 0; k < 36; ++k) dst[k] = acc[k];
-}
+// One CTA per handle i computes the upper block row S_ij (j >= i) with R_i never leaving the
+// SM.  For each chunk of kGalChunk vertices u of U_i:
+//   phase A (two threads per u, each half of the (i,u) neighbour list, summed in a fixed order):
+//            R_i(u) = sum_{v in N(u), i in supp(v)} w_vi kron H_vu   -> shared Rs[u][36]
+//   phase B (warp per upper slot j): S_ij += sum_{u in chunk, j in supp(u)} R_i(u) w_uj^T; the
+//            warp stages 32 list entries (u, w_uj) at a time in shared memory (one round trip
+//            per 32 entries); three 9-lane groups work on three entries at once.
+// Every accumulator has one owner thread and a fixed summation order -> deterministic.
+// R_i(u) entry l = 3 (4c'+k') + c; accumulator layout [slot][k][36] (conflict-free in l).
+constexpr int kGalThreads = 2 * kGalChunk;
+constexpr int kGalWarps = kGalThreads / 32;
 
-// S block (i, j): warp per block, lane l owns R entries l and 32 + l (l < 4).
-__global__ void __launch_bounds__(256) k_galerkin_S(int64_t nblk, const int32_t *__restrict__ srow,
-                                                    const int32_t *__restrict__ scol,
-                                                    const int32_t *__restrict__ sc_ptr,
-                                                    const int32_t *__restrict__ sc_R,
-                                                    const int32_t *__restrict__ sc_phi,
-                                                    const int32_t *__restrict__ Ru,
-                                                    const double *__restrict__ bphi,
-                                                    const double *__restrict__ X,
-                                                    const double *__restrict__ origins,
-                                                    const double *__restrict__ R, double *__restrict__ S) {
-  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (b >= nblk) return;
-  const int j = scol[b];
-  const double o0 = origins[3 * j], o1 = origins[3 * j + 1], o2 = origins[3 * j + 2];
-  double a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0};
-  for (int k = sc_ptr[b]; k < sc_ptr[b + 1]; ++k) {
-    const int r = sc_R[k];
-    const int u = Ru[r];
-    const double f = bphi[sc_phi[k]];
-    const double w[4] = {f, f * (X[3 * u] - o0), f * (X[3 * u + 1] - o1), f * (X[3 * u + 2] - o2)};
-    const double *Rr = R + 36 * (size_t)r;
-    const double r0 = Rr[lane];
-    const double r1 = lane < 4 ? Rr[32 + lane] : 0.0;
+__global__ void __launch_bounds__(kGalThreads, 2) k_galerkin_fused(
+    HView H, const int32_t *__restrict__ gU_ptr, const int32_t *__restrict__ gU,
+    const int32_t *__restrict__ ga_off, const uint32_t *__restrict__ ga_ent,
+    const int32_t *__restrict__ gj_ptr, const int32_t *__restrict__ gj_blk,
+    const int32_t *__restrict__ gl_base, const int32_t *__restrict__ gl_off,
+    const uint32_t *__restrict__ gl_ent, const double *__restrict__ W, const int32_t *__restrict__ sT,
+    double *__restrict__ S) {
+  extern __shared__ double gsm[];
+  double *Rs = gsm;                                   // [kGalChunk][36]
+  double *stW = Rs + kGalChunk * 36;                  // [warps][32][4]
+  int *stU = reinterpret_cast<int *>(stW + kGalWarps * 32 * 4);   // [warps][32]
+  double *Sacc = stW + kGalWarps * 32 * 4 + kGalWarps * 16;       // [nup][4][36]
+  const int i = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int ul_a = t & (kGalChunk - 1), half = t / kGalChunk;
+  const int u0 = gU_ptr[i], nU = gU_ptr[i + 1] - u0;
+  const int j0 = gj_ptr[i], nup = gj_ptr[i + 1] - j0;
+  for (int e = t; e < nup * 144; e += kGalThreads) Sacc[e] = 0.0;
+  const int nch = (nU + kGalChunk - 1) / kGalChunk;
+  const int *off = gl_off + gl_base[i];
+  double *myW = stW + warp * 128;
+  int *myU = stU + warp * 32;
+  for (int ch = 0; ch < nch; ++ch) {
+    // ---- phase A
+    double acc[36];
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      a0[kk] = fma(r0, w[kk], a0[kk]);
-      a1[kk] = fma(r1, w[kk], a1[kk]);
+    for (int k = 0; k < 36; ++k) acc[k] = 0.0;
+    const int uq = ch * kGalChunk + ul_a;
+    if (uq < nU) {
+      const int q = u0 + uq;
+      const int u = __ldg(&gU[q]);
+      const int ln_ = u & 31;
+      const int base = __ldg(&H.sl_ptr[u >> 5]);
+      const int e1 = __ldg(&ga_off[q + 1]);
+#pragma unroll 2
+      for (int e = __ldg(&ga_off[q]) + half; e < e1; e += 2) {
+        const uint32_t en = __ldg(&ga_ent[e]);
+        const size_t cs = (size_t)base + (en & 63);
+        const size_t p = en >> 6;
+        const double2 w01 = __ldg(reinterpret_cast<const double2 *>(W + 4 * p));
+        const double2 w23 = __ldg(reinterpret_cast<const double2 *>(W + 4 * p + 2));
+        const double w[4] = {w01.x, w01.y, w23.x, w23.y};
+        // H_vu[c'][c] = H_uv[c][c'] = vals plane 3c + c'
+        double Hvu[3][3];
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc)
+#pragma unroll
+          for (int cp = 0; cp < 3; ++cp) Hvu[cp][cc] = __ldg(&H.vals[(cs * 9 + 3 * cc + cp) * 32 + ln_]);
+#pragma unroll
+        for (int cp = 0; cp < 3; ++cp)
+#pragma unroll
+          for (int kp = 0; kp < 4; ++kp)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc)
+              acc[(4 * cp + kp) * 3 + cc] = fma(w[kp], Hvu[cp][cc], acc[(4 * cp + kp) * 3 + cc]);
+      }
+    }
+    __syncthreads();   // previous chunk's phase B is done with Rs
+    if (half == 0) {
+#pragma unroll
+      for (int k = 0; k < 36; ++k) Rs[ul_a * 36 + k] = acc[k];
+    }
+    __syncthreads();
+    if (half == 1) {
+#pragma unroll
+      for (int k = 0; k < 36; ++k) Rs[ul_a * 36 + k] += acc[k];
+    }
+    __syncthreads();
+    // ---- phase B: three groups of 9 lanes per warp take every third staged entry; lane g of
+    // a group owns R entries 4g..4g+3 x the 4 monomials k (16 accumulators); the groups are
+    // summed in a fixed order at the end of the slot
+    const int *o = off + ch * (nup + 1);
+    const int grp = lane / 9, g = lane - 9 * grp;   // grp 3: lanes 27..31 idle in the FMA loop
+    for (int q = warp; q < nup; q += kGalWarps) {
+      double a[4][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a[r][k] = 0.0;
+      const int e1 = __ldg(&o[q + 1]);
+      for (int eb = __ldg(&o[q]); eb < e1; eb += 32) {
+        const int n = min(32, e1 - eb);
+        __syncwarp();
+        if (lane < n) {
+          const uint32_t en = __ldg(&gl_ent[eb + lane]);
+          const size_t p = en >> 7;
+          const double2 w01 = __ldg(reinterpret_cast<const double2 *>(W + 4 * p));
+          const double2 w23 = __ldg(reinterpret_cast<const double2 *>(W + 4 * p + 2));
+          reinterpret_cast<double2 *>(myW)[2 * lane] = w01;
+          reinterpret_cast<double2 *>(myW)[2 * lane + 1] = w23;
+          myU[lane] = (int)(en & (kGalChunk - 1)) * 36;
+        }
+        __syncwarp();
+        if (grp < 3) {
+#pragma unroll 2
+          for (int k = grp; k < n; k += 3) {
+            const double2 w01 = reinterpret_cast<const double2 *>(myW)[2 * k];
+            const double2 w23 = reinterpret_cast<const double2 *>(myW)[2 * k + 1];
+            const double *rr = Rs + myU[k] + 4 * g;
+            const double2 r01 = reinterpret_cast<const double2 *>(rr)[0];
+            const double2 r23 = reinterpret_cast<const double2 *>(rr)[1];
+            const double rv[4] = {r01.x, r01.y, r23.x, r23.y}, wv[4] = {w01.x, w01.y, w23.x, w23.y};
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+              for (int k2 = 0; k2 < 4; ++k2) a[r][k2] = fma(rv[r], wv[k2], a[r][k2]);
+          }
+        }
+      }
+      // a (group 0) + a (group 1) + a (group 2), then add to the slot accumulator
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double v1 = __shfl_down_sync(0xffffffffu, a[r][k], 9);
+          const double v2 = __shfl_down_sync(0xffffffffu, a[r][k], 18);
+          a[r][k] = (a[r][k] + v1) + v2;
+        }
+      if (grp == 0) {
+        double *sa = Sacc + q * 144;
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) sa[k * 36 + 4 * g + r] += a[r][k];
+      }
     }
   }
-  double *dst = S + 144 * (size_t)b;
-  {
-    const int l = lane, row = l / 3, c = l % 3;
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) dst[row * 12 + 4 * c + kk] = a0[kk];
+  __syncthreads();
+  // ---- write S_ij (row-major 12x12: row 4c'+k', column 4c+k) and its transpose S_ji
+  for (int e = t; e < nup * 144; e += kGalThreads) {
+    const int q = e / 144, r = e % 144, k = r / 36, l = r % 36;
+    const int row = l / 3, cc = l % 3;
+    const int b = __ldg(&gj_blk[j0 + q]);
+    const double val = Sacc[e];
+    S[144 * (size_t)b + row * 12 + 4 * cc + k] = val;
+    const int bt = __ldg(&sT[b]);
+    if (bt != b) S[144 * (size_t)bt + (4 * cc + k) * 12 + row] = val;
   }
-  if (lane < 4) {
-    const int l = 32 + lane, row = l / 3, c = l % 3;
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) dst[row * 12 + 4 * c + kk] = a1[kk];
-  }
-  (void)srow;
 }
 
 // Affine: Ra(u) = sum_{v in N(u)} w_a(v) kron H_vu  stored SoA [36][nv]
@@ -362,78 +425,26 @@ void launch_basis_W(Ctx &c) {
   MS_CUDA(cudaGetLastError());
 }
 
-// S block b: warp per block; 8 lane groups of 4 stride over the contributions, lane `sub` of a
-// group owns the 9 R entries 9 sub .. 9 sub + 8 (x 4 monomials); groups reduced by shuffles.
-__global__ void __launch_bounds__(256) k_galerkin_S2(int64_t nblk, const int32_t *__restrict__ sc_ptr,
-                                                     const int32_t *__restrict__ sc_R,
-                                                     const int32_t *__restrict__ sc_phi,
-                                                     const double *__restrict__ W, const double *__restrict__ R,
-                                                     const int32_t *__restrict__ srow,
-                                                     const int32_t *__restrict__ scol,
-                                                     const int32_t *__restrict__ sT, double *__restrict__ S) {
-  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31, grp = lane >> 2, sub = lane & 3;
-  if (b >= nblk) return;
-  if (srow[b] > scol[b]) return;   // S symmetric: block (j,i) = (i,j)^T is written by (i,j)
-  double acc[9][4];
-#pragma unroll
-  for (int q = 0; q < 9; ++q)
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) acc[q][kk] = 0.0;
-  const int k1 = sc_ptr[b + 1];
-#pragma unroll 2
-  for (int k = sc_ptr[b] + grp; k < k1; k += 8) {
-    const int r = __ldg(&sc_R[k]), p = __ldg(&sc_phi[k]);
-    const double2 w01 = __ldg(reinterpret_cast<const double2 *>(W + 4 * (size_t)p));
-    const double2 w23 = __ldg(reinterpret_cast<const double2 *>(W + 4 * (size_t)p + 2));
-    const double w[4] = {w01.x, w01.y, w23.x, w23.y};
-    const double *Rr = R + 36 * (size_t)r + 9 * sub;
-    double rv[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) rv[q] = __ldg(&Rr[q]);
-#pragma unroll
-    for (int q = 0; q < 9; ++q)
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) acc[q][kk] = fma(rv[q], w[kk], acc[q][kk]);
-  }
-#pragma unroll
-  for (int q = 0; q < 9; ++q)
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      double v = acc[q][kk];
-      v += __shfl_xor_sync(0xffffffffu, v, 4);
-      v += __shfl_xor_sync(0xffffffffu, v, 8);
-      v += __shfl_xor_sync(0xffffffffu, v, 16);
-      acc[q][kk] = v;
-    }
-  if (grp == 0) {
-    double *dst = S + 144 * (size_t)b;
-    double *dstT = S + 144 * (size_t)sT[b];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) {
-      const int l = 9 * sub + q, row = l / 3, cc = l % 3;
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        dst[row * 12 + 4 * cc + kk] = acc[q][kk];
-        dstT[(4 * cc + kk) * 12 + row] = acc[q][kk];
-      }
-    }
-  }
-}
-
 // ------------------------------------------------------------------ launchers
 void launch_coarse_S(Ctx &c) {
-  k_galerkin_R<<<div_up(c.n_R, 128), 128, 0, c.stream>>>(c.n_R, c.R_i, c.R_u, hview(c), c.bvptr, c.bhandle,
-                                                         c.bphi, c.X, c.origins, c.Rbuf);
-  k_galerkin_S2<<<div_up(c.nnzb_S * 32, 256), 256, 0, c.stream>>>(c.nnzb_S, c.sc_ptr, c.sc_R, c.sc_phi, c.Wphi,
-                                                                   c.Rbuf, c.srow, c.scol, c.sT, c.Sblk);
+  const size_t smem = sizeof(double) * ((size_t)kGalChunk * 36 + kGalWarps * (32 * 4 + 16) +
+                                        (size_t)c.gal_max_jup * 144);
+  static size_t smem_set = 0;
+  if (smem > smem_set) {
+    MS_REQUIRE(smem <= 227 * 1024, MS_ERR_ARG, "coarse S row too wide for the fused Galerkin kernel");
+    MS_CUDA(cudaFuncSetAttribute(k_galerkin_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_set = smem;
+  }
+  k_galerkin_fused<<<c.m, kGalThreads, smem, c.stream>>>(hview(c), c.gU_ptr, c.gU, c.ga_off, c.ga_ent, c.gj_ptr,
+                                                         c.gj_blk, c.gl_base, c.gl_off, c.gl_ent, c.Wphi, c.sT,
+                                                         c.Sblk);
   const double *o = c.aff_origin;
   k_galerkin_Ra<<<div_up(c.nv, 128), 128, 0, c.stream>>>(c.nv, hview(c), c.phi_aff, c.X, o[0], o[1], o[2], c.Ra);
   const int nch = 64;
   k_galerkin_Sa_partial<<<dim3(36, nch), 256, 0, c.stream>>>(c.nv, c.Ra, c.phi_aff, c.X, o[0], o[1], o[2],
                                                               c.partial);
   k_galerkin_Sa_final<<<1, 160, 0, c.stream>>>(nch, c.partial, c.Sa);
-  c.launches += 5;
+  c.launches += 4;
   MS_CUDA(cudaGetLastError());
 }
 

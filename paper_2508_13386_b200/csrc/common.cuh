@@ -72,6 +72,8 @@ struct Reducer {
 };
 
 // ---------------------------------------------------------------- tile Cholesky schedule
+constexpr int kGalChunk = 128;   // vertices of U_i per Galerkin chunk (7-bit local index)
+
 struct CholTask {      // one trailing update A_ij -= L_ik L_jk^T (tiles)
   int32_t i, j;
 };
@@ -137,13 +139,14 @@ struct Ctx {
   DBuf<int32_t> sptr, scol, srow, sT;   // sT[b]: block index of the transposed block
   DBuf<double> Sblk;                // [nnzb_S * 144]
   DBuf<double> Wphi;                // [nnz_phi * 4] phi [1, X - c] per basis entry
-  // R contributions: R_i(u) for (i,u) pairs; S contributions
-  int64_t n_R = 0;                  // number of (i,u) pairs
-  DBuf<int32_t> R_i, R_u;           // [n_R]
-  DBuf<double> Rbuf;                // [n_R * 36]
-  DBuf<int32_t> sc_ptr;             // [nnzb_S + 1] S block -> contributions
-  DBuf<int32_t> sc_R, sc_phi;       // [n_sc] (R index, phi index of (u, j))
-  // affine
+  // fused Galerkin (coarse.cu k_galerkin_fused): U_i lists, upper S slots, chunked entries
+  DBuf<int32_t> gU_ptr, gU;         // [m+1], [sum |U_i|]
+  DBuf<int32_t> ga_off;             // [sum |U_i| + 1] per (i,u) pair: range in ga_ent
+  DBuf<uint32_t> ga_ent;            // Hessian row slot j of u | (basis entry p of (v, i)) << 6
+  DBuf<int32_t> gj_ptr, gj_blk;     // upper slots j >= i of row i -> S block index
+  DBuf<int32_t> gl_base, gl_off;    // per (i, chunk, slot) entry ranges
+  DBuf<uint32_t> gl_ent;            // u_local | (basis entry p) << 7
+  int32_t gal_max_jup = 0;
   DBuf<double> Sa;                  // 144
   DBuf<double> Ra;                  // [nv * 36]
   // dense coarse factor (tile-banded)

@@ -1,5 +1,5 @@
 // Host-side symbolic setup: validation, per-tet rest data, BSR pattern and the atomic-free
-// assembly maps; basis CSR (vertex- and handle-major), coarse S pattern, the R_i(u) pair
+// assembly maps; basis CSR (vertex- and handle-major), coarse S pattern, the fused Galerkin
 // list and the S-block contribution lists; tile-envelope schedule of the coarse Cholesky.
 //
 // SURVEY §8(a) a4 (BSR assembly into precomputed slots), a5 (Galerkin projection), a6
@@ -241,15 +241,13 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   for (int32_t i = 0; i < m; ++i)
     MS_REQUIRE(hptr[i + 1] > hptr[i], MS_ERR_ARG, "handle with empty support");
 
-  // U_i = vertices adjacent (BSR) to supp(i); R pairs (i,u); J_i = handles of U_i;
-  // S block (i,j) contributions (R index, phi index of (u,j)).
+  // U_i = vertices adjacent (BSR) to supp(i); J_i = handles of U_i (the S pattern row i);
+  // fused Galerkin lists (coarse.cu k_galerkin_fused): per handle i, per chunk of kGalChunk
+  // vertices of U_i, per upper slot j >= i of J_i the entries (u_local | p << 7) with p the
+  // basis entry of (u, j).
   std::vector<int32_t> mark(nv, -1), hmark(m, -1), jslot(m, -1);
   std::vector<int32_t> sptr(1, 0), scol;
-  std::vector<std::vector<std::pair<int32_t, int32_t>>> lists;
-  std::vector<int32_t> sc_ptr(1, 0), sc_R, sc_phi;
   const int32_t *rp = c.h_rowptr.data(), *ci = c.h_colidx.data();
-  // pass 1: U_i for every handle; the (i,u) pairs of R_i(u) are stored u-major so that the
-  // threads of a warp share the Hessian row u and the handle lists of its neighbours
   std::vector<int32_t> Uptr(m + 1, 0), Uall;
   for (int32_t i = 0; i < m; ++i) {
     const size_t b0 = Uall.size();
@@ -263,59 +261,77 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
         }
       }
     }
-    std::sort(Uall.begin() + b0, Uall.end());
+    std::sort(Uall.begin() + b0, Uall.end());   // vertex order: coalesced SELL row reads
     Uptr[i + 1] = (int32_t)Uall.size();
   }
-  std::vector<int32_t> rstart(nv + 1, 0);
-  for (int32_t u : Uall) rstart[u + 1]++;
-  for (int32_t u = 0; u < nv; ++u) rstart[u + 1] += rstart[u];
-  std::vector<int32_t> Ri(Uall.size()), Ru(Uall.size());
-  {
-    std::vector<int32_t> fill(rstart.begin(), rstart.end() - 1);
-    for (int32_t i = 0; i < m; ++i)                    // i ascending -> sorted within each u
-      for (int32_t q = Uptr[i]; q < Uptr[i + 1]; ++q) {
-        const int32_t u = Uall[q];
-        Ri[fill[u]] = i;
-        Ru[fill[u]] = u;
-        fill[u]++;
+  MS_REQUIRE(nnz < (int64_t(1) << 25), MS_ERR_ARG, "basis too large for the fused Galerkin entry encoding");
+  // per (i, u) pair: the Hessian row slots j of u whose vertex v lies in supp(i): (j | p << 6)
+  std::vector<int32_t> ga_off(1, 0);
+  std::vector<uint32_t> ga_ent;
+  ga_off.reserve(Uall.size() + 1);
+  for (int32_t i = 0; i < m; ++i)
+    for (int32_t q = Uptr[i]; q < Uptr[i + 1]; ++q) {
+      const int32_t u = Uall[q];
+      MS_REQUIRE(rp[u + 1] - rp[u] <= 64, MS_ERR_ARG, "Hessian row longer than 64 blocks (Galerkin encoding)");
+      for (int32_t j = 0; j < rp[u + 1] - rp[u]; ++j) {
+        const int32_t v = ci[rp[u] + j];
+        const int32_t *hb = handle + vptr[v], *he = handle + vptr[v + 1];
+        const int32_t *f = std::lower_bound(hb, he, i);
+        if (f != he && *f == i) ga_ent.push_back((uint32_t)j | ((uint32_t)(vptr[v] + (f - hb)) << 6));
       }
-  }
-  auto pair_index = [&](int32_t i, int32_t u) {
-    const int32_t *b = Ri.data() + rstart[u], *e = Ri.data() + rstart[u + 1];
-    return (int32_t)(std::lower_bound(b, e, i) - Ri.data());
-  };
-  std::vector<int32_t> U, Jl;
+      MS_REQUIRE(ga_ent.size() < (size_t)INT32_MAX, MS_ERR_ARG, "Galerkin pair list too large");
+      ga_off.push_back((int32_t)ga_ent.size());
+    }
+  std::vector<int32_t> gj_ptr(m + 1, 0), gj_blk, gl_base(m + 1, 0), gl_off;
+  std::vector<uint32_t> gl_ent;
+  std::vector<int32_t> Jl;
+  std::vector<std::vector<uint32_t>> lists;
+  int32_t max_jup = 0;
   for (int32_t i = 0; i < m; ++i) {
-    U.assign(Uall.begin() + Uptr[i], Uall.begin() + Uptr[i + 1]);
     Jl.clear();
-    for (int32_t u : U)
+    for (int32_t q = Uptr[i]; q < Uptr[i + 1]; ++q) {
+      const int32_t u = Uall[q];
       for (int64_t k = vptr[u]; k < vptr[u + 1]; ++k)
         if (hmark[handle[k]] != i) {
           hmark[handle[k]] = i;
           Jl.push_back(handle[k]);
         }
+    }
     std::sort(Jl.begin(), Jl.end());
-    for (size_t q = 0; q < Jl.size(); ++q) jslot[Jl[q]] = (int32_t)q;
-    lists.assign(Jl.size(), {});
-    for (int32_t u : U) {
-      const int32_t r = pair_index(i, u);
-      for (int64_t k = vptr[u]; k < vptr[u + 1]; ++k) lists[jslot[handle[k]]].push_back({r, (int32_t)k});
-    }
-    for (size_t q = 0; q < Jl.size(); ++q) {
-      scol.push_back(Jl[q]);
-      for (auto &pr : lists[q]) {
-        sc_R.push_back(pr.first);
-        sc_phi.push_back(pr.second);
-      }
-      MS_REQUIRE(sc_R.size() < (size_t)INT32_MAX, MS_ERR_ARG, "coarse contribution list too large");
-      sc_ptr.push_back((int32_t)sc_R.size());
-    }
+    const int32_t row0 = (int32_t)scol.size();
+    scol.insert(scol.end(), Jl.begin(), Jl.end());
     sptr.push_back((int32_t)scol.size());
+    const int32_t first_up = (int32_t)(std::lower_bound(Jl.begin(), Jl.end(), i) - Jl.begin());
+    const int32_t nup = (int32_t)Jl.size() - first_up;
+    max_jup = std::max(max_jup, nup);
+    for (int32_t q = 0; q < nup; ++q) {
+      jslot[Jl[first_up + q]] = q;
+      gj_blk.push_back(row0 + first_up + q);
+    }
+    gj_ptr[i + 1] = (int32_t)gj_blk.size();
+    const int32_t nU = Uptr[i + 1] - Uptr[i];
+    const int32_t nch = (nU + kGalChunk - 1) / kGalChunk;
+    gl_base[i + 1] = gl_base[i] + nch * (nup + 1);
+    lists.assign(nup, {});
+    for (int32_t ch = 0; ch < nch; ++ch) {
+      for (auto &l : lists) l.clear();
+      for (int32_t t = 0; t < kGalChunk && ch * kGalChunk + t < nU; ++t) {
+        const int32_t u = Uall[Uptr[i] + ch * kGalChunk + t];
+        for (int64_t k = vptr[u]; k < vptr[u + 1]; ++k)
+          if (handle[k] >= i) lists[jslot[handle[k]]].push_back((uint32_t)t | ((uint32_t)k << 7));
+      }
+      for (int32_t q = 0; q < nup; ++q) {
+        gl_off.push_back((int32_t)gl_ent.size());
+        gl_ent.insert(gl_ent.end(), lists[q].begin(), lists[q].end());
+      }
+      gl_off.push_back((int32_t)gl_ent.size());
+      MS_REQUIRE(gl_ent.size() < (size_t)INT32_MAX, MS_ERR_ARG, "coarse contribution list too large");
+    }
   }
   c.h_sptr = sptr;
   c.h_scol = scol;
   c.nnzb_S = (int64_t)scol.size();
-  c.n_R = (int64_t)Ri.size();
+  c.gal_max_jup = max_jup;
 
   // ---- fill-reducing order of the handles: geometric nested dissection on the coupling graph
   // (one-sided vertex separators from recursive median bisection of the handle origins).
@@ -501,12 +517,15 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
     c.sT.upload(sT, s);
   }
   c.Sblk.alloc((size_t)144 * c.nnzb_S);
-  c.R_i.upload(Ri, s);
-  c.R_u.upload(Ru, s);
-  c.Rbuf.alloc((size_t)36 * c.n_R);
-  c.sc_ptr.upload(sc_ptr, s);
-  c.sc_R.upload(sc_R, s);
-  c.sc_phi.upload(sc_phi, s);
+  c.gU_ptr.upload(Uptr, s);
+  c.gU.upload(Uall, s);
+  c.ga_off.upload(ga_off, s);
+  c.ga_ent.upload(ga_ent.empty() ? std::vector<uint32_t>{0} : ga_ent, s);
+  c.gj_ptr.upload(gj_ptr, s);
+  c.gj_blk.upload(gj_blk, s);
+  c.gl_base.upload(gl_base, s);
+  c.gl_off.upload(gl_off, s);
+  c.gl_ent.upload(gl_ent.empty() ? std::vector<uint32_t>{0} : gl_ent, s);
   c.Sa.alloc(144);
   c.Ra.alloc((size_t)36 * nv);
   c.Lden.alloc((size_t)c.nS_pad * c.nS_pad);
