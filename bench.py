@@ -275,6 +275,7 @@ def run_ours(args):
                     "h2d_bytes_per_step": 2 * 3 * 8 * s.n_verts, "d2h_bytes_per_step": 2 * 3 * 8 * s.n_verts},
             "clocks": clk.summary(),
             "basis_build_s": t_basis,
+            "coarse": ctx.coarse_info(),
         }
         if not args.no_cpu_baseline:
             sec, desc, _ = oracle_newton_sample(s, b)

@@ -208,6 +208,20 @@ ms_status ms_set_profiling(ms_ctx *ctx, int32_t on);      /* resets the accumula
 ms_status ms_get_phase_times(ms_ctx *ctx, ms_phase_times *out);
 /* Number of kernel launches (graph-embedded kernels included) issued by this context. */
 int64_t ms_kernel_launches(ms_ctx *ctx);
+/* Structure of the coarse factorisation chosen at ms_basis_upload (reading R4):
+ * S is n_s x n_s (n_s = 12 m), factorised in tile x tile tiles of a dense padded array; only the
+ * lower_tiles tiles of the symbolic factor are touched.  ordering: 0 = handles in centroid
+ * x-order, 1 = geometric nested dissection (whichever needs fewer tile flops).  flops: flop count
+ * of one factorisation at tile granularity (flops_xorder / flops_nd: both candidates); n_tasks:
+ * tile tasks (factor, panel, update); critical_path: longest task chain of the tile DAG. */
+typedef struct ms_coarse_info {
+  int64_t n_s, tile, ntiles, lower_tiles, n_tasks, critical_path, nnzb_s;
+  int64_t critical_path_xorder, critical_path_nd;
+  int32_t ordering, pad_;
+  double flops, flops_xorder, flops_nd;
+} ms_coarse_info;
+ms_status ms_get_coarse_info(ms_ctx *ctx, ms_coarse_info *out);
+
 /* Sizes: n_verts, n_tets, nnzb (BSR blocks), m (handles), nnz_phi, nnzb_S (coupled handle
  * pairs incl. diagonal) — any pointer may be NULL. */
 ms_status ms_get_sizes(ms_ctx *ctx, int64_t *n_verts, int64_t *n_tets, int64_t *nnzb,

@@ -692,4 +692,14 @@ ms_status ms_get_sizes(ms_ctx *ctx, int64_t *n_verts, int64_t *n_tets, int64_t *
   return MS_OK;
 }
 
+ms_status ms_get_coarse_info(ms_ctx *ctx, ms_coarse_info *out) {
+  if (!ctx || !out) return MS_ERR_ARG;
+  if (ctx->c.m <= 0) {
+    ctx->c.last_error = "no basis uploaded";
+    return MS_ERR_STATE;
+  }
+  *out = ctx->c.chol_info;
+  return MS_OK;
+}
+
 }  // extern "C"

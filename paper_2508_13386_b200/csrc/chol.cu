@@ -27,242 +27,7 @@ __device__ __forceinline__ size_t tile_off(int ti, int tj, int nSp) {
   return (size_t)(tj * TB) * nSp + (size_t)ti * TB;
 }
 
-// ------------------------------------------------------------------ D(k): potrf + inverse
-// smem: A [64][LD], Li [64][LD], Tb [3*16*17], invd [64]
-constexpr int kDiagSmemDoubles = 2 * TB * LD + 3 * 16 * 17 + TB;
-
-// Register-blocked right-looking Cholesky of the 64x64 diagonal tile with the inverse built in
-// the same sweep (Gauss-Jordan on [L | I]): L = L_0 ... L_63 with L_j the identity whose column j
-// is l_j, so L^-1 = L_63^-1 ... L_0^-1 and applying L_j^-1 from the left is
-//   Z_j <- Z_j / l_jj,   Z_r <- Z_r - (l_rj / l_jj) Z_j^old  (r > j).
-// Thread t = rb + 16 cb owns the 4x4 blocks (rows 4rb.., cols 4cb..) of A and of Z; the 16
-// owners of column j form one half-warp, so the pivot is a shuffle and each step needs ONE
-// barrier (the pivot column and row j of Z are double-buffered in shared memory).
-__device__ void diag_factor_gj(int k, int nSp, double *__restrict__ L, double *__restrict__ U,
-                               int *__restrict__ flag, double *sm) {
-  double *colL = sm;          // [2][64] pivot column l_.j (zero above the diagonal)
-  double *rowZ = sm + 128;    // [2][64] row j of Z before scaling
-  double *sinv = sm + 256;    // [2]     1 / l_jj
-  const int t = threadIdx.x, rb = t & 15, cb = t >> 4, lane = t & 31;
-  const int r0 = 4 * rb, c0 = 4 * cb;
-  const size_t okk = tile_off(k, k, nSp);
-  double a[4][4], z[4][4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const int r = r0 + p, c = c0 + q;
-      a[p][q] = r >= c ? __ldcg(&L[okk + (size_t)c * nSp + r]) : 0.0;
-      z[p][q] = r == c ? 1.0 : 0.0;
-    }
-  if (rb == 0) {   // row 0 of Z = e_0
-#pragma unroll
-    for (int q = 0; q < 4; ++q) rowZ[c0 + q] = (c0 + q == 0) ? 1.0 : 0.0;
-  }
-  bool bad = false;
-#pragma unroll 1
-  for (int j = 0; j < TB; ++j) {
-    const int buf = j & 1, jb = j >> 2, jq = j & 3;
-    // phase A: the half-warp owning column j (cb == jb) forms l_.j
-    if (cb == jb) {
-      double mine = 0.0;
-#pragma unroll
-      for (int p = 0; p < 4; ++p)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (q == jq && p == jq) mine = a[p][q];
-      const double d = __shfl_sync(0xffffu << (lane & 16), mine, (lane & 16) + jb, 32);
-      const bool ok = d > 0.0;
-      if (!ok) bad = true;
-      const double inv = ok ? rsqrt_nr2(d) : 1.0;
-      const double ljj = ok ? d * inv : 1.0;
-#pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        const int r = r0 + p;
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (q == jq) {
-            const double l = r > j ? a[p][q] * inv : (r == j ? ljj : 0.0);
-            a[p][q] = l;
-            colL[buf * 64 + r] = l;
-          }
-      }
-      if (rb == 0) sinv[buf] = inv;
-    }
-    __syncthreads();
-    // phase B: trailing update of A and Z
-    const double inv = sinv[buf];
-    double lr[4], lc[4], zj[4];
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      lr[p] = colL[buf * 64 + r0 + p];
-      lc[p] = (c0 + p > j) ? colL[buf * 64 + c0 + p] : 0.0;
-      zj[p] = rowZ[buf * 64 + c0 + p];
-    }
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const int r = r0 + p;
-      const double fz = r > j ? lr[p] * inv : 0.0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        a[p][q] = fma(-lr[p], lc[q], a[p][q]);   // lc = 0 for c <= j; lr = 0 for r < j
-        z[p][q] = fma(-fz, zj[q], z[p][q]);
-        if (r == j) z[p][q] *= inv;
-      }
-    }
-    // row j+1 of Z is final now: publish it for the next step
-    if (j + 1 < TB && rb == ((j + 1) >> 2)) {
-#pragma unroll
-      for (int p = 0; p < 4; ++p)
-        if (r0 + p == j + 1)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) rowZ[(buf ^ 1) * 64 + c0 + q] = z[p][q];
-    }
-  }
-  if (bad && flag) *flag = 1;
-  // store L_kk (lower, column-major) and U_kk = Z^T (row-major: U[c][r] at c*64 + r = Z[r][c])
-  double *Uk = U + (size_t)k * TB * TB;
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const int r = r0 + p, c = c0 + q;
-      if (r >= c) __stcg(&L[okk + (size_t)c * nSp + r], a[p][q]);
-      __stcg(&Uk[(size_t)c * TB + r], z[p][q]);
-    }
-  __syncthreads();
-}
-
-__device__ void diag_factor(int k, int nSp, double *__restrict__ L, double *__restrict__ U,
-                            int *__restrict__ flag, double *sm) {
-  double *A = sm;              // row-major [64][LD]: the factor
-  double *Li = sm + TB * LD;   // row-major [64][LD]: its inverse
-  double(*Tb)[16][17] = reinterpret_cast<double(*)[16][17]>(sm + 2 * TB * LD);
-  double *invd = sm + 2 * TB * LD + 3 * 16 * 17;
-  const int t = threadIdx.x, w = t >> 5, lane = t & 31;
-  const size_t okk = tile_off(k, k, nSp);
-  {
-    double v[16];
-#pragma unroll
-    for (int it = 0; it < 16; ++it) {
-      const int e = t + it * 256;
-      v[it] = __ldcg(&L[okk + (size_t)(e >> 6) * nSp + (e & 63)]);
-    }
-#pragma unroll
-    for (int it = 0; it < 16; ++it) {
-      const int e = t + it * 256, r = e & 63, c = e >> 6;
-      A[r * LD + c] = r >= c ? v[it] : 0.0;
-      Li[r * LD + c] = 0.0;
-    }
-  }
-  __syncthreads();
-  bool bad = false;
-  for (int p = 0; p < 4; ++p) {
-    const int j0 = 16 * p;
-    if (w == 0) {
-      // panel rows j0 + lane and j0 + 32 + lane, columns j0 .. j0+15
-      const int ra = j0 + lane, rb = j0 + 32 + lane;
-      const bool va = ra < TB, vb = rb < TB;
-      double a[16], b[16];
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        a[c] = va ? A[ra * LD + j0 + c] : 0.0;
-        b[c] = vb ? A[rb * LD + j0 + c] : 0.0;
-      }
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const double d = __shfl_sync(0xffffffffu, a[j], j);
-        if (!(d > 0.0)) bad = true;
-        const double inv = d > 0.0 ? rsqrt_nr2(d) : 1.0;   // 1 / sqrt(d)
-        const double ljj = d > 0.0 ? d * inv : 1.0;
-        if (lane == 0) invd[j0 + j] = inv;
-        a[j] = lane == j ? ljj : (lane > j ? a[j] * inv : a[j]);
-        b[j] *= inv;
-#pragma unroll
-        for (int c = j + 1; c < 16; ++c) {
-          const double lc = __shfl_sync(0xffffffffu, a[j], c);
-          a[c] = fma(-a[j], lc, a[c]);
-          b[c] = fma(-b[j], lc, b[c]);
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        if (va && ra >= j0 + c) A[ra * LD + j0 + c] = a[c];
-        if (vb) A[rb * LD + j0 + c] = b[c];
-      }
-    }
-    __syncthreads();
-    // trailing update of rows/cols >= j0 + 16
-    const int s0 = j0 + 16;
-    for (int r = s0 + (t >> 2); r < TB; r += 64) {
-      for (int c = s0 + (t & 3); c <= r; c += 8) {   // two columns, four partial sums each
-        const bool two = c + 4 <= r;
-        double s0a = 0.0, s1a = 0.0, s0b = 0.0, s1b = 0.0;
-#pragma unroll
-        for (int j = 0; j < 16; j += 2) {
-          const double x0 = A[r * LD + j0 + j], x1 = A[r * LD + j0 + j + 1];
-          s0a = fma(x0, A[c * LD + j0 + j], s0a);
-          s1a = fma(x1, A[c * LD + j0 + j + 1], s1a);
-          if (two) {
-            s0b = fma(x0, A[(c + 4) * LD + j0 + j], s0b);
-            s1b = fma(x1, A[(c + 4) * LD + j0 + j + 1], s1b);
-          }
-        }
-        A[r * LD + c] -= s0a + s1a;
-        if (two) A[r * LD + c + 4] -= s0b + s1b;
-      }
-    }
-    __syncthreads();
-  }
-  if (w == 0 && lane == 0 && bad && flag) *flag = 1;
-  // inverse: diagonal 16x16 blocks (warp p, lane l < 16 solves column l)
-  if (w < 4 && lane < 16) {
-    const int o = 16 * w;
-    double x[16];
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      double s = r == lane ? 1.0 : 0.0, s2 = 0.0;
-#pragma unroll
-      for (int q = 0; q < r; q += 2) {
-        s = fma(-A[(o + r) * LD + o + q], x[q], s);
-        if (q + 1 < r) s2 = fma(-A[(o + r) * LD + o + q + 1], x[q + 1], s2);
-      }
-      x[r] = (s + s2) * invd[o + r];
-    }
-#pragma unroll
-    for (int r = 0; r < 16; ++r) Li[(o + r) * LD + o + lane] = x[r];
-  }
-  __syncthreads();
-  // off-diagonal blocks: Li_pq = -Li_pp sum_{s=q}^{p-1} L_ps Li_sq, p = 1..3
-  for (int p = 1; p < 4; ++p) {
-    for (int e = t; e < p * 256; e += 256) {
-      const int q = e >> 8, r = (e >> 4) & 15, cc = e & 15;
-      double s4[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int m = 16 * q; m < 16 * p; m += 4) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) s4[u] = fma(A[(16 * p + r) * LD + m + u], Li[(m + u) * LD + 16 * q + cc], s4[u]);
-      }
-      Tb[q][r][cc] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-    }
-    __syncthreads();
-    for (int e = t; e < p * 256; e += 256) {
-      const int q = e >> 8, r = (e >> 4) & 15, cc = e & 15;
-      double s4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-      for (int m = 0; m < 16; ++m) s4[m & 3] = fma(Li[(16 * p + r) * LD + 16 * p + m], Tb[q][m][cc], s4[m & 3]);
-      Li[(16 * p + r) * LD + 16 * q + cc] = -((s4[0] + s4[1]) + (s4[2] + s4[3]));
-    }
-    __syncthreads();
-  }
-  // store L_kk (lower, column-major) and U_kk = Li^T (row-major: U[r][c] at r*64 + c = Li[c][r])
-  double *Uk = U + (size_t)k * TB * TB;
-#pragma unroll 4
-  for (int it = 0; it < 16; ++it) {
-    const int e = t + it * 256, r = e & 63, c = e >> 6;
-    if (r >= c) __stcg(&L[okk + (size_t)c * nSp + r], A[r * LD + c]);
-    __stcg(&Uk[(size_t)c * TB + r], Li[r * LD + c]);   // U[c][r] = Li[r][c]
-  }
-}
+#include "chol_diag.cuh"
 
 __global__ void __launch_bounds__(256) k_chol_diag(int k, int nSp, double *__restrict__ L,
                                                    double *__restrict__ U, int *__restrict__ flag) {
@@ -377,9 +142,10 @@ __global__ void __launch_bounds__(256) k_chol_update(int k, const int32_t *__res
 }
 
 // ------------------------------------------------------------------ dataflow factorisation
-// One cooperative launch runs the whole tile DAG: task t is executed by CTA t mod G in task
-// order; a task waits only on tasks that precede it in the (topological) task order, so the
-// earliest unfinished task is always runnable (all CTAs are co-resident).  Tasks:
+// One cooperative launch runs the whole tile DAG: tasks are handed out in (topological) task
+// order through an atomic counter to whichever CTA is free; a task waits only on tasks that
+// precede it, so the earliest unfinished task is always runnable (all CTAs are co-resident).
+// Tasks:
 //   D(k):     wait upd[k][k] == need;         factor + invert the diagonal tile;   dfl[k] = 1
 //   P(i,k):   wait dfl[k], upd[i][k] == need; L_ik = A_ik U_kk;                     pfl[i][k] = 1
 //   U(i,j,k): wait pfl[i][k], pfl[j][k], upd[i][j] == rank (updates of a tile are applied in
@@ -405,10 +171,19 @@ __device__ __forceinline__ void df_signal(int *p, int val) {
 __global__ void __launch_bounds__(256, 2) k_chol_dataflow(int ntask, const int4 *__restrict__ tasks, int NT, int nSp,
                                                        double *__restrict__ L, double *__restrict__ U,
                                                        int *__restrict__ upd, int *__restrict__ dfl,
-                                                       int *__restrict__ pfl, int *__restrict__ flag) {
+                                                       int *__restrict__ pfl, int *__restrict__ flag,
+                                                       int *__restrict__ next) {
   extern __shared__ double sm[];
+  __shared__ int s_id;
   const int t = threadIdx.x, tr = t & 15, tc = t >> 4;
-  for (int id = blockIdx.x; id < ntask; id += gridDim.x) {
+  for (;;) {
+    // dynamic in-order dispensing: the next unclaimed task in topological order goes to the
+    // first CTA that is free (all earlier tasks are claimed by running CTAs -> no deadlock)
+    if (t == 0) s_id = atomicAdd(next, 1);
+    __syncthreads();
+    const int id = s_id;
+    __syncthreads();
+    if (id >= ntask) break;
     const int4 tk = tasks[id];
     const int type = tk.x, i = tk.y, j = tk.z & 0xffff, k = tk.z >> 16, cnt = tk.w;
     if (type == 0) {
@@ -675,13 +450,13 @@ void enqueue_chol_factor(Ctx &c) {
   if (nSp > c.nS) k_pad_identity2<<<div_up(nSp - c.nS, 64), 64, 0, c.stream>>>(c.nS, nSp, c.Lden);
   if (c.chol_dataflow) {
     const int NT = c.ntiles;
-    MS_CUDA(cudaMemsetAsync(c.df_flags, 0, sizeof(int) * ((size_t)2 * NT * NT + NT), c.stream));
+    MS_CUDA(cudaMemsetAsync(c.df_flags, 0, sizeof(int) * ((size_t)2 * NT * NT + NT + 1), c.stream));
     int ntask = (int)c.n_dag, NTv = NT, nSpv = nSp;
     const int4 *tk = reinterpret_cast<const int4 *>(c.chol_dag.p);
     double *Lp = c.Lden, *Up = c.Uinv;
     int *upd = c.df_flags, *pfl = c.df_flags + (size_t)NT * NT, *dfl = c.df_flags + (size_t)2 * NT * NT;
-    int *fl = c.flags + 0;
-    void *args[] = {&ntask, &tk, &NTv, &nSpv, &Lp, &Up, &upd, &dfl, &pfl, &fl};
+    int *fl = c.flags + 0, *nx = c.df_flags + (size_t)2 * NT * NT + NT;
+    void *args[] = {&ntask, &tk, &NTv, &nSpv, &Lp, &Up, &upd, &dfl, &pfl, &fl, &nx};
     MS_CUDA(cudaLaunchCooperativeKernel((const void *)k_chol_dataflow, dim3(dataflow_grid(c)), dim3(256), args,
                                         kUpdSmem, c.stream));
     return;

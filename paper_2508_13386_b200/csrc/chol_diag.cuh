@@ -1,0 +1,437 @@
+// Diagonal-tile factorisation D(k) of the coarse tile Cholesky (chol.cu): L_kk = chol(A_kk) and
+// U_kk = L_kk^-T for one 64 x 64 tile by one 256-thread CTA.  SURVEY §8(a) a6; reading R4.
+// Variants (selected by MSIM_DIAG_VARIANT; timed by tools/bench_diag.cu):
+//   0 diag_factor_rec      2 x 2 recursion on 32 x 32 blocks, single-warp panel work
+//   1 diag_factor_blocked  right-looking, 16-column panels factored by one warp in registers
+//   2 diag_factor_gj       register-blocked right-looking Cholesky + Gauss-Jordan inverse
+// All take the tile from L (column-major, leading dimension nSp) and write L_kk back there
+// and U_kk (row-major 64 x 64) to U + k 64^2; *flag = 1 if a pivot is not positive.
+// Requires TB = 64, LD = 65 and tile_off() from the including file.
+#pragma once
+#ifndef DIAG_TS
+#define DIAG_TS(i)
+#endif
+#ifndef MSIM_DIAG_VARIANT
+#define MSIM_DIAG_VARIANT 1
+#endif
+
+// ---------------------------------------------------------------- variant 0: recursive
+//   F11 (warp 0)              L11 = chol(A11)                    lane r owns row r
+//   TRSM (warp 1) | INV (w 2) L21 = A21 L11^-T   |   Li11 = L11^-1  lane = row of L21 / column of Li11
+//   SYRK (all)                A22 -= L21 L21^T
+//   F22 + INV (warp 0) | T (warps 1-7)   L22, Li22   |   T = L21 Li11
+//   all                       Li21 = -Li22 T
+// Loops are rolled (the D task runs once per tile: straight-line code would be fetched cold).
+// smem: A [64][LD] (row-major: the factor), Li [64][LD] (row-major: the inverse; its upper-right
+// 32 x 32 block holds T), invd [64].
+constexpr int kDiagSmemDoublesRec = 2 * TB * LD + TB + 64;
+constexpr unsigned kFull = 0xffffffffu;
+
+// The three single-warp kernels below keep one row (or column) per lane in registers, rotated
+// so that the current column is always element 0: the loop over columns stays rolled (compact
+// code: a D task runs once per tile, straight-line code would be fetched cold) while every
+// register index is static, and the rotation costs nothing (each FMA writes the next slot).
+// Entries beyond index 31 read rows >= 32 of the 64-row buffers: they only ever feed slots of
+// columns >= 32, which are never used.
+
+// Cholesky of the 32 x 32 block at A (row-major, ld) in place (lower part); invd[r] = 1 / L_rr;
+// col: 64-double warp scratch, col[32..63] = 0.  Returns false if a pivot is not positive.
+__device__ __forceinline__ bool warp_potrf32(double *A, int ld, double *invd, double *col, int lane) {
+  double a[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) a[c] = c <= lane ? A[lane * ld + c] : 0.0;
+  bool ok = true;
+#pragma unroll 1
+  for (int j = 0; j < 32; ++j) {
+    double iv = 0.0;
+    if (lane == j) {
+      if (!(a[0] > 0.0)) {
+        ok = false;
+        a[0] = 1.0;
+      }
+      iv = rsqrt_nr2(a[0]);
+      invd[j] = iv;
+    }
+    const double inv = __shfl_sync(kFull, iv, j);
+    const double l = lane >= j ? a[0] * inv : 0.0;   // L_lane,j (L_jj = a_jj / sqrt(a_jj))
+    col[lane] = l;
+    if (lane >= j) A[lane * ld + j] = l;
+    __syncwarp();
+#pragma unroll
+    for (int c = 1; c < 32; ++c) a[c - 1] = fma(-l, col[j + c], a[c]);   // column j + c
+    a[31] = 0.0;
+    __syncwarp();
+  }
+  return __all_sync(kFull, ok);
+}
+
+// Li (32 x 32, row-major ld) = L^-1 for the lower L at A (rows 32.. of A must be finite): lane c
+// forms column c by column-oriented forward substitution.
+__device__ __forceinline__ void warp_trinv32(const double *A, int ld, const double *invd, double *Li, int lane) {
+  double s[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) s[r] = r == lane ? 1.0 : 0.0;
+#pragma unroll 1
+  for (int q = 0; q < 32; ++q) {
+    const double x = s[0] * invd[q];   // zero for q < lane
+    Li[q * ld + lane] = x;
+#pragma unroll
+    for (int r = 1; r < 32; ++r) s[r - 1] = fma(-A[(q + r) * ld + q], x, s[r]);   // row q + r
+    s[31] = 0.0;
+  }
+}
+
+// X (32 rows at A21, row-major ld) <- X L^-T for the lower L at A11 (A11 rows continue into
+// A21): lane r solves row r, column-oriented.
+__device__ __forceinline__ void warp_trsm32(const double *A11, double *A21, int ld, const double *invd, int lane) {
+  double x[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) x[c] = A21[lane * ld + c];
+#pragma unroll 1
+  for (int c = 0; c < 32; ++c) {
+    const double v = x[0] * invd[c];
+    A21[lane * ld + c] = v;
+#pragma unroll
+    for (int c2 = 1; c2 < 32; ++c2) x[c2 - 1] = fma(-v, A11[(c + c2) * ld + c], x[c2]);
+    x[31] = 0.0;
+  }
+}
+
+__device__ void diag_factor_rec(int k, int nSp, double *__restrict__ L, double *__restrict__ U,
+                                int *__restrict__ flag, double *sm) {
+  double *A = sm;              // row-major [64][LD]: the factor
+  double *Li = sm + TB * LD;   // row-major [64][LD]: its inverse (+ T in the upper-right block)
+  double *invd = sm + 2 * TB * LD;
+  double *col = invd + TB;     // [64] broadcast buffer of warp 0 (col[32..63] = 0)
+  const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+  const size_t okk = tile_off(k, k, nSp);
+  if (t < 64) col[t] = 0.0;
+#pragma unroll 4
+  for (int it = 0; it < 16; ++it) {
+    const int e = t + it * 256, r = e & 63, c = e >> 6;
+    const double v = __ldcg(&L[okk + (size_t)c * nSp + r]);
+    A[r * LD + c] = r >= c ? v : 0.0;
+    Li[r * LD + c] = 0.0;
+  }
+  __syncthreads();
+  DIAG_TS(0);
+  bool ok = true;
+  if (w == 0) ok = warp_potrf32(A, LD, invd, col, lane);
+  __syncthreads();
+  DIAG_TS(1);
+  if (w == 1) warp_trsm32(A, A + 32 * LD, LD, invd, lane);
+  else if (w == 2) warp_trinv32(A, LD, invd, Li, lane);
+  __syncthreads();
+  DIAG_TS(2);
+  // A22 -= L21 L21^T (lower): thread (r, cg) = (t >> 3, t & 7) takes columns cg, cg + 8, ... <= r
+  {
+    const int r = t >> 3, cg = t & 7;
+    const double *xr = A + (32 + r) * LD;
+#pragma unroll 1
+    for (int c = cg; c <= r; c += 8) {
+      const double *xc = A + (32 + c) * LD;
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int q = 0; q < 32; ++q) s4[q & 3] = fma(xr[q], xc[q], s4[q & 3]);
+      A[(32 + r) * LD + 32 + c] -= (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    }
+  }
+  __syncthreads();
+  DIAG_TS(3);
+  if (w == 0) {
+    ok = warp_potrf32(A + 32 * LD + 32, LD, invd + 32, col, lane) && ok;
+    __syncwarp();
+    warp_trinv32(A + 32 * LD + 32, LD, invd + 32, Li + 32 * LD + 32, lane);
+  } else {
+    // T = L21 Li11 (32 x 32) into Li[r][32 + c] (r, c < 32): warps 1..7 stride over the entries
+#pragma unroll 1
+    for (int e = t - 32; e < 1024; e += 224) {
+      const int r = e >> 5, c = e & 31;
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};   // Li11 lower: terms q < c vanish
+#pragma unroll
+      for (int q = 0; q < 32; ++q) s4[q & 3] = fma(A[(32 + r) * LD + q], Li[q * LD + c], s4[q & 3]);
+      Li[r * LD + 32 + c] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    }
+  }
+  __syncthreads();
+  DIAG_TS(4);
+  // Li21 = -Li22 T
+#pragma unroll 1
+  for (int it = 0; it < 4; ++it) {
+    const int e = t + 256 * it, r = e >> 5, c = e & 31;
+    double s4[4] = {0.0, 0.0, 0.0, 0.0};   // Li22 lower: terms q > r vanish
+#pragma unroll
+    for (int q = 0; q < 32; ++q) s4[q & 3] = fma(Li[(32 + r) * LD + 32 + q], Li[q * LD + 32 + c], s4[q & 3]);
+    Li[(32 + r) * LD + c] = -((s4[0] + s4[1]) + (s4[2] + s4[3]));
+  }
+  if (!__syncthreads_and(ok) && t == 0 && flag) *flag = 1;
+  // store L_kk (lower, column-major) and U_kk = Li^T (row-major: U[c][r] at c*64 + r = Li[r][c])
+  double *Uk = U + (size_t)k * TB * TB;
+#pragma unroll 4
+  for (int it = 0; it < 16; ++it) {
+    const int e = t + it * 256, r = e & 63, c = e >> 6;
+    if (r >= c) __stcg(&L[okk + (size_t)c * nSp + r], A[r * LD + c]);
+    __stcg(&Uk[(size_t)c * TB + r], r >= c ? Li[r * LD + c] : 0.0);   // U[c][r] = Li[r][c]
+  }
+  __syncthreads();
+  DIAG_TS(5);
+}
+
+// ---------------------------------------------------------------- variants 1, 2
+// smem: A [64][LD], Li [64][LD], Tb [3*16*17], invd [64]
+constexpr int kDiagSmemDoublesBlocked = 2 * TB * LD + 3 * 16 * 17 + TB;
+
+// Register-blocked right-looking Cholesky of the 64x64 diagonal tile with the inverse built in
+// the same sweep (Gauss-Jordan on [L | I]): L = L_0 ... L_63 with L_j the identity whose column j
+// is l_j, so L^-1 = L_63^-1 ... L_0^-1 and applying L_j^-1 from the left is
+//   Z_j <- Z_j / l_jj,   Z_r <- Z_r - (l_rj / l_jj) Z_j^old  (r > j).
+// Thread t = rb + 16 cb owns the 4x4 blocks (rows 4rb.., cols 4cb..) of A and of Z; the 16
+// owners of column j form one half-warp, so the pivot is a shuffle and each step needs ONE
+// barrier (the pivot column and row j of Z are double-buffered in shared memory).
+__device__ void diag_factor_gj(int k, int nSp, double *__restrict__ L, double *__restrict__ U,
+                               int *__restrict__ flag, double *sm) {
+  double *colL = sm;          // [2][64] pivot column l_.j (zero above the diagonal)
+  double *rowZ = sm + 128;    // [2][64] row j of Z before scaling
+  double *sinv = sm + 256;    // [2]     1 / l_jj
+  const int t = threadIdx.x, rb = t & 15, cb = t >> 4, lane = t & 31;
+  const int r0 = 4 * rb, c0 = 4 * cb;
+  const size_t okk = tile_off(k, k, nSp);
+  double a[4][4], z[4][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int r = r0 + p, c = c0 + q;
+      a[p][q] = r >= c ? __ldcg(&L[okk + (size_t)c * nSp + r]) : 0.0;
+      z[p][q] = r == c ? 1.0 : 0.0;
+    }
+  if (rb == 0) {   // row 0 of Z = e_0
+#pragma unroll
+    for (int q = 0; q < 4; ++q) rowZ[c0 + q] = (c0 + q == 0) ? 1.0 : 0.0;
+  }
+  bool bad = false;
+#pragma unroll 1
+  for (int j = 0; j < TB; ++j) {
+    const int buf = j & 1, jb = j >> 2, jq = j & 3;
+    // phase A: the half-warp owning column j (cb == jb) forms l_.j
+    if (cb == jb) {
+      double mine = 0.0;
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q == jq && p == jq) mine = a[p][q];
+      const double d = __shfl_sync(0xffffu << (lane & 16), mine, (lane & 16) + jb, 32);
+      const bool ok = d > 0.0;
+      if (!ok) bad = true;
+      const double inv = ok ? rsqrt_nr2(d) : 1.0;
+      const double ljj = ok ? d * inv : 1.0;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const int r = r0 + p;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q == jq) {
+            const double l = r > j ? a[p][q] * inv : (r == j ? ljj : 0.0);
+            a[p][q] = l;
+            colL[buf * 64 + r] = l;
+          }
+      }
+      if (rb == 0) sinv[buf] = inv;
+    }
+    __syncthreads();
+    // phase B: trailing update of A and Z
+    const double inv = sinv[buf];
+    double lr[4], lc[4], zj[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      lr[p] = colL[buf * 64 + r0 + p];
+      lc[p] = (c0 + p > j) ? colL[buf * 64 + c0 + p] : 0.0;
+      zj[p] = rowZ[buf * 64 + c0 + p];
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int r = r0 + p;
+      const double fz = r > j ? lr[p] * inv : 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a[p][q] = fma(-lr[p], lc[q], a[p][q]);   // lc = 0 for c <= j; lr = 0 for r < j
+        z[p][q] = fma(-fz, zj[q], z[p][q]);
+        if (r == j) z[p][q] *= inv;
+      }
+    }
+    // row j+1 of Z is final now: publish it for the next step
+    if (j + 1 < TB && rb == ((j + 1) >> 2)) {
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+        if (r0 + p == j + 1)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) rowZ[(buf ^ 1) * 64 + c0 + q] = z[p][q];
+    }
+  }
+  if (bad && flag) *flag = 1;
+  // store L_kk (lower, column-major) and U_kk = Z^T (row-major: U[c][r] at c*64 + r = Z[r][c])
+  double *Uk = U + (size_t)k * TB * TB;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int r = r0 + p, c = c0 + q;
+      if (r >= c) __stcg(&L[okk + (size_t)c * nSp + r], a[p][q]);
+      __stcg(&Uk[(size_t)c * TB + r], z[p][q]);
+    }
+  __syncthreads();
+}
+
+__device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, double *__restrict__ U,
+                            int *__restrict__ flag, double *sm) {
+  double *A = sm;              // row-major [64][LD]: the factor
+  double *Li = sm + TB * LD;   // row-major [64][LD]: its inverse
+  double(*Tb)[16][17] = reinterpret_cast<double(*)[16][17]>(sm + 2 * TB * LD);
+  double *invd = sm + 2 * TB * LD + 3 * 16 * 17;
+  const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+  const size_t okk = tile_off(k, k, nSp);
+  {
+    double v[16];
+#pragma unroll
+    for (int it = 0; it < 16; ++it) {
+      const int e = t + it * 256;
+      v[it] = __ldcg(&L[okk + (size_t)(e >> 6) * nSp + (e & 63)]);
+    }
+#pragma unroll
+    for (int it = 0; it < 16; ++it) {
+      const int e = t + it * 256, r = e & 63, c = e >> 6;
+      A[r * LD + c] = r >= c ? v[it] : 0.0;
+      Li[r * LD + c] = 0.0;
+    }
+  }
+  __syncthreads();
+  DIAG_TS(0);
+  bool bad = false;
+  for (int p = 0; p < 4; ++p) {
+    const int j0 = 16 * p;
+    if (w == 0) {
+      // panel rows j0 + lane and j0 + 32 + lane, columns j0 .. j0+15
+      const int ra = j0 + lane, rb = j0 + 32 + lane;
+      const bool va = ra < TB, vb = rb < TB;
+      double a[16], b[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        a[c] = va ? A[ra * LD + j0 + c] : 0.0;
+        b[c] = vb ? A[rb * LD + j0 + c] : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const double d = __shfl_sync(0xffffffffu, a[j], j);
+        if (!(d > 0.0)) bad = true;
+        const double inv = d > 0.0 ? rsqrt_nr2(d) : 1.0;   // 1 / sqrt(d)
+        const double ljj = d > 0.0 ? d * inv : 1.0;
+        if (lane == 0) invd[j0 + j] = inv;
+        a[j] = lane == j ? ljj : (lane > j ? a[j] * inv : a[j]);
+        b[j] *= inv;
+#pragma unroll
+        for (int c = j + 1; c < 16; ++c) {
+          const double lc = __shfl_sync(0xffffffffu, a[j], c);
+          a[c] = fma(-a[j], lc, a[c]);
+          b[c] = fma(-b[j], lc, b[c]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        if (va && ra >= j0 + c) A[ra * LD + j0 + c] = a[c];
+        if (vb) A[rb * LD + j0 + c] = b[c];
+      }
+    }
+    __syncthreads();
+    DIAG_TS(1 + 2 * p);
+    // trailing update of rows/cols >= j0 + 16
+    const int s0 = j0 + 16;
+    for (int r = s0 + (t >> 2); r < TB; r += 64) {
+      for (int c = s0 + (t & 3); c <= r; c += 8) {   // two columns, four partial sums each
+        const bool two = c + 4 <= r;
+        double s0a = 0.0, s1a = 0.0, s0b = 0.0, s1b = 0.0;
+#pragma unroll
+        for (int j = 0; j < 16; j += 2) {
+          const double x0 = A[r * LD + j0 + j], x1 = A[r * LD + j0 + j + 1];
+          s0a = fma(x0, A[c * LD + j0 + j], s0a);
+          s1a = fma(x1, A[c * LD + j0 + j + 1], s1a);
+          if (two) {
+            s0b = fma(x0, A[(c + 4) * LD + j0 + j], s0b);
+            s1b = fma(x1, A[(c + 4) * LD + j0 + j + 1], s1b);
+          }
+        }
+        A[r * LD + c] -= s0a + s1a;
+        if (two) A[r * LD + c + 4] -= s0b + s1b;
+      }
+    }
+    __syncthreads();
+    DIAG_TS(2 + 2 * p);
+  }
+  if (w == 0 && lane == 0 && bad && flag) *flag = 1;
+  // inverse: diagonal 16x16 blocks (warp p, lane l < 16 solves column l)
+  if (w < 4 && lane < 16) {
+    const int o = 16 * w;
+    double x[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      double s = r == lane ? 1.0 : 0.0, s2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < r; q += 2) {
+        s = fma(-A[(o + r) * LD + o + q], x[q], s);
+        if (q + 1 < r) s2 = fma(-A[(o + r) * LD + o + q + 1], x[q + 1], s2);
+      }
+      x[r] = (s + s2) * invd[o + r];
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) Li[(o + r) * LD + o + lane] = x[r];
+  }
+  __syncthreads();
+  DIAG_TS(9);
+  // off-diagonal blocks: Li_pq = -Li_pp sum_{s=q}^{p-1} L_ps Li_sq, p = 1..3
+  for (int p = 1; p < 4; ++p) {
+    for (int e = t; e < p * 256; e += 256) {
+      const int q = e >> 8, r = (e >> 4) & 15, cc = e & 15;
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int m = 16 * q; m < 16 * p; m += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s4[u] = fma(A[(16 * p + r) * LD + m + u], Li[(m + u) * LD + 16 * q + cc], s4[u]);
+      }
+      Tb[q][r][cc] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    }
+    __syncthreads();
+    DIAG_TS(8 + 2 * p);
+    for (int e = t; e < p * 256; e += 256) {
+      const int q = e >> 8, r = (e >> 4) & 15, cc = e & 15;
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int m = 0; m < 16; ++m) s4[m & 3] = fma(Li[(16 * p + r) * LD + 16 * p + m], Tb[q][m][cc], s4[m & 3]);
+      Li[(16 * p + r) * LD + 16 * q + cc] = -((s4[0] + s4[1]) + (s4[2] + s4[3]));
+    }
+    __syncthreads();
+    DIAG_TS(9 + 2 * p);
+  }
+  // store L_kk (lower, column-major) and U_kk = Li^T (row-major: U[r][c] at r*64 + c = Li[c][r])
+  double *Uk = U + (size_t)k * TB * TB;
+#pragma unroll 4
+  for (int it = 0; it < 16; ++it) {
+    const int e = t + it * 256, r = e & 63, c = e >> 6;
+    if (r >= c) __stcg(&L[okk + (size_t)c * nSp + r], A[r * LD + c]);
+    __stcg(&Uk[(size_t)c * TB + r], Li[r * LD + c]);   // U[c][r] = Li[r][c]
+  }
+}
+
+
+// ---------------------------------------------------------------- dispatch
+constexpr int kDiagSmemDoubles = kDiagSmemDoublesBlocked > kDiagSmemDoublesRec ? kDiagSmemDoublesBlocked
+                                                                                : kDiagSmemDoublesRec;
+
+__device__ __noinline__ void diag_factor(int k, int nSp, double *__restrict__ L, double *__restrict__ U,
+                                         int *__restrict__ flag, double *sm) {
+#if MSIM_DIAG_VARIANT == 0
+  diag_factor_rec(k, nSp, L, U, flag, sm);
+#elif MSIM_DIAG_VARIANT == 1
+  diag_factor_blocked(k, nSp, L, U, flag, sm);
+#else
+  diag_factor_gj(k, nSp, L, U, flag, sm);
+#endif
+}

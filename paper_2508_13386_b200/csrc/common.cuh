@@ -165,6 +165,7 @@ struct Ctx {
   DBuf<int32_t> chol_rows;          // per tile k: tile columns j < k with L_kj != 0 (flattened)
   std::vector<int64_t> h_chol_rows_off;
   double chol_flops = 0.0;          // flops of one factorisation (tile granularity)
+  ms_coarse_info chol_info{};
   DBuf<int32_t> chol_rows_ptr, chol_panel_ptr, sym_tiles;
   int64_t n_sym_tiles = 0;
   DBuf<double> Uinv;                // [ntiles][64*64] U_kk = L_kk^-T (column-major)

@@ -391,6 +391,8 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
     std::vector<std::vector<int32_t>> panel, rows;
     std::vector<std::vector<char>> nz;
     double flops = 0.0;
+    int64_t ntask = 0;
+    int32_t crit = 0;
   };
   auto symbolic = [&](const std::vector<int32_t> &ord) {
     Sym y;
@@ -416,15 +418,49 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
       for (int32_t i : P) y.rows[i].push_back(k);
       const double np = (double)P.size();
       y.flops += (double)T * T * T / 3.0 + np * T * T * T + np * (np + 1) * T * T * T;
+      y.ntask += 1 + (int64_t)P.size() + (int64_t)(P.size() * (P.size() + 1) / 2);
+    }
+    // critical path of the tile DAG in tasks (D(k) -> P(i,k) -> U(i,j,k) -> ..., updates of a
+    // tile applied in k order)
+    std::vector<int32_t> ready((size_t)NT * NT, 0), pk(NT, 0);
+    for (int32_t k = 0; k < NT; ++k) {
+      const int32_t dk = ready[(size_t)k * NT + k] + 1;
+      for (int32_t i : y.panel[k]) pk[i] = std::max(dk, ready[(size_t)i * NT + k]) + 1;
+      const auto &P = y.panel[k];
+      for (size_t a = 0; a < P.size(); ++a)
+        for (size_t b = 0; b <= a; ++b) {
+          int32_t &r = ready[(size_t)P[a] * NT + P[b]];
+          r = std::max(r, std::max(pk[P[a]], pk[P[b]])) + 1;
+        }
+      y.crit = dk;
     }
     return y;
   };
   std::vector<int32_t> ident(m);
   std::iota(ident.begin(), ident.end(), 0);
   Sym sx = symbolic(ident), snd = symbolic(order);
-  Sym &best = snd.flops < sx.flops ? snd : sx;
+  const char *ord_env = std::getenv("MSIM_COARSE_ORDER");   // "x" / "nd": force (diagnostics)
+  Sym &best = ord_env ? (ord_env[0] == 'n' ? snd : sx) : (snd.flops < sx.flops ? snd : sx);
   c.h_perm = best.perm;
   c.chol_flops = best.flops;
+  c.chol_info.n_s = c.nS;
+  c.chol_info.tile = T;
+  c.chol_info.ntiles = NT;
+  c.chol_info.ordering = &best == &snd ? 1 : 0;
+  c.chol_info.flops = best.flops;
+  c.chol_info.flops_xorder = sx.flops;
+  c.chol_info.flops_nd = snd.flops;
+  c.chol_info.n_tasks = best.ntask;
+  c.chol_info.critical_path = best.crit;
+  c.chol_info.critical_path_xorder = sx.crit;
+  c.chol_info.critical_path_nd = snd.crit;
+  c.chol_info.nnzb_s = c.nnzb_S;
+  {
+    int64_t nzt = 0;
+    for (int32_t i = 0; i < NT; ++i)
+      for (int32_t j = 0; j <= i; ++j) nzt += best.nz[i][j];
+    c.chol_info.lower_tiles = nzt;
+  }
   c.h_chol_panel = best.panel;
   std::vector<int32_t> panel_flat, task_flat, rows_flat, sym_tiles;
   std::vector<int32_t> panel_ptr(NT + 1, 0), rows_ptr(NT + 1, 0);
@@ -539,7 +575,7 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
     const char *e = std::getenv("MSIM_CHOL_DATAFLOW");   // 0: per-step launches (diagnostics)
     c.chol_dataflow = !(e && e[0] == '0');
   }
-  c.df_flags.alloc((size_t)2 * NT * NT + NT);
+  c.df_flags.alloc((size_t)2 * NT * NT + NT + 1);   // + the task dispenser
   c.Uinv.alloc((size_t)NT * T * T);
   c.solve_flags.alloc(2 * (size_t)NT);
   {

@@ -47,6 +47,14 @@ class PhaseTimes(C.Structure):
     _fields_ = [("ms", C.c_double * 8), ("count", C.c_int64 * 8)]
 
 
+class CoarseInfo(C.Structure):
+    _fields_ = [("n_s", C.c_int64), ("tile", C.c_int64), ("ntiles", C.c_int64), ("lower_tiles", C.c_int64),
+                ("n_tasks", C.c_int64), ("critical_path", C.c_int64), ("nnzb_s", C.c_int64),
+                ("critical_path_xorder", C.c_int64), ("critical_path_nd", C.c_int64),
+                ("ordering", C.c_int32), ("pad_", C.c_int32), ("flops", C.c_double),
+                ("flops_xorder", C.c_double), ("flops_nd", C.c_double)]
+
+
 class PcgStats(C.Structure):
     _fields_ = [("iters", C.c_int32), ("rz0", C.c_double), ("rz", C.c_double)]
 
@@ -92,6 +100,7 @@ def _load():
         "ms_get_phase_times": ([P, C.POINTER(PhaseTimes)], C.c_int32),
         "ms_kernel_launches": ([P], C.c_int64),
         "ms_get_sizes": ([P, I64, I64, I64, I32, I64, I64], C.c_int32),
+        "ms_get_coarse_info": ([P, C.POINTER(CoarseInfo)], C.c_int32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -331,6 +340,12 @@ class Context:
         self._chk(lib.ms_get_sizes(self.h, _i64(a[0]), _i64(a[1]), _i64(a[2]), _i32(m), _i64(b[0]), _i64(b[1])))
         return dict(n_verts=int(a[0][0]), n_tets=int(a[1][0]), nnzb=int(a[2][0]), m=int(m[0]),
                     nnz_phi=int(b[0][0]), nnzb_S=int(b[1][0]))
+
+
+    def coarse_info(self):
+        ci = CoarseInfo()
+        self._chk(lib.ms_get_coarse_info(self.h, C.byref(ci)))
+        return {k: getattr(ci, k) for k, _ in CoarseInfo._fields_ if k != "pad_"}
 
 
 def context_from_scene(scene, basis, device=0, stream=None, **params):

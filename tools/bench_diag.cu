@@ -1,0 +1,96 @@
+// Micro-benchmark of the diagonal-tile factorisation variants (csrc/chol_diag.cuh): cycles per
+// 64 x 64 Cholesky + inverse by one CTA (clock64 inside the kernel), and a correctness check.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include -I paper_2508_13386_b200/csrc \
+//        tools/bench_diag.cu -o /tmp/bench_diag && /tmp/bench_diag
+#include <cstdio>
+#include <cstdlib>
+#include <cmath>
+#include <vector>
+#include <cuda_runtime.h>
+#include "fastmath.cuh"
+
+namespace msim {
+constexpr int TB = 64;
+constexpr int LD = TB + 1;
+__device__ __forceinline__ size_t tile_off(int ti, int tj, int nSp) { return (size_t)(tj * TB) * nSp + (size_t)ti * TB; }
+__device__ long long g_ts[16];
+#define DIAG_TS(i) do { if (threadIdx.x == 0 && blockIdx.x == 0) g_ts[i] = clock64(); } while (0)
+#include "chol_diag.cuh"
+}  // namespace msim
+using namespace msim;
+
+template <int V>
+__global__ void __launch_bounds__(256) kbench(const double *A0, double *L, double *U, int *flag, int reps,
+                                              long long *cyc) {
+  extern __shared__ double sm[];
+  double *Lb = L + (size_t)blockIdx.x * TB * TB, *Ub = U + (size_t)blockIdx.x * TB * TB;
+  long long tot = 0;
+  for (int r = 0; r < reps; ++r) {
+    for (int e = threadIdx.x; e < TB * TB; e += 256) Lb[e] = A0[e];
+    __syncthreads();
+    __threadfence_block();
+    long long t0 = clock64();
+    if (threadIdx.x == 0 && blockIdx.x == 0) g_ts[15] = t0;
+    if (V == 0) diag_factor_rec(0, TB, Lb, Ub, flag, sm);
+    else if (V == 1) diag_factor_blocked(0, TB, Lb, Ub, flag, sm);
+    else diag_factor_gj(0, TB, Lb, Ub, flag, sm);
+    __syncthreads();
+    tot += clock64() - t0;
+  }
+  if (threadIdx.x == 0) cyc[blockIdx.x] = tot / reps;
+}
+
+template <int V>
+void run(const std::vector<double> &A, int nblk) {
+  double *dA, *dL, *dU; int *dflag; long long *dc;
+  cudaMalloc(&dA, 8 * 4096); cudaMalloc(&dL, 8 * 4096 * nblk); cudaMalloc(&dU, 8 * 4096 * nblk);
+  cudaMalloc(&dflag, 4); cudaMalloc(&dc, 8 * nblk); cudaMemset(dflag, 0, 4);
+  cudaMemcpy(dA, A.data(), 8 * 4096, cudaMemcpyHostToDevice);
+  const int smem = 8 * kDiagSmemDoubles;
+  cudaFuncSetAttribute(kbench<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  kbench<V><<<nblk, 256, smem>>>(dA, dL, dU, dflag, 3, dc);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  kbench<V><<<nblk, 256, smem>>>(dA, dL, dU, dflag, 20, dc);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  std::vector<long long> c(nblk); cudaMemcpy(c.data(), dc, 8 * nblk, cudaMemcpyDeviceToHost);
+  std::vector<double> L(4096), U(4096); cudaMemcpy(L.data(), dL, 8 * 4096, cudaMemcpyDeviceToHost);
+  cudaMemcpy(U.data(), dU, 8 * 4096, cudaMemcpyDeviceToHost);
+  int flag; cudaMemcpy(&flag, dflag, 4, cudaMemcpyDeviceToHost);
+  if (nblk == 1) {
+    long long ts[16]; cudaMemcpyFromSymbol(ts, g_ts, sizeof(ts));
+    printf("v%d phases", V); printf(" (cycles from start): load %lld |", ts[0] - ts[15]);
+    for (int q = 1; q < 16 - 1; ++q) printf(" %d:%lld", q, ts[q] - ts[15]);
+    printf("\n");
+  }
+  // checks: L L^T = A (lower L column-major), U = L^-T (row-major U[c][r] at c*64 + r)
+  double e1n = 0, e2n = 0, an = 0;
+  for (int i = 0; i < 64; ++i)
+    for (int j = 0; j <= i; ++j) {
+      double s = 0; for (int q = 0; q <= j; ++q) s += L[q * 64 + i] * L[q * 64 + j];
+      e1n = fmax(e1n, fabs(s - A[j * 64 + i])); an = fmax(an, fabs(A[j * 64 + i]));
+    }
+  for (int i = 0; i < 64; ++i)   // (L^-1)[i][j] = U[j][i]; check L^-1 L = I
+    for (int j = 0; j < 64; ++j) {
+      double s = 0; for (int q = 0; q < 64; ++q) s += U[q * 64 + i] * (j <= q ? L[j * 64 + q] : 0.0);
+      e2n = fmax(e2n, fabs(s - (i == j ? 1.0 : 0.0)));
+    }
+  printf("variant %d  ctas %4d  cycles/factor %8lld  (%.2f us @1.965GHz)  wall %.1f us/factor-wave  |LL^T-A|/|A| %.1e  |Linv L - I| %.1e flag %d\n",
+         V, nblk, c[0], c[0] / 1965.0, 1e3 * ms / 20, e1n / an, e2n, flag);
+  cudaFree(dA); cudaFree(dL); cudaFree(dU); cudaFree(dflag); cudaFree(dc);
+}
+
+int main() {
+  std::vector<double> M(4096), A(4096);
+  srand(1);
+  for (auto &v : M) v = rand() / (double)RAND_MAX - 0.5;
+  for (int i = 0; i < 64; ++i)
+    for (int j = 0; j < 64; ++j) {
+      double s = i == j ? 64.0 : 0.0;
+      for (int q = 0; q < 64; ++q) s += M[i * 64 + q] * M[j * 64 + q];
+      A[j * 64 + i] = s;
+    }
+  for (int nb : {1, 148, 296}) { run<0>(A, nb); run<1>(A, nb); run<2>(A, nb); }
+  return 0;
+}
