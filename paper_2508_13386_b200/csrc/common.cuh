@@ -118,6 +118,8 @@ struct Ctx {
   DBuf<double> p, q, z, tmp;               // PCG vectors
   DBuf<double> stage_g;             // [nt*12] element gradients (unscaled by h^2)
   DBuf<double> stage_h;             // [nt*90] 10 upper 3x3 blocks of P+(H_e)
+  DBuf<int32_t> hess_work;          // [nt] tets whose reduced Hessian needs the eigen-clamp
+  DBuf<unsigned int> hess_nwork;    // [1] their count
   bool step_begun = false;
   bool assembled = false;
   bool coarse_ready = false;

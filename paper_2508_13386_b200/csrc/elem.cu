@@ -15,9 +15,13 @@
 // tests/test_oracle_fem.py::test_psd_element_reduction_equivalence).  The 9x9 symmetric
 // eigenproblem is solved in registers by cyclic Jacobi in the Brent-Luk parallel ordering
 // (9 rounds x 4 disjoint rotations per sweep -> 4 independent angle chains for ILP).
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "fastmath.cuh"
 #include "reduce.cuh"
+#include "eig9.cuh"
 
 namespace msim {
 
@@ -365,19 +369,19 @@ __device__ __forceinline__ double lift_entry(const double (&p9)[45], int a, int 
   return 0.25 * acc;
 }
 
-// true if M + tau ||M||_F I admits a Cholesky factorisation (packed symmetric 9x9)
-__device__ __forceinline__ bool psd_by_cholesky(const double (&a)[45], double tau) {
+// true if M + tau ||M||_F I admits a Cholesky factorisation (packed symmetric 9x9); a is
+// overwritten by the factor
+__device__ __forceinline__ bool psd_by_cholesky_inplace(double (&l)[45], double tau) {
   double fro2 = 0.0;
 #pragma unroll
   for (int i = 0; i < 9; ++i)
 #pragma unroll
-    for (int j = i; j < 9; ++j) fro2 += (i == j ? 1.0 : 2.0) * a[sidx(i, j)] * a[sidx(i, j)];
+    for (int j = i; j < 9; ++j) fro2 += (i == j ? 1.0 : 2.0) * l[sidx(i, j)] * l[sidx(i, j)];
   const double shift = tau * fro2 * rsqrt_nr2(fro2 > 0.0 ? fro2 : 1.0);
-  double l[45];
   bool ok = true;
 #pragma unroll
   for (int j = 0; j < 9; ++j) {
-    double d = a[sidx(j, j)] + shift;
+    double d = l[sidx(j, j)] + shift;
 #pragma unroll
     for (int q = 0; q < j; ++q) d = fma(-l[sidx(j, q)], l[sidx(j, q)], d);
     ok = ok && (d > 0.0);
@@ -385,7 +389,7 @@ __device__ __forceinline__ bool psd_by_cholesky(const double (&a)[45], double ta
     l[sidx(j, j)] = d * inv;
 #pragma unroll
     for (int i = j + 1; i < 9; ++i) {
-      double s = a[sidx(i, j)];
+      double s = l[sidx(i, j)];
 #pragma unroll
       for (int q = 0; q < j; ++q) s = fma(-l[sidx(i, q)], l[sidx(j, q)], s);
       l[sidx(i, j)] = s * inv;
@@ -394,26 +398,10 @@ __device__ __forceinline__ bool psd_by_cholesky(const double (&a)[45], double ta
   return ok;
 }
 
-// stage_h[e*90 + blk4(a,a2)*9 + 3 i + i2] = P+(H_e) block (a, a2), a <= a2 (unscaled by h^2)
-__global__ void __launch_bounds__(128) k_elem_hess(MeshView M, const double *__restrict__ x,
-                                                   double *__restrict__ stage_h) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= M.nt) return;
-  TetKin k;
-  load_tet_kin(M, x, e, k);
-  double a[45], p9[45];
-  reduced_hessian(k, a);
-  // PSD already (lambda_min > -1e-12 ||M||_F, Cholesky test): P+ = M to within 1e-11 relative,
-  // well inside the 1e-10 parity tolerance -- the Jacobi eigensolve is skipped
-  if (psd_by_cholesky(a, 1e-12)) {
-#pragma unroll
-    for (int q = 0; q < 45; ++q) p9[q] = a[q];
-  } else {
-    eig_clamp(a, p9);
-  }
-  double *dst = stage_h + (size_t)e * 90;
-  // H_e = Q P9 Q^T with Q4 = 1/2 [[1,1,1],[1,-1,-1],[-1,1,-1],[-1,-1,1]]: for each (i, i2) the
-  // 4x4 block over (A, A2) is 1/4 H4 P H4^T, formed with the Hadamard pattern (42 adds)
+// dst[blk4(a,a2)*9 + 3 i + i2] = block (a, a2), a <= a2, of H_e = Q P9 Q^T with
+// Q4 = 1/2 [[1,1,1],[1,-1,-1],[-1,1,-1],[-1,-1,1]]: for each (i, i2) the 4x4 block over (A, A2)
+// is 1/4 H4 P H4^T, formed with the Hadamard pattern (42 adds)
+__device__ __forceinline__ void lift_store(const double (&p9)[45], double *__restrict__ dst) {
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -437,6 +425,50 @@ __global__ void __launch_bounds__(128) k_elem_hess(MeshView M, const double *__r
         for (int A2 = A; A2 < 4; ++A2) dst[blk4(A, A2) * 9 + 3 * i + i2] = 0.25 * w[A2];
       }
     }
+}
+
+// stage_h[e*90 + blk4(a,a2)*9 + 3 i + i2] = P+(H_e) block (a, a2), a <= a2 (unscaled by h^2).
+// Pass 1 (every tet): reduced Hessian, P+ by e9::psd_project (tridiagonal QL + inverse iteration
+// on the negative eigenvalues, eig9.cuh).  A tet with more than kMaxNeg negative eigenvalues (or
+// no QL convergence) goes to a work list for pass 2, the cyclic-Jacobi eigen-clamp (the list
+// order depends on atomics, the per-tet result does not -> deterministic).
+constexpr int kMaxNeg = 4;
+
+constexpr int kHessThreads = 128;
+constexpr int kHessScratch = 35 + 9 * kMaxNeg;   // doubles per thread (eig9.cuh)
+
+#ifndef MSIM_HESS_MINB
+#define MSIM_HESS_MINB 2
+#endif
+__global__ void __launch_bounds__(kHessThreads, MSIM_HESS_MINB) k_elem_hess(MeshView M, const double *__restrict__ x,
+                                                            double *__restrict__ stage_h,
+                                                            int32_t *__restrict__ work,
+                                                            unsigned int *__restrict__ nwork) {
+  extern __shared__ double hsm[];   // [kHessScratch][kHessThreads], thread-minor (conflict-free)
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= M.nt) return;
+  TetKin k;
+  load_tet_kin(M, x, e, k);
+  double a[45], p9[45];
+  reduced_hessian(k, a);
+  if (e9::psd_project<kMaxNeg>(a, p9, hsm + threadIdx.x, kHessThreads) >= 0) lift_store(p9, stage_h + (size_t)e * 90);
+  else work[atomicAdd(nwork, 1u)] = e;
+}
+
+__global__ void __launch_bounds__(128) k_elem_hess_eig(MeshView M, const double *__restrict__ x,
+                                                       double *__restrict__ stage_h,
+                                                       const int32_t *__restrict__ work,
+                                                       const unsigned int *__restrict__ nwork) {
+  const int n = (int)*nwork;
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < n; w += gridDim.x * blockDim.x) {
+    const int e = work[w];
+    TetKin k;
+    load_tet_kin(M, x, e, k);
+    double a[45], p9[45];
+    reduced_hessian(k, a);
+    eig_clamp(a, p9);
+    lift_store(p9, stage_h + (size_t)e * 90);
+  }
 }
 
 // Expand staged element data to the parity-hook layout (full 12x12 row-major).
@@ -463,9 +495,24 @@ void launch_elem_grad_to(Ctx &c, const double *x, double *Ee) {
 void launch_elem_grad(Ctx &c) { launch_elem_grad_to(c, c.x, nullptr); }
 
 void launch_elem_hess_to(Ctx &c, const double *x) {
-  const int bs = 128, nb = div_up(c.nt, bs);
-  k_elem_hess<<<nb, bs, 0, c.stream>>>(mesh_view(c), x, c.stage_h);
-  c.launches++;
+  MS_CUDA(cudaMemsetAsync(c.hess_nwork, 0, sizeof(unsigned int), c.stream));
+  constexpr int smem = sizeof(double) * kHessScratch * kHessThreads;
+  static bool attr = false;
+  if (!attr) {
+    MS_CUDA(cudaFuncSetAttribute(k_elem_hess, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  k_elem_hess<<<div_up(c.nt, kHessThreads), kHessThreads, smem, c.stream>>>(
+      mesh_view(c), x, c.stage_h, c.hess_work, c.hess_nwork);
+  k_elem_hess_eig<<<148 * 2, 128, 0, c.stream>>>(mesh_view(c), x, c.stage_h, c.hess_work, c.hess_nwork);
+  c.launches += 2;
+  static const bool dbg = std::getenv("MSIM_DEBUG_HESS") != nullptr;   // diagnostics only
+  if (dbg) {
+    unsigned int nw = 0;
+    MS_CUDA(cudaMemcpyAsync(&nw, c.hess_nwork, sizeof(nw), cudaMemcpyDeviceToHost, c.stream));
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+    fprintf(stderr, "[msim] hess: %u of %d tets need the eigen-clamp (%.1f%%)\n", nw, c.nt, 100.0 * nw / c.nt);
+  }
   MS_CUDA(cudaGetLastError());
 }
 
