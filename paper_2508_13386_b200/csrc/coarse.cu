@@ -127,7 +127,7 @@ struct HView {                      // SELL-32 Hessian (sell.cuh)
 
 // One CTA per handle i computes the upper block row S_ij (j >= i) with R_i never leaving the
 // SM.  For each chunk of kGalChunk vertices u of U_i:
-//   phase A (two threads per u, each half of the (i,u) neighbour list, summed in a fixed order):
+//   phase A (two threads per u, even / odd Hessian row slots, summed in a fixed order):
 //            R_i(u) = sum_{v in N(u), i in supp(v)} w_vi kron H_vu   -> shared Rs[u][36]
 //   phase B (warp per upper slot j): S_ij += sum_{u in chunk, j in supp(u)} R_i(u) w_uj^T; the
 //            warp stages 32 list entries (u, w_uj) at a time in shared memory (one round trip
@@ -140,6 +140,7 @@ constexpr int kGalWarps = kGalThreads / 32;
 __global__ void __launch_bounds__(kGalThreads, 2) k_galerkin_fused(
     HView H, const int32_t *__restrict__ gU_ptr, const int32_t *__restrict__ gU,
     const int32_t *__restrict__ ga_off, const uint32_t *__restrict__ ga_ent,
+    const unsigned long long *__restrict__ ga_mask,
     const int32_t *__restrict__ gj_ptr, const int32_t *__restrict__ gj_blk,
     const int32_t *__restrict__ gl_base, const int32_t *__restrict__ gl_off,
     const uint32_t *__restrict__ gl_ent, const double *__restrict__ W, const int32_t *__restrict__ sT,
@@ -165,15 +166,19 @@ __global__ void __launch_bounds__(kGalThreads, 2) k_galerkin_fused(
     for (int k = 0; k < 36; ++k) acc[k] = 0.0;
     const int uq = ch * kGalChunk + ul_a;
     if (uq < nU) {
+      // slot-synchronous walk of row u: lanes of a warp (consecutive u of one SELL slice) read
+      // the same slot j together (coalesced value planes); the two halves take even / odd slots
       const int q = u0 + uq;
       const int u = __ldg(&gU[q]);
       const int ln_ = u & 31;
-      const int base = __ldg(&H.sl_ptr[u >> 5]);
-      const int e1 = __ldg(&ga_off[q + 1]);
+      const int base = __ldg(&H.sl_ptr[u >> 5]), len = __ldg(&H.sl_ptr[(u >> 5) + 1]) - base;
+      const unsigned long long mask = __ldg(&ga_mask[q]);
+      const int e0 = __ldg(&ga_off[q]);
 #pragma unroll 2
-      for (int e = __ldg(&ga_off[q]) + half; e < e1; e += 2) {
-        const uint32_t en = __ldg(&ga_ent[e]);
-        const size_t cs = (size_t)base + (en & 63);
+      for (int j = half; j < len; j += 2) {
+        if (!((mask >> j) & 1ull)) continue;
+        const uint32_t en = __ldg(&ga_ent[e0 + __popcll(mask & ((1ull << j) - 1ull))]);
+        const size_t cs = (size_t)base + j;
         const size_t p = en >> 6;
         const double2 w01 = __ldg(reinterpret_cast<const double2 *>(W + 4 * p));
         const double2 w23 = __ldg(reinterpret_cast<const double2 *>(W + 4 * p + 2));
@@ -435,7 +440,7 @@ void launch_coarse_S(Ctx &c) {
     MS_CUDA(cudaFuncSetAttribute(k_galerkin_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     smem_set = smem;
   }
-  k_galerkin_fused<<<c.m, kGalThreads, smem, c.stream>>>(hview(c), c.gU_ptr, c.gU, c.ga_off, c.ga_ent, c.gj_ptr,
+  k_galerkin_fused<<<c.m, kGalThreads, smem, c.stream>>>(hview(c), c.gU_ptr, c.gU, c.ga_off, c.ga_ent, c.ga_mask, c.gj_ptr,
                                                          c.gj_blk, c.gl_base, c.gl_off, c.gl_ent, c.Wphi, c.sT,
                                                          c.Sblk);
   const double *o = c.aff_origin;

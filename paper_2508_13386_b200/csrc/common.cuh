@@ -145,6 +145,7 @@ struct Ctx {
   DBuf<int32_t> gU_ptr, gU;         // [m+1], [sum |U_i|]
   DBuf<int32_t> ga_off;             // [sum |U_i| + 1] per (i,u) pair: range in ga_ent
   DBuf<uint32_t> ga_ent;            // Hessian row slot j of u | (basis entry p of (v, i)) << 6
+  DBuf<unsigned long long> ga_mask; // per (i,u) pair: bit j set if slot j is listed
   DBuf<int32_t> gj_ptr, gj_blk;     // upper slots j >= i of row i -> S block index
   DBuf<int32_t> gl_base, gl_off;    // per (i, chunk, slot) entry ranges
   DBuf<uint32_t> gl_ent;            // u_local | (basis entry p) << 7

@@ -270,17 +270,24 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   // per (i, u) pair: the Hessian row slots j of u whose vertex v lies in supp(i): (j | p << 6)
   std::vector<int32_t> ga_off(1, 0);
   std::vector<uint32_t> ga_ent;
+  std::vector<unsigned long long> ga_mask;   // bit j: slot j of row u is in the list
   ga_off.reserve(Uall.size() + 1);
+  ga_mask.reserve(Uall.size());
   for (int32_t i = 0; i < m; ++i)
     for (int32_t q = Uptr[i]; q < Uptr[i + 1]; ++q) {
       const int32_t u = Uall[q];
       MS_REQUIRE(rp[u + 1] - rp[u] <= 64, MS_ERR_ARG, "Hessian row longer than 64 blocks (Galerkin encoding)");
+      unsigned long long mask = 0;
       for (int32_t j = 0; j < rp[u + 1] - rp[u]; ++j) {
         const int32_t v = ci[rp[u] + j];
         const int32_t *hb = handle + vptr[v], *he = handle + vptr[v + 1];
         const int32_t *f = std::lower_bound(hb, he, i);
-        if (f != he && *f == i) ga_ent.push_back((uint32_t)j | ((uint32_t)(vptr[v] + (f - hb)) << 6));
+        if (f != he && *f == i) {
+          ga_ent.push_back((uint32_t)j | ((uint32_t)(vptr[v] + (f - hb)) << 6));
+          mask |= 1ull << j;
+        }
       }
+      ga_mask.push_back(mask);
       MS_REQUIRE(ga_ent.size() < (size_t)INT32_MAX, MS_ERR_ARG, "Galerkin pair list too large");
       ga_off.push_back((int32_t)ga_ent.size());
     }
@@ -558,6 +565,7 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   c.gU_ptr.upload(Uptr, s);
   c.gU.upload(Uall, s);
   c.ga_off.upload(ga_off, s);
+  c.ga_mask.upload(ga_mask.empty() ? std::vector<unsigned long long>{0} : ga_mask, s);
   c.ga_ent.upload(ga_ent.empty() ? std::vector<uint32_t>{0} : ga_ent, s);
   c.gj_ptr.upload(gj_ptr, s);
   c.gj_blk.upload(gj_blk, s);

@@ -177,6 +177,26 @@ void launch_assemble(Ctx &c) {
 }
 
 // ------------------------------------------------------------------ SpMV (SELL-32, thread per row)
+#ifndef MSIM_SPMV_UNROLL
+#define MSIM_SPMV_UNROLL 16   // = full unroll for rows of <= 16 blocks: every load of a row in flight
+#endif
+#ifndef MSIM_SPMV_NOLDG
+#define MSIM_SPMV_LDG
+#endif
+constexpr int kSpmvUnroll = MSIM_SPMV_UNROLL;
+
+// matrix values are streamed once per product: read-only path, no L1 allocation (keeps L1 for
+// the x gathers)
+__device__ __forceinline__ double ld_stream(const double *p) {
+#ifdef MSIM_SPMV_L1ALLOC
+  return __ldg(p);
+#else
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+#endif
+}
+
 static SellView sell_view(const Ctx &c) { return SellView{c.nv, c.sl_ptr, c.sell_col, c.vals}; }
 
 __device__ __forceinline__ void sell_row_product(const SellView &H, int row, const double *__restrict__ xin,
@@ -184,14 +204,20 @@ __device__ __forceinline__ void sell_row_product(const SellView &H, int row, con
   const int sl = row >> 5, lane = row & 31;
   const int c0 = __ldg(&H.sl_ptr[sl]), c1 = __ldg(&H.sl_ptr[sl + 1]);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-#pragma unroll 4
+#pragma unroll(kSpmvUnroll)
   for (int cc = c0; cc < c1; ++cc) {
     const int col = __ldg(&H.col[(size_t)cc * 32 + lane]);
     const double *v = H.vals + (size_t)cc * 288 + lane;
+#if defined(MSIM_SPMV_NOGATHER)   // diagnostics only (wrong results): streaming cost without the x gather
+    const double x0 = 1.0 + col * 1e-30, x1 = x0, x2 = x0;
+#elif defined(MSIM_SPMV_LDG)
+    const double x0 = __ldg(&xin[3 * col]), x1 = __ldg(&xin[3 * col + 1]), x2 = __ldg(&xin[3 * col + 2]);
+#else
     const double x0 = xin[3 * col], x1 = xin[3 * col + 1], x2 = xin[3 * col + 2];
-    a0 = fma(__ldg(v), x0, fma(__ldg(v + 32), x1, fma(__ldg(v + 64), x2, a0)));
-    a1 = fma(__ldg(v + 96), x0, fma(__ldg(v + 128), x1, fma(__ldg(v + 160), x2, a1)));
-    a2 = fma(__ldg(v + 192), x0, fma(__ldg(v + 224), x1, fma(__ldg(v + 256), x2, a2)));
+#endif
+    a0 = fma(ld_stream(v), x0, fma(ld_stream(v + 32), x1, fma(ld_stream(v + 64), x2, a0)));
+    a1 = fma(ld_stream(v + 96), x0, fma(ld_stream(v + 128), x1, fma(ld_stream(v + 160), x2, a1)));
+    a2 = fma(ld_stream(v + 192), x0, fma(ld_stream(v + 224), x1, fma(ld_stream(v + 256), x2, a2)));
   }
   o[0] = a0;
   o[1] = a1;
