@@ -172,7 +172,6 @@ struct Ctx {
   DBuf<int32_t> chol_rows_ptr, chol_panel_ptr, sym_tiles;
   int64_t n_sym_tiles = 0;
   DBuf<double> Uinv;                // [ntiles][64*64] U_kk = L_kk^-T (column-major)
-  DBuf<int> solve_flags;            // [2 ntiles] tile-ready flags of the cooperative solves
   DBuf<int32_t> chol_dag;           // dataflow factorisation tasks (int4 each)
   int64_t n_dag = 0;
   DBuf<int> df_flags;               // upd[NT*NT], pfl[NT*NT], dfl[NT]
@@ -181,6 +180,7 @@ struct Ctx {
   cudaGraphExec_t factor_graph = nullptr, solve_graph = nullptr;
   int64_t factor_graph_kernels = 0, solve_graph_kernels = 0;
   DBuf<double> qa, qs, za, zs, yp;  // coarse vectors (qs/yp: permuted work space)
+  DBuf<double> xsol;                // [nS_pad] permuted solution of the backward sweep
   DBuf<int32_t> flags;              // [8]: 0 = chol not SPD (S), 1 = not SPD (Sa), 2 = infeasible
 
   // ---- scalars / reductions

@@ -587,7 +587,6 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   }
   c.df_flags.alloc((size_t)2 * NT * NT + NT + 1);   // + the task dispenser
   c.Uinv.alloc((size_t)NT * T * T);
-  c.solve_flags.alloc(2 * (size_t)NT);
   {
     int nsm = 0;
     MS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));
@@ -600,6 +599,7 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   c.qs.alloc(c.nS_pad);
   c.zs.alloc(c.nS_pad);
   c.yp.alloc(c.nS_pad);
+  c.xsol.alloc(c.nS_pad);
   coarse_reset_graphs(c);
   launch_basis_W(c);
   MS_CUDA(cudaStreamSynchronize(s));
