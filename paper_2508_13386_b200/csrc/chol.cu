@@ -14,6 +14,7 @@
 // on the solution tiles it depends on (the vectors carry their own ready pattern) and applies
 // U_kk as a GEMV.
 #include <cooperative_groups.h>
+#include <cstdio>
 #include <cuda_pipeline.h>
 
 #include "common.cuh"
@@ -152,6 +153,20 @@ __global__ void __launch_bounds__(256) k_chol_update(int k, const int32_t *__res
 //   U(i,j,k): wait pfl[i][k], pfl[j][k], upd[i][j] == rank (updates of a tile are applied in
 //             step order -> deterministic);  A_ij -= L_ik L_jk^T;               upd[i][j] = rank + 1
 // Tile data produced by other CTAs is read through L2 only (cp.async.cg / ld.global.cg).
+#ifdef MSIM_DF_PROF   // diagnostics: global-timer stamps of the critical-path (type-4) tasks
+__device__ unsigned long long g_df_prof[1024][6];
+#define DF_STAMP(i, s)                                                              \
+  do {                                                                              \
+    if (threadIdx.x == 0) {                                                         \
+      unsigned long long tt;                                                        \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));                        \
+      g_df_prof[(i) & 1023][s] = tt;                                                \
+    }                                                                               \
+  } while (0)
+#else
+#define DF_STAMP(i, s)
+#endif
+
 __device__ __forceinline__ void df_wait(const int *p, int val) {
   if (threadIdx.x == 0) {
     const volatile int *f = p;
@@ -169,7 +184,10 @@ __device__ __forceinline__ void df_signal(int *p, int val) {
   }
 }
 
-__global__ void __launch_bounds__(256, 2) k_chol_dataflow(int ntask, const int4 *__restrict__ tasks, int NT, int nSp,
+#ifndef MSIM_DF_MINB
+#define MSIM_DF_MINB 2
+#endif
+__global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(int ntask, const int4 *__restrict__ tasks, int NT, int nSp,
                                                        double *__restrict__ L, double *__restrict__ U,
                                                        int *__restrict__ upd, int *__restrict__ dfl,
                                                        int *__restrict__ pfl, int *__restrict__ flag,
@@ -194,8 +212,10 @@ __global__ void __launch_bounds__(256, 2) k_chol_dataflow(int ntask, const int4 
     } else if (type == 4) {
       // critical-path task of step k (i = k+1): P(i,k), U(i,i,k) and D(i) in one CTA.
       // cnt = updates tile (i,k) must have seen; tk.w >> 16 unused; rank of (i,i) is upd order
+      DF_STAMP(i, 0);
       df_wait(&dfl[k], 1);
       df_wait(&upd[i * NT + k], cnt & 0xffff);
+      DF_STAMP(i, 1);
       double *SA = sm, *SU = sm + TB * TB;
       const size_t oik = tile_off(i, k, nSp);
       stage_colmajor(SA, L + oik, nSp);
@@ -209,6 +229,7 @@ __global__ void __launch_bounds__(256, 2) k_chol_dataflow(int ntask, const int4 
 #pragma unroll
         for (int a = 0; a < 4; ++a) __stcg(&L[oik + (size_t)(tc + 16 * b) * nSp + tr + 16 * a], acc[a][b]);
       df_signal(&pfl[i * NT + k], 1);             // panel tile published early for the other updates
+      DF_STAMP(i, 2);
       // X = L_ik into k-major smem: SX[c*64 + r] = X[r][c]
       double *SX = sm;
 #pragma unroll
@@ -216,6 +237,7 @@ __global__ void __launch_bounds__(256, 2) k_chol_dataflow(int ntask, const int4 
 #pragma unroll
         for (int a = 0; a < 4; ++a) SX[(tc + 16 * b) * TB + tr + 16 * a] = acc[a][b];
       df_wait(&upd[i * NT + i], cnt >> 16);
+      DF_STAMP(i, 3);
       const size_t oii = tile_off(i, i, nSp);
       double old[4][4];
 #pragma unroll
@@ -224,17 +246,19 @@ __global__ void __launch_bounds__(256, 2) k_chol_dataflow(int ntask, const int4 
         for (int a = 0; a < 4; ++a) old[a][b] = __ldcg(&L[oii + (size_t)(tc + 16 * b) * nSp + tr + 16 * a]);
       __syncthreads();
       gemm64(SX, SX, acc, tr, tc);
+      __syncthreads();   // SX consumed: the updated tile goes straight into D's smem layout
 #pragma unroll
       for (int b = 0; b < 4; ++b)
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
           const int r = tr + 16 * a, c = tc + 16 * b;
-          if (r >= c) __stcg(&L[oii + (size_t)c * nSp + r], old[a][b] - acc[a][b]);
+          sm[r * LD + c] = r >= c ? old[a][b] - acc[a][b] : 0.0;
         }
-      __syncthreads();
-      diag_factor(i, nSp, L, U, flag, sm);
+      DF_STAMP(i, 4);
+      diag_factor(i, nSp, L, U, flag, sm, true);
       df_signal(&dfl[i], 1);
       df_signal(&upd[i * NT + i], (cnt >> 16) + 1);
+      DF_STAMP(i, 5);
     } else if (type == 1) {
       df_wait(&dfl[k], 1);
       df_wait(&upd[i * NT + k], cnt);
@@ -452,12 +476,17 @@ static bool step_updates_diag(const Ctx &c, int k) {   // is tile (k+1, k+1) amo
   return !P.empty() && P.front() == k + 1;
 }
 
+#ifndef MSIM_DF_PER_SM
+#define MSIM_DF_PER_SM 1   // the critical-path CTA gets a whole SM (measured: 3.68 -> 3.25 ms at C4)
+#endif
+constexpr int kDfCtasPerSm = MSIM_DF_PER_SM;   // CTAs per SM of the dataflow factorisation
+
 static int dataflow_grid(const Ctx &c) {
   static int per_sm = -1;
   if (per_sm < 0) {
     MS_CUDA(cudaFuncSetAttribute(k_chol_dataflow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem));
     MS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chol_dataflow, 256, kUpdSmem));
-    per_sm = std::max(per_sm, 1);
+    per_sm = std::max(std::min(per_sm, kDfCtasPerSm), 1);
   }
   return (int)std::min<int64_t>(c.n_dag, (int64_t)per_sm * c.coop_grid);
 }
@@ -480,6 +509,22 @@ void enqueue_chol_factor(Ctx &c) {
     void *args[] = {&ntask, &tk, &NTv, &nSpv, &Lp, &Up, &upd, &dfl, &pfl, &fl, &nx};
     MS_CUDA(cudaLaunchCooperativeKernel((const void *)k_chol_dataflow, dim3(dataflow_grid(c)), dim3(256), args,
                                         kUpdSmem, c.stream));
+#ifdef MSIM_DF_PROF
+    {
+      static unsigned long long h[1024][6];
+      MS_CUDA(cudaStreamSynchronize(c.stream));
+      MS_CUDA(cudaMemcpyFromSymbol(h, g_df_prof, sizeof(h)));
+      double seg[5] = {0, 0, 0, 0, 0}, gap = 0;
+      int n = 0;
+      for (int i = 1; i < NT && i < 1024; ++i) {
+        for (int q = 0; q < 5; ++q) seg[q] += 1e-3 * (double)(h[i][q + 1] - h[i][q]);
+        if (i > 1) gap += 1e-3 * (double)(h[i][1] - h[i - 1][5]);
+        n++;
+      }
+      fprintf(stderr, "[msim] chol type-4 avg us: wait %.2f  P %.2f  wait-ii %.2f  U %.2f  D %.2f | ready-after-prev-D %.2f | total %.1f us\n",
+              seg[0] / n, seg[1] / n, seg[2] / n, seg[3] / n, seg[4] / n, gap / n, 1e-3 * (double)(h[NT - 1][5] - h[1][0]));
+    }
+#endif
     return;
   }
   k_chol_diag<<<1, 256, kDiagSmem, c.stream>>>(0, nSp, c.Lden, c.Uinv, c.flags + 0);

@@ -3,8 +3,8 @@
 // Variants (selected by MSIM_DIAG_VARIANT; timed by tools/bench_diag.cu):
 //   0 diag_factor_rec      2 x 2 recursion on 32 x 32 blocks, single-warp panel work
 //   1 diag_factor_blocked  right-looking, 16-column panels factored by one warp in registers
-//   2 diag_factor_gj       register-blocked right-looking Cholesky + Gauss-Jordan inverse
-// All take the tile from L (column-major, leading dimension nSp) and write L_kk back there
+// Both take the tile from L (column-major, leading dimension nSp) or preloaded in shared memory,
+// and write L_kk back there
 // and U_kk (row-major 64 x 64) to U + k 64^2; *flag = 1 if a pivot is not positive.
 // Requires TB = 64, LD = 65 and tile_off() from the including file.
 #pragma once
@@ -98,7 +98,7 @@ __device__ __forceinline__ void warp_trsm32(const double *A11, double *A21, int 
 }
 
 __device__ void diag_factor_rec(int k, int nSp, double *__restrict__ L, double *__restrict__ U,
-                                int *__restrict__ flag, double *sm) {
+                                int *__restrict__ flag, double *sm, bool preloaded) {
   double *A = sm;              // row-major [64][LD]: the factor
   double *Li = sm + TB * LD;   // row-major [64][LD]: its inverse (+ T in the upper-right block)
   double *invd = sm + 2 * TB * LD;
@@ -109,8 +109,10 @@ __device__ void diag_factor_rec(int k, int nSp, double *__restrict__ L, double *
 #pragma unroll 4
   for (int it = 0; it < 16; ++it) {
     const int e = t + it * 256, r = e & 63, c = e >> 6;
-    const double v = __ldcg(&L[okk + (size_t)c * nSp + r]);
-    A[r * LD + c] = r >= c ? v : 0.0;
+    if (!preloaded) {
+      const double v = __ldcg(&L[okk + (size_t)c * nSp + r]);
+      A[r * LD + c] = r >= c ? v : 0.0;
+    }
     Li[r * LD + c] = 0.0;
   }
   __syncthreads();
@@ -181,117 +183,15 @@ __device__ void diag_factor_rec(int k, int nSp, double *__restrict__ L, double *
 // smem: A [64][LD], Li [64][LD], Tb [3*16*17], invd [64]
 constexpr int kDiagSmemDoublesBlocked = 2 * TB * LD + 3 * 16 * 17 + TB;
 
-// Register-blocked right-looking Cholesky of the 64x64 diagonal tile with the inverse built in
-// the same sweep (Gauss-Jordan on [L | I]): L = L_0 ... L_63 with L_j the identity whose column j
-// is l_j, so L^-1 = L_63^-1 ... L_0^-1 and applying L_j^-1 from the left is
-//   Z_j <- Z_j / l_jj,   Z_r <- Z_r - (l_rj / l_jj) Z_j^old  (r > j).
-// Thread t = rb + 16 cb owns the 4x4 blocks (rows 4rb.., cols 4cb..) of A and of Z; the 16
-// owners of column j form one half-warp, so the pivot is a shuffle and each step needs ONE
-// barrier (the pivot column and row j of Z are double-buffered in shared memory).
-__device__ void diag_factor_gj(int k, int nSp, double *__restrict__ L, double *__restrict__ U,
-                               int *__restrict__ flag, double *sm) {
-  double *colL = sm;          // [2][64] pivot column l_.j (zero above the diagonal)
-  double *rowZ = sm + 128;    // [2][64] row j of Z before scaling
-  double *sinv = sm + 256;    // [2]     1 / l_jj
-  const int t = threadIdx.x, rb = t & 15, cb = t >> 4, lane = t & 31;
-  const int r0 = 4 * rb, c0 = 4 * cb;
-  const size_t okk = tile_off(k, k, nSp);
-  double a[4][4], z[4][4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const int r = r0 + p, c = c0 + q;
-      a[p][q] = r >= c ? __ldcg(&L[okk + (size_t)c * nSp + r]) : 0.0;
-      z[p][q] = r == c ? 1.0 : 0.0;
-    }
-  if (rb == 0) {   // row 0 of Z = e_0
-#pragma unroll
-    for (int q = 0; q < 4; ++q) rowZ[c0 + q] = (c0 + q == 0) ? 1.0 : 0.0;
-  }
-  bool bad = false;
-#pragma unroll 1
-  for (int j = 0; j < TB; ++j) {
-    const int buf = j & 1, jb = j >> 2, jq = j & 3;
-    // phase A: the half-warp owning column j (cb == jb) forms l_.j
-    if (cb == jb) {
-      double mine = 0.0;
-#pragma unroll
-      for (int p = 0; p < 4; ++p)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (q == jq && p == jq) mine = a[p][q];
-      const double d = __shfl_sync(0xffffu << (lane & 16), mine, (lane & 16) + jb, 32);
-      const bool ok = d > 0.0;
-      if (!ok) bad = true;
-      const double inv = ok ? rsqrt_nr2(d) : 1.0;
-      const double ljj = ok ? d * inv : 1.0;
-#pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        const int r = r0 + p;
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (q == jq) {
-            const double l = r > j ? a[p][q] * inv : (r == j ? ljj : 0.0);
-            a[p][q] = l;
-            colL[buf * 64 + r] = l;
-          }
-      }
-      if (rb == 0) sinv[buf] = inv;
-    }
-    __syncthreads();
-    // phase B: trailing update of A and Z
-    const double inv = sinv[buf];
-    double lr[4], lc[4], zj[4];
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      lr[p] = colL[buf * 64 + r0 + p];
-      lc[p] = (c0 + p > j) ? colL[buf * 64 + c0 + p] : 0.0;
-      zj[p] = rowZ[buf * 64 + c0 + p];
-    }
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const int r = r0 + p;
-      const double fz = r > j ? lr[p] * inv : 0.0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        a[p][q] = fma(-lr[p], lc[q], a[p][q]);   // lc = 0 for c <= j; lr = 0 for r < j
-        z[p][q] = fma(-fz, zj[q], z[p][q]);
-        if (r == j) z[p][q] *= inv;
-      }
-    }
-    // row j+1 of Z is final now: publish it for the next step
-    if (j + 1 < TB && rb == ((j + 1) >> 2)) {
-#pragma unroll
-      for (int p = 0; p < 4; ++p)
-        if (r0 + p == j + 1)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) rowZ[(buf ^ 1) * 64 + c0 + q] = z[p][q];
-    }
-  }
-  if (bad && flag) *flag = 1;
-  // store L_kk (lower, column-major) and U_kk = Z^T (row-major: U[c][r] at c*64 + r = Z[r][c])
-  double *Uk = U + (size_t)k * TB * TB;
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const int r = r0 + p, c = c0 + q;
-      if (r >= c) __stcg(&L[okk + (size_t)c * nSp + r], a[p][q]);
-      __stcg(&Uk[(size_t)c * TB + r], z[p][q]);
-    }
-  __syncthreads();
-}
-
 __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, double *__restrict__ U,
-                            int *__restrict__ flag, double *sm) {
+                                    int *__restrict__ flag, double *sm, bool preloaded) {
   double *A = sm;              // row-major [64][LD]: the factor
   double *Li = sm + TB * LD;   // row-major [64][LD]: its inverse
   double(*Tb)[16][17] = reinterpret_cast<double(*)[16][17]>(sm + 2 * TB * LD);
   double *invd = sm + 2 * TB * LD + 3 * 16 * 17;
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
   const size_t okk = tile_off(k, k, nSp);
-  {
+  if (!preloaded) {
     double v[16];
 #pragma unroll
     for (int it = 0; it < 16; ++it) {
@@ -302,8 +202,12 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
     for (int it = 0; it < 16; ++it) {
       const int e = t + it * 256, r = e & 63, c = e >> 6;
       A[r * LD + c] = r >= c ? v[it] : 0.0;
-      Li[r * LD + c] = 0.0;
     }
+  }
+#pragma unroll
+  for (int it = 0; it < 16; ++it) {
+    const int e = t + it * 256;
+    Li[(e & 63) * LD + (e >> 6)] = 0.0;
   }
   __syncthreads();
   DIAG_TS(0);
@@ -425,13 +329,13 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
 constexpr int kDiagSmemDoubles = kDiagSmemDoublesBlocked > kDiagSmemDoublesRec ? kDiagSmemDoublesBlocked
                                                                                 : kDiagSmemDoublesRec;
 
+// preloaded: the caller has already placed the (updated) tile in sm as A [64][LD] row-major,
+// lower part, zeros above the diagonal (skips the global round trip on the critical path).
 __device__ __noinline__ void diag_factor(int k, int nSp, double *__restrict__ L, double *__restrict__ U,
-                                         int *__restrict__ flag, double *sm) {
+                                         int *__restrict__ flag, double *sm, bool preloaded = false) {
 #if MSIM_DIAG_VARIANT == 0
-  diag_factor_rec(k, nSp, L, U, flag, sm);
-#elif MSIM_DIAG_VARIANT == 1
-  diag_factor_blocked(k, nSp, L, U, flag, sm);
+  diag_factor_rec(k, nSp, L, U, flag, sm, preloaded);
 #else
-  diag_factor_gj(k, nSp, L, U, flag, sm);
+  diag_factor_blocked(k, nSp, L, U, flag, sm, preloaded);
 #endif
 }

@@ -461,7 +461,12 @@ void launch_scatter_S(Ctx &c) {
 // Capture a fixed launch sequence once (pointers are fixed per basis) and replay it.
 template <typename F>
 static void run_captured(Ctx &c, cudaGraphExec_t &exec, F enqueue) {
-  if (!c.params.use_graphs) {
+#ifdef MSIM_DF_PROF
+  const bool graphs = false;   // the profiling read-back synchronises
+#else
+  const bool graphs = c.params.use_graphs;
+#endif
+  if (!graphs) {
     enqueue(c);
     return;
   }

@@ -31,9 +31,8 @@ __global__ void __launch_bounds__(256) kbench(const double *A0, double *L, doubl
     __threadfence_block();
     long long t0 = clock64();
     if (threadIdx.x == 0 && blockIdx.x == 0) g_ts[15] = t0;
-    if (V == 0) diag_factor_rec(0, TB, Lb, Ub, flag, sm);
-    else if (V == 1) diag_factor_blocked(0, TB, Lb, Ub, flag, sm);
-    else diag_factor_gj(0, TB, Lb, Ub, flag, sm);
+    if (V == 0) diag_factor_rec(0, TB, Lb, Ub, flag, sm, false);
+    else diag_factor_blocked(0, TB, Lb, Ub, flag, sm, false);
     __syncthreads();
     tot += clock64() - t0;
   }
@@ -91,6 +90,6 @@ int main() {
       for (int q = 0; q < 64; ++q) s += M[i * 64 + q] * M[j * 64 + q];
       A[j * 64 + i] = s;
     }
-  for (int nb : {1, 148, 296}) { run<0>(A, nb); run<1>(A, nb); run<2>(A, nb); }
+  for (int nb : {1, 148, 296}) { run<0>(A, nb); run<1>(A, nb); }
   return 0;
 }
