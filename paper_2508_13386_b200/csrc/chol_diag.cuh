@@ -224,6 +224,7 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
         a[c] = va ? A[ra * LD + j0 + c] : 0.0;
         b[c] = vb ? A[rb * LD + j0 + c] : 0.0;
       }
+#ifdef MSIM_PANEL_SHFL
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const double d = __shfl_sync(0xffffffffu, a[j], j);
@@ -240,6 +241,41 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
           b[c] = fma(-b[j], lc, b[c]);
         }
       }
+#else
+      // the pivot's lane takes the rsqrt of its own (final) diagonal; the column of L is then
+      // broadcast through shared memory (one store, 15 - j broadcast loads)
+      // (the next pivot, a_{j+1,j+1} - l_{j+1,j}^2, is formed by its own lane from its own values,
+      // off the shared-memory round trip)
+      double *pc = Tb[0][0];   // 16-double scratch (Tb is free until the inverse)
+      double piv = a[0];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        double iv = 0.0;
+        if (lane == j) {
+          if (!(piv > 0.0)) {
+            bad = true;
+            piv = 1.0;
+            a[j] = 1.0;
+          }
+          iv = rsqrt_nr2(piv);
+          invd[j0 + j] = iv;
+        }
+        const double inv = __shfl_sync(0xffffffffu, iv, j);
+        const double l = a[j] * inv;   // L_jj = a_jj / sqrt(a_jj); rows above: a = 0
+        a[j] = l;
+        b[j] *= inv;
+        if (j + 1 < 16) piv = fma(-l, l, a[j + 1]);   // meaningful in lane j + 1
+        if (lane < 16) pc[lane] = l;
+        __syncwarp();
+#pragma unroll
+        for (int c = j + 1; c < 16; ++c) {
+          const double lc = pc[c];
+          a[c] = fma(-l, lc, a[c]);
+          b[c] = fma(-b[j], lc, b[c]);
+        }
+        __syncwarp();
+      }
+#endif
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
         if (va && ra >= j0 + c) A[ra * LD + j0 + c] = a[c];
