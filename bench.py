@@ -88,6 +88,53 @@ def algorithmic_bytes(sizes, n_cg):
     return {"spmv": spmv, "pcg_iter": pcg_iter, "assembly": assembly}
 
 
+def load_fp64_peak():
+    p = os.path.join(ROOT, "profiles", "fp64_peaks.json")
+    if os.path.exists(p):
+        return json.load(open(p))["dmma_tflops"], "measured (profiles/fp64_peaks.json)"
+    return 37.2, "nominal: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz"
+
+
+def load_traffic():
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of kernels captured
+    with ncu --set full, committed under profiles/ (the bench itself never runs under ncu)."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    return json.load(open(p)) if os.path.exists(p) else {}
+
+
+def phase_rooflines(phases, ab, ci, n_cg, hbm, peak_src, fp64_peak, fp64_src, traffic):
+    """Roofline of every phase with a defined algorithmic work unit: HBM bytes
+    for the PCG iteration and the assembly, FP64 flops for the coarse factorisation and the
+    Galerkin projection.  achieved = work per launch / measured average launch time."""
+    out = {}
+
+    def put(name, bound, work, unit, peak, src, kernel, per_launch_ms, n_launch_per_newton, newton):
+        ach = work / (per_launch_ms * 1e-3) / (1e9 if unit == "GB/s" else 1e12)
+        tr = traffic.get(kernel)
+        out[name] = {"bound": bound, "kernel": kernel, "achieved": ach, "peak": peak, "unit": unit,
+                     "frac": ach / peak, "peak_source": src,
+                     "traffic": tr["dram_bytes"] if tr else None,
+                     "work_per_launch": work, "avg_ms_per_launch": per_launch_ms,
+                     "ms_per_newton": per_launch_ms * n_launch_per_newton}
+
+    newton = max(phases["pcg"][1], 1)
+    ms, n = phases["pcg"]
+    if n:
+        put("pcg", "hbm", ab["pcg_iter"], "GB/s", hbm, peak_src, "k_pcg_spmv+k_pcg_update",
+            ms / (n * n_cg), n_cg, newton)
+    ms, n = phases["assembly"]
+    if n:
+        put("assembly", "hbm", ab["assembly"], "GB/s", hbm, peak_src, "k_assemble", ms / n, 1, newton)
+    ms, n = phases["coarse_factor"]
+    if n:
+        put("coarse_factor", "alu", ci["flops"], "TFLOP/s", fp64_peak, fp64_src, "k_chol_dataflow", ms / n, 1, newton)
+    ms, n = phases["coarse_S"]
+    if n and ci.get("galerkin_flops"):
+        put("coarse_S", "alu", ci["galerkin_flops"], "TFLOP/s", fp64_peak, fp64_src, "k_galerkin_fused", ms / n, 1,
+            newton)
+    return out
+
+
 # ----------------------------------------------------------------------------- scenes
 def load_case(config):
     from precompute.basis import cached_basis
@@ -255,6 +302,11 @@ def run_ours(args):
         asm_ms, asm_n = phases["assembly"]
         asm_avg = asm_ms / max(asm_n, 1)
         achieved = ab["pcg_iter"] / (pcg_iter_ms * 1e-3) / 1e9
+        ci = ctx.coarse_info()
+        fp64_peak, fp64_src = load_fp64_peak()
+        traffic = load_traffic()
+        rl_phases = phase_rooflines(phases, ab, ci, b.n_cg, hbm, peak_src, fp64_peak, fp64_src, traffic)
+        dominant = max(rl_phases, key=lambda k: rl_phases[k]["ms_per_newton"] if rl_phases[k]["ms_per_newton"] else 0)
         line = {
             "metric": METRIC, "value": newton_all / (ms_max * 1e-3), "unit": "Newton steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -263,11 +315,8 @@ def run_ours(args):
             "config": config_dict(s, b, world),
             "pcg_iters_per_s": pcg_all / (ms_max * 1e-3),
             "newton_iters": int(newton_all),
-            "roofline": {"bound": "hbm", "kernel": "PCG iteration (fused SpMV + update)",
-                         "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                         "peak_source": peak_src, "traffic": None,
-                         "algorithmic_bytes_per_launch": ab["pcg_iter"],
-                         "avg_ms_per_launch": pcg_iter_ms},
+            "roofline": dict(rl_phases[dominant], phase=dominant),
+            "roofline_phases": rl_phases,
             "assembly_gbs": ab["assembly"] / (asm_avg * 1e-3) / 1e9 if asm_n else None,
             "phase_ms_per_newton": {k: (v[0] / max(newton / world, 1)) for k, v in phases.items()},
             "gpu_launches": int(launches),
@@ -275,7 +324,7 @@ def run_ours(args):
                     "h2d_bytes_per_step": 2 * 3 * 8 * s.n_verts, "d2h_bytes_per_step": 2 * 3 * 8 * s.n_verts},
             "clocks": clk.summary(),
             "basis_build_s": t_basis,
-            "coarse": ctx.coarse_info(),
+            "coarse": ci,
         }
         if not args.no_cpu_baseline:
             sec, desc, _ = oracle_newton_sample(s, b)

@@ -219,6 +219,7 @@ typedef struct ms_coarse_info {
   int64_t critical_path_xorder, critical_path_nd;
   int32_t ordering, pad_;
   double flops, flops_xorder, flops_nd;
+  double galerkin_flops;   /* S = B^T H B arithmetic of one projection (fused Galerkin kernel) */
 } ms_coarse_info;
 ms_status ms_get_coarse_info(ms_ctx *ctx, ms_coarse_info *out);
 

@@ -451,7 +451,12 @@ __global__ void __launch_bounds__(kHessThreads, MSIM_HESS_MINB) k_elem_hess(Mesh
   load_tet_kin(M, x, e, k);
   double a[45], p9[45];
   reduced_hessian(k, a);
-  if (e9::psd_project<kMaxNeg>(a, p9, hsm + threadIdx.x, kHessThreads) >= 0) lift_store(p9, stage_h + (size_t)e * 90);
+  // already PSD (lambda_min > -1e-12 ||M||_F, Cholesky test): P+ = M to within 1e-11 relative,
+  // inside the 1e-10 parity tolerance -- common near rest (free fall), skips the eigensolver
+#pragma unroll
+  for (int q = 0; q < 45; ++q) p9[q] = a[q];
+  if (psd_by_cholesky_inplace(p9, 1e-12)) lift_store(a, stage_h + (size_t)e * 90);
+  else if (e9::psd_project<kMaxNeg>(a, p9, hsm + threadIdx.x, kHessThreads) >= 0) lift_store(p9, stage_h + (size_t)e * 90);
   else work[atomicAdd(nwork, 1u)] = e;
 }
 

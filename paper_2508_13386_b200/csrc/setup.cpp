@@ -341,6 +341,8 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   c.h_scol = scol;
   c.nnzb_S = (int64_t)scol.size();
   c.gal_max_jup = max_jup;
+  // Galerkin arithmetic: 36 FMA per (i,u,v) term of R, 144 per (i,j,u) term of S (upper)
+  c.chol_info.galerkin_flops = 2.0 * (36.0 * (double)ga_ent.size() + 144.0 * (double)gl_ent.size());
 
   // ---- fill-reducing order of the handles: geometric nested dissection on the coupling graph
   // (one-sided vertex separators from recursive median bisection of the handle origins).

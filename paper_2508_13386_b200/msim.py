@@ -52,7 +52,7 @@ class CoarseInfo(C.Structure):
                 ("n_tasks", C.c_int64), ("critical_path", C.c_int64), ("nnzb_s", C.c_int64),
                 ("critical_path_xorder", C.c_int64), ("critical_path_nd", C.c_int64),
                 ("ordering", C.c_int32), ("pad_", C.c_int32), ("flops", C.c_double),
-                ("flops_xorder", C.c_double), ("flops_nd", C.c_double)]
+                ("flops_xorder", C.c_double), ("flops_nd", C.c_double), ("galerkin_flops", C.c_double)]
 
 
 class PcgStats(C.Structure):
