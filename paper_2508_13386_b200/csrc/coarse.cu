@@ -123,8 +123,10 @@ void launch_restrict(Ctx &c, const double *y, double *z) {
 
 __global__ void __launch_bounds__(kGalThreads, 2) k_galerkin_fused(GalParams G) {
   extern __shared__ double gsm[];
-  galerkin_row(G, blockIdx.x, gsm);
+  galerkin_row(G, blockIdx.x / G.nparts, blockIdx.x % G.nparts, gsm);
 }
+
+__global__ void __launch_bounds__(256) k_galerkin_reduce(GalParams G) { galerkin_reduce_row(G, blockIdx.x); }
 
 // Affine: Ra(u) = sum_{v in N(u)} w_a(v) kron H_vu  stored SoA [36][nv]
 __global__ void __launch_bounds__(128) k_galerkin_Ra(int nv, HView H, const double *__restrict__ phi_a,
@@ -208,6 +210,9 @@ static GalParams galerkin_params(const Ctx &c) {
   G.W = c.Wphi;
   G.sT = c.sT;
   G.S = c.Sblk;
+  G.Spart = c.Spart;
+  G.nparts = c.gal_parts;
+  G.pstride = 144 * c.gal_max_jup;
   return G;
 }
 
@@ -303,8 +308,13 @@ void launch_coarse_S(Ctx &c) {
     MS_CUDA(cudaFuncSetAttribute(k_galerkin_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     smem_set = smem;
   }
-  k_galerkin_fused<<<c.m, kGalThreads, smem, c.stream>>>(galerkin_params(c));
+  const GalParams G = galerkin_params(c);
+  k_galerkin_fused<<<c.m * G.nparts, kGalThreads, smem, c.stream>>>(G);
   c.launches++;
+  if (G.nparts > 1) {
+    k_galerkin_reduce<<<c.m, 256, 0, c.stream>>>(G);
+    c.launches++;
+  }
   const double *o = c.aff_origin;
   k_galerkin_Ra<<<div_up(c.nv, 128), 128, 0, c.stream>>>(c.nv, hview(c), c.phi_aff, c.X, o[0], o[1], o[2], c.Ra);
   const int nch = 64;

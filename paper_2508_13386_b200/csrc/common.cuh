@@ -150,6 +150,8 @@ struct Ctx {
   DBuf<int32_t> gl_base, gl_off;    // per (i, chunk, slot) entry ranges
   DBuf<uint32_t> gl_ent;            // u_local | (basis entry p) << 7
   int32_t gal_max_jup = 0;
+  int32_t gal_parts = 4;            // CTAs per handle row (partial rows summed in a fixed order)
+  DBuf<double> Spart;               // [m * gal_parts][144 gal_max_jup]
   DBuf<double> Sa;                  // 144
   DBuf<double> Ra;                  // [nv * 36]
   // dense coarse factor (tile-banded)

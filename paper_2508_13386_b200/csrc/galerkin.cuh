@@ -21,6 +21,8 @@ struct GalParams {
   const double *W;
   const int32_t *sT;
   double *S;                        // [nnzb_S][144] block storage
+  double *Spart;                    // [m * nparts][pstride] partial rows (nparts > 1)
+  int nparts, pstride;
 };
 
 constexpr int kGalThreads = 2 * kGalChunk;
@@ -40,7 +42,12 @@ __host__ __device__ constexpr size_t galerkin_smem_doubles(int max_jup) {
 // Every accumulator has one owner thread and a fixed summation order -> deterministic.
 // R_i(u) entry l = 3 (4c'+k') + c; accumulator layout [slot][k][36] (conflict-free in l).
 
-__device__ __forceinline__ void galerkin_row(const GalParams &G, int i, double *gsm) {
+// Part `part` of `nparts` of handle i's row: the contiguous chunk range
+// [part nch / nparts, (part + 1) nch / nparts) of U_i (vertex order, so the CTAs resident at one
+// time -- consecutive handles, all parts -- work on one x-slab of the mesh and share H rows in L2).
+// nparts == 1 writes S directly; otherwise the partial row goes to Spart and k_galerkin_reduce
+// sums the parts in a fixed order.
+__device__ __forceinline__ void galerkin_row(const GalParams &G, int i, int part, double *gsm) {
   const HView &H = G.H;
   const int32_t *__restrict__ gU_ptr = G.gU_ptr, *__restrict__ gU = G.gU, *__restrict__ ga_off = G.ga_off;
   const uint32_t *__restrict__ ga_ent = G.ga_ent;
@@ -62,10 +69,11 @@ __device__ __forceinline__ void galerkin_row(const GalParams &G, int i, double *
   const int j0 = gj_ptr[i], nup = gj_ptr[i + 1] - j0;
   for (int e = t; e < nup * 144; e += kGalThreads) Sacc[e] = 0.0;
   const int nch = (nU + kGalChunk - 1) / kGalChunk;
+  const int ch0 = (int)((int64_t)part * nch / G.nparts), ch1 = (int)((int64_t)(part + 1) * nch / G.nparts);
   const int *off = gl_off + gl_base[i];
   double *myW = stW + warp * 128;
   int *myU = stU + warp * 32;
-  for (int ch = 0; ch < nch; ++ch) {
+  for (int ch = ch0; ch < ch1; ++ch) {
     // ---- phase A
     double acc[36];
 #pragma unroll
@@ -175,6 +183,12 @@ __device__ __forceinline__ void galerkin_row(const GalParams &G, int i, double *
     }
   }
   __syncthreads();
+  if (G.nparts > 1) {
+    double *dst = G.Spart + (size_t)(i * G.nparts + part) * G.pstride;
+    for (int e = t; e < nup * 144; e += kGalThreads) dst[e] = Sacc[e];
+    __syncthreads();
+    return;
+  }
   // ---- write S_ij (row-major 12x12: row 4c'+k', column 4c+k) and its transpose S_ji
   for (int e = t; e < nup * 144; e += kGalThreads) {
     const int q = e / 144, r = e % 144, k = r / 36, l = r % 36;
@@ -186,6 +200,22 @@ __device__ __forceinline__ void galerkin_row(const GalParams &G, int i, double *
     if (bt != b) S[144 * (size_t)bt + (4 * cc + k) * 12 + row] = val;
   }
   __syncthreads();
+}
+
+// S_i. = sum of the parts (fixed order), written as S_ij and its transpose S_ji
+__device__ __forceinline__ void galerkin_reduce_row(const GalParams &G, int i) {
+  const int j0 = G.gj_ptr[i], nup = G.gj_ptr[i + 1] - j0;
+  const double *src = G.Spart + (size_t)i * G.nparts * G.pstride;
+  for (int e = threadIdx.x; e < nup * 144; e += blockDim.x) {
+    double val = src[e];
+    for (int p = 1; p < G.nparts; ++p) val += src[(size_t)p * G.pstride + e];
+    const int q = e / 144, r = e % 144, k = r / 36, l = r % 36;
+    const int row = l / 3, cc = l % 3;
+    const int b = __ldg(&G.gj_blk[j0 + q]);
+    G.S[144 * (size_t)b + row * 12 + 4 * cc + k] = val;
+    const int bt = __ldg(&G.sT[b]);
+    if (bt != b) G.S[144 * (size_t)bt + (4 * cc + k) * 12 + row] = val;
+  }
 }
 
 }  // namespace msim

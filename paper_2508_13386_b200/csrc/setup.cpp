@@ -564,6 +564,11 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
     c.sT.upload(sT, s);
   }
   c.Sblk.alloc((size_t)144 * c.nnzb_S);
+  {
+    const char *e = std::getenv("MSIM_GAL_PARTS");   // tuning / diagnostics
+    c.gal_parts = e ? std::max(1, std::atoi(e)) : 4;
+  }
+  if (c.gal_parts > 1) c.Spart.alloc((size_t)m * c.gal_parts * 144 * (size_t)std::max(c.gal_max_jup, 1));
   c.gU_ptr.upload(Uptr, s);
   c.gU.upload(Uall, s);
   c.ga_off.upload(ga_off, s);
