@@ -1,0 +1,125 @@
+"""Full-size parity on C4 (64^3 cubes x 6 = 1,572,864 tets, m = 512), the configuration bench.py
+times, through the same C-ABI context construction (context_from_scene, default parameters).
+
+Checked at full size:
+  * energy and full gradient against the oracle (Eq. 2; oracle/ip.py);
+  * PSD-projected Hessian rows of sampled vertices (bottom layer in the barrier zone, interior,
+    faces) against the oracle assembled on the sub-mesh of their incident tets (every
+    contribution to a sampled row is present there);
+  * the BSR SpMV and 20 Jacobi-PCG iterations against the oracle's products / PCG on the
+    exported device matrix;
+  * S = B^T H B and the two-stage subspace direction (Alg. 2, reading R4) against the
+    oracle's Galerkin product and dense Cholesky on the exported device matrix.
+The state is compressed by 1% in z and pushed into the ground-barrier band so that most element
+Hessians are indefinite (the PSD projection is exercised) and the barrier terms are active.
+Tolerances as in tests/test_gpu_parity.py.
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+pytestmark = pytest.mark.gpu
+
+from oracle import coarse, ip, solver  # noqa: E402
+from precompute.basis import cached_basis  # noqa: E402
+from precompute.mesh import make_scene, random_state  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def c4():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2508_13386_b200 import msim
+    s = make_scene(4)
+    b = cached_basis(s)
+    ctx = msim.context_from_scene(s, b)
+    dhat = s.ground["dhat"]
+    x = random_state(s, 0.002, seed=21)
+    z0 = s.X[:, 2].min()
+    x[:, 2] = 0.99 * (x[:, 2] - z0) + 0.5 * dhat          # 1% compression, bottom in the barrier band
+    x[:, 2] = np.maximum(x[:, 2], 0.3 * dhat)
+    rng = np.random.default_rng(22)
+    xhat = s.X + 1e-3 * rng.standard_normal(s.X.shape)
+    ctx.set_step_state(s.X, xhat, x)
+    E = ctx.assemble()
+    g = ctx.get_gradient()
+    rp, ci, vals = ctx.export_bsr()
+    n = s.n_verts
+    H = sp.bsr_matrix((vals, ci, rp), shape=(3 * n, 3 * n)).tocsr()
+    return dict(s=s, b=b, ctx=ctx, x=x, xhat=xhat, E=E, g=g, rp=rp, ci=ci, vals=vals, H=H)
+
+
+def rel_err(a, b):
+    return np.linalg.norm(np.ravel(a) - np.ravel(b)) / max(np.linalg.norm(np.ravel(b)), 1e-300)
+
+
+def test_fullsize_energy_gradient(c4):
+    s, x, xhat = c4["s"], c4["x"], c4["xhat"]
+    m = ip.make_model(s)
+    E_o = ip.energy(m, x, xhat)
+    assert abs(c4["E"] - E_o) <= 1e-10 * abs(E_o)
+    g_o = ip.gradient(m, x, xhat)
+    assert np.abs(c4["g"] - g_o).max() <= 1e-10 * np.abs(g_o).max()
+
+
+def test_fullsize_hessian_sampled_rows(c4):
+    s, x, xhat, rp, ci, vals = c4["s"], c4["x"], c4["xhat"], c4["rp"], c4["ci"], c4["vals"]
+    rng = np.random.default_rng(23)
+    bottom = np.flatnonzero(x[:, 2] < s.ground["dhat"])
+    assert len(bottom) > 100                       # barrier active on the bottom layer
+    sample = np.unique(np.concatenate([rng.choice(bottom, 60, replace=False),
+                                       rng.choice(s.n_verts, 140, replace=False)]))
+    tets = np.asarray(s.tets)
+    incident = np.flatnonzero(np.isin(tets, sample).any(axis=1))
+    verts = np.unique(tets[incident])                  # sub-mesh, renumbered
+    loc = np.full(s.n_verts, -1)
+    loc[verts] = np.arange(len(verts))
+    dbc = np.asarray(s.dbc)
+    sub = dataclasses.replace(s, X=s.X[verts], tets=loc[tets[incident]].astype(np.int32), E=s.E[incident],
+                              nu=s.nu[incident], rho=s.rho[incident], dbc=loc[dbc[np.isin(dbc, verts)]])
+    Hb = ip.hessian(ip.make_model(sub), x[verts], xhat[verts])   # 3x3-block BSR of the sub-mesh
+    worst = 0.0
+    for u in sample:
+        cols_d = ci[rp[u]:rp[u + 1]]
+        lu = loc[u]
+        cols_o = verts[Hb.indices[Hb.indptr[lu]:Hb.indptr[lu + 1]]]
+        assert np.array_equal(np.sort(cols_d), np.sort(cols_o)), u
+        blk_d = vals[rp[u]:rp[u + 1]][np.argsort(cols_d)]
+        blk_o = Hb.data[Hb.indptr[lu]:Hb.indptr[lu + 1]][np.argsort(cols_o)]
+        err = np.abs(blk_d - blk_o).max(axis=(1, 2)) / np.maximum(np.abs(blk_o).max(axis=(1, 2)), 1e-300)
+        worst = max(worst, err.max())
+    assert worst <= 1e-10, worst
+
+
+def test_fullsize_spmv_pcg(c4):
+    ctx, H = c4["ctx"], c4["H"]
+    rng = np.random.default_rng(24)
+    v = rng.standard_normal(H.shape[0])
+    y = ctx.spmv(v)
+    y_o = H @ v
+    assert np.abs(y - y_o).max() <= 1e-12 * np.abs(y_o).max()
+    m = ip.make_model(c4["s"])
+    rhs = rng.standard_normal(H.shape[0])
+    rhs.reshape(-1, 3)[~m.free] = 0.0
+    n_cg = c4["b"].n_cg
+    sol, st = ctx.pcg_solve(rhs, n_cg)
+    sol_o = solver.pcg(H, rhs, n_cg)
+    assert st.iters == n_cg
+    assert rel_err(sol, sol_o) < 1e-8
+
+
+def test_fullsize_coarse(c4):
+    s, b, ctx, H, g = c4["s"], c4["b"], c4["ctx"], c4["H"], c4["g"]
+    Us, Ua = coarse.sms_matrix(s.X, b), coarse.affine_matrix(s.X, b)
+    S, Sa = ctx.export_coarse()
+    S_o = coarse.galerkin(Us, H)
+    Sa_o = coarse.galerkin(Ua, H)
+    assert np.abs(S - S_o).max() <= 1e-11 * np.abs(S_o).max()
+    assert np.abs(Sa - Sa_o).max() <= 1e-11 * np.abs(Sa_o).max()
+    ds, da = ctx.subspace_direction()
+    ds_o, da_o, _, _ = solver.subspace_direction(H, g.ravel(), Ua, Us)
+    assert rel_err(da, da_o) < 1e-9
+    assert rel_err(ds, ds_o) < 1e-8
