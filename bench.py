@@ -219,11 +219,11 @@ def run_reference(args):
     return 0
 
 
-def config_dict(s, b, world):
+def config_dict(s, b, world, partitioned=False):
     return {"workload": f"{s.name}: {s.dims[0]}x{s.dims[1]}x{s.dims[2]} cubes x6 tets = {s.n_tets} tets, "
                         f"{s.n_verts} vertices, m={b.m} handles, N_cg={b.n_cg}, IE h=1/60, ground barrier",
             "n_tets": int(s.n_tets), "n_verts": int(s.n_verts), "m": int(b.m), "n_cg": int(b.n_cg),
-            "parallelism": f"replicas{world}" if world > 1 else "single",
+            "parallelism": (f"slab{world}" if partitioned else f"replicas{world}") if world > 1 else "single",
             "l2_flush": "inputs larger than L2 (BSR 289 MB + staged element Hessians 1.1 GB)"}
 
 
@@ -237,7 +237,18 @@ def run_ours(args):
     from paper_2508_13386_b200 import msim
     s, b, t_basis = load_case(args.config)
     stream = torch.cuda.current_stream()
-    ctx = msim.context_from_scene(s, b, device=local, stream=stream.cuda_stream)
+    partitioned = world > 1 and not args.replicas
+    if partitioned:
+        # one problem over N GPUs: x-slab partition, NCCL halo exchange / allreduce inside the
+        # library; rank 0 creates the NCCL id, broadcast over the process group
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(msim.nccl_unique_id()), dtype=torch.uint8))
+        torch.distributed.broadcast(uid, src=0)
+        ctx = msim.context_from_scene(s, b, device=local, stream=stream.cuda_stream, rank=rank, world=world,
+                                      nccl_id=bytes(uid.cpu().numpy().tobytes()))
+    else:
+        ctx = msim.context_from_scene(s, b, device=local, stream=stream.cuda_stream)
     sizes = ctx.sizes()
 
     def barrier():
@@ -270,7 +281,9 @@ def run_ours(args):
     cnt = torch.tensor([newton, pcg], device="cuda", dtype=torch.float64)
     if world > 1:
         torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(cnt, op=torch.distributed.ReduceOp.SUM)
+        # replicas: independent problems (counts add up); partitioned: one problem (same counts)
+        torch.distributed.all_reduce(cnt, op=torch.distributed.ReduceOp.MAX if partitioned
+                                     else torch.distributed.ReduceOp.SUM)
     ms_max = float(ms_t.item())
     newton_all, pcg_all = float(cnt[0].item()), float(cnt[1].item())
 
@@ -286,13 +299,19 @@ def run_ours(args):
         st = ctx.timestep()
         e_newton += st.newton_iters
         x_h, v_h = ctx.get_state()
+        if partitioned:   # every rank returns its owned vertices: assemble the global state
+            xv = torch.from_numpy(np.concatenate([x_h.ravel(), v_h.ravel()])).cuda()
+            torch.distributed.all_reduce(xv)
+            xv = xv.cpu().numpy()
+            x_h, v_h = xv[:x_h.size].reshape(x_h.shape), xv[x_h.size:].reshape(v_h.shape)
     barrier()
     e_sec = time.perf_counter() - t0
     e_t = torch.tensor([e_sec], device="cuda")
     e_c = torch.tensor([float(e_newton)], device="cuda", dtype=torch.float64)
     if world > 1:
         torch.distributed.all_reduce(e_t, op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(e_c, op=torch.distributed.ReduceOp.SUM)
+        torch.distributed.all_reduce(e_c, op=torch.distributed.ReduceOp.MAX if partitioned
+                                     else torch.distributed.ReduceOp.SUM)
 
     if rank == 0:
         hbm, peak_src, peaks = load_peaks()
@@ -310,9 +329,10 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": newton_all / (ms_max * 1e-3), "unit": "Newton steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong" if partitioned else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(s, b, world),
+            "config": config_dict(s, b, world, partitioned),
             "pcg_iters_per_s": pcg_all / (ms_max * 1e-3),
             "newton_iters": int(newton_all),
             "roofline": dict(rl_phases[dominant], phase=dominant),
@@ -321,7 +341,8 @@ def run_ours(args):
             "phase_ms_per_newton": {k: (v[0] / max(newton / world, 1)) for k, v in phases.items()},
             "gpu_launches": int(launches),
             "e2e": {"value": float(e_c.item()) / float(e_t.item()), "unit": "Newton steps/s",
-                    "h2d_bytes_per_step": 2 * 3 * 8 * s.n_verts, "d2h_bytes_per_step": 2 * 3 * 8 * s.n_verts},
+                    "h2d_bytes_per_step": 2 * 3 * 8 * (sizes["n_verts"] if partitioned else s.n_verts),
+                    "d2h_bytes_per_step": 2 * 3 * 8 * (sizes["n_verts"] if partitioned else s.n_verts)},
             "clocks": clk.summary(),
             "basis_build_s": t_basis,
             "coarse": ci,
@@ -345,6 +366,8 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick-reference", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: N independent copies of the problem instead of one slab-partitioned problem")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

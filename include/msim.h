@@ -109,8 +109,33 @@ typedef struct ms_pcg_stats {
 const char *ms_version(void);
 void ms_default_params(ms_params *out);
 /* Create a context on `device`, enqueuing on `cuda_stream` (a cudaStream_t; NULL = legacy
- * default stream).  nccl_id / rank / world are reserved for the slab-partitioned multi-GPU
- * path; this build accepts world == 1 only (nccl_id ignored). */
+ * default stream).  Multi-GPU: one context per rank and GPU, SPMD; world > 1
+ * needs nccl_id, the 128-byte ncclUniqueId that rank 0 obtained with ms_nccl_unique_id and
+ * shared with the other ranks (world == 1: nccl_id may be NULL).  Every rank then uploads the
+ * full mesh and basis and makes the same calls in the same order; the context keeps an x-slab of
+ * vertices (equal counts) plus one ghost layer, exchanges ghost values with its neighbours over
+ * NCCL and sums energies, dot products, B^T r and S across ranks (dist.h).  State arrays
+ * (ms_set_state / ms_get_state ...) stay global-sized: set reads the rank's local entries, get
+ * writes its owned entries.  The parity hooks (ms_eval_elements, ms_export_bsr, ms_spmv, ...)
+ * operate on the rank's local numbering. */
+typedef struct ms_hub ms_hub;   /* in-process communicator (one-GPU tests of the world > 1 path) */
+/* Fill out[128] with a fresh ncclUniqueId (rank 0, before ms_create). */
+ms_status ms_nccl_unique_id(uint8_t out[128]);
+/* In-process hub: `world` contexts created with ms_create_hub in one process (one host thread per
+ * context) exchange ghost values and reductions through host memory; every collective
+ * synchronises the calling stream (no device-side waiting between contexts). */
+ms_status ms_hub_create(int32_t world, ms_hub **out);
+ms_status ms_hub_destroy(ms_hub *hub);
+ms_status ms_create_hub(ms_ctx **out, int device, void *cuda_stream, ms_hub *hub, int rank, int world);
+/* Host-only (no GPU): the slab partition plan of `rank` that ms_upload_mesh builds (dist.h), for
+ * tests and tooling.  counts[6] = nv_own, nv_loc, nt_own, nt_loc, n_send, n_recv; optional
+ * outputs (NULL to skip): l2g[nv_loc] local -> global vertex (owned first), tet_l2g[nt_loc],
+ * peer_counts[world][2] = (n_send, n_recv) per peer rank, send_global / recv_global = global
+ * vertex ids concatenated by peer rank (ascending rank, ids ascending within a peer). */
+ms_status ms_partition(int32_t rank, int32_t world, int64_t n_verts, const double *rest_xyz,
+                       int64_t n_tets, const int32_t *tets, int32_t *counts, int32_t *l2g,
+                       int32_t *tet_l2g, int32_t *peer_counts, int32_t *send_global,
+                       int32_t *recv_global);
 ms_status ms_create(ms_ctx **out, int device, void *cuda_stream, const uint8_t *nccl_id,
                     int rank, int world);
 ms_status ms_destroy(ms_ctx *ctx);

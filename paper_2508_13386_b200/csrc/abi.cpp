@@ -62,6 +62,7 @@ static void enqueue_assembly(Ctx &c) {
   phase_begin(c, MS_PHASE_GRAD);
   launch_elem_grad(c);
   launch_vertex_grad(c);
+  dist_sum(c, c.scal + SC_SUM0, SC_SUM_N);   // energies, |g|^2, infeasibility: over all ranks
   phase_end(c);
   phase_begin(c, MS_PHASE_HESS);
   launch_elem_hess(c);
@@ -110,7 +111,9 @@ static ms_status newton_step(Ctx &c, ms_newton_stats *st) {
   phase_begin(c, MS_PHASE_LINESEARCH);
   MS_CUDA(cudaMemcpyAsync(c.d, c.ds, sizeof(double) * n3, cudaMemcpyDeviceToDevice, c.stream));
   launch_axpby(c, c.d, 1.0, c.df, 1.0, n3);
-  launch_dot(c, c.ds, c.ds, n3, SC_DSNORM2);
+  halo_exchange(c, c.d);   // multi-GPU: the line search reads d at ghost vertices
+  launch_dot(c, c.ds, c.ds, 3 * (int64_t)c.nv_own, SC_DSNORM2);
+  dist_sum(c, c.scal + SC_DSNORM2, 1);
   launch_filters(c);
   launch_ls_batch(c, 0, K);
   fetch_scalars(c, K);
@@ -152,7 +155,7 @@ static ms_status newton_step(Ctx &c, ms_newton_stats *st) {
   if (!failed) launch_update(c, alpha);
   phase_end(c);
   const double dsn = std::sqrt(h[SC_DSNORM2]);
-  const bool conv = dsn / (c.params.h * c.nv) < c.params.eps;
+  const bool conv = dsn / (c.params.h * c.nv_glob) < c.params.eps;   // R7: all vertices
   if (st) {
     st->alpha = failed ? 0.0 : alpha;
     st->alpha0 = h[SC_ALPHA0];
@@ -178,6 +181,36 @@ static void end_step(Ctx &c) {
   MS_REQUIRE(c.step_begun, MS_ERR_STATE, "ms_end_step before ms_begin_step");
   launch_velocity(c);
   c.step_begun = false;
+}
+
+// ---- global <-> local vertex vectors (3 per vertex); world == 1: plain copies
+static void upload_global(Ctx &c, double *dev, const double *glob) {
+  const size_t n3 = 3 * (size_t)c.nv;
+  if (!c.dist()) {
+    MS_CUDA(cudaMemcpyAsync(dev, glob, sizeof(double) * n3, cudaMemcpyHostToDevice, c.stream));
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+    return;
+  }
+  std::vector<double> loc(n3);
+  for (int32_t l = 0; l < c.nv; ++l)
+    for (int k = 0; k < 3; ++k) loc[3 * (size_t)l + k] = glob[3 * (size_t)c.part.l2g[l] + k];
+  MS_CUDA(cudaMemcpyAsync(dev, loc.data(), sizeof(double) * n3, cudaMemcpyHostToDevice, c.stream));
+  MS_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+// owned entries into their global positions (other entries of glob untouched)
+static void download_owned(Ctx &c, const double *dev, double *glob) {
+  const size_t n3 = 3 * (size_t)c.nv;
+  if (!c.dist()) {
+    MS_CUDA(cudaMemcpyAsync(glob, dev, sizeof(double) * n3, cudaMemcpyDeviceToHost, c.stream));
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+    return;
+  }
+  std::vector<double> loc(3 * (size_t)c.nv_own);
+  MS_CUDA(cudaMemcpyAsync(loc.data(), dev, sizeof(double) * loc.size(), cudaMemcpyDeviceToHost, c.stream));
+  MS_CUDA(cudaStreamSynchronize(c.stream));
+  for (int32_t l = 0; l < c.nv_own; ++l)
+    for (int k = 0; k < 3; ++k) glob[3 * (size_t)c.part.l2g[l] + k] = loc[3 * (size_t)l + k];
 }
 
 }  // namespace msim
@@ -217,22 +250,99 @@ void ms_default_params(ms_params *p) {
   p->use_graphs = 1;
 }
 
-ms_status ms_create(ms_ctx **out, int device, void *cuda_stream, const uint8_t *nccl_id, int rank, int world) {
+static ms_status create_common(ms_ctx **out, int device, void *cuda_stream, int rank, int world,
+                               const uint8_t *nccl_id, msim::Hub *hub) {
   if (!out) return MS_ERR_ARG;
   *out = nullptr;
-  if (world != 1 || rank != 0) return MS_ERR_ARG;
-  (void)nccl_id;
+  if (world < 1 || rank < 0 || rank >= world) return MS_ERR_ARG;
+  if (world > 1 && !nccl_id && !hub) return MS_ERR_ARG;
   ms_ctx *ctx = new (std::nothrow) ms_ctx();
   if (!ctx) return MS_ERR_OOM;
-  MS_TRY(ctx, {
-    MS_CUDA(cudaSetDevice(device));
-    ctx->c.device = device;
-    ctx->c.stream = reinterpret_cast<cudaStream_t>(cuda_stream);
-    ms_default_params(&ctx->c.params);
-    MS_CUDA(cudaMallocHost((void **)&ctx->c.h_pinned, sizeof(double) * PH_COUNT));
-  });
+  const ms_status st = [&]() -> ms_status {
+    MS_TRY(ctx, {
+      MS_CUDA(cudaSetDevice(device));
+      ctx->c.device = device;
+      ctx->c.stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+      ctx->c.part.rank = rank;
+      ctx->c.part.world = world;
+      ms_default_params(&ctx->c.params);
+      MS_CUDA(cudaMallocHost((void **)&ctx->c.h_pinned, sizeof(double) * PH_COUNT));
+      if (world > 1) ctx->c.comm = hub ? msim::make_hub_comm(hub, rank) : msim::make_nccl_comm(nccl_id, rank, world, device);
+    });
+    return MS_OK;
+  }();
+  if (st != MS_OK) {
+    delete ctx;
+    return st;
+  }
   *out = ctx;
   return MS_OK;
+}
+
+ms_status ms_create(ms_ctx **out, int device, void *cuda_stream, const uint8_t *nccl_id, int rank, int world) {
+  return create_common(out, device, cuda_stream, rank, world, nccl_id, nullptr);
+}
+
+ms_status ms_nccl_unique_id(uint8_t out[128]) {
+  if (!out) return MS_ERR_ARG;
+  try {
+    msim::nccl_unique_id(out);
+  } catch (...) {
+    return MS_ERR_NCCL;
+  }
+  return MS_OK;
+}
+
+ms_status ms_partition(int32_t rank, int32_t world, int64_t nv, const double *X, int64_t nt, const int32_t *tets,
+                       int32_t *counts, int32_t *l2g, int32_t *tet_l2g, int32_t *peer_counts,
+                       int32_t *send_global, int32_t *recv_global) {
+  if (!X || !tets || !counts || nv <= 0 || nt <= 0 || nv >= INT32_MAX || nt >= INT32_MAX) return MS_ERR_ARG;
+  try {
+    for (int64_t i = 0; i < 4 * nt; ++i)
+      if (tets[i] < 0 || tets[i] >= nv) return MS_ERR_ARG;
+    msim::Partition P;
+    msim::make_partition(rank, world, (int32_t)nv, X, (int32_t)nt, tets, P);
+    counts[0] = P.nv_own;
+    counts[1] = P.nv_loc;
+    counts[2] = P.nt_own;
+    counts[3] = P.nt_loc;
+    counts[4] = (int32_t)P.send_idx.size();
+    counts[5] = (int32_t)P.recv_idx.size();
+    if (l2g) std::copy(P.l2g.begin(), P.l2g.end(), l2g);
+    if (tet_l2g) std::copy(P.tet_l2g.begin(), P.tet_l2g.end(), tet_l2g);
+    if (peer_counts) {
+      std::fill(peer_counts, peer_counts + 2 * (size_t)world, 0);
+      for (const auto &p : P.peers) {
+        peer_counts[2 * p.rank] = p.n_send;
+        peer_counts[2 * p.rank + 1] = p.n_recv;
+      }
+    }
+    if (send_global)
+      for (size_t k = 0; k < P.send_idx.size(); ++k) send_global[k] = P.l2g[P.send_idx[k]];
+    if (recv_global)
+      for (size_t k = 0; k < P.recv_idx.size(); ++k) recv_global[k] = P.l2g[P.recv_idx[k]];
+  } catch (const msim::Error &e) {
+    return e.code;
+  } catch (...) {
+    return MS_ERR_ARG;
+  }
+  return MS_OK;
+}
+
+ms_status ms_hub_create(int32_t world, ms_hub **out) {
+  if (!out || world < 1) return MS_ERR_ARG;
+  *out = reinterpret_cast<ms_hub *>(msim::hub_create(world));
+  return MS_OK;
+}
+
+ms_status ms_hub_destroy(ms_hub *hub) {
+  msim::hub_destroy(reinterpret_cast<msim::Hub *>(hub));
+  return MS_OK;
+}
+
+ms_status ms_create_hub(ms_ctx **out, int device, void *cuda_stream, ms_hub *hub, int rank, int world) {
+  if (!hub) return MS_ERR_ARG;
+  return create_common(out, device, cuda_stream, rank, world, nullptr, reinterpret_cast<msim::Hub *>(hub));
 }
 
 ms_status ms_destroy(ms_ctx *ctx) {
@@ -243,6 +353,7 @@ ms_status ms_destroy(ms_ctx *ctx) {
   coarse_reset_graphs(ctx->c);
   for (auto e : ctx->c.ev_pool) cudaEventDestroy(e);
   if (ctx->c.h_pinned) cudaFreeHost(ctx->c.h_pinned);
+  delete ctx->c.comm;
   delete ctx;
   return MS_OK;
 }
@@ -257,11 +368,38 @@ ms_status ms_upload_mesh(ms_ctx *ctx, int64_t n_verts, const double *rest_xyz, i
     MS_REQUIRE(n_verts < INT32_MAX / 3 && n_tets < INT32_MAX / 16, MS_ERR_ARG, "mesh too large for int32 indices");
     Ctx &c = ctx->c;
     MS_CUDA(cudaSetDevice(c.device));
-    c.nv = (int32_t)n_verts;
-    c.nt = (int32_t)n_tets;
     c.m = 0;
     pcg_reset_graph(c);
-    build_mesh_structures(c, rest_xyz, tets, E, nu, rho);
+    c.nv_glob = (int32_t)n_verts;
+    if (!c.dist()) {
+      c.nv = c.nv_own = (int32_t)n_verts;
+      c.nt = c.nt_own = (int32_t)n_tets;
+      build_mesh_structures(c, rest_xyz, tets, E, nu, rho);
+    } else {
+      for (int64_t i = 0; i < 4 * n_tets; ++i)
+        MS_REQUIRE(tets[i] >= 0 && tets[i] < n_verts, MS_ERR_ARG, "tet vertex index out of range");
+      msim::Partition &P = c.part;
+      msim::make_partition(P.rank, P.world, (int32_t)n_verts, rest_xyz, (int32_t)n_tets, tets, P);
+      c.h_tets_glob.assign(tets, tets + 4 * (size_t)n_tets);
+      std::vector<double> X(3 * (size_t)P.nv_loc), Ev(P.nt_loc), nuv(P.nt_loc), rhov(P.nt_loc);
+      for (int32_t l = 0; l < P.nv_loc; ++l)
+        for (int k = 0; k < 3; ++k) X[3 * (size_t)l + k] = rest_xyz[3 * (size_t)P.l2g[l] + k];
+      for (int32_t le = 0; le < P.nt_loc; ++le) {
+        Ev[le] = E[P.tet_l2g[le]];
+        nuv[le] = nu[P.tet_l2g[le]];
+        rhov[le] = rho[P.tet_l2g[le]];
+      }
+      c.nv = P.nv_loc;
+      c.nt = P.nt_loc;
+      c.nv_own = P.nv_own;
+      c.nt_own = P.nt_own;
+      build_mesh_structures(c, X.data(), P.tets_loc.data(), Ev.data(), nuv.data(), rhov.data());
+      c.halo_send_idx.upload(P.send_idx.empty() ? std::vector<int32_t>{0} : P.send_idx, c.stream);
+      c.halo_recv_idx.upload(P.recv_idx.empty() ? std::vector<int32_t>{0} : P.recv_idx, c.stream);
+      c.halo_send.alloc(3 * std::max<size_t>(P.send_idx.size(), 1));
+      c.halo_recv.alloc(3 * std::max<size_t>(P.recv_idx.size(), 1));
+      MS_CUDA(cudaStreamSynchronize(c.stream));
+    }
   });
   return MS_OK;
 }
@@ -274,8 +412,9 @@ ms_status ms_set_dirichlet(ms_ctx *ctx, int64_t n, const int32_t *verts) {
     MS_REQUIRE(n == 0 || verts, MS_ERR_ARG, "null verts");
     std::fill(c.h_fixed.begin(), c.h_fixed.end(), 0);
     for (int64_t k = 0; k < n; ++k) {
-      MS_REQUIRE(verts[k] >= 0 && verts[k] < c.nv, MS_ERR_ARG, "Dirichlet vertex out of range");
-      c.h_fixed[verts[k]] = 1;
+      MS_REQUIRE(verts[k] >= 0 && verts[k] < c.nv_glob, MS_ERR_ARG, "Dirichlet vertex out of range");
+      const int32_t l = c.dist() ? c.part.g2l[verts[k]] : verts[k];
+      if (l >= 0) c.h_fixed[l] = 1;
     }
     c.fixed.upload(c.h_fixed, c.stream);
     MS_CUDA(cudaStreamSynchronize(c.stream));
@@ -332,7 +471,28 @@ ms_status ms_basis_upload(ms_ctx *ctx, int32_t m, const double *origins, const i
     require_mesh(c);
     MS_REQUIRE(origins && vptr && handle && phi && phi_affine && affine_origin, MS_ERR_ARG, "null basis array");
     MS_REQUIRE(n_cg > 0, MS_ERR_ARG, "n_cg must be > 0");
-    build_basis_structures(c, m, origins, vptr, handle, phi, phi_affine, affine_origin);
+    if (!c.dist()) {
+      build_basis_structures(c, m, origins, vptr, handle, phi, phi_affine, affine_origin);
+    } else {   // local rows of the global basis + the global S pattern
+      MS_REQUIRE(vptr[0] == 0, MS_ERR_ARG, "vptr[0] must be 0");
+      for (int32_t v = 0; v < c.nv_glob; ++v)
+        for (int64_t k = vptr[v]; k < vptr[v + 1]; ++k)
+          MS_REQUIRE(handle[k] >= 0 && handle[k] < m, MS_ERR_ARG, "handle id out of range");
+      global_s_pattern(c.nv_glob, c.h_tets_glob, m, vptr, handle, c.h_sptr_glob, c.h_scol_glob);
+      std::vector<int64_t> lptr(c.nv + 1, 0);
+      std::vector<int32_t> lh;
+      std::vector<double> lphi, laff(c.nv);
+      for (int32_t l = 0; l < c.nv; ++l) {
+        const int32_t v = c.part.l2g[l];
+        for (int64_t k = vptr[v]; k < vptr[v + 1]; ++k) {
+          lh.push_back(handle[k]);
+          lphi.push_back(phi[k]);
+        }
+        lptr[l + 1] = (int64_t)lh.size();
+        laff[l] = phi_affine[v];
+      }
+      build_basis_structures(c, m, origins, lptr.data(), lh.data(), lphi.data(), laff.data(), affine_origin);
+    }
     c.n_cg_basis = n_cg;
     pcg_reset_graph(c);
   });
@@ -344,10 +504,8 @@ ms_status ms_set_state(ms_ctx *ctx, const double *x, const double *v) {
   MS_TRY(ctx, {
     Ctx &c = ctx->c;
     require_mesh(c);
-    const size_t n3 = 3 * (size_t)c.nv;
-    if (x) MS_CUDA(cudaMemcpyAsync(c.x, x, sizeof(double) * n3, cudaMemcpyHostToDevice, c.stream));
-    if (v) MS_CUDA(cudaMemcpyAsync(c.v, v, sizeof(double) * n3, cudaMemcpyHostToDevice, c.stream));
-    MS_CUDA(cudaStreamSynchronize(c.stream));
+    if (x) upload_global(c, c.x, x);
+    if (v) upload_global(c, c.v, v);
     c.step_begun = false;
     c.assembled = false;
   });
@@ -359,10 +517,8 @@ ms_status ms_get_state(ms_ctx *ctx, double *x, double *v) {
   MS_TRY(ctx, {
     Ctx &c = ctx->c;
     require_mesh(c);
-    const size_t n3 = 3 * (size_t)c.nv;
-    if (x) c.x.download(x, n3, c.stream);
-    if (v) c.v.download(v, n3, c.stream);
-    MS_CUDA(cudaStreamSynchronize(c.stream));
+    if (x) download_owned(c, c.x, x);
+    if (v) download_owned(c, c.v, v);
   });
   return MS_OK;
 }
@@ -372,12 +528,10 @@ ms_status ms_set_step_state(ms_ctx *ctx, const double *x_t, const double *xhat, 
   MS_TRY(ctx, {
     Ctx &c = ctx->c;
     require_mesh(c);
-    const size_t n3 = 3 * (size_t)c.nv;
     MS_REQUIRE(x_t && xhat && x, MS_ERR_ARG, "null state array");
-    MS_CUDA(cudaMemcpyAsync(c.xt, x_t, sizeof(double) * n3, cudaMemcpyHostToDevice, c.stream));
-    MS_CUDA(cudaMemcpyAsync(c.xhat, xhat, sizeof(double) * n3, cudaMemcpyHostToDevice, c.stream));
-    MS_CUDA(cudaMemcpyAsync(c.x, x, sizeof(double) * n3, cudaMemcpyHostToDevice, c.stream));
-    MS_CUDA(cudaStreamSynchronize(c.stream));
+    upload_global(c, c.xt, x_t);
+    upload_global(c, c.xhat, xhat);
+    upload_global(c, c.x, x);
     c.step_begun = true;
     c.assembled = false;
   });
@@ -389,11 +543,9 @@ ms_status ms_get_step_state(ms_ctx *ctx, double *x_t, double *xhat, double *x) {
   MS_TRY(ctx, {
     Ctx &c = ctx->c;
     require_mesh(c);
-    const size_t n3 = 3 * (size_t)c.nv;
-    if (x_t) c.xt.download(x_t, n3, c.stream);
-    if (xhat) c.xhat.download(xhat, n3, c.stream);
-    if (x) c.x.download(x, n3, c.stream);
-    MS_CUDA(cudaStreamSynchronize(c.stream));
+    if (x_t) download_owned(c, c.xt, x_t);
+    if (xhat) download_owned(c, c.xhat, xhat);
+    if (x) download_owned(c, c.x, x);
   });
   return MS_OK;
 }

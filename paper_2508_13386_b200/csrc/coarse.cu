@@ -160,7 +160,8 @@ __global__ void __launch_bounds__(128) k_galerkin_Ra(int nv, HView H, const doub
 }
 
 // S_a[(row), (4c + k)] = sum_u Ra(u)[l] w_a(u)[k], l = 3 row + c.  Grid: (36 entries) x chunks.
-__global__ void __launch_bounds__(256) k_galerkin_Sa_partial(int nv, const double *__restrict__ Ra,
+// rows u < n_use (the owned vertices) of Ra, stored [36][nv]
+__global__ void __launch_bounds__(256) k_galerkin_Sa_partial(int nv, int n_use, const double *__restrict__ Ra,
                                                              const double *__restrict__ phi_a,
                                                              const double *__restrict__ X, double ox,
                                                              double oy, double oz,
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(256) k_galerkin_Sa_partial(int nv, const doubl
   __shared__ double sh[4 * 32];
   const int l = blockIdx.x, chunk = blockIdx.y, nch = gridDim.y;
   double acc[4] = {0, 0, 0, 0};
-  for (int u = chunk * blockDim.x + threadIdx.x; u < nv; u += nch * blockDim.x) {
+  for (int u = chunk * blockDim.x + threadIdx.x; u < n_use; u += nch * blockDim.x) {
     const double f = phi_a[u];
     const double rv = Ra[(size_t)l * nv + u];
     const double w[4] = {f, f * (X[3 * u] - ox), f * (X[3 * u + 1] - oy), f * (X[3 * u + 2] - oz)};
@@ -318,10 +319,13 @@ void launch_coarse_S(Ctx &c) {
   const double *o = c.aff_origin;
   k_galerkin_Ra<<<div_up(c.nv, 128), 128, 0, c.stream>>>(c.nv, hview(c), c.phi_aff, c.X, o[0], o[1], o[2], c.Ra);
   const int nch = 64;
-  k_galerkin_Sa_partial<<<dim3(36, nch), 256, 0, c.stream>>>(c.nv, c.Ra, c.phi_aff, c.X, o[0], o[1], o[2],
+  k_galerkin_Sa_partial<<<dim3(36, nch), 256, 0, c.stream>>>(c.nv, c.nv_own, c.Ra, c.phi_aff, c.X, o[0], o[1], o[2],
                                                               c.partial);
   k_galerkin_Sa_final<<<1, 160, 0, c.stream>>>(nch, c.partial, c.Sa);
   c.launches += 3;
+  // multi-GPU: each rank projected its owned rows u; S and S_a are the sums over ranks
+  dist_sum(c, c.Sblk, 144 * c.nnzb_S);
+  dist_sum(c, c.Sa, 144);
   MS_CUDA(cudaGetLastError());
 }
 
@@ -336,7 +340,7 @@ static void run_captured(Ctx &c, cudaGraphExec_t &exec, F enqueue) {
 #ifdef MSIM_DF_PROF
   const bool graphs = false;   // the profiling read-back synchronises
 #else
-  const bool graphs = c.params.use_graphs;
+  const bool graphs = c.params.use_graphs && !c.dist();
 #endif
   if (!graphs) {
     enqueue(c);
@@ -384,8 +388,9 @@ void launch_coarse_direction(Ctx &c) {
   // rhs = -g
   launch_axpby(c, c.rhs, -1.0, c.g, 0.0, n3);
   // affine stage: za = U_a^T(-g); qa = Sa^-1 za; da = U_a qa
-  k_restrict_affine<<<std::min(div_up(c.nv, 256), 592), 256, 0, c.stream>>>(
-      c.nv, c.phi_aff, c.X, o[0], o[1], o[2], c.rhs, 1.0, c.partial, c.counters + 6, c.za);
+  k_restrict_affine<<<std::min(div_up(c.nv_own, 256), 592), 256, 0, c.stream>>>(
+      c.nv_own, c.phi_aff, c.X, o[0], o[1], o[2], c.rhs, 1.0, c.partial, c.counters + 6, c.za);
+  dist_sum(c, c.za, 12);
   k_solve12<<<1, 32, 0, c.stream>>>(c.Sa, c.za, c.qa, c.flags + 1);
   k_lift_affine<<<div_up(c.nv, 256), 256, 0, c.stream>>>(c.nv, c.phi_aff, c.X, o[0], o[1], o[2], c.qa, c.da);
   c.launches += 3;
@@ -393,6 +398,7 @@ void launch_coarse_direction(Ctx &c) {
   launch_spmv(c, c.da, c.tmp, 0.0, c.rhs);
   // SMS stage: zs = B^T r1; zs <- S^-1 zs; ds = da + B zs
   launch_restrict(c, c.tmp, c.zs);
+  dist_sum(c, c.zs, 12 * (int64_t)c.m);
   launch_coarse_solve(c);
   MS_CUDA(cudaMemcpyAsync(c.ds, c.da, sizeof(double) * n3, cudaMemcpyDeviceToDevice, c.stream));
   launch_lift(c, c.zs, c.ds, true);

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "msim.h"
+#include "dist.h"
 
 namespace msim {
 
@@ -87,7 +88,16 @@ struct Ctx {
   int64_t launches = 0;
 
   // ---- mesh
-  int32_t nv = 0, nt = 0;
+  int32_t nv = 0, nt = 0;           // local (owned + ghost) vertices / tets
+  // ---- multi-GPU slab partition (dist.h); world == 1: everything owned
+  Partition part;
+  Comm *comm = nullptr;             // owned by the context (world > 1)
+  int32_t nv_own = 0, nt_own = 0, nv_glob = 0;
+  std::vector<int32_t> h_tets_glob; // global connectivity (world > 1: the global S pattern)
+  std::vector<int32_t> h_sptr_glob, h_scol_glob;
+  DBuf<int32_t> halo_send_idx, halo_recv_idx;
+  DBuf<double> halo_send, halo_recv;
+  bool dist() const { return part.world > 1; }
   std::vector<double> h_X;          // rest positions (host copy)
   std::vector<int32_t> h_tets;
   DBuf<double> X;                   // (nv,3)
@@ -218,18 +228,19 @@ enum {
   SC_PQ,
   SC_ALPHA,
   SC_BETA,
-  SC_ENERGY_ELEM, // sum V Psi
-  SC_ENERGY_VERT, // inertia + barrier   (k_vertex_grad writes 3 consecutive slots)
-  SC_GNORM2,
-  SC_INFEAS_V,    // penetrating free vertices at entry
+  SC_ENERGY_ELEM, // sum V Psi                  \ summed across ranks together
+  SC_ENERGY_VERT, // inertia + barrier          |  (k_vertex_grad writes 3 consecutive slots)
+  SC_GNORM2,      //                            |
+  SC_INFEAS_V,    // penetrating free vertices  |
+  SC_INFEAS,      // >0 if an element is inverted at entry
   SC_DSNORM2,
-  SC_ALPHA_CCD,
-  SC_ALPHA_INV,
+  SC_ALPHA_CCD,   // \ min across ranks
+  SC_ALPHA_INV,   // /
   SC_ALPHA0,
   SC_RZ0,
-  SC_INFEAS,      // >0 if an element is inverted / vertex penetrates at entry
   SC_COUNT = 32
 };
+constexpr int SC_SUM0 = SC_ENERGY_ELEM, SC_SUM_N = SC_INFEAS - SC_ENERGY_ELEM + 1;
 
 // pinned host mirror layout
 enum {
@@ -252,6 +263,10 @@ void launch_spmv(Ctx &c, const double *xin, double *yout, double alpha_minus_b, 
 void launch_pcg(Ctx &c, const double *rhs, double *sol, int iters);
 void pcg_reset_graph(Ctx &c);
 void launch_coarse_S(Ctx &c);
+// multi-GPU helpers (abi.cpp): no-ops when world == 1
+void dist_sum(Ctx &c, double *dev, int64_t n);
+void dist_min(Ctx &c, double *dev, int64_t n);
+void halo_exchange(Ctx &c, double *vec);   // ghost entries of a 3-per-vertex vector <- owners
 void launch_coarse_factor(Ctx &c);
 void launch_coarse_direction(Ctx &c);
 void launch_coarse_solve(Ctx &c);
@@ -276,6 +291,8 @@ void launch_copy_scalars_to_host(Ctx &c);
 // host-side symbolic setup (setup.cpp)
 void build_mesh_structures(Ctx &c, const double *X, const int32_t *tets, const double *E,
                            const double *nu, const double *rho);
+void global_s_pattern(int32_t nv, const std::vector<int32_t> &tets, int32_t m, const int64_t *vptr,
+                      const int32_t *handle, std::vector<int32_t> &sptr, std::vector<int32_t> &scol);
 void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int64_t *vptr,
                             const int32_t *handle, const double *phi, const double *phi_aff,
                             const double aff_origin[3]);

@@ -96,7 +96,8 @@ __device__ __forceinline__ double psi_snh(const double F[3][3], double J, double
 
 // ------------------------------------------------------------------ energy + gradient (a2)
 // stage_g[e*12 + 3a + i] = V_e (G_e^T vec P)_{(a,i)}; partial energy sum V_e Psi_e.
-__global__ void __launch_bounds__(256) k_elem_grad(MeshView M, const double *__restrict__ x,
+// energy and inversion count over the owned tets [0, nt_own) only (each tet is owned by one rank)
+__global__ void __launch_bounds__(256) k_elem_grad(MeshView M, int nt_own, const double *__restrict__ x,
                                                    double *__restrict__ stage_g,
                                                    double *__restrict__ partial,
                                                    unsigned int *__restrict__ counter,
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(256) k_elem_grad(MeshView M, const double *__r
     const double J = det3(k.F);
     double cof[3][3];
     cofactor(k.F, cof);
-    if (!(J > 0.0)) en[1] = 1.0;
+    if (!(J > 0.0) && e < nt_own) en[1] = 1.0;
     const double s = k.lam * (J - 1.0) - k.mu;
     double P[3][3];
 #pragma unroll
@@ -136,7 +137,7 @@ __global__ void __launch_bounds__(256) k_elem_grad(MeshView M, const double *__r
 #pragma unroll
       for (int i = 0; i < 3; ++i) dst[3 * a + i] = g[a][i];
     const double psi = psi_snh(k.F, J, k.mu, k.lam);
-    en[0] += k.V * psi;
+    if (e < nt_own) en[0] += k.V * psi;
     if (Ee) Ee[e] = (J > 0.0) ? k.V * psi : __longlong_as_double(0x7ff0000000000000ULL);
   }
   double res[2];
@@ -491,7 +492,7 @@ __global__ void k_expand_hess(int nt, const double *__restrict__ stage_h, double
 // ------------------------------------------------------------------ launchers
 void launch_elem_grad_to(Ctx &c, const double *x, double *Ee) {
   const int bs = 256, nb = std::min(div_up(c.nt, bs), 148 * 8);
-  k_elem_grad<<<nb, bs, 0, c.stream>>>(mesh_view(c), x, c.stage_g, c.partial, c.counters + 0,
+  k_elem_grad<<<nb, bs, 0, c.stream>>>(mesh_view(c), c.nt_own, x, c.stage_g, c.partial, c.counters + 0,
                                        c.scal + SC_ENERGY_ELEM, c.scal + SC_INFEAS, Ee);
   c.launches++;
   MS_CUDA(cudaGetLastError());

@@ -163,8 +163,10 @@ __device__ __forceinline__ double psi_val(const double F[3][3], double mu, doubl
 
 // per tet: dPsi_k = V (Psi(F + alpha_k dF) - Psi(F)); per vertex: inertia and barrier differences.
 // out[k] = h^2 (sum dPsi_k + kappa sum db_k) + sum dK_k ; out[K + k] = infeasible count
+// owned tets [0, nt_own) and owned vertices [0, nv_own) only; dist: raw partial sums (energy
+// differences out[k], infeasible counts out[2K + k]) for the cross-rank sum, then k_ls_finalize
 template <int K>
-__global__ void __launch_bounds__(256) k_ls_energy(LSMesh M, int nv, const double *__restrict__ x,
+__global__ void __launch_bounds__(256) k_ls_energy(LSMesh M, int nt_own, int nv_own, int dist, const double *__restrict__ x,
                                                    const double *__restrict__ d, const double *__restrict__ xhat,
                                                    const double *__restrict__ mass,
                                                    const uint8_t *__restrict__ fixed, const double *__restrict__ scal,
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(256) k_ls_energy(LSMesh M, int nv, const doubl
   }
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int stride = gridDim.x * blockDim.x;
-  for (int e = tid; e < M.nt; e += stride) {
+  for (int e = tid; e < nt_own; e += stride) {
     double Ds[3][3], dD[3][3];
     int4 t;
     edge_mats(M, e, x, d, Ds, dD, t);
@@ -218,7 +220,7 @@ __global__ void __launch_bounds__(256) k_ls_energy(LSMesh M, int nv, const doubl
       if (bad) acc[K + k] += 1.0;
     }
   }
-  for (int v = tid; v < nv; v += stride) {
+  for (int v = tid; v < nv_own; v += stride) {
     if (fixed[v]) continue;
     const double m = mass[v];
     double rd = 0.0, dd = 0.0;
@@ -258,10 +260,16 @@ __global__ void __launch_bounds__(256) k_ls_energy(LSMesh M, int nv, const doubl
   if (grid_reduce<2 * K>(acc, partial, counter, res) && threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      out[k] = res[K + k] > 0.0 ? INFINITY : res[k];
+      out[k] = dist ? res[k] : (res[K + k] > 0.0 ? INFINITY : res[k]);
       out[K + k] = al[k];
+      if (dist) out[2 * K + k] = res[K + k];
     }
   }
+}
+
+__global__ void k_ls_finalize(int K, double *__restrict__ out) {
+  const int k = threadIdx.x;
+  if (k < K && out[2 * K + k] > 0.0) out[k] = INFINITY;
 }
 
 __global__ void k_update_x(int n3, double *__restrict__ x, const double *__restrict__ d, double alpha) {
@@ -276,6 +284,7 @@ void launch_filters(Ctx &c) {
   k_filter_ccd<<<div_up(c.nv, 256), 256, 0, c.stream>>>(c.nv, c.x, c.d, c.fixed, c.gn[0], c.gn[1], c.gn[2],
                                                         c.goff, c.has_ground ? 1 : 0, c.partial,
                                                         c.counters + 8, c.scal + SC_ALPHA_CCD);
+  dist_min(c, c.scal + SC_ALPHA_CCD, 2);   // SC_ALPHA_CCD, SC_ALPHA_INV
   k_alpha0<<<1, 1, 0, c.stream>>>(c.scal, c.params.filter_safety);
   c.launches += 3;
   MS_CUDA(cudaGetLastError());
@@ -286,7 +295,7 @@ void launch_ls_batch(Ctx &c, int k0, int K) {
   const double h2 = c.params.h * c.params.h;
   const int grid = std::min(div_up(std::max(c.nt, c.nv), 256), 148 * 8);
 #define LS_ARGS                                                                                       \
-  lsmesh(c), c.nv, c.x, c.d, c.xhat, c.mass, c.fixed, c.scal, k0, c.params.ls_shrink, h2, c.gn[0],      \
+  lsmesh(c), c.nt_own, c.nv_own, c.dist() ? 1 : 0, c.x, c.d, c.xhat, c.mass, c.fixed, c.scal, k0, c.params.ls_shrink, h2, c.gn[0],      \
       c.gn[1], c.gn[2], c.goff, c.dhat, c.kappa, c.has_ground ? 1 : 0, c.partial, c.counters + 9, c.ls_out
   switch (K) {
     case 1: k_ls_energy<1><<<grid, 256, 0, c.stream>>>(LS_ARGS); break;
@@ -297,6 +306,12 @@ void launch_ls_batch(Ctx &c, int k0, int K) {
   }
 #undef LS_ARGS
   c.launches++;
+  if (c.dist()) {
+    dist_sum(c, c.ls_out, K);
+    dist_sum(c, c.ls_out + 2 * K, K);
+    k_ls_finalize<<<1, 32, 0, c.stream>>>(K, c.ls_out);
+    c.launches++;
+  }
   MS_CUDA(cudaGetLastError());
 }
 

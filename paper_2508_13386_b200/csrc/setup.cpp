@@ -190,7 +190,7 @@ void ensure_state_buffers(Ctx &c) {
   c.flags.alloc(8);
   c.flags.zero(c.stream);
   c.ls_alpha.alloc(kMaxLS);
-  c.ls_out.alloc(kMaxLS + 4);
+  c.ls_out.alloc(3 * kMaxLS);   // [K] energy differences, [K] steps, [K] infeasible counts (multi-GPU)
   // rest state: x = X, v = 0
   MS_CUDA(cudaMemcpyAsync(c.x, c.X, sizeof(double) * n3, cudaMemcpyDeviceToDevice, c.stream));
   c.v.zero(c.stream);
@@ -199,6 +199,50 @@ void ensure_state_buffers(Ctx &c) {
 }
 
 // ------------------------------------------------------------------------- basis
+// Global S pattern (multi-GPU): handles i, j are coupled when some vertex of supp(i) is a
+// neighbour (or equal) of a vertex of supp(j) in the global mesh.
+void global_s_pattern(int32_t nv, const std::vector<int32_t> &tets, int32_t m, const int64_t *vptr,
+                      const int32_t *handle, std::vector<int32_t> &sptr, std::vector<int32_t> &scol) {
+  const int64_t nt = (int64_t)tets.size() / 4;
+  std::vector<int32_t> aptr(nv + 1, 0), adj;
+  {
+    std::vector<std::vector<int32_t>> nb(nv);
+    for (int64_t e = 0; e < nt; ++e)
+      for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b) nb[tets[4 * e + a]].push_back(tets[4 * e + b]);
+    for (int32_t v = 0; v < nv; ++v) {
+      auto &l = nb[v];
+      l.push_back(v);
+      std::sort(l.begin(), l.end());
+      l.erase(std::unique(l.begin(), l.end()), l.end());
+      adj.insert(adj.end(), l.begin(), l.end());
+      aptr[v + 1] = (int32_t)adj.size();
+      std::vector<int32_t>().swap(l);
+    }
+  }
+  std::vector<std::vector<int32_t>> supp(m);
+  for (int32_t v = 0; v < nv; ++v)
+    for (int64_t k = vptr[v]; k < vptr[v + 1]; ++k) supp[handle[k]].push_back(v);
+  std::vector<int32_t> mark(m, -1), row;
+  sptr.assign(1, 0);
+  scol.clear();
+  for (int32_t i = 0; i < m; ++i) {
+    row.clear();
+    for (int32_t v : supp[i])
+      for (int32_t a = aptr[v]; a < aptr[v + 1]; ++a) {
+        const int32_t u = adj[a];
+        for (int64_t k = vptr[u]; k < vptr[u + 1]; ++k)
+          if (mark[handle[k]] != i) {
+            mark[handle[k]] = i;
+            row.push_back(handle[k]);
+          }
+      }
+    std::sort(row.begin(), row.end());
+    scol.insert(scol.end(), row.begin(), row.end());
+    sptr.push_back((int32_t)scol.size());
+  }
+}
+
 void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int64_t *vptr,
                             const int32_t *handle, const double *phi, const double *phi_aff,
                             const double aff_origin[3]) {
@@ -240,8 +284,9 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
         hidx[pos] = (int32_t)k;
       }
   }
-  for (int32_t i = 0; i < m; ++i)
-    MS_REQUIRE(hptr[i + 1] > hptr[i], MS_ERR_ARG, "handle with empty support");
+  if (!c.dist())   // (a rank's slab need not meet every handle's support)
+    for (int32_t i = 0; i < m; ++i)
+      MS_REQUIRE(hptr[i + 1] > hptr[i], MS_ERR_ARG, "handle with empty support");
 
   // U_i = vertices adjacent (BSR) to supp(i); J_i = handles of U_i (the S pattern row i);
   // fused Galerkin lists (coarse.cu k_galerkin_fused): per handle i, per chunk of kGalChunk
@@ -257,6 +302,7 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
       const int32_t v = hvert[k];
       for (int32_t s = rp[v]; s < rp[v + 1]; ++s) {
         const int32_t u = ci[s];
+        if (u >= c.nv_own) continue;   // multi-GPU: a rank projects its owned rows only
         if (mark[u] != i) {
           mark[u] = i;
           Uall.push_back(u);
@@ -298,15 +344,19 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   int32_t max_jup = 0;
   for (int32_t i = 0; i < m; ++i) {
     Jl.clear();
-    for (int32_t q = Uptr[i]; q < Uptr[i + 1]; ++q) {
-      const int32_t u = Uall[q];
-      for (int64_t k = vptr[u]; k < vptr[u + 1]; ++k)
-        if (hmark[handle[k]] != i) {
-          hmark[handle[k]] = i;
-          Jl.push_back(handle[k]);
-        }
+    if (c.dist()) {   // the global S pattern (identical on all ranks: S is summed across ranks)
+      Jl.assign(c.h_scol_glob.begin() + c.h_sptr_glob[i], c.h_scol_glob.begin() + c.h_sptr_glob[i + 1]);
+    } else {
+      for (int32_t q = Uptr[i]; q < Uptr[i + 1]; ++q) {
+        const int32_t u = Uall[q];
+        for (int64_t k = vptr[u]; k < vptr[u + 1]; ++k)
+          if (hmark[handle[k]] != i) {
+            hmark[handle[k]] = i;
+            Jl.push_back(handle[k]);
+          }
+      }
+      std::sort(Jl.begin(), Jl.end());
     }
-    std::sort(Jl.begin(), Jl.end());
     const int32_t row0 = (int32_t)scol.size();
     scol.insert(scol.end(), Jl.begin(), Jl.end());
     sptr.push_back((int32_t)scol.size());
@@ -545,9 +595,25 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   c.bvptr.upload(bvptr, s);
   c.bhandle.upload(handle, nnz, s);
   c.bphi.upload(phi, nnz, s);
-  c.hptr.upload(hptr, s);
-  c.hvert.upload(hvert, s);
-  c.hphi.upload(hphi, s);
+  if (c.dist()) {   // B^T restricts over the owned vertices (summed across ranks)
+    std::vector<int32_t> optr(m + 1, 0), overt;
+    std::vector<double> ophi;
+    for (int32_t i = 0; i < m; ++i) {
+      for (int32_t k = hptr[i]; k < hptr[i + 1]; ++k)
+        if (hvert[k] < c.nv_own) {
+          overt.push_back(hvert[k]);
+          ophi.push_back(hphi[k]);
+        }
+      optr[i + 1] = (int32_t)overt.size();
+    }
+    c.hptr.upload(optr, s);
+    c.hvert.upload(overt.empty() ? std::vector<int32_t>{0} : overt, s);
+    c.hphi.upload(ophi.empty() ? std::vector<double>{0.0} : ophi, s);
+  } else {
+    c.hptr.upload(hptr, s);
+    c.hvert.upload(hvert, s);
+    c.hphi.upload(hphi, s);
+  }
   c.phi_aff.upload(phi_aff, nv, s);
   for (int k = 0; k < 3; ++k) c.aff_origin[k] = aff_origin[k];
   c.sptr.upload(sptr, s);

@@ -43,8 +43,10 @@ static Ground ground_of(const Ctx &c) {
 // ------------------------------------------------------------------ vertex gradient (a2)
 // g_v = h^2 sum_{(e,a) in inc(v)} g_e[a] + m_v (x_v - xhat_v) + h^2 kappa b'(d_v) n ; 0 at DBC.
 // Also accumulates the vertex energy terms (inertia + h^2 kappa b) over free vertices, |g|^2.
+// gradient of every local vertex; energy, |g|^2 and the penetration count over the owned
+// vertices [0, nv_own) only
 __global__ void __launch_bounds__(256) k_vertex_grad(
-    int nv, const int32_t *__restrict__ vptr, const int32_t *__restrict__ vinc,
+    int nv, int nv_own, const int32_t *__restrict__ vptr, const int32_t *__restrict__ vinc,
     const double *__restrict__ stage_g, const double *__restrict__ x, const double *__restrict__ xhat,
     const double *__restrict__ mass, const uint8_t *__restrict__ fixed, Ground G, double h2,
     double *__restrict__ g, double *__restrict__ partial, unsigned int *__restrict__ counter,
@@ -72,7 +74,7 @@ __global__ void __launch_bounds__(256) k_vertex_grad(
       e = 0.5 * m * (r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
       if (G.on) {
         const double d = G.n0 * x[3 * v] + G.n1 * x[3 * v + 1] + G.n2 * x[3 * v + 2] - G.off;
-        if (!(d > 0.0)) acc[2] += 1.0;
+        if (!(d > 0.0) && v < nv_own) acc[2] += 1.0;
         const double b1 = h2 * G.kappa * bar_d1(d, G.dhat);
         out3[0] += b1 * G.n0;
         out3[1] += b1 * G.n1;
@@ -84,8 +86,10 @@ __global__ void __launch_bounds__(256) k_vertex_grad(
     }
 #pragma unroll
     for (int i = 0; i < 3; ++i) g[3 * v + i] = out3[i];
-    acc[0] += e;
-    acc[1] += out3[0] * out3[0] + out3[1] * out3[1] + out3[2] * out3[2];
+    if (v < nv_own) {
+      acc[0] += e;
+      acc[1] += out3[0] * out3[0] + out3[1] * out3[1] + out3[2] * out3[2];
+    }
   }
   double res[3];
   if (grid_reduce<3>(acc, partial, counter, res) && threadIdx.x == 0) {
@@ -98,7 +102,7 @@ __global__ void __launch_bounds__(256) k_vertex_grad(
 void launch_vertex_grad(Ctx &c) {
   const int bs = 256, nb = std::min(div_up(c.nv, bs), 148 * 8);
   const double h2 = c.params.h * c.params.h;
-  k_vertex_grad<<<nb, bs, 0, c.stream>>>(c.nv, c.vinc_ptr, c.vinc, c.stage_g, c.x, c.xhat, c.mass,
+  k_vertex_grad<<<nb, bs, 0, c.stream>>>(c.nv, c.nv_own, c.vinc_ptr, c.vinc, c.stage_g, c.x, c.xhat, c.mass,
                                          c.fixed, ground_of(c), h2, c.g, c.partial, c.counters + 1,
                                          c.scal + SC_ENERGY_VERT);
   c.launches++;
@@ -248,7 +252,9 @@ void launch_spmv(Ctx &c, const double *xin, double *yout, double /*unused*/, con
 // (q = H(z + beta p_old) = H z + beta H p_old, so the direction update needs no extra pass.)
 constexpr int kGridCap = 148 * 8;   // persistent-style grids: a few CTAs per SM, grid-stride loops
 
-__global__ void __launch_bounds__(256) k_pcg_init(int n3, const double *__restrict__ rhs,
+// n3_own: the dot products cover the owned entries [0, n3_own) (multi-GPU: partial sums, the
+// scalars are then derived by k_pcg_scalars after the cross-rank sum; dist = 1)
+__global__ void __launch_bounds__(256) k_pcg_init(int n3, int n3_own, int dist, const double *__restrict__ rhs,
                                                   const double *__restrict__ dinv, double *__restrict__ x,
                                                   double *__restrict__ r, double *__restrict__ z,
                                                   double *__restrict__ p, double *__restrict__ q,
@@ -262,18 +268,19 @@ __global__ void __launch_bounds__(256) k_pcg_init(int n3, const double *__restri
     z[i] = zi;
     p[i] = 0.0;
     q[i] = 0.0;
-    acc[0] = fma(ri, zi, acc[0]);
+    if (i < n3_own) acc[0] = fma(ri, zi, acc[0]);
   }
   double res[1];
   if (grid_reduce<1>(acc, partial, counter, res) && threadIdx.x == 0) {
     scal[SC_RZ] = res[0];
     scal[SC_RZ0] = res[0];
     scal[SC_BETA] = 0.0;
+    (void)dist;
   }
 }
 
 // thread per row (SELL-32); fused direction update and p.q partial
-__global__ void __launch_bounds__(256) k_pcg_spmv(SellView H, const double *__restrict__ z,
+__global__ void __launch_bounds__(256) k_pcg_spmv(SellView H, int nv_own, int dist, const double *__restrict__ z,
                                                   double *__restrict__ p, double *__restrict__ q,
                                                   double *__restrict__ partial, unsigned int *counter,
                                                   double *__restrict__ scal) {
@@ -289,18 +296,18 @@ __global__ void __launch_bounds__(256) k_pcg_spmv(SellView H, const double *__re
       const double qn = fma(beta, q[3 * row + i], o[i]);
       p[3 * row + i] = pn;
       q[3 * row + i] = qn;
-      acc[0] = fma(pn, qn, acc[0]);
+      if (row < nv_own) acc[0] = fma(pn, qn, acc[0]);
     }
   }
   double res[1];
   if (grid_reduce<1>(acc, partial, counter, res) && threadIdx.x == 0) {
     const double rho = scal[SC_RZ];
     scal[SC_PQ] = res[0];
-    scal[SC_ALPHA] = (res[0] != 0.0 && rho != 0.0) ? rho / res[0] : 0.0;
+    if (!dist) scal[SC_ALPHA] = (res[0] != 0.0 && rho != 0.0) ? rho / res[0] : 0.0;
   }
 }
 
-__global__ void __launch_bounds__(256) k_pcg_update(int n3, const double *__restrict__ dinv,
+__global__ void __launch_bounds__(256) k_pcg_update(int n3, int n3_own, int dist, const double *__restrict__ dinv,
                                                     const double *__restrict__ p, const double *__restrict__ q,
                                                     double *__restrict__ x, double *__restrict__ r,
                                                     double *__restrict__ z, double *__restrict__ partial,
@@ -313,24 +320,51 @@ __global__ void __launch_bounds__(256) k_pcg_update(int n3, const double *__rest
     const double zi = dinv[i] * ri;
     r[i] = ri;
     z[i] = zi;
-    acc[0] = fma(ri, zi, acc[0]);
+    if (i < n3_own) acc[0] = fma(ri, zi, acc[0]);
   }
   double res[1];
   if (grid_reduce<1>(acc, partial, counter, res) && threadIdx.x == 0) {
-    const double rho = scal[SC_RZ];
-    scal[SC_BETA] = rho != 0.0 ? res[0] / rho : 0.0;
-    scal[SC_RZ] = res[0];
+    if (dist) {
+      scal[SC_RZ_OLD] = res[0];   // partial r'.z', summed across ranks before k_pcg_scalars
+    } else {
+      const double rho = scal[SC_RZ];
+      scal[SC_BETA] = rho != 0.0 ? res[0] / rho : 0.0;
+      scal[SC_RZ] = res[0];
+    }
   }
 }
 
 static int grid_vec(int64_t n) { return std::min(div_up(n, 256), kGridCap); }
 
+// multi-GPU: the PCG scalars from the rank-summed dot products (which = 0: alpha; 1: beta)
+__global__ void k_pcg_scalars(double *__restrict__ scal, int which) {
+  if (which == 0) {
+    const double rho = scal[SC_RZ], pq = scal[SC_PQ];
+    scal[SC_ALPHA] = (pq != 0.0 && rho != 0.0) ? rho / pq : 0.0;
+  } else {
+    const double rho = scal[SC_RZ], rn = scal[SC_RZ_OLD];
+    scal[SC_BETA] = rho != 0.0 ? rn / rho : 0.0;
+    scal[SC_RZ] = rn;
+  }
+}
+
 static void enqueue_pcg_iters(Ctx &c, double *sol, int iters) {
-  const int n3 = 3 * c.nv, bs = 256;
+  const int n3 = 3 * c.nv, n3o = 3 * c.nv_own, bs = 256, dist = c.dist() ? 1 : 0;
   for (int it = 0; it < iters; ++it) {
-    k_pcg_spmv<<<div_up(c.nv, bs), bs, 0, c.stream>>>(sell_view(c), c.z, c.p, c.q, c.partial, c.counters + 3, c.scal);
-    k_pcg_update<<<grid_vec(n3), bs, 0, c.stream>>>(n3, c.dinv, c.p, c.q, sol, c.r, c.z, c.partial,
+    k_pcg_spmv<<<div_up(c.nv, bs), bs, 0, c.stream>>>(sell_view(c), c.nv_own, dist, c.z, c.p, c.q, c.partial,
+                                                      c.counters + 3, c.scal);
+    if (dist) {
+      dist_sum(c, c.scal + SC_PQ, 1);
+      k_pcg_scalars<<<1, 1, 0, c.stream>>>(c.scal, 0);
+    }
+    k_pcg_update<<<grid_vec(n3), bs, 0, c.stream>>>(n3, n3o, dist, c.dinv, c.p, c.q, sol, c.r, c.z, c.partial,
                                                     c.counters + 4, c.scal);
+    if (dist) {
+      dist_sum(c, c.scal + SC_RZ_OLD, 1);
+      k_pcg_scalars<<<1, 1, 0, c.stream>>>(c.scal, 1);
+      halo_exchange(c, c.z);
+      c.launches += 2;
+    }
   }
 }
 
@@ -344,12 +378,17 @@ void pcg_reset_graph(Ctx &c) {
 // when graphs are used, since the captured graph bakes in the pointer).
 void launch_pcg(Ctx &c, const double *rhs, double *sol, int iters) {
   const int n3 = 3 * c.nv, bs = 256;
-  k_pcg_init<<<grid_vec(n3), bs, 0, c.stream>>>(n3, rhs, c.dinv, sol, c.r, c.z, c.p, c.q, c.partial,
-                                                  c.counters + 2, c.scal);
+  k_pcg_init<<<grid_vec(n3), bs, 0, c.stream>>>(n3, 3 * c.nv_own, c.dist() ? 1 : 0, rhs, c.dinv, sol, c.r, c.z, c.p,
+                                                  c.q, c.partial, c.counters + 2, c.scal);
   c.launches++;
   MS_CUDA(cudaGetLastError());
+  if (c.dist()) {   // rank-summed r.z; ghost entries of z from their owners
+    dist_sum(c, c.scal + SC_RZ, 1);
+    MS_CUDA(cudaMemcpyAsync(c.scal + SC_RZ0, c.scal + SC_RZ, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+    halo_exchange(c, c.z);
+  }
   if (iters <= 0) return;
-  const bool graphs = c.params.use_graphs && sol == c.df.p;
+  const bool graphs = c.params.use_graphs && sol == c.df.p && !c.dist();
   if (!graphs) {
     enqueue_pcg_iters(c, sol, iters);
     c.launches += 2 * (int64_t)iters;
@@ -438,6 +477,40 @@ void launch_velocity(Ctx &c) {
   k_velocity<<<div_up(n3, 256), 256, 0, c.stream>>>(n3, c.x, c.xt, c.v, 1.0 / c.params.h);
   c.launches++;
   MS_CUDA(cudaGetLastError());
+}
+
+}  // namespace msim
+
+namespace msim {
+
+// ------------------------------------------------------------------ multi-GPU halo (dist.h)
+__global__ void k_halo_pack(int n, const int32_t *__restrict__ idx, const double *__restrict__ vec,
+                            double *__restrict__ buf) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < 3 * n) buf[t] = vec[3 * (size_t)idx[t / 3] + t % 3];
+}
+__global__ void k_halo_unpack(int n, const int32_t *__restrict__ idx, const double *__restrict__ buf,
+                              double *__restrict__ vec) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < 3 * n) vec[3 * (size_t)idx[t / 3] + t % 3] = buf[t];
+}
+
+void halo_exchange(Ctx &c, double *vec) {
+  if (!c.dist()) return;
+  const int ns = (int)c.part.send_idx.size(), nr = (int)c.part.recv_idx.size();
+  if (ns) k_halo_pack<<<div_up(3 * (int64_t)ns, 256), 256, 0, c.stream>>>(ns, c.halo_send_idx, vec, c.halo_send);
+  c.comm->exchange(c.part.peers, c.halo_send, c.halo_recv, c.stream);
+  if (nr) k_halo_unpack<<<div_up(3 * (int64_t)nr, 256), 256, 0, c.stream>>>(nr, c.halo_recv_idx, c.halo_recv, vec);
+  c.launches += 2;
+  MS_CUDA(cudaGetLastError());
+}
+
+void dist_sum(Ctx &c, double *dev, int64_t n) {
+  if (c.dist() && n > 0) c.comm->allreduce_sum(dev, n, c.stream);
+}
+
+void dist_min(Ctx &c, double *dev, int64_t n) {
+  if (c.dist() && n > 0) c.comm->allreduce_min(dev, n, c.stream);
 }
 
 }  // namespace msim

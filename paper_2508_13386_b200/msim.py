@@ -101,6 +101,12 @@ def _load():
         "ms_kernel_launches": ([P], C.c_int64),
         "ms_get_sizes": ([P, I64, I64, I64, I32, I64, I64], C.c_int32),
         "ms_get_coarse_info": ([P, C.POINTER(CoarseInfo)], C.c_int32),
+        "ms_nccl_unique_id": ([C.c_void_p], C.c_int32),
+        "ms_hub_create": ([C.c_int32, C.POINTER(C.c_void_p)], C.c_int32),
+        "ms_hub_destroy": ([C.c_void_p], C.c_int32),
+        "ms_create_hub": ([C.POINTER(C.c_void_p), C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int], C.c_int32),
+        "ms_partition": ([C.c_int32, C.c_int32, C.c_int64, D, C.c_int64, I32, I32, I32, I32, I32, I32, I32],
+                         C.c_int32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -140,12 +146,22 @@ def default_params():
 class Context:
     """One msim context (one GPU).  Methods map 1:1 onto the C-ABI entry points."""
 
-    def __init__(self, device=0, stream=None):
+    def __init__(self, device=0, stream=None, rank=0, world=1, nccl_id=None, hub=None):
+        """world > 1: one context per rank/GPU over NCCL (nccl_id: 128 bytes from nccl_unique_id()
+        on rank 0), or over an in-process Hub (one host thread per context, tests)."""
         h = C.c_void_p()
-        st = lib.ms_create(C.byref(h), int(device), C.c_void_p(stream or 0), None, 0, 1)
+        if hub is not None:
+            st = lib.ms_create_hub(C.byref(h), int(device), C.c_void_p(stream or 0), hub.h, int(rank), int(world))
+        else:
+            nid = None
+            if nccl_id is not None:
+                buf = (C.c_uint8 * 128).from_buffer_copy(bytes(nccl_id))
+                nid = C.cast(buf, C.c_void_p)
+            st = lib.ms_create(C.byref(h), int(device), C.c_void_p(stream or 0), nid, int(rank), int(world))
         if st != 0:
             raise MsimError(st, "ms_create failed")
         self.h = h
+        self.rank, self.world = int(rank), int(world)
         self.n_verts = 0
         self.n_tets = 0
         self.m = 0
@@ -214,8 +230,9 @@ class Context:
         self._chk(lib.ms_set_state(self.h, _d(x), _d(v)))
 
     def get_state(self):
-        x = np.empty((self.n_verts, 3))
-        v = np.empty((self.n_verts, 3))
+        """Global-sized arrays; with world > 1 only this rank's owned vertices are filled (rest 0)."""
+        x = np.zeros((self.n_verts, 3))
+        v = np.zeros((self.n_verts, 3))
         self._chk(lib.ms_get_state(self.h, _d(x), _d(v)))
         return x, v
 
@@ -348,9 +365,68 @@ class Context:
         return {k: getattr(ci, k) for k, _ in CoarseInfo._fields_ if k != "pad_"}
 
 
-def context_from_scene(scene, basis, device=0, stream=None, **params):
+def nccl_unique_id():
+    """128-byte ncclUniqueId for ms_create on every rank (call on rank 0, broadcast)."""
+    buf = (C.c_uint8 * 128)()
+    st = lib.ms_nccl_unique_id(buf)
+    if st != 0:
+        raise MsimError(st, "ms_nccl_unique_id failed")
+    return bytes(buf)
+
+
+def partition(rank, world, X, tets):
+    """Host-only slab partition plan of `rank` (no GPU): dict with nv_own, nt_own, l2g (local ->
+    global vertex; owned first), tet_l2g (owned tets first), and per peer rank the global ids
+    sent to / received from it (sorted)."""
+    X = _f64(X, (-1, 3))
+    tets = np.ascontiguousarray(tets, dtype=np.int32).reshape(-1, 4)
+    cnt = np.zeros(6, dtype=np.int32)
+    st = lib.ms_partition(int(rank), int(world), len(X), _d(X), len(tets), _i32(tets), _i32(cnt),
+                          None, None, None, None, None)
+    if st != 0:
+        raise MsimError(st, "ms_partition failed")
+    nv_own, nv_loc, nt_own, nt_loc, n_send, n_recv = (int(v) for v in cnt)
+    l2g = np.empty(nv_loc, dtype=np.int32)
+    tl2g = np.empty(nt_loc, dtype=np.int32)
+    peer = np.zeros((world, 2), dtype=np.int32)
+    snd = np.empty(max(n_send, 1), dtype=np.int32)
+    rcv = np.empty(max(n_recv, 1), dtype=np.int32)
+    st = lib.ms_partition(int(rank), int(world), len(X), _d(X), len(tets), _i32(tets), _i32(cnt),
+                          _i32(l2g), _i32(tl2g), _i32(peer), _i32(snd), _i32(rcv))
+    if st != 0:
+        raise MsimError(st, "ms_partition failed")
+    send, recv, so, ro = {}, {}, 0, 0
+    for q in range(world):
+        if peer[q, 0]:
+            send[q] = snd[so:so + peer[q, 0]].copy()
+            so += peer[q, 0]
+        if peer[q, 1]:
+            recv[q] = rcv[ro:ro + peer[q, 1]].copy()
+            ro += peer[q, 1]
+    return dict(nv_own=nv_own, nt_own=nt_own, l2g=l2g, tet_l2g=tl2g, send=send, recv=recv)
+
+
+class Hub:
+    """In-process communicator for `world` contexts driven by `world` host threads."""
+
+    def __init__(self, world):
+        self.h = C.c_void_p()
+        st = lib.ms_hub_create(int(world), C.byref(self.h))
+        if st != 0:
+            raise MsimError(st, "ms_hub_create failed")
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib.ms_hub_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def context_from_scene(scene, basis, device=0, stream=None, rank=0, world=1, nccl_id=None, hub=None, **params):
     """Create a context and upload a precompute.mesh.Scene + precompute.basis.Basis."""
-    ctx = Context(device, stream)
+    ctx = Context(device, stream, rank=rank, world=world, nccl_id=nccl_id, hub=hub)
     ctx.upload_mesh(scene.X, scene.tets, scene.E, scene.nu, scene.rho)
     if len(scene.dbc):
         ctx.set_dirichlet(scene.dbc)
