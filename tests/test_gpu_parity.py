@@ -206,8 +206,15 @@ def test_newton_iteration_bootstrapped(msim, name):
         ctx.end_step()
 
 
-@pytest.mark.parametrize("name,steps", [("c1", 10), ("drop_tiny", 12), ("drop", 6)])
+@pytest.mark.parametrize("name,steps", [("c1", 10), ("c2", 3), ("drop_tiny", 12), ("drop", 6)])
 def test_timestep_free_running(msim, name, steps):
+    """Free-running timesteps (reading R10): max_v |x_gpu - x_oracle| <= 1e-6 bbox diagonal.
+    C1 over its full 10 steps; C2 (heterogeneous 1e9/1e5 Pa, ~56 Newton iterations per step) over
+    3 here -- its full 20-step run passed on B200 in 18.5 min of oracle time
+    (profiles/r01_c2_20step_parity.log; MSIM_FULL_STEPS=1 runs it)."""
+    import os
+    if name == "c2" and os.environ.get("MSIM_FULL_STEPS"):
+        steps = 20
     s, b = scene_and_basis(name)
     ctx = msim.context_from_scene(s, b)
     sim = solver.OracleSim(s, b)
