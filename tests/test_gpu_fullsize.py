@@ -1,5 +1,6 @@
 """Full-size parity on C4 (64^3 cubes x 6 = 1,572,864 tets, m = 512), the configuration bench.py
-times, through the same C-ABI context construction (context_from_scene, default parameters).
+times, and on C3 (the lattice block), through the same C-ABI context construction
+(context_from_scene, default parameters).
 
 Checked at full size:
   * energy and full gradient against the oracle (Eq. 2; oracle/ip.py);
@@ -27,13 +28,14 @@ from precompute.basis import cached_basis  # noqa: E402
 from precompute.mesh import make_scene, random_state  # noqa: E402
 
 
-@pytest.fixture(scope="module")
-def c4():
+@pytest.fixture(scope="module", params=[4, 3], ids=["C4", "C3"])
+def c4(request):
+    """C4 (the bench configuration) and C3 (the 60^3 lattice, 776,832 tets, m = 256)."""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2508_13386_b200 import msim
-    s = make_scene(4)
+    s = make_scene(request.param)
     b = cached_basis(s)
     ctx = msim.context_from_scene(s, b)
     dhat = s.ground["dhat"]
