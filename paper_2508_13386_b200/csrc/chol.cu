@@ -213,12 +213,21 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(int ntask, 
       // critical-path task of step k (i = k+1): P(i,k), U(i,i,k) and D(i) in one CTA.
       // cnt = updates tile (i,k) must have seen; tk.w >> 16 unused; rank of (i,i) is upd order
       DF_STAMP(i, 0);
-      df_wait(&dfl[k], 1);
-      df_wait(&upd[i * NT + k], cnt & 0xffff);
-      DF_STAMP(i, 1);
+      // everything that does not depend on D(k) is fetched before waiting for it: A_ik (its
+      // updates are done) and the diagonal tile A_ii (its earlier updates are done)
       double *SA = sm, *SU = sm + TB * TB;
-      const size_t oik = tile_off(i, k, nSp);
+      const size_t oik = tile_off(i, k, nSp), oii = tile_off(i, i, nSp);
+      df_wait(&upd[i * NT + k], cnt & 0xffff);
       stage_colmajor(SA, L + oik, nSp);
+      asm volatile("cp.async.commit_group;\n" ::);
+      df_wait(&upd[i * NT + i], cnt >> 16);
+      double old[4][4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) old[a][b] = __ldcg(&L[oii + (size_t)(tc + 16 * b) * nSp + tr + 16 * a]);
+      df_wait(&dfl[k], 1);
+      DF_STAMP(i, 1);
       stage_colmajor(SU, U + (size_t)k * TB * TB, TB);
       cp_async_commit_wait();
       __syncthreads();
@@ -236,14 +245,7 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(int ntask, 
       for (int b = 0; b < 4; ++b)
 #pragma unroll
         for (int a = 0; a < 4; ++a) SX[(tc + 16 * b) * TB + tr + 16 * a] = acc[a][b];
-      df_wait(&upd[i * NT + i], cnt >> 16);
       DF_STAMP(i, 3);
-      const size_t oii = tile_off(i, i, nSp);
-      double old[4][4];
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int a = 0; a < 4; ++a) old[a][b] = __ldcg(&L[oii + (size_t)(tc + 16 * b) * nSp + tr + 16 * a]);
       __syncthreads();
       gemm64(SX, SX, acc, tr, tc);
       __syncthreads();   // SX consumed: the updated tile goes straight into D's smem layout
