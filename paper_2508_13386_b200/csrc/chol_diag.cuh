@@ -181,7 +181,49 @@ __device__ void diag_factor_rec(int k, int nSp, double *__restrict__ L, double *
 
 // ---------------------------------------------------------------- variants 1, 2
 // smem: A [64][LD], Li [64][LD], Tb [3*16*17], invd [64]
-constexpr int kDiagSmemDoublesBlocked = 2 * TB * LD + 3 * 16 * 17 + TB;
+constexpr int kDiagSmemDoublesBlocked = 2 * TB * LD + 3 * 16 * 17 + TB + 16;
+
+// Row-block pb (16 rows) of Li = L^-1 for the first 16 (pb + 1) columns of L final: the diagonal
+// block inverse (threads tt < 16, one column each) and Li_{pb,q} = -Li_{pb,pb} sum_{s=q}^{pb-1}
+// L_{pb,s} Li_{s,q} for q < pb.  Run by nth threads (tt = 0 .. nth-1) with named barrier bar_id.
+__device__ __forceinline__ void inv_rowblock(int pb, const double *A, double *Li, double (*Tb)[16][17],
+                                             const double *invd, int tt, int nth, int bar_id) {
+  const int o = 16 * pb;
+  if (tt < 16) {
+    double x[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      double s = r == tt ? 1.0 : 0.0, s2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < r; q += 2) {
+        s = fma(-A[(o + r) * LD + o + q], x[q], s);
+        if (q + 1 < r) s2 = fma(-A[(o + r) * LD + o + q + 1], x[q + 1], s2);
+      }
+      x[r] = (s + s2) * invd[o + r];
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) Li[(o + r) * LD + o + tt] = x[r];
+  } else {
+    for (int e = tt - 16; e < pb * 256; e += nth - 16) {
+      const int q = e >> 8, r = (e >> 4) & 15, cc = e & 15;
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int m = 16 * q; m < o; m += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s4[u] = fma(A[(o + r) * LD + m + u], Li[(m + u) * LD + 16 * q + cc], s4[u]);
+      }
+      Tb[q][r][cc] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    }
+  }
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nth) : "memory");
+  for (int e = tt; e < pb * 256; e += nth) {
+    const int q = e >> 8, r = (e >> 4) & 15, cc = e & 15;
+    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int m = 0; m < 16; ++m) s4[m & 3] = fma(Li[(o + r) * LD + o + m], Tb[q][m][cc], s4[m & 3]);
+    Li[(o + r) * LD + 16 * q + cc] = -((s4[0] + s4[1]) + (s4[2] + s4[3]));
+  }
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nth) : "memory");
+}
 
 __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, double *__restrict__ U,
                                     int *__restrict__ flag, double *sm, bool preloaded) {
@@ -214,7 +256,11 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
   bool bad = false;
   for (int p = 0; p < 4; ++p) {
     const int j0 = 16 * p;
-    if (w == 0) {
+    if (w != 0) {
+      // warps 1-7: row-block p-1 of the inverse (its columns of L are final) while warp 0
+      // factors panel p
+      if (p > 0) inv_rowblock(p - 1, A, Li, Tb, invd, t - 32, 224, 1);
+    } else {
       // panel rows j0 + lane and j0 + 32 + lane, columns j0 .. j0+15
       const int ra = j0 + lane, rb = j0 + 32 + lane;
       const bool va = ra < TB, vb = rb < TB;
@@ -246,25 +292,30 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
       // broadcast through shared memory (one store, 15 - j broadcast loads)
       // (the next pivot, a_{j+1,j+1} - l_{j+1,j}^2, is formed by its own lane from its own values,
       // off the shared-memory round trip)
-      double *pc = Tb[0][0];   // 16-double scratch (Tb is free until the inverse)
+      // (the next pivot's rsqrt is issued right after the column scaling, ahead of the trailing
+      // FMAs, in every lane -- lane j + 1's is the one used)
+      double *pc = invd + TB;   // 16-double broadcast scratch
       double piv = a[0];
+      bool pos = piv > 0.0;
+      double ivn = rsqrt_nr2(pos ? piv : 1.0);
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        double iv = 0.0;
         if (lane == j) {
-          if (!(piv > 0.0)) {
+          if (!pos) {
             bad = true;
-            piv = 1.0;
             a[j] = 1.0;
           }
-          iv = rsqrt_nr2(piv);
-          invd[j0 + j] = iv;
+          invd[j0 + j] = ivn;
         }
-        const double inv = __shfl_sync(0xffffffffu, iv, j);
+        const double inv = __shfl_sync(0xffffffffu, ivn, j);
         const double l = a[j] * inv;   // L_jj = a_jj / sqrt(a_jj); rows above: a = 0
         a[j] = l;
         b[j] *= inv;
-        if (j + 1 < 16) piv = fma(-l, l, a[j + 1]);   // meaningful in lane j + 1
+        if (j + 1 < 16) {
+          piv = fma(-l, l, a[j + 1]);   // meaningful in lane j + 1
+          pos = piv > 0.0;
+          ivn = rsqrt_nr2(pos ? piv : 1.0);
+        }
         if (lane < 16) pc[lane] = l;
         __syncwarp();
 #pragma unroll
@@ -308,48 +359,9 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
     DIAG_TS(2 + 2 * p);
   }
   if (w == 0 && lane == 0 && bad && flag) *flag = 1;
-  // inverse: diagonal 16x16 blocks (warp p, lane l < 16 solves column l)
-  if (w < 4 && lane < 16) {
-    const int o = 16 * w;
-    double x[16];
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      double s = r == lane ? 1.0 : 0.0, s2 = 0.0;
-#pragma unroll
-      for (int q = 0; q < r; q += 2) {
-        s = fma(-A[(o + r) * LD + o + q], x[q], s);
-        if (q + 1 < r) s2 = fma(-A[(o + r) * LD + o + q + 1], x[q + 1], s2);
-      }
-      x[r] = (s + s2) * invd[o + r];
-    }
-#pragma unroll
-    for (int r = 0; r < 16; ++r) Li[(o + r) * LD + o + lane] = x[r];
-  }
-  __syncthreads();
+  // last row-block of the inverse (the others were formed during the panels)
+  inv_rowblock(3, A, Li, Tb, invd, t, 256, 1);
   DIAG_TS(9);
-  // off-diagonal blocks: Li_pq = -Li_pp sum_{s=q}^{p-1} L_ps Li_sq, p = 1..3
-  for (int p = 1; p < 4; ++p) {
-    for (int e = t; e < p * 256; e += 256) {
-      const int q = e >> 8, r = (e >> 4) & 15, cc = e & 15;
-      double s4[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int m = 16 * q; m < 16 * p; m += 4) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) s4[u] = fma(A[(16 * p + r) * LD + m + u], Li[(m + u) * LD + 16 * q + cc], s4[u]);
-      }
-      Tb[q][r][cc] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-    }
-    __syncthreads();
-    DIAG_TS(8 + 2 * p);
-    for (int e = t; e < p * 256; e += 256) {
-      const int q = e >> 8, r = (e >> 4) & 15, cc = e & 15;
-      double s4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-      for (int m = 0; m < 16; ++m) s4[m & 3] = fma(Li[(16 * p + r) * LD + 16 * p + m], Tb[q][m][cc], s4[m & 3]);
-      Li[(16 * p + r) * LD + 16 * q + cc] = -((s4[0] + s4[1]) + (s4[2] + s4[3]));
-    }
-    __syncthreads();
-    DIAG_TS(9 + 2 * p);
-  }
   // store L_kk (lower, column-major) and U_kk = Li^T (row-major: U[r][c] at r*64 + c = Li[c][r])
   double *Uk = U + (size_t)k * TB * TB;
 #pragma unroll 4
