@@ -433,32 +433,63 @@ __device__ __forceinline__ void lift_store(const double (&p9)[45], double *__res
 // on the negative eigenvalues, eig9.cuh).  A tet with more than kMaxNeg negative eigenvalues (or
 // no QL convergence) goes to a work list for pass 2, the cyclic-Jacobi eigen-clamp (the list
 // order depends on atomics, the per-tet result does not -> deterministic).
-constexpr int kMaxNeg = 4;
+#ifndef MSIM_KMAXNEG
+#define MSIM_KMAXNEG 4
+#endif
+constexpr int kMaxNeg = MSIM_KMAXNEG;
 
-constexpr int kHessThreads = 128;
+#ifndef MSIM_HESS_THREADS
+#define MSIM_HESS_THREADS 128
+#endif
+constexpr int kHessThreads = MSIM_HESS_THREADS;
 constexpr int kHessScratch = 35 + 9 * kMaxNeg;   // doubles per thread (eig9.cuh)
 
 #ifndef MSIM_HESS_MINB
 #define MSIM_HESS_MINB 2
 #endif
+// The projected blocks leave through shared memory: each warp writes its 32 tets' 90 doubles
+// (row stride 91 against bank conflicts) and copies them to the contiguous stage_h rows of those
+// tets with coalesced stores (a direct per-thread store has a 720-byte stride).
+constexpr int kHessStg = 91;
+
 __global__ void __launch_bounds__(kHessThreads, MSIM_HESS_MINB) k_elem_hess(MeshView M, const double *__restrict__ x,
                                                             double *__restrict__ stage_h,
                                                             int32_t *__restrict__ work,
                                                             unsigned int *__restrict__ nwork) {
-  extern __shared__ double hsm[];   // [kHessScratch][kHessThreads], thread-minor (conflict-free)
+  extern __shared__ double hsm[];   // eig9 scratch [kHessScratch][kHessThreads] / store staging
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= M.nt) return;
-  TetKin k;
-  load_tet_kin(M, x, e, k);
-  double a[45], p9[45];
-  reduced_hessian(k, a);
-  // already PSD (lambda_min > -1e-12 ||M||_F, Cholesky test): P+ = M to within 1e-11 relative,
-  // inside the 1e-10 parity tolerance -- common near rest (free fall), skips the eigensolver
+  const int lane = threadIdx.x & 31, wbase = threadIdx.x & ~31;
+  bool store = false;
+  double p9[45];
+  if (e < M.nt) {
+    TetKin k;
+    load_tet_kin(M, x, e, k);
+    double a[45];
+    reduced_hessian(k, a);
+    // already PSD (lambda_min > -1e-12 ||M||_F, Cholesky test): P+ = M to within 1e-11 relative,
+    // inside the 1e-10 parity tolerance -- common near rest (free fall), skips the eigensolver
 #pragma unroll
-  for (int q = 0; q < 45; ++q) p9[q] = a[q];
-  if (psd_by_cholesky_inplace(p9, 1e-12)) lift_store(a, stage_h + (size_t)e * 90);
-  else if (e9::psd_project<kMaxNeg>(a, p9, hsm + threadIdx.x, kHessThreads) >= 0) lift_store(p9, stage_h + (size_t)e * 90);
-  else work[atomicAdd(nwork, 1u)] = e;
+    for (int q = 0; q < 45; ++q) p9[q] = a[q];
+    if (psd_by_cholesky_inplace(p9, 1e-12)) {
+#pragma unroll
+      for (int q = 0; q < 45; ++q) p9[q] = a[q];
+      store = true;
+    } else if (e9::psd_project<kMaxNeg>(a, p9, hsm + threadIdx.x, kHessThreads) >= 0) {
+      store = true;
+    } else {
+      work[atomicAdd(nwork, 1u)] = e;
+    }
+  }
+  __syncthreads();   // the eig9 scratch is dead: reuse it for the store staging
+  double *stg = hsm + (size_t)threadIdx.x * kHessStg;
+  if (store) lift_store(p9, stg);
+  __syncwarp();
+  const int e0 = blockIdx.x * blockDim.x + wbase;
+  const int ntet = min(32, M.nt - e0);
+  double *dst = stage_h + (size_t)e0 * 90;
+  const double *src = hsm + (size_t)wbase * kHessStg;
+  // (tets of the warp that went to the Jacobi list are rewritten by k_elem_hess_eig)
+  for (int idx = lane; idx < ntet * 90; idx += 32) dst[idx] = src[(idx / 90) * kHessStg + idx % 90];
 }
 
 __global__ void __launch_bounds__(128) k_elem_hess_eig(MeshView M, const double *__restrict__ x,
@@ -502,7 +533,7 @@ void launch_elem_grad(Ctx &c) { launch_elem_grad_to(c, c.x, nullptr); }
 
 void launch_elem_hess_to(Ctx &c, const double *x) {
   MS_CUDA(cudaMemsetAsync(c.hess_nwork, 0, sizeof(unsigned int), c.stream));
-  constexpr int smem = sizeof(double) * kHessScratch * kHessThreads;
+  constexpr int smem = sizeof(double) * (kHessScratch > kHessStg ? kHessScratch : kHessStg) * kHessThreads;
   static bool attr = false;
   if (!attr) {
     MS_CUDA(cudaFuncSetAttribute(k_elem_hess, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
