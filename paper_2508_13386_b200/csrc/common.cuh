@@ -73,6 +73,9 @@ struct Reducer {
 };
 
 // ---------------------------------------------------------------- tile Cholesky schedule
+// staged element Hessian: 10 upper 3x3 blocks per tet, each padded to 10 doubles so every
+// block starts 16-byte aligned (the assembly gathers it with 5 vector loads)
+constexpr int kStageB = 10, kStageH = 10 * kStageB;
 constexpr int kGalChunk = 128;   // vertices of U_i per Galerkin chunk (7-bit local index)
 
 struct CholTask {      // one trailing update A_ij -= L_ik L_jk^T (tiles)
@@ -127,7 +130,7 @@ struct Ctx {
   DBuf<double> g, ds, da, df, d, r, rhs;   // 3nv
   DBuf<double> p, q, z, tmp;               // PCG vectors
   DBuf<double> stage_g;             // [nt*12] element gradients (unscaled by h^2)
-  DBuf<double> stage_h;             // [nt*90] 10 upper 3x3 blocks of P+(H_e)
+  DBuf<double> stage_h;             // [nt*kStageH] 10 upper 3x3 blocks of P+(H_e), kStageB apart
   DBuf<int32_t> hess_work;          // [nt] tets whose reduced Hessian needs the eigen-clamp
   DBuf<unsigned int> hess_nwork;    // [1] their count
   bool step_begun = false;

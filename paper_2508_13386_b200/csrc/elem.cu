@@ -399,7 +399,7 @@ __device__ __forceinline__ bool psd_by_cholesky_inplace(double (&l)[45], double 
   return ok;
 }
 
-// dst[blk4(a,a2)*9 + 3 i + i2] = block (a, a2), a <= a2, of H_e = Q P9 Q^T with
+// dst[blk4(a,a2)*kStageB + 3 i + i2] = block (a, a2), a <= a2, of H_e = Q P9 Q^T with
 // Q4 = 1/2 [[1,1,1],[1,-1,-1],[-1,1,-1],[-1,-1,1]]: for each (i, i2) the 4x4 block over (A, A2)
 // is 1/4 H4 P H4^T, formed with the Hadamard pattern (42 adds)
 __device__ __forceinline__ void lift_store(const double (&p9)[45], double *__restrict__ dst) {
@@ -423,12 +423,12 @@ __device__ __forceinline__ void lift_store(const double (&p9)[45], double *__res
         const double t1 = u[A][1] + u[A][2], t2 = u[A][1] - u[A][2];
         const double w[4] = {u[A][0] + t1, u[A][0] - t1, t2 - u[A][0], -t2 - u[A][0]};
 #pragma unroll
-        for (int A2 = A; A2 < 4; ++A2) dst[blk4(A, A2) * 9 + 3 * i + i2] = 0.25 * w[A2];
+        for (int A2 = A; A2 < 4; ++A2) dst[blk4(A, A2) * kStageB + 3 * i + i2] = 0.25 * w[A2];
       }
     }
 }
 
-// stage_h[e*90 + blk4(a,a2)*9 + 3 i + i2] = P+(H_e) block (a, a2), a <= a2 (unscaled by h^2).
+// stage_h[e*kStageH + blk4(a,a2)*kStageB + 3 i + i2] = P+(H_e) block (a, a2), a <= a2 (unscaled by h^2).
 // Pass 1 (every tet): reduced Hessian, P+ by e9::psd_project (tridiagonal QL + inverse iteration
 // on the negative eigenvalues, eig9.cuh).  A tet with more than kMaxNeg negative eigenvalues (or
 // no QL convergence) goes to a work list for pass 2, the cyclic-Jacobi eigen-clamp (the list
@@ -450,7 +450,7 @@ constexpr int kHessScratch = 35 + 9 * kMaxNeg;   // doubles per thread (eig9.cuh
 // The projected blocks leave through shared memory: each warp writes its 32 tets' 90 doubles
 // (row stride 91 against bank conflicts) and copies them to the contiguous stage_h rows of those
 // tets with coalesced stores (a direct per-thread store has a 720-byte stride).
-constexpr int kHessStg = 91;
+constexpr int kHessStg = kStageH + 1;
 
 __global__ void __launch_bounds__(kHessThreads, MSIM_HESS_MINB) k_elem_hess(MeshView M, const double *__restrict__ x,
                                                             double *__restrict__ stage_h,
@@ -486,10 +486,10 @@ __global__ void __launch_bounds__(kHessThreads, MSIM_HESS_MINB) k_elem_hess(Mesh
   __syncwarp();
   const int e0 = blockIdx.x * blockDim.x + wbase;
   const int ntet = min(32, M.nt - e0);
-  double *dst = stage_h + (size_t)e0 * 90;
+  double *dst = stage_h + (size_t)e0 * kStageH;
   const double *src = hsm + (size_t)wbase * kHessStg;
   // (tets of the warp that went to the Jacobi list are rewritten by k_elem_hess_eig)
-  for (int idx = lane; idx < ntet * 90; idx += 32) dst[idx] = src[(idx / 90) * kHessStg + idx % 90];
+  for (int idx = lane; idx < ntet * kStageH; idx += 32) dst[idx] = src[(idx / kStageH) * kHessStg + idx % kStageH];
 }
 
 __global__ void __launch_bounds__(128) k_elem_hess_eig(MeshView M, const double *__restrict__ x,
@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(128) k_elem_hess_eig(MeshView M, const double 
     double a[45], p9[45];
     reduced_hessian(k, a);
     eig_clamp(a, p9);
-    lift_store(p9, stage_h + (size_t)e * 90);
+    lift_store(p9, stage_h + (size_t)e * kStageH);
   }
 }
 
@@ -515,8 +515,8 @@ __global__ void k_expand_hess(int nt, const double *__restrict__ stage_h, double
   const int e = (int)(idx / 144), rc = (int)(idx % 144), r = rc / 12, cc = rc % 12;
   const int a = r / 3, i = r % 3, a2 = cc / 3, i2 = cc % 3;
   double v;
-  if (a <= a2) v = stage_h[(size_t)e * 90 + blk4(a, a2) * 9 + 3 * i + i2];
-  else v = stage_h[(size_t)e * 90 + blk4(a2, a) * 9 + 3 * i2 + i];
+  if (a <= a2) v = stage_h[(size_t)e * kStageH + blk4(a, a2) * kStageB + 3 * i + i2];
+  else v = stage_h[(size_t)e * kStageH + blk4(a2, a) * kStageB + 3 * i2 + i];
   He[idx] = v;
 }
 

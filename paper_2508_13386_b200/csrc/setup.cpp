@@ -178,7 +178,7 @@ void ensure_state_buffers(Ctx &c) {
                           &c.p, &c.q, &c.z, &c.tmp, &c.dinv})
     b->alloc(n3);
   c.stage_g.alloc((size_t)12 * c.nt);
-  c.stage_h.alloc((size_t)90 * c.nt);
+  c.stage_h.alloc((size_t)kStageH * c.nt);
   c.hess_work.alloc((size_t)c.nt);
   c.hess_nwork.alloc(1);
   c.max_blocks = std::max(div_up(c.nt, 128), div_up(c.nv, 128)) + 1024;

@@ -128,17 +128,20 @@ __global__ void __launch_bounds__(256) k_assemble(
   for (int q = 0; q < 9; ++q) acc[q] = 0.0;
   if (s >= 0) {
     for (int k = cptr[s]; k < cptr[s + 1]; ++k) {
-      const int code = contrib[k];
+      const int code = __ldg(&contrib[k]);
       const int e = code >> 4, a = (code >> 2) & 3, b = code & 3;
-      if (a <= b) {
-        const double *src = stage_h + (size_t)e * 90 + blk4s(a, b) * 9;
+      const bool up = a <= b;
+      const double2 *src = reinterpret_cast<const double2 *>(
+          stage_h + (size_t)e * kStageH + (up ? blk4s(a, b) : blk4s(b, a)) * kStageB);
+      double v[10];
 #pragma unroll
-        for (int q = 0; q < 9; ++q) acc[q] += src[q];
-      } else {
-        const double *src = stage_h + (size_t)e * 90 + blk4s(b, a) * 9;
-#pragma unroll
-        for (int q = 0; q < 9; ++q) acc[q] += src[(q % 3) * 3 + q / 3];
+      for (int h = 0; h < 5; ++h) {
+        const double2 t2 = __ldg(&src[h]);
+        v[2 * h] = t2.x;
+        v[2 * h + 1] = t2.y;
       }
+#pragma unroll
+      for (int q = 0; q < 9; ++q) acc[q] += up ? v[q] : v[(q % 3) * 3 + q / 3];
     }
     const int row = slot_row[s], col = sell_col[pos];
 #pragma unroll
