@@ -112,6 +112,11 @@ void launch_vertex_grad(Ctx &c) {
 // ------------------------------------------------------------------ assembly (a4)
 __host__ __device__ constexpr int blk4s(int a, int b) { return a * 4 - (a * (a - 1)) / 2 + (b - a); }
 
+#ifndef MSIM_ASM_UNROLL
+#define MSIM_ASM_UNROLL 2   // two contributions' gathers in flight (measured: 0.545 -> 0.526 ms at C4)
+#endif
+constexpr int kAsmUnroll = MSIM_ASM_UNROLL;
+
 // thread per SELL position (coalesced value writes); slot s = sell_slot[pos] (-1: padding)
 __global__ void __launch_bounds__(256) k_assemble(
     int64_t npos, const int32_t *__restrict__ sell_slot, const int32_t *__restrict__ sell_col,
@@ -127,7 +132,9 @@ __global__ void __launch_bounds__(256) k_assemble(
 #pragma unroll
   for (int q = 0; q < 9; ++q) acc[q] = 0.0;
   if (s >= 0) {
-    for (int k = cptr[s]; k < cptr[s + 1]; ++k) {
+    const int k1 = __ldg(&cptr[s + 1]);
+#pragma unroll(kAsmUnroll)
+    for (int k = __ldg(&cptr[s]); k < k1; ++k) {
       const int code = __ldg(&contrib[k]);
       const int e = code >> 4, a = (code >> 2) & 3, b = code & 3;
       const bool up = a <= b;
