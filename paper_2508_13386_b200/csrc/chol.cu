@@ -62,6 +62,56 @@ __device__ __forceinline__ void gemm64(const double *S1, const double *S2, doubl
   }
 }
 
+// ------------------------------------------------------------------ tile GEMM of the dataflow kernel
+// acc = S1^T S2 over the 64-long k dimension (S1[kk*64 + r], S2[kk*64 + c]); thread-owned elements
+// idx = 0..15 at (r, c) = tile_rc(idx).  MSIM_TILE_MMA: FP64 tensor cores (mma.sync m8n8k4): warp w
+// owns rows 16 (w & 3) .. +15 and columns 32 (w >> 2) .. +31 as 2 x 4 blocks of 8 x 8; otherwise
+// the DFMA register-blocked gemm64.
+#ifndef MSIM_TILE_MMA
+#define MSIM_TILE_MMA 1
+#endif
+
+__device__ __forceinline__ void tile_rc(int idx, int &r, int &c) {
+#if MSIM_TILE_MMA
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int j = idx & 1, bj = (idx >> 1) & 3, bi = idx >> 3;
+  r = 16 * (w & 3) + 8 * bi + (lane >> 2);
+  c = 32 * (w >> 2) + 8 * bj + 2 * (lane & 3) + j;
+#else
+  r = (threadIdx.x & 15) + 16 * (idx >> 2);
+  c = (threadIdx.x >> 4) + 16 * (idx & 3);
+#endif
+}
+
+__device__ __forceinline__ void tile_gemm(const double *S1, const double *S2, double (&acc)[16]) {
+#if MSIM_TILE_MMA
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int r0 = 16 * (w & 3) + (lane >> 2), c0 = 32 * (w >> 2) + (lane >> 2), kl = lane & 3;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+#pragma unroll 4
+  for (int k0 = 0; k0 < TB; k0 += 4) {
+    const double *s1 = S1 + (k0 + kl) * TB, *s2 = S2 + (k0 + kl) * TB;
+    const double a0 = s1[r0], a1 = s1[r0 + 8];
+    double b[4];
+#pragma unroll
+    for (int bj = 0; bj < 4; ++bj) b[bj] = s2[c0 + 8 * bj];
+#pragma unroll
+    for (int bi = 0; bi < 2; ++bi)
+#pragma unroll
+      for (int bj = 0; bj < 4; ++bj)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(acc[(bi * 4 + bj) * 2]), "+d"(acc[(bi * 4 + bj) * 2 + 1])
+                     : "d"(bi ? a1 : a0), "d"(b[bj]));
+  }
+#else
+  double a4[4][4];
+  gemm64(S1, S2, a4, threadIdx.x & 15, threadIdx.x >> 4);
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q] = a4[q >> 2][q & 3];
+#endif
+}
+
 // stage a column-major global tile (leading dim nSp) into k-major smem S[kk*64 + r] (cp.async)
 // cp.async.cg: 16-byte global -> shared copy through L2 only (L1 is not coherent across SMs, and
 // the dataflow kernel reads tiles other CTAs wrote during the same launch)
@@ -221,41 +271,46 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(int ntask, 
       stage_colmajor(SA, L + oik, nSp);
       asm volatile("cp.async.commit_group;\n" ::);
       df_wait(&upd[i * NT + i], cnt >> 16);
-      double old[4][4];
+      double old[16];
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int a = 0; a < 4; ++a) old[a][b] = __ldcg(&L[oii + (size_t)(tc + 16 * b) * nSp + tr + 16 * a]);
+      for (int q = 0; q < 16; ++q) {
+        int r, c;
+        tile_rc(q, r, c);
+        old[q] = __ldcg(&L[oii + (size_t)c * nSp + r]);
+      }
       df_wait(&dfl[k], 1);
       DF_STAMP(i, 1);
       stage_colmajor(SU, U + (size_t)k * TB * TB, TB);
       cp_async_commit_wait();
       __syncthreads();
-      double acc[4][4];
-      gemm64(SA, SU, acc, tr, tc);
+      double acc[16];
+      tile_gemm(SA, SU, acc);
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int a = 0; a < 4; ++a) __stcg(&L[oik + (size_t)(tc + 16 * b) * nSp + tr + 16 * a], acc[a][b]);
+      for (int q = 0; q < 16; ++q) {
+        int r, c;
+        tile_rc(q, r, c);
+        __stcg(&L[oik + (size_t)c * nSp + r], acc[q]);
+      }
       df_signal(&pfl[i * NT + k], 1);             // panel tile published early for the other updates
       DF_STAMP(i, 2);
       // X = L_ik into k-major smem: SX[c*64 + r] = X[r][c]
       double *SX = sm;
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int a = 0; a < 4; ++a) SX[(tc + 16 * b) * TB + tr + 16 * a] = acc[a][b];
+      for (int q = 0; q < 16; ++q) {
+        int r, c;
+        tile_rc(q, r, c);
+        SX[c * TB + r] = acc[q];
+      }
       DF_STAMP(i, 3);
       __syncthreads();
-      gemm64(SX, SX, acc, tr, tc);
+      tile_gemm(SX, SX, acc);
       __syncthreads();   // SX consumed: the updated tile goes straight into D's smem layout
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          const int r = tr + 16 * a, c = tc + 16 * b;
-          sm[r * LD + c] = r >= c ? old[a][b] - acc[a][b] : 0.0;
-        }
+      for (int q = 0; q < 16; ++q) {
+        int r, c;
+        tile_rc(q, r, c);
+        sm[r * LD + c] = r >= c ? old[q] - acc[q] : 0.0;
+      }
       DF_STAMP(i, 4);
       diag_factor(i, nSp, L, U, flag, sm, true);
       df_signal(&dfl[i], 1);
@@ -270,12 +325,14 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(int ntask, 
       stage_colmajor(SU, U + (size_t)k * TB * TB, TB);
       cp_async_commit_wait();
       __syncthreads();
-      double acc[4][4];
-      gemm64(SA, SU, acc, tr, tc);
+      double acc[16];
+      tile_gemm(SA, SU, acc);
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int a = 0; a < 4; ++a) __stcg(&L[oik + (size_t)(tc + 16 * b) * nSp + tr + 16 * a], acc[a][b]);
+      for (int q = 0; q < 16; ++q) {
+        int r, c;
+        tile_rc(q, r, c);
+        __stcg(&L[oik + (size_t)c * nSp + r], acc[q]);
+      }
       df_signal(&pfl[i * NT + k], 1);
     } else {
       df_wait(&pfl[i * NT + k], 1);
@@ -285,22 +342,23 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(int ntask, 
       stage_colmajor(Sj, L + tile_off(j, k, nSp), nSp);
       df_wait(&upd[i * NT + j], cnt);
       const size_t oij = tile_off(i, j, nSp);
-      double old[4][4];
+      double old[16];
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int a = 0; a < 4; ++a) old[a][b] = __ldcg(&L[oij + (size_t)(tc + 16 * b) * nSp + tr + 16 * a]);
+      for (int q = 0; q < 16; ++q) {
+        int r, c;
+        tile_rc(q, r, c);
+        old[q] = __ldcg(&L[oij + (size_t)c * nSp + r]);
+      }
       cp_async_commit_wait();
       __syncthreads();
-      double acc[4][4];
-      gemm64(Si, Sj, acc, tr, tc);
+      double acc[16];
+      tile_gemm(Si, Sj, acc);
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          const int r = tr + 16 * a, c = tc + 16 * b;
-          if (i != j || r >= c) __stcg(&L[oij + (size_t)c * nSp + r], old[a][b] - acc[a][b]);
-        }
+      for (int q = 0; q < 16; ++q) {
+        int r, c;
+        tile_rc(q, r, c);
+        if (i != j || r >= c) __stcg(&L[oij + (size_t)c * nSp + r], old[q] - acc[q]);
+      }
       if (type == 3) {   // fused U(k+1,k+1,k) + D(k+1): the updated diagonal tile is factorised at once
         __syncthreads();
         diag_factor(i, nSp, L, U, flag, sm);
