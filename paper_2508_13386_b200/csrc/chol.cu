@@ -14,6 +14,7 @@
 // on the solution tiles it depends on (the vectors carry their own ready pattern) and applies
 // U_kk as a GEMV.
 #include <cooperative_groups.h>
+#include <algorithm>
 #include <cstdio>
 #include <cuda_pipeline.h>
 
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(256) k_chol_update(int k, const int32_t *__res
 //             step order -> deterministic);  A_ij -= L_ik L_jk^T;               upd[i][j] = rank + 1
 // Tile data produced by other CTAs is read through L2 only (cp.async.cg / ld.global.cg).
 #ifdef MSIM_DF_PROF   // diagnostics: global-timer stamps of the critical-path (type-4) tasks
-__device__ unsigned long long g_df_prof[1024][6];
+__device__ unsigned long long g_df_prof[1024][8];
 #define DF_STAMP(i, s)                                                              \
   do {                                                                              \
     if (threadIdx.x == 0) {                                                         \
@@ -268,9 +269,11 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(int ntask, 
       double *SA = sm, *SU = sm + TB * TB;
       const size_t oik = tile_off(i, k, nSp), oii = tile_off(i, i, nSp);
       df_wait(&upd[i * NT + k], cnt & 0xffff);
+      DF_STAMP(i, 6);
       stage_colmajor(SA, L + oik, nSp);
       asm volatile("cp.async.commit_group;\n" ::);
       df_wait(&upd[i * NT + i], cnt >> 16);
+      DF_STAMP(i, 7);
       double old[16];
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
@@ -571,7 +574,7 @@ void enqueue_chol_factor(Ctx &c) {
                                         kUpdSmem, c.stream));
 #ifdef MSIM_DF_PROF
     {
-      static unsigned long long h[1024][6];
+      static unsigned long long h[1024][8];
       MS_CUDA(cudaStreamSynchronize(c.stream));
       MS_CUDA(cudaMemcpyFromSymbol(h, g_df_prof, sizeof(h)));
       double seg[5] = {0, 0, 0, 0, 0}, gap = 0;
@@ -581,8 +584,16 @@ void enqueue_chol_factor(Ctx &c) {
         if (i > 1) gap += 1e-3 * (double)(h[i][1] - h[i - 1][5]);
         n++;
       }
-      fprintf(stderr, "[msim] chol type-4 avg us: wait %.2f  P %.2f  wait-ii %.2f  U %.2f  D %.2f | ready-after-prev-D %.2f | total %.1f us\n",
-              seg[0] / n, seg[1] / n, seg[2] / n, seg[3] / n, seg[4] / n, gap / n, 1e-3 * (double)(h[NT - 1][5] - h[1][0]));
+      double wik = 0, wii = 0, wd = 0;
+      for (int i = 2; i < NT && i < 1024; ++i) {
+        const double t5 = (double)h[i - 1][5];
+        wik += 1e-3 * std::max(0.0, (double)h[i][6] - t5);
+        wii += 1e-3 * std::max(0.0, (double)h[i][7] - std::max(t5, (double)h[i][6]));
+        wd += 1e-3 * std::max(0.0, (double)h[i][1] - std::max(t5, (double)h[i][7]));
+      }
+      fprintf(stderr, "[msim] chol type-4 avg us: wait %.2f  P %.2f  wait-ii %.2f  U %.2f  D %.2f | ready-after-prev-D %.2f (A_ik %.2f, A_ii %.2f, D %.2f) | total %.1f us\n",
+              seg[0] / n, seg[1] / n, seg[2] / n, seg[3] / n, seg[4] / n, gap / n, wik / n, wii / n, wd / n,
+              1e-3 * (double)(h[NT - 1][5] - h[1][0]));
     }
 #endif
     return;
