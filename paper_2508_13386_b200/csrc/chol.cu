@@ -195,17 +195,33 @@ __global__ void __launch_bounds__(256) k_chol_update(int k, const int32_t *__res
 }
 
 // ------------------------------------------------------------------ dataflow factorisation
-// One cooperative launch runs the whole tile DAG: tasks are handed out in (topological) task
-// order through an atomic counter to whichever CTA is free; a task waits only on tasks that
-// precede it, so the earliest unfinished task is always runnable (all CTAs are co-resident).
-// Tasks:
-//   D(k):     wait upd[k][k] == need;         factor + invert the diagonal tile;   dfl[k] = 1
-//   P(i,k):   wait dfl[k], upd[i][k] == need; L_ik = A_ik U_kk;                     pfl[i][k] = 1
-//   U(i,j,k): wait pfl[i][k], pfl[j][k], upd[i][j] == rank (updates of a tile are applied in
-//             step order -> deterministic);  A_ij -= L_ik L_jk^T;               upd[i][j] = rank + 1
+// One cooperative launch runs the whole tile DAG (setup.cpp builds the task list, the counted
+// inputs of every task and its successors):
+//   CTA 0      the critical chain T(k) = P(k+1,k) + U(k+1,k+1,k) + D(k+1), in order, waiting on
+//              flags and prefetching the tiles that do not depend on D(k);
+//   CTA 1      release helper: follows CTA 0's flags and hands T(k)'s successors to the queues;
+//   CTAs 2..   pop ready tasks from two FIFO queues (high: D, P and updates of tiles that become
+//              panel tiles within two steps; low: the bulk updates), each served by its own CTA
+//              set through tickets.  A task is pushed by whoever delivers its last input; a CTA
+//              that completes a task's last input keeps that task as its next one instead.
+// A popped task never waits, CTA 0 waits only on earlier tasks, so the launch cannot deadlock.
+// Tasks (the flags serve CTA 0's waits):
+//   D(k):     factor + invert the diagonal tile;                       dfl[k] = 1
+//   P(i,k):   L_ik = A_ik U_kk;                                          pfl[i][k] = 1
+//   U(i,j,k): A_ij -= L_ik L_jk^T (updates of a tile are chained in step order -> deterministic);
+//             upd[i][j] = rank + 1
 // Tile data produced by other CTAs is read through L2 only (cp.async.cg / ld.global.cg).
 #ifdef MSIM_DF_PROF   // diagnostics: global-timer stamps of the critical-path (type-4) tasks
 __device__ unsigned long long g_df_prof[1024][8];
+__device__ unsigned long long g_df_prof2[1024][6];   // [i]: P(i,i-2) claim/start/end, U(i,i-1,i-2) claim/start/end
+#define DF_STAMP2(i, s)                                                             \
+  do {                                                                              \
+    if (threadIdx.x == 0) {                                                         \
+      unsigned long long tt;                                                        \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));                        \
+      g_df_prof2[(i) & 1023][s] = tt;                                               \
+    }                                                                               \
+  } while (0)
 #define DF_STAMP(i, s)                                                              \
   do {                                                                              \
     if (threadIdx.x == 0) {                                                         \
@@ -214,8 +230,22 @@ __device__ unsigned long long g_df_prof[1024][8];
       g_df_prof[(i) & 1023][s] = tt;                                                \
     }                                                                               \
   } while (0)
+// per task: claim, ready (all waits satisfied), end, CTA
+constexpr int kDfTaskMax = 1 << 17;
+__device__ unsigned long long g_df_task[kDfTaskMax][4];
+#define DF_TSTAMP(id, s)                                                            \
+  do {                                                                              \
+    if (threadIdx.x == 0 && (id) < kDfTaskMax) {                                    \
+      unsigned long long tt;                                                        \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));                        \
+      g_df_task[id][s] = tt;                                                        \
+      if ((s) == 0) g_df_task[id][3] = blockIdx.x;                                  \
+    }                                                                               \
+  } while (0)
 #else
+#define DF_TSTAMP(id, s)
 #define DF_STAMP(i, s)
+#define DF_STAMP2(i, s)
 #endif
 
 __device__ __forceinline__ void df_wait(const int *p, int val) {
@@ -235,31 +265,142 @@ __device__ __forceinline__ void df_signal(int *p, int val) {
   }
 }
 
+// two flags with one poll pass, one fence and one barrier
+__device__ __forceinline__ void df_wait2(const int *p1, int v1, const int *p2, int v2) {
+  if (threadIdx.x == 0) {
+    const volatile int *f1 = p1, *f2 = p2;
+    while (*f1 != v1) __nanosleep(20);
+    while (*f2 != v2) __nanosleep(20);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void df_signal2(int *p1, int v1, int *p2, int v2) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicExch(p1, v1);
+    atomicExch(p2, v2);
+  }
+}
+
+struct DfParams {
+  int NT, nSp, ncrit, npool, nhi_cta, qstride;
+  const int4 *tasks;           // (type, i, j | k << 16, count) per task
+  double *L, *U;               // tiled factor / inverse diagonal tiles
+  int *upd, *dfl, *pfl, *flag; // progress flags (NT*NT, NT, NT*NT) and the pivot flag
+  const int32_t *crit;         // CTA 0's tasks in order
+  const uint8_t *cls;          // per task: 0/1 low/high-priority queue, 2 CTA 0's list
+  const int32_t *succ_ptr, *succ_mid, *succ;
+  int *ndep;                   // counted inputs still missing per task
+  int *queue;                  // queue q at q * qstride: [head, tail, task ids (-1: not yet pushed)]
+  int *done;                   // queue tasks finished
+};
+
+// successors [b, e) of a finished task: one input fewer each.  A queue task whose last input
+// this was is kept by the CTA as its next task if it has none yet (*keep, shared; continuation:
+// the per-tile update chains U(i,j,k) -> U(i,j,k') then run back to back without a queue trip)
+// or pushed to its class's queue, a FIFO served by tickets (no CAS contention: measured 60 us
+// claim latency with 147 CTAs CAS-polling two shared queues).  Called right after the task's
+// df_signal (CTA barrier, thread 0's fence); the second barrier orders that fence before the
+// other threads' atomics.
+__device__ __forceinline__ void df_release(const DfParams &P, int b, int e, int *keep) {
+  if (e - b > 1) __syncthreads();
+  for (int q = b + (int)threadIdx.x; q < e; q += blockDim.x) {
+    const int s = P.succ[q];
+    if (atomicSub(&P.ndep[s], 1) == 1) {
+      const int c = P.cls[s];
+      if (c < 2) {
+        if (keep && atomicCAS(keep, -1, s) == -1) {
+          __threadfence();   // acquire: the other producers' tiles
+        } else {
+          int *Q = P.queue + (size_t)c * P.qstride;
+          const int slot = atomicAdd(&Q[1], 1);
+          atomicExch(&Q[2 + slot], s);
+        }
+      }
+    }
+  }
+}
+
+// thread 0: ticket on queue Q: wait until the ticket's entry is pushed, or return -1 once every
+// queue task has finished (kept tasks never enter a queue, so the entry may never come)
+__device__ __forceinline__ int df_pop(int *Q, const int *done, int npool) {
+  const int h = atomicAdd(&Q[0], 1);
+  const volatile int *qe = Q + 2 + h, *dn = done;
+  for (;;) {
+    if (h < npool) {
+      const int v = *qe;
+      if (v >= 0) return v;
+    }
+    if (*dn >= npool) return -1;
+    __nanosleep(32);
+  }
+}
+
 #ifndef MSIM_DF_MINB
 #define MSIM_DF_MINB 2
 #endif
-__global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(int ntask, const int4 *__restrict__ tasks, int NT, int nSp,
-                                                       double *__restrict__ L, double *__restrict__ U,
-                                                       int *__restrict__ upd, int *__restrict__ dfl,
-                                                       int *__restrict__ pfl, int *__restrict__ flag,
-                                                       int *__restrict__ next) {
+__global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfParams P) {
   extern __shared__ double sm[];
-  __shared__ int s_id;
-  const int t = threadIdx.x, tr = t & 15, tc = t >> 4;
+  __shared__ int s_id, s_keep;
+  const int t = threadIdx.x;
+  if (t == 0) s_keep = -1;
+  __syncthreads();
+  const int NT = P.NT, nSp = P.nSp;
+  double *__restrict__ L = P.L;
+  double *__restrict__ U = P.U;
+  int *upd = P.upd, *dfl = P.dfl, *pfl = P.pfl, *flag = P.flag;
+  if (blockIdx.x == 1) {
+    // release helper: follows the chain and hands the successors of each chain task to the
+    // queues as its flags appear, so that CTA 0 never spends the atomics' round trips (measured
+    // ~2 us per release, twice per chain step)
+    for (int q = 0; q < P.ncrit; ++q) {
+      const int id = P.crit[q];
+      const int4 tk = P.tasks[id];
+      const int i = tk.y, k = tk.z >> 16;
+      df_wait(&pfl[i * NT + k], 1);
+      df_release(P, P.succ_ptr[id], P.succ_mid[id], nullptr);
+      df_wait2(&dfl[i], 1, &upd[i * NT + i], (tk.w >> 16) + 1);
+      df_release(P, P.succ_mid[id], P.succ_ptr[id + 1], nullptr);
+      __syncthreads();
+    }
+    return;
+  }
+  int ccur = 0, my_d = -1;
   for (;;) {
-    // dynamic in-order dispensing: the next unclaimed task in topological order goes to the
-    // first CTA that is free (all earlier tasks are claimed by running CTAs -> no deadlock)
-    if (t == 0) s_id = atomicAdd(next, 1);
-    __syncthreads();
-    const int id = s_id;
-    __syncthreads();
-    if (id >= ntask) break;
-    const int4 tk = tasks[id];
+    // (measured at C4: in-order dispensing from one counter left tasks 10-17 us unclaimed after
+    // their inputs were done -- 1.3 of 3.0 ms on the critical path)
+    int id;
+    if (blockIdx.x == 0) {
+      if (ccur >= P.ncrit) break;
+      id = P.crit[ccur++];
+    } else {
+      if (t == 0) {
+        if (s_keep >= 0) {
+          s_id = s_keep;
+          s_keep = -1;
+        } else {
+          const int c = blockIdx.x <= P.nhi_cta + 1 ? 1 : 0;   // CTAs 2..nhi_cta+1: high queue
+          s_id = df_pop(P.queue + (size_t)c * P.qstride, P.done, P.npool);
+          __threadfence();
+        }
+      }
+      __syncthreads();
+      id = s_id;
+      __syncthreads();
+      if (id < 0) break;
+    }
+    const int4 tk = P.tasks[id];
     const int type = tk.x, i = tk.y, j = tk.z & 0xffff, k = tk.z >> 16, cnt = tk.w;
-    if (type == 0) {
-      df_wait(&upd[k * NT + k], cnt);
+    DF_TSTAMP(id, 0);
+    if (type == 0) {   // popped from the ready queue: its inputs are done
+      (void)cnt;
+      DF_TSTAMP(id, 1);
       diag_factor(k, nSp, L, U, flag, sm);
       df_signal(&dfl[k], 1);
+      df_release(P, P.succ_ptr[id], P.succ_ptr[id + 1], &s_keep);
     } else if (type == 4) {
       // critical-path task of step k (i = k+1): P(i,k), U(i,i,k) and D(i) in one CTA.
       // cnt = updates tile (i,k) must have seen; tk.w >> 16 unused; rank of (i,i) is upd order
@@ -268,12 +409,11 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(int ntask, 
       // updates are done) and the diagonal tile A_ii (its earlier updates are done)
       double *SA = sm, *SU = sm + TB * TB;
       const size_t oik = tile_off(i, k, nSp), oii = tile_off(i, i, nSp);
-      df_wait(&upd[i * NT + k], cnt & 0xffff);
+      df_wait2(&upd[i * NT + k], cnt & 0xffff, &upd[i * NT + i], cnt >> 16);
       DF_STAMP(i, 6);
+      DF_STAMP(i, 7);
       stage_colmajor(SA, L + oik, nSp);
       asm volatile("cp.async.commit_group;\n" ::);
-      df_wait(&upd[i * NT + i], cnt >> 16);
-      DF_STAMP(i, 7);
       double old[16];
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
@@ -281,8 +421,9 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(int ntask, 
         tile_rc(q, r, c);
         old[q] = __ldcg(&L[oii + (size_t)c * nSp + r]);
       }
-      df_wait(&dfl[k], 1);
+      if (k != my_d) df_wait(&dfl[k], 1);   // D(k) is this CTA's previous task (usually)
       DF_STAMP(i, 1);
+      DF_TSTAMP(id, 1);
       stage_colmajor(SU, U + (size_t)k * TB * TB, TB);
       cp_async_commit_wait();
       __syncthreads();
@@ -316,12 +457,13 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(int ntask, 
       }
       DF_STAMP(i, 4);
       diag_factor(i, nSp, L, U, flag, sm, true);
-      df_signal(&dfl[i], 1);
-      df_signal(&upd[i * NT + i], (cnt >> 16) + 1);
+      df_signal2(&dfl[i], 1, &upd[i * NT + i], (cnt >> 16) + 1);
+      my_d = i;
       DF_STAMP(i, 5);
     } else if (type == 1) {
-      df_wait(&dfl[k], 1);
-      df_wait(&upd[i * NT + k], cnt);
+      if (i == k + 2) DF_STAMP2(i, 0);
+      if (i == k + 2) DF_STAMP2(i, 1);
+      DF_TSTAMP(id, 1);
       double *SA = sm, *SU = sm + TB * TB;
       const size_t oik = tile_off(i, k, nSp);
       stage_colmajor(SA, L + oik, nSp);
@@ -337,13 +479,16 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(int ntask, 
         __stcg(&L[oik + (size_t)c * nSp + r], acc[q]);
       }
       df_signal(&pfl[i * NT + k], 1);
+      df_release(P, P.succ_ptr[id], P.succ_ptr[id + 1], &s_keep);
+      if (i == k + 2) DF_STAMP2(i, 2);
     } else {
-      df_wait(&pfl[i * NT + k], 1);
-      df_wait(&pfl[j * NT + k], 1);
+      const bool col = (i == k + 2 && j == k + 1);
+      if (col) DF_STAMP2(i, 3);
       double *Si = sm, *Sj = sm + TB * TB;
       stage_colmajor(Si, L + tile_off(i, k, nSp), nSp);
       stage_colmajor(Sj, L + tile_off(j, k, nSp), nSp);
-      df_wait(&upd[i * NT + j], cnt);
+      if (col) DF_STAMP2(i, 4);
+      DF_TSTAMP(id, 1);
       const size_t oij = tile_off(i, j, nSp);
       double old[16];
 #pragma unroll
@@ -362,14 +507,13 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(int ntask, 
         tile_rc(q, r, c);
         if (i != j || r >= c) __stcg(&L[oij + (size_t)c * nSp + r], old[q] - acc[q]);
       }
-      if (type == 3) {   // fused U(k+1,k+1,k) + D(k+1): the updated diagonal tile is factorised at once
-        __syncthreads();
-        diag_factor(i, nSp, L, U, flag, sm);
-        df_signal(&dfl[i], 1);
-      }
       df_signal(&upd[i * NT + j], cnt + 1);
+      df_release(P, P.succ_ptr[id], P.succ_ptr[id + 1], &s_keep);
+      if (col) DF_STAMP2(i, 5);
     }
+    DF_TSTAMP(id, 2);
     __syncthreads();
+    if (t == 0 && type != 4) atomicAdd(P.done, 1);   // after this task's pushes (barrier above)
   }
 }
 
@@ -551,7 +695,8 @@ static int dataflow_grid(const Ctx &c) {
     MS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chol_dataflow, 256, kUpdSmem));
     per_sm = std::max(std::min(per_sm, kDfCtasPerSm), 1);
   }
-  return (int)std::min<int64_t>(c.n_dag, (int64_t)per_sm * c.coop_grid);
+  // the chain CTA, the release helper, at least one CTA per queue
+  return (int)std::max<int64_t>(4, (int64_t)per_sm * c.coop_grid);
 }
 
 // D(0); then for each k: P(k), U(k) with D(k+1) fused (look-ahead) -- or the single-launch
@@ -564,12 +709,35 @@ void enqueue_chol_factor(Ctx &c) {
   if (c.chol_dataflow) {
     const int NT = c.ntiles;
     MS_CUDA(cudaMemsetAsync(c.df_flags, 0, sizeof(int) * ((size_t)2 * NT * NT + NT + 1), c.stream));
-    int ntask = (int)c.n_dag, NTv = NT, nSpv = nSp;
-    const int4 *tk = reinterpret_cast<const int4 *>(c.chol_dag.p);
-    double *Lp = c.Lden, *Up = c.Uinv;
-    int *upd = c.df_flags, *pfl = c.df_flags + (size_t)NT * NT, *dfl = c.df_flags + (size_t)2 * NT * NT;
-    int *fl = c.flags + 0, *nx = c.df_flags + (size_t)2 * NT * NT + NT;
-    void *args[] = {&ntask, &tk, &NTv, &nSpv, &Lp, &Up, &upd, &dfl, &pfl, &fl, &nx};
+    MS_CUDA(cudaMemcpyAsync(c.chol_ndep.p, c.chol_ndep0.p, sizeof(int32_t) * c.chol_ndep0.n,
+                            cudaMemcpyDeviceToDevice, c.stream));
+    MS_CUDA(cudaMemcpyAsync(c.chol_queue.p, c.chol_queue0.p, sizeof(int32_t) * c.chol_queue0.n,
+                            cudaMemcpyDeviceToDevice, c.stream));
+    const int ntask = (int)c.n_dag;
+    (void)ntask;
+    DfParams prm;
+    prm.NT = NT;
+    prm.nSp = nSp;
+    prm.ncrit = (int)c.n_crit;
+    prm.npool = (int)c.n_pool;
+    prm.qstride = (int)c.n_pool + 2;
+    prm.nhi_cta = std::max(1, std::min(c.df_hi_ctas, dataflow_grid(c) - 3));
+    prm.tasks = reinterpret_cast<const int4 *>(c.chol_dag.p);
+    prm.L = c.Lden;
+    prm.U = c.Uinv;
+    prm.upd = c.df_flags;
+    prm.pfl = c.df_flags + (size_t)NT * NT;
+    prm.dfl = c.df_flags + (size_t)2 * NT * NT;
+    prm.flag = c.flags + 0;
+    prm.crit = c.chol_crit;
+    prm.cls = c.chol_cls;
+    prm.succ_ptr = c.chol_succ_ptr;
+    prm.succ = c.chol_succ;
+    prm.succ_mid = c.chol_succ_mid;
+    prm.ndep = c.chol_ndep;
+    prm.queue = c.chol_queue;
+    prm.done = c.chol_queue + 2 * prm.qstride;
+    void *args[] = {&prm};
     MS_CUDA(cudaLaunchCooperativeKernel((const void *)k_chol_dataflow, dim3(dataflow_grid(c)), dim3(256), args,
                                         kUpdSmem, c.stream));
 #ifdef MSIM_DF_PROF
@@ -590,6 +758,50 @@ void enqueue_chol_factor(Ctx &c) {
         wik += 1e-3 * std::max(0.0, (double)h[i][6] - t5);
         wii += 1e-3 * std::max(0.0, (double)h[i][7] - std::max(t5, (double)h[i][6]));
         wd += 1e-3 * std::max(0.0, (double)h[i][1] - std::max(t5, (double)h[i][7]));
+      }
+      {
+        static unsigned long long h2[1024][6];
+        MS_CUDA(cudaMemcpyFromSymbol(h2, g_df_prof2, sizeof(h2)));
+        // relative to D(i-2)'s end = critical task i-3's stamp 5 ... use D(k) end with k = i-2: h[i-2][5]
+        double pc = 0, ps = 0, pe = 0, uc = 0, us = 0, ue = 0;
+        int m2 = 0;
+        for (int i = 4; i < NT && i < 1024; ++i) {
+          const double t0 = (double)h[i - 2][5];   // D(i-2) done
+          pc += 1e-3 * ((double)h2[i][0] - t0);
+          ps += 1e-3 * ((double)h2[i][1] - t0);
+          pe += 1e-3 * ((double)h2[i][2] - t0);
+          uc += 1e-3 * ((double)h2[i][3] - t0);
+          us += 1e-3 * ((double)h2[i][4] - t0);
+          ue += 1e-3 * ((double)h2[i][5] - t0);
+          m2++;
+        }
+        {
+          static int dumped = 0;
+          if (++dumped == 4 && ntask <= kDfTaskMax) {   // one launch after warm-up
+            std::vector<unsigned long long> ht((size_t)ntask * 4);
+            std::vector<int32_t> hd((size_t)ntask * 4);
+            MS_CUDA(cudaMemcpyFromSymbol(ht.data(), g_df_task, sizeof(unsigned long long) * ht.size()));
+            MS_CUDA(cudaMemcpy(hd.data(), c.chol_dag.p, sizeof(int32_t) * hd.size(), cudaMemcpyDeviceToHost));
+            if (FILE *fd = std::fopen("gpurun_out/dftask.bin", "wb")) {
+              const int32_t hdr[2] = {ntask, NT};
+              std::fwrite(hdr, sizeof(int32_t), 2, fd);
+              std::fwrite(hd.data(), sizeof(int32_t), hd.size(), fd);
+              std::fwrite(ht.data(), sizeof(unsigned long long), ht.size(), fd);
+              std::fclose(fd);
+            }
+          }
+        }
+        if (FILE *fd = std::fopen("gpurun_out/dfprof_raw.txt", "w")) {
+          for (int i = 0; i < NT && i < 1024; ++i) {
+            std::fprintf(fd, "%d", i);
+            for (int q = 0; q < 8; ++q) std::fprintf(fd, " %llu", h[i][q]);
+            for (int q = 0; q < 6; ++q) std::fprintf(fd, " %llu", h2[i][q]);
+            std::fprintf(fd, "\n");
+          }
+          std::fclose(fd);
+        }
+        fprintf(stderr, "[msim] relative to D(k) done: P(k+2,k) claim %.2f start %.2f end %.2f | U(k+2,k+1,k) claim %.2f start %.2f end %.2f | D(k+1) done %.2f us\n",
+                pc / m2, ps / m2, pe / m2, uc / m2, us / m2, ue / m2, (seg[0] + seg[1] + seg[2] + seg[3] + seg[4]) / n);
       }
       fprintf(stderr, "[msim] chol type-4 avg us: wait %.2f  P %.2f  wait-ii %.2f  U %.2f  D %.2f | ready-after-prev-D %.2f (A_ik %.2f, A_ii %.2f, D %.2f) | total %.1f us\n",
               seg[0] / n, seg[1] / n, seg[2] / n, seg[3] / n, seg[4] / n, gap / n, wik / n, wii / n, wd / n,

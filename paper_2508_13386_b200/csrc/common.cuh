@@ -188,6 +188,13 @@ struct Ctx {
   int64_t n_sym_tiles = 0;
   DBuf<double> Uinv;                // [ntiles][64*64] U_kk = L_kk^-T (column-major)
   DBuf<int32_t> chol_dag;           // dataflow factorisation tasks (int4 each)
+  DBuf<int32_t> chol_crit;          // task ids run by CTA 0 in order (the type-4 chain)
+  DBuf<uint8_t> chol_cls;           // per task: 0/1 low/high-priority queue, 2 CTA 0's list
+  DBuf<int32_t> chol_succ_ptr, chol_succ_mid, chol_succ;   // successors (setup.cpp dataflow_graph)
+  DBuf<int32_t> chol_ndep0, chol_ndep;                     // inputs per task: pristine / live
+  DBuf<int32_t> chol_queue0, chol_queue;                   // two ready queues: pristine / live
+  int64_t n_crit = 0, n_pool = 0;
+  int df_hi_ctas = 32;   // CTAs serving the high-priority queue
   int64_t n_dag = 0;
   DBuf<int> df_flags;               // upd[NT*NT], pfl[NT*NT], dfl[NT]
   bool chol_dataflow = true;

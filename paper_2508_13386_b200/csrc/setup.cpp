@@ -243,6 +243,68 @@ void global_s_pattern(int32_t nv, const std::vector<int32_t> &tets, int32_t m, c
   }
 }
 
+// Dependency graph of the dataflow factorisation's tasks (chol.cu k_chol_dataflow): per task the
+// number of inputs and its successors.  A type-4 task (P(k+1,k) U(k+1,k+1,k) D(k+1)) releases
+// the readers of its panel tile P(k+1,k) before D(k+1): [succ_ptr, succ_mid) are those,
+// [succ_mid, succ_ptr+1) the readers of D(k+1) and of the diagonal tile's update count.  (A
+// queue task must never wait on an uncounted input: all queue CTAs could end up waiting on the
+// chain while the chain waits on a queued task.)
+static void dataflow_graph(const std::vector<int32_t> &dag, int NT, std::vector<int32_t> &succ_ptr,
+                           std::vector<int32_t> &succ_mid, std::vector<int32_t> &succ, std::vector<int32_t> &ndep) {
+  const int n = (int)(dag.size() / 4);
+  std::vector<int32_t> dfl(NT, -1), pfl((size_t)NT * NT, -1);
+  std::vector<std::vector<int32_t>> updt((size_t)NT * NT);
+  auto put = [](std::vector<int32_t> &v, int r, int32_t q) {
+    if ((int)v.size() <= r) v.resize(r + 1, -1);
+    v[r] = q;
+  };
+  for (int q = 0; q < n; ++q) {
+    const int ty = dag[4 * q], i = dag[4 * q + 1], j = dag[4 * q + 2] & 0xffff, k = dag[4 * q + 2] >> 16,
+              cnt = dag[4 * q + 3];
+    if (ty == 0) dfl[k] = q;
+    else if (ty == 4) {
+      dfl[i] = q;
+      pfl[(size_t)i * NT + k] = q;
+      put(updt[(size_t)i * NT + i], cnt >> 16, q);
+    } else if (ty == 1) pfl[(size_t)i * NT + k] = q;
+    else put(updt[(size_t)i * NT + j], cnt, q);
+  }
+  std::vector<std::vector<int32_t>> early(n), late(n);
+  ndep.assign(n, 0);
+  auto dep = [&](int q, int32_t d, bool via_panel) {
+    MS_REQUIRE(d >= 0 && d < q, MS_ERR_STATE, "tile DAG: dependency missing or out of order");
+    (via_panel && dag[4 * d] == 4 ? early : late)[d].push_back(q);
+    ndep[q]++;
+  };
+  for (int q = 0; q < n; ++q) {
+    const int ty = dag[4 * q], i = dag[4 * q + 1], j = dag[4 * q + 2] & 0xffff, k = dag[4 * q + 2] >> 16,
+              cnt = dag[4 * q + 3];
+    if (ty == 0) {
+      if (cnt) dep(q, updt[(size_t)k * NT + k][cnt - 1], false);
+    } else if (ty == 4) {
+      if (cnt & 0xffff) dep(q, updt[(size_t)i * NT + k][(cnt & 0xffff) - 1], false);
+      if (cnt >> 16) dep(q, updt[(size_t)i * NT + i][(cnt >> 16) - 1], false);
+      dep(q, dfl[k], false);
+    } else if (ty == 1) {
+      dep(q, dfl[k], false);
+      if (cnt) dep(q, updt[(size_t)i * NT + k][cnt - 1], false);
+    } else {
+      dep(q, pfl[(size_t)i * NT + k], true);
+      if (j != i) dep(q, pfl[(size_t)j * NT + k], true);
+      if (cnt) dep(q, updt[(size_t)i * NT + j][cnt - 1], false);
+    }
+  }
+  succ_ptr.assign(n + 1, 0);
+  succ_mid.assign(n, 0);
+  succ.clear();
+  for (int q = 0; q < n; ++q) {
+    succ.insert(succ.end(), early[q].begin(), early[q].end());
+    succ_mid[q] = (int32_t)succ.size();
+    succ.insert(succ.end(), late[q].begin(), late[q].end());
+    succ_ptr[q + 1] = (int32_t)succ.size();
+  }
+}
+
 void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int64_t *vptr,
                             const int32_t *handle, const double *phi, const double *phi_aff,
                             const double aff_origin[3]) {
@@ -589,6 +651,42 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
     }
   }
   c.n_dag = (int64_t)dag.size() / 4;
+  // CTA 0 of k_chol_dataflow runs the fused diagonal chain (type 4) in order; every other task
+  // is handed out through one of two ready queues (served by disjoint CTA sets) as soon as its
+  // inputs exist
+  std::vector<int32_t> crit, succ_ptr, succ_mid, succ, ndep;
+  std::vector<uint8_t> cls(c.n_dag, 0);
+  dataflow_graph(dag, NT, succ_ptr, succ_mid, succ, ndep);
+  c.n_pool = 0;
+  int hi_dj = 2;   // measured best at C4 (2..4)
+  {
+    const char *e = std::getenv("MSIM_DF_HIDJ");
+    if (e) hi_dj = std::max(1, std::atoi(e));
+  }
+  for (int64_t q = 0; q < c.n_dag; ++q) {
+    const int ty = dag[4 * q], i = dag[4 * q + 1], j = dag[4 * q + 2] & 0xffff, k = dag[4 * q + 2] >> 16;
+    // high: diagonal factors, panel tiles, and the updates of tiles that become panel tiles
+    // within hi_dj steps: each band row is a chain P(i,k) -> U(i,k+1,k) -> P(i,k+1) -> ... fed by
+    // the update chains of its tiles, which must not queue behind the bulk updates
+    cls[q] = ty == 4 ? 2 : (ty == 0 || ty == 1 || j <= k + hi_dj) ? 1 : 0;
+    if (ty == 4) crit.push_back((int32_t)q);
+    else c.n_pool++;
+  }
+  {
+    const char *e = std::getenv("MSIM_DF_HI");   // CTAs serving the high-priority queue
+    c.df_hi_ctas = e ? std::max(1, std::atoi(e)) : 32;   // measured best at C4 (24..56)
+  }
+  c.n_crit = (int64_t)crit.size();
+  // queue q (0: low, 1: high) at offset q * (n_pool + 2): head, tail, entries (-1: not yet pushed)
+  std::vector<int32_t> queue0((size_t)2 * (c.n_pool + 2) + 1, -1);   // + finished-task count
+  queue0.back() = 0;
+  for (int qq = 0; qq < 2; ++qq) {
+    int32_t *Q = queue0.data() + (size_t)qq * (c.n_pool + 2);
+    Q[0] = Q[1] = 0;
+    for (int64_t q = 0; q < c.n_dag; ++q)
+      if (cls[q] == qq && !ndep[q]) Q[2 + Q[1]++] = (int32_t)q;
+  }
+  if (crit.empty()) crit.push_back(0);
 
   cudaStream_t s = c.stream;
   c.origins.upload(origins, 3 * (size_t)m, s);
@@ -654,11 +752,20 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   c.chol_panel_ptr.upload(panel_ptr, s);
   c.sym_tiles.upload(sym_tiles, s);
   c.chol_dag.upload(dag, s);
+  c.chol_crit.upload(crit, s);
+  c.chol_cls.upload(cls, s);
+  c.chol_succ_ptr.upload(succ_ptr, s);
+  c.chol_succ_mid.upload(succ_mid, s);
+  c.chol_succ.upload(succ.empty() ? std::vector<int32_t>{0} : succ, s);
+  c.chol_ndep0.upload(ndep, s);
+  c.chol_ndep.alloc(ndep.size());
+  c.chol_queue0.upload(queue0, s);
+  c.chol_queue.alloc(queue0.size());
   {
     const char *e = std::getenv("MSIM_CHOL_DATAFLOW");   // 0: per-step launches (diagnostics)
     c.chol_dataflow = !(e && e[0] == '0');
   }
-  c.df_flags.alloc((size_t)2 * NT * NT + NT + 1);   // + the task dispenser
+  c.df_flags.alloc((size_t)2 * NT * NT + NT + 1);
   c.Uinv.alloc((size_t)NT * T * T);
   {
     int nsm = 0;
