@@ -135,19 +135,32 @@ __device__ __forceinline__ void galerkin_row(const GalParams &G, int i, int part
 #pragma unroll
         for (int k = 0; k < 4; ++k) a[r][k] = 0.0;
       const int e1 = __ldg(&o[q + 1]);
-      for (int eb = __ldg(&o[q]); eb < e1; eb += 32) {
+      // the list entries of batch b+1 (index, then the gathered w_uj) are loaded while batch b
+      // is multiplied: two dependent global round trips per batch otherwise stall the warp
+      uint32_t en_n = 0;
+      double2 w01_n = make_double2(0.0, 0.0), w23_n = w01_n;
+      int eb = __ldg(&o[q]);
+      if (eb + lane < e1) {
+        en_n = __ldg(&gl_ent[eb + lane]);
+        const size_t p = en_n >> 7;
+        w01_n = __ldg(reinterpret_cast<const double2 *>(W + 4 * p));
+        w23_n = __ldg(reinterpret_cast<const double2 *>(W + 4 * p + 2));
+      }
+      for (; eb < e1; eb += 32) {
         const int n = min(32, e1 - eb);
         __syncwarp();
         if (lane < n) {
-          const uint32_t en = __ldg(&gl_ent[eb + lane]);
-          const size_t p = en >> 7;
-          const double2 w01 = __ldg(reinterpret_cast<const double2 *>(W + 4 * p));
-          const double2 w23 = __ldg(reinterpret_cast<const double2 *>(W + 4 * p + 2));
-          reinterpret_cast<double2 *>(myW)[2 * lane] = w01;
-          reinterpret_cast<double2 *>(myW)[2 * lane + 1] = w23;
-          myU[lane] = (int)(en & (kGalChunk - 1)) * 36;
+          reinterpret_cast<double2 *>(myW)[2 * lane] = w01_n;
+          reinterpret_cast<double2 *>(myW)[2 * lane + 1] = w23_n;
+          myU[lane] = (int)(en_n & (kGalChunk - 1)) * 36;
         }
         __syncwarp();
+        if (eb + 32 + lane < e1) {
+          en_n = __ldg(&gl_ent[eb + 32 + lane]);
+          const size_t p = en_n >> 7;
+          w01_n = __ldg(reinterpret_cast<const double2 *>(W + 4 * p));
+          w23_n = __ldg(reinterpret_cast<const double2 *>(W + 4 * p + 2));
+        }
         if (grp < 3) {
 #pragma unroll 2
           for (int k = grp; k < n; k += 3) {
