@@ -225,6 +225,67 @@ __device__ __forceinline__ void inv_rowblock(int pb, const double *A, double *Li
   asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nth) : "memory");
 }
 
+#ifndef MSIM_INV_MMA
+#define MSIM_INV_MMA 1
+#endif
+__device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// inv_rowblock with the two off-diagonal products on the FP64 tensor cores (mma.sync m8n8k4,
+// one 8 x 8 output tile per warp at a time):
+//   T = L_{pb, 0:o} Li_{0:o, 0:o}      (16 x o; Li lower triangular: k from the tile's column)
+//   Li_{pb, 0:o} = -Li_{pb,pb} T       (Li_{pb,pb} lower triangular: k up to the tile's row)
+// the diagonal block inverse (threads tt < 16) runs alongside the first product on the other
+// warps.  Measured on the chain: the scalar version's last row block took ~6 k cycles.
+__device__ __forceinline__ void inv_rowblock_mma(int pb, const double *A, double *Li, double *T,
+                                                 const double *invd, int tt, int nth, int bar_id) {
+  constexpr int TS = 49;   // T row stride (16 x 49 <= the 3 x 16 x 17 scratch)
+  const int o = 16 * pb, lane = tt & 31, gw = tt >> 5, nw = nth >> 5;
+  const int lr = lane >> 2, lk = lane & 3;
+  if (tt < 16) {
+    double x[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      double s = r == tt ? 1.0 : 0.0, s2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < r; q += 2) {
+        s = fma(-A[(o + r) * LD + o + q], x[q], s);
+        if (q + 1 < r) s2 = fma(-A[(o + r) * LD + o + q + 1], x[q + 1], s2);
+      }
+      x[r] = (s + s2) * invd[o + r];
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) Li[(o + r) * LD + o + tt] = x[r];
+  } else if (gw >= 1) {
+    for (int tile = gw - 1; tile < 4 * pb; tile += nw - 1) {
+      const int ri = tile & 1, cj = tile >> 1;
+      double c0 = 0.0, c1 = 0.0;
+      const double *ar = A + (o + 8 * ri + lr) * LD + lk;
+      const double *bc = Li + lk * LD + 8 * cj + lr;
+      for (int k0 = 8 * cj; k0 < o; k0 += 4) dmma884(c0, c1, ar[k0], bc[k0 * LD]);
+      T[(8 * ri + lr) * TS + 8 * cj + 2 * lk] = c0;
+      T[(8 * ri + lr) * TS + 8 * cj + 2 * lk + 1] = c1;
+    }
+  }
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nth) : "memory");
+  if (pb == 0) return;
+  for (int tile = gw; tile < 4 * pb; tile += nw) {
+    const int ri = tile & 1, cj = tile >> 1;
+    double c0 = 0.0, c1 = 0.0;
+    const double *ar = Li + (o + 8 * ri + lr) * LD + o + lk;
+    const double *bc = T + lk * TS + 8 * cj + lr;
+#pragma unroll
+    for (int k0 = 0; k0 < 16; k0 += 4)
+      if (k0 < 8 * ri + 8) dmma884(c0, c1, ar[k0], bc[k0 * TS]);
+    Li[(o + 8 * ri + lr) * LD + 8 * cj + 2 * lk] = -c0;
+    Li[(o + 8 * ri + lr) * LD + 8 * cj + 2 * lk + 1] = -c1;
+  }
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nth) : "memory");
+}
+
 __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, double *__restrict__ U,
                                     int *__restrict__ flag, double *sm, bool preloaded) {
   double *A = sm;              // row-major [64][LD]: the factor
@@ -256,10 +317,17 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
   bool bad = false;
   for (int p = 0; p < 4; ++p) {
     const int j0 = 16 * p;
-    if (w != 0) {
-      // warps 1-7: row-block p-1 of the inverse (its columns of L are final) while warp 0
+    if (w == 4) {
+      // idle: warp 4 shares warp 0's scheduler and the panel is a serial chain (measured ~1%)
+    } else if (w != 0) {
+      // warps 1-3, 5-7: row-block p-1 of the inverse (its columns of L are final) while warp 0
       // factors panel p
-      if (p > 0) inv_rowblock(p - 1, A, Li, Tb, invd, t - 32, 224, 1);
+      const int tt = (w < 4 ? w - 1 : w - 2) * 32 + lane;
+#if MSIM_INV_MMA
+      if (p > 0) inv_rowblock_mma(p - 1, A, Li, reinterpret_cast<double *>(Tb), invd, tt, 192, 1);
+#else
+      if (p > 0) inv_rowblock(p - 1, A, Li, Tb, invd, tt, 192, 1);
+#endif
     } else {
       // panel rows j0 + lane and j0 + 32 + lane, columns j0 .. j0+15
       const int ra = j0 + lane, rb = j0 + 32 + lane;
@@ -332,6 +400,7 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
         if (va && ra >= j0 + c) A[ra * LD + j0 + c] = a[c];
         if (vb) A[rb * LD + j0 + c] = b[c];
       }
+      DIAG_TS(10 + p);   // warp 0's panel done (before waiting for the inverse warps)
     }
     __syncthreads();
     DIAG_TS(1 + 2 * p);
@@ -360,7 +429,11 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
   }
   if (w == 0 && lane == 0 && bad && flag) *flag = 1;
   // last row-block of the inverse (the others were formed during the panels)
+#if MSIM_INV_MMA
+  inv_rowblock_mma(3, A, Li, reinterpret_cast<double *>(Tb), invd, t, 256, 1);
+#else
   inv_rowblock(3, A, Li, Tb, invd, t, 256, 1);
+#endif
   DIAG_TS(9);
   // store L_kk (lower, column-major) and U_kk = Li^T (row-major: U[r][c] at r*64 + c = Li[c][r])
   double *Uk = U + (size_t)k * TB * TB;
