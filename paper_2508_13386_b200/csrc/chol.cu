@@ -617,45 +617,60 @@ __global__ void __launch_bounds__(256) k_chol_fwd(int NT, const int32_t *__restr
   }
 }
 
-// backward: x_k = U_kk (y_k - sum_{i in panel(k)} L_ik^T x_i), tiles owned round-robin from the end
+// backward: x_k = U_kk (y_k - sum_{i in panel(k)} L_ik^T x_i), tiles owned round-robin from the end.
+// Thread (r, q) reads row r, columns 16q..16q+15 of each L_ik (consecutive lanes: consecutive
+// rows of a column-major tile -> coalesced) and keeps 16 column partial sums across all i; the
+// rows are reduced once per tile.  (Thread-per-column reads were uncoalesced: 3.3 us per sweep
+// step against 1.15 for the forward sweep, which has the coalesced pattern.)
 __global__ void __launch_bounds__(256) k_chol_bwd(int NT, const int32_t *__restrict__ pan_ptr,
                                                   const int32_t *__restrict__ panel, int nSp,
                                                   const double *__restrict__ L, const double *__restrict__ U,
                                                   const double *__restrict__ y, double *__restrict__ x) {
   __shared__ double xi[TB];
   __shared__ double part[4][TB];
-  const int t = threadIdx.x, cidx = t >> 2, q = t & 3;
+  __shared__ double red[TB][TB + 1];
+  const int t = threadIdx.x, r = t & 63, q = t >> 6;
   for (int s = blockIdx.x; s < NT; s += gridDim.x) {
     const int k = NT - 1 - s;
-    // x_k[r] = sum_c U[r][c] v[c] (U row-major: U[r][c] at r*64 + c); thread (r = cidx, q):
-    // prefetched with y_k (y is complete: the forward launch finished)
-    const double *Uk = U + (size_t)k * TB * TB + (size_t)cidx * TB;
+    // x_k[r] = sum_c U[r][c] v[c] (U row-major: U[r][c] at r*64 + c): prefetched with y_k
+    const double *Uk = U + (size_t)k * TB * TB + (size_t)r * TB + q * 16;
     double uv[16];
 #pragma unroll
-    for (int c = 0; c < 16; ++c) uv[c] = __ldg(&Uk[q * 16 + c]);
+    for (int c = 0; c < 16; ++c) uv[c] = __ldg(&Uk[c]);
     const double yk = t < TB ? y[k * TB + t] : 0.0;
-    double acc = 0.0;   // thread (c = cidx, q): rows 16q..16q+15 of column c
+    double acc[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) acc[c] = 0.0;
     // largest i first (ready first in the backward sweep); operand prefetched before the wait
     for (int p = pan_ptr[k + 1] - 1; p >= pan_ptr[k]; --p) {
       const int i = panel[p];
-      const double *Lik = L + tile_off(i, k, nSp) + (size_t)cidx * nSp + q * 16;
+      const double *Lik = L + tile_off(i, k, nSp) + (size_t)(q * 16) * nSp + r;
       double lv[16];
 #pragma unroll
-      for (int rr = 0; rr < 16; ++rr) lv[rr] = Lik[rr];
+      for (int c = 0; c < 16; ++c) lv[c] = Lik[(size_t)c * nSp];
       if (t < TB) xi[t] = poll_ready(&x[i * TB + t]);
       __syncthreads();
+      const double xr = xi[r];
 #pragma unroll
-      for (int rr = 0; rr < 16; ++rr) acc = fma(lv[rr], xi[q * 16 + rr], acc);
+      for (int c = 0; c < 16; ++c) acc[c] = fma(lv[c], xr, acc[c]);
       __syncthreads();
     }
-    part[q][cidx] = acc;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) red[r][q * 16 + c] = acc[c];
+    __syncthreads();
+    {   // column sums: thread (column r, row quarter q)
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int rr = 0; rr < 16; ++rr) s4[rr & 3] += red[q * 16 + rr][r];
+      part[q][r] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    }
     __syncthreads();
     if (t < TB) xi[t] = yk - ((part[0][t] + part[1][t]) + (part[2][t] + part[3][t]));
     __syncthreads();
     double sacc = 0.0;
 #pragma unroll
     for (int c = 0; c < 16; ++c) sacc = fma(uv[c], xi[q * 16 + c], sacc);
-    part[q][cidx] = sacc;
+    part[q][r] = sacc;
     __syncthreads();
     if (t < TB) __stcg(&x[k * TB + t], (part[0][t] + part[1][t]) + (part[2][t] + part[3][t]));
     __syncthreads();
