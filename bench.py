@@ -287,10 +287,11 @@ def run_ours(args):
     ms_max = float(ms_t.item())
     newton_all, pcg_all = float(cnt[0].item()), float(cnt[1].item())
 
-    # ---- end-to-end through the C-ABI with host buffers (H2D state, timestep, D2H state)
-    x_h, v_h = ctx.get_state()
-    x_h = np.ascontiguousarray(x_h)
-    v_h = np.ascontiguousarray(v_h)
+    # ---- end-to-end through the C-ABI with host buffers (H2D state, timestep, D2H state); the
+    # host state lives in pinned memory (torch pin_memory, viewed as numpy)
+    x_h = torch.zeros((s.n_verts, 3), dtype=torch.float64, pin_memory=True).numpy()
+    v_h = torch.zeros((s.n_verts, 3), dtype=torch.float64, pin_memory=True).numpy()
+    ctx.get_state(out=(x_h, v_h))
     e_newton = 0
     barrier()
     t0 = time.perf_counter()
@@ -298,12 +299,16 @@ def run_ours(args):
         ctx.set_state(x_h, v_h)
         st = ctx.timestep()
         e_newton += st.newton_iters
-        x_h, v_h = ctx.get_state()
+        if partitioned:
+            x_h.fill(0.0)
+            v_h.fill(0.0)
+        ctx.get_state(out=(x_h, v_h))
         if partitioned:   # every rank returns its owned vertices: assemble the global state
             xv = torch.from_numpy(np.concatenate([x_h.ravel(), v_h.ravel()])).cuda()
             torch.distributed.all_reduce(xv)
             xv = xv.cpu().numpy()
-            x_h, v_h = xv[:x_h.size].reshape(x_h.shape), xv[x_h.size:].reshape(v_h.shape)
+            x_h[...] = xv[:x_h.size].reshape(x_h.shape)
+            v_h[...] = xv[x_h.size:].reshape(v_h.shape)
     barrier()
     e_sec = time.perf_counter() - t0
     e_t = torch.tensor([e_sec], device="cuda")

@@ -229,10 +229,18 @@ class Context:
         v = None if v is None else _f64(v, (-1, 3))
         self._chk(lib.ms_set_state(self.h, _d(x), _d(v)))
 
-    def get_state(self):
-        """Global-sized arrays; with world > 1 only this rank's owned vertices are filled (rest 0)."""
-        x = np.zeros((self.n_verts, 3))
-        v = np.zeros((self.n_verts, 3))
+    def get_state(self, out=None):
+        """Global-sized arrays; with world > 1 only this rank's owned vertices are filled (rest 0).
+        out = (x, v): C-contiguous float64 (n_verts, 3) arrays to fill (e.g. views of pinned host
+        memory, so the device->host copies run at full PCIe rate)."""
+        if out is None:
+            x = np.zeros((self.n_verts, 3))
+            v = np.zeros((self.n_verts, 3))
+        else:
+            x, v = out
+            for a in (x, v):
+                if a.dtype != np.float64 or a.shape != (self.n_verts, 3) or not a.flags.c_contiguous:
+                    raise ValueError("get_state(out=...): C-contiguous float64 (n_verts, 3) arrays expected")
         self._chk(lib.ms_get_state(self.h, _d(x), _d(v)))
         return x, v
 

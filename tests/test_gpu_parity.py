@@ -271,3 +271,26 @@ def test_invalid_mesh_rejected(msim):
     assert e.value.code == -1
     with pytest.raises(msim.MsimError):
         ctx.upload_mesh(s.X, s.tets, s.E, np.full(s.n_tets, 0.5), s.rho)
+
+
+def test_state_roundtrip_pinned(msim):
+    """set_state / get_state(out=...) with pinned host buffers (the bench's e2e leg) move the
+    state bit-exactly and agree with the allocating get_state."""
+    import torch
+    s, b = scene_and_basis("drop_tiny")
+    ctx = msim.context_from_scene(s, b)
+    x = perturbed(s, 0.01, 3)
+    v = np.random.default_rng(4).standard_normal(x.shape)
+    xp = torch.zeros(x.shape, dtype=torch.float64, pin_memory=True).numpy()
+    vp = torch.zeros(x.shape, dtype=torch.float64, pin_memory=True).numpy()
+    xp[...] = x
+    vp[...] = v
+    ctx.set_state(xp, vp)
+    xo = torch.zeros(x.shape, dtype=torch.float64, pin_memory=True).numpy()
+    vo = torch.zeros(x.shape, dtype=torch.float64, pin_memory=True).numpy()
+    ctx.get_state(out=(xo, vo))
+    assert np.array_equal(xo, x) and np.array_equal(vo, v)
+    xa, va = ctx.get_state()
+    assert np.array_equal(xa, xo) and np.array_equal(va, vo)
+    with pytest.raises(ValueError):
+        ctx.get_state(out=(xo[:-1], vo))
