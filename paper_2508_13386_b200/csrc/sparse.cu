@@ -324,7 +324,23 @@ __global__ void __launch_bounds__(256) k_pcg_update(int n3, int n3_own, int dist
                                                     unsigned int *counter, double *__restrict__ scal) {
   const double alpha = scal[SC_ALPHA];
   double acc[1] = {0.0};
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n3; i += gridDim.x * blockDim.x) {
+  // pairs of entries through 16-byte accesses (cudaMalloc'd vectors: 16-byte aligned); an odd
+  // last entry is taken by the first thread
+  const int n2 = n3 >> 1;
+  for (int i2 = blockIdx.x * blockDim.x + threadIdx.x; i2 < n2; i2 += gridDim.x * blockDim.x) {
+    const double2 pv = reinterpret_cast<const double2 *>(p)[i2], qv = reinterpret_cast<const double2 *>(q)[i2];
+    const double2 xv = reinterpret_cast<const double2 *>(x)[i2], rv = reinterpret_cast<const double2 *>(r)[i2];
+    const double2 dv = reinterpret_cast<const double2 *>(dinv)[i2];
+    const double r0 = fma(-alpha, qv.x, rv.x), r1 = fma(-alpha, qv.y, rv.y);
+    const double z0 = dv.x * r0, z1 = dv.y * r1;
+    reinterpret_cast<double2 *>(x)[i2] = make_double2(fma(alpha, pv.x, xv.x), fma(alpha, pv.y, xv.y));
+    reinterpret_cast<double2 *>(r)[i2] = make_double2(r0, r1);
+    reinterpret_cast<double2 *>(z)[i2] = make_double2(z0, z1);
+    if (2 * i2 < n3_own) acc[0] = fma(r0, z0, acc[0]);
+    if (2 * i2 + 1 < n3_own) acc[0] = fma(r1, z1, acc[0]);
+  }
+  if ((n3 & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int i = n3 - 1;
     x[i] = fma(alpha, p[i], x[i]);
     const double ri = fma(-alpha, q[i], r[i]);
     const double zi = dinv[i] * ri;
@@ -367,7 +383,7 @@ static void enqueue_pcg_iters(Ctx &c, double *sol, int iters) {
       dist_sum(c, c.scal + SC_PQ, 1);
       k_pcg_scalars<<<1, 1, 0, c.stream>>>(c.scal, 0);
     }
-    k_pcg_update<<<grid_vec(n3), bs, 0, c.stream>>>(n3, n3o, dist, c.dinv, c.p, c.q, sol, c.r, c.z, c.partial,
+    k_pcg_update<<<grid_vec((n3 + 1) / 2), bs, 0, c.stream>>>(n3, n3o, dist, c.dinv, c.p, c.q, sol, c.r, c.z, c.partial,
                                                     c.counters + 4, c.scal);
     if (dist) {
       dist_sum(c, c.scal + SC_RZ_OLD, 1);
