@@ -286,7 +286,8 @@ __device__ __forceinline__ void df_signal2(int *p1, int v1, int *p2, int v2) {
 }
 
 struct DfParams {
-  int NT, nSp, ncrit, npool, nhi_cta, qstride;
+  int NT, nSp, ncrit, npool, nhi_cta, qstride, per_sm;
+  int *chain_sm;               // SM of CTA 0 + 1 (0: not yet known)
   const int4 *tasks;           // (type, i, j | k << 16, count) per task
   double *L, *U;               // tiled factor / inverse diagonal tiles
   int *upd, *dfl, *pfl, *flag; // progress flags (NT*NT, NT, NT*NT) and the pivot flag
@@ -352,6 +353,24 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
   double *__restrict__ L = P.L;
   double *__restrict__ U = P.U;
   int *upd = P.upd, *dfl = P.dfl, *pfl = P.pfl, *flag = P.flag;
+  if (P.per_sm > 1) {
+    // several CTAs per SM: the chain CTA keeps its SM to itself (a queue CTA that lands on the
+    // same SM leaves at once; measured: sharing it cost more than the extra queue CTAs gained)
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (blockIdx.x == 0) {
+      if (t == 0) atomicExch(P.chain_sm, (int)smid + 1);
+    } else if (blockIdx.x >= 2) {
+      if (t == 0) {
+        const volatile int *f = P.chain_sm;
+        int v;
+        while ((v = *f) == 0) __nanosleep(32);
+        s_id = v - 1 == (int)smid;
+      }
+      __syncthreads();
+      if (s_id) return;
+    }
+  }
   if (blockIdx.x == 1) {
     // release helper: follows the chain and hands the successors of each chain task to the
     // queues as its flags appear, so that CTA 0 never spends the atomics' round trips (measured
@@ -699,17 +718,24 @@ static bool step_updates_diag(const Ctx &c, int k) {   // is tile (k+1, k+1) amo
 }
 
 #ifndef MSIM_DF_PER_SM
-#define MSIM_DF_PER_SM 1   // the critical-path CTA gets a whole SM (measured: 3.68 -> 3.25 ms at C4)
+#define MSIM_DF_PER_SM 2   // two queue CTAs per SM, the chain CTA alone on its SM (measured at C4:
+                           // 2.82 -> 2.50 ms; sharing the chain's SM made two per SM slower)
 #endif
 constexpr int kDfCtasPerSm = MSIM_DF_PER_SM;   // CTAs per SM of the dataflow factorisation
 
-static int dataflow_grid(const Ctx &c) {
+static int dataflow_per_sm() {
   static int per_sm = -1;
   if (per_sm < 0) {
     MS_CUDA(cudaFuncSetAttribute(k_chol_dataflow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem));
     MS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chol_dataflow, 256, kUpdSmem));
-    per_sm = std::max(std::min(per_sm, kDfCtasPerSm), 1);
+    const char *e = std::getenv("MSIM_DF_PER_SM");
+    per_sm = std::max(std::min(per_sm, e ? std::atoi(e) : kDfCtasPerSm), 1);
   }
+  return per_sm;
+}
+
+static int dataflow_grid(const Ctx &c) {
+  const int per_sm = dataflow_per_sm();
   // the chain CTA, the release helper, at least one CTA per queue
   return (int)std::max<int64_t>(4, (int64_t)per_sm * c.coop_grid);
 }
@@ -752,6 +778,8 @@ void enqueue_chol_factor(Ctx &c) {
     prm.ndep = c.chol_ndep;
     prm.queue = c.chol_queue;
     prm.done = c.chol_queue + 2 * prm.qstride;
+    prm.per_sm = dataflow_per_sm();
+    prm.chain_sm = c.df_flags + (size_t)2 * NT * NT + NT;   // zeroed with the flags
     void *args[] = {&prm};
     MS_CUDA(cudaLaunchCooperativeKernel((const void *)k_chol_dataflow, dim3(dataflow_grid(c)), dim3(256), args,
                                         kUpdSmem, c.stream));

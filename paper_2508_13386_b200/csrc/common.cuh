@@ -194,7 +194,7 @@ struct Ctx {
   DBuf<int32_t> chol_ndep0, chol_ndep;                     // inputs per task: pristine / live
   DBuf<int32_t> chol_queue0, chol_queue;                   // two ready queues: pristine / live
   int64_t n_crit = 0, n_pool = 0;
-  int df_hi_ctas = 32;   // CTAs serving the high-priority queue
+  int df_hi_ctas = 64;   // CTAs serving the high-priority queue
   int64_t n_dag = 0;
   DBuf<int> df_flags;               // upd[NT*NT], pfl[NT*NT], dfl[NT]
   bool chol_dataflow = true;

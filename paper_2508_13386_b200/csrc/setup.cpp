@@ -674,7 +674,7 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   }
   {
     const char *e = std::getenv("MSIM_DF_HI");   // CTAs serving the high-priority queue
-    c.df_hi_ctas = e ? std::max(1, std::atoi(e)) : 32;   // measured best at C4 (24..56)
+    c.df_hi_ctas = e ? std::max(1, std::atoi(e)) : 64;   // measured at C4 (48..80 at 2 CTAs per SM)
   }
   c.n_crit = (int64_t)crit.size();
   // queue q (0: low, 1: high) at offset q * (n_pool + 2): head, tail, entries (-1: not yet pushed)
