@@ -84,6 +84,9 @@ __device__ __forceinline__ void tile_rc(int idx, int &r, int &c) {
 #endif
 }
 
+// LI: the second operand is a row-major inverse diagonal tile Li [64][LD] left in shared memory
+// by diag_factor (S2[kk*64 + c] = U[kk][c] = Li[c][kk]) instead of a staged k-major tile
+template <bool LI = false>
 __device__ __forceinline__ void tile_gemm(const double *S1, const double *S2, double (&acc)[16]) {
 #if MSIM_TILE_MMA
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -96,7 +99,7 @@ __device__ __forceinline__ void tile_gemm(const double *S1, const double *S2, do
     const double a0 = s1[r0], a1 = s1[r0 + 8];
     double b[4];
 #pragma unroll
-    for (int bj = 0; bj < 4; ++bj) b[bj] = s2[c0 + 8 * bj];
+    for (int bj = 0; bj < 4; ++bj) b[bj] = LI ? S2[(c0 + 8 * bj) * LD + k0 + kl] : s2[c0 + 8 * bj];
 #pragma unroll
     for (int bi = 0; bi < 2; ++bi)
 #pragma unroll
@@ -440,14 +443,17 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
         tile_rc(q, r, c);
         old[q] = __ldcg(&L[oii + (size_t)c * nSp + r]);
       }
-      if (k != my_d) df_wait(&dfl[k], 1);   // D(k) is this CTA's previous task (usually)
+      // D(k) is usually this CTA's previous task: its inverse is still in shared memory
+      const bool own_d = k == my_d;
+      if (!own_d) df_wait(&dfl[k], 1);
       DF_STAMP(i, 1);
       DF_TSTAMP(id, 1);
-      stage_colmajor(SU, U + (size_t)k * TB * TB, TB);
+      if (!own_d) stage_colmajor(SU, U + (size_t)k * TB * TB, TB);
       cp_async_commit_wait();
       __syncthreads();
       double acc[16];
-      tile_gemm(SA, SU, acc);
+      if (own_d) tile_gemm<true>(SA, sm + TB * LD, acc);
+      else tile_gemm(SA, SU, acc);
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         int r, c;
