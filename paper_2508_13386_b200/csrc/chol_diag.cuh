@@ -428,6 +428,15 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
     DIAG_TS(2 + 2 * p);
   }
   if (w == 0 && lane == 0 && bad && flag) *flag = 1;
+  // store L_kk (lower, column-major) and the final rows 0..47 of Li as U_kk = Li^T (row-major:
+  // U[c][r] = Li[r][c]) now: the stores drain while the last row block of the inverse is formed
+  double *Uk = U + (size_t)k * TB * TB;
+#pragma unroll 4
+  for (int it = 0; it < 16; ++it) {
+    const int e = t + it * 256, r = e & 63, c = e >> 6;
+    if (r >= c) __stcg(&L[okk + (size_t)c * nSp + r], A[r * LD + c]);
+    if (r < 48) __stcg(&Uk[(size_t)c * TB + r], Li[r * LD + c]);
+  }
   // last row-block of the inverse (the others were formed during the panels)
 #if MSIM_INV_MMA
   inv_rowblock_mma(3, A, Li, reinterpret_cast<double *>(Tb), invd, t, 256, 1);
@@ -435,13 +444,10 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
   inv_rowblock(3, A, Li, Tb, invd, t, 256, 1);
 #endif
   DIAG_TS(9);
-  // store L_kk (lower, column-major) and U_kk = Li^T (row-major: U[r][c] at r*64 + c = Li[c][r])
-  double *Uk = U + (size_t)k * TB * TB;
-#pragma unroll 4
-  for (int it = 0; it < 16; ++it) {
-    const int e = t + it * 256, r = e & 63, c = e >> 6;
-    if (r >= c) __stcg(&L[okk + (size_t)c * nSp + r], A[r * LD + c]);
-    __stcg(&Uk[(size_t)c * TB + r], Li[r * LD + c]);   // U[c][r] = Li[r][c]
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {   // rows 48..63 of Li: 16 x 64 entries
+    const int e = t + it * 256, r = 48 + (e & 15), c = e >> 4;
+    __stcg(&Uk[(size_t)c * TB + r], Li[r * LD + c]);
   }
 }
 
