@@ -88,10 +88,12 @@ def algorithmic_bytes(sizes, n_cg):
     return {"spmv": spmv, "pcg_iter": pcg_iter, "assembly": assembly}
 
 
-def load_fp64_peak():
+def load_fp64_peak(kind="dmma"):
+    """FP64 peak (TFLOP/s) of the FP64 tensor cores (kind "dmma": the factorisation's tile GEMMs
+    are mma.sync m8n8k4 f64) or of the scalar FMA pipe ("dfma": the Galerkin product)."""
     p = os.path.join(ROOT, "profiles", "fp64_peaks.json")
     if os.path.exists(p):
-        return json.load(open(p))["dmma_tflops"], "measured (profiles/fp64_peaks.json)"
+        return json.load(open(p))[kind + "_tflops"], f"measured {kind.upper()} (profiles/fp64_peaks.json)"
     return 37.2, "nominal: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz"
 
 
@@ -127,10 +129,12 @@ def phase_rooflines(phases, ab, ci, n_cg, hbm, peak_src, fp64_peak, fp64_src, tr
         put("assembly", "hbm", ab["assembly"], "GB/s", hbm, peak_src, "k_assemble", ms / n, 1, newton)
     ms, n = phases["coarse_factor"]
     if n:
-        put("coarse_factor", "alu", ci["flops"], "TFLOP/s", fp64_peak, fp64_src, "k_chol_dataflow", ms / n, 1, newton)
+        put("coarse_factor", "tensor", ci["flops"], "TFLOP/s", fp64_peak, fp64_src, "k_chol_dataflow", ms / n, 1,
+            newton)
     ms, n = phases["coarse_S"]
     if n and ci.get("galerkin_flops"):
-        put("coarse_S", "alu", ci["galerkin_flops"], "TFLOP/s", fp64_peak, fp64_src, "k_galerkin_fused", ms / n, 1,
+        dfma, dfma_src = load_fp64_peak("dfma")
+        put("coarse_S", "alu", ci["galerkin_flops"], "TFLOP/s", dfma, dfma_src, "k_galerkin_fused", ms / n, 1,
             newton)
     return out
 
