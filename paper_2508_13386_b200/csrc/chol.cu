@@ -433,7 +433,6 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
       const size_t oik = tile_off(i, k, nSp), oii = tile_off(i, i, nSp);
       df_wait2(&upd[i * NT + k], cnt & 0xffff, &upd[i * NT + i], cnt >> 16);
       DF_STAMP(i, 6);
-      DF_STAMP(i, 7);
       stage_colmajor(SA, L + oik, nSp);
       asm volatile("cp.async.commit_group;\n" ::);
       double old[16];
@@ -482,6 +481,7 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
       }
       DF_STAMP(i, 4);
       diag_factor(i, nSp, L, U, flag, sm, true);
+      DF_STAMP(i, 7);   // D computed and stored; the signal (barrier, fence, flags) follows
       df_signal2(&dfl[i], 1, &upd[i * NT + i], (cnt >> 16) + 1);
       my_d = i;
       DF_STAMP(i, 5);

@@ -14,6 +14,9 @@
 #ifndef MSIM_DIAG_VARIANT
 #define MSIM_DIAG_VARIANT 1
 #endif
+#ifndef MSIM_STORE_LKK
+#define MSIM_STORE_LKK 0
+#endif
 
 // ---------------------------------------------------------------- variant 0: recursive
 //   F11 (warp 0)              L11 = chol(A11)                    lane r owns row r
@@ -428,13 +431,17 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
     DIAG_TS(2 + 2 * p);
   }
   if (w == 0 && lane == 0 && bad && flag) *flag = 1;
-  // store L_kk (lower, column-major) and the final rows 0..47 of Li as U_kk = Li^T (row-major:
-  // U[c][r] = Li[r][c]) now: the stores drain while the last row block of the inverse is formed
+  // store the final rows 0..47 of Li as U_kk = Li^T (row-major: U[c][r] = Li[r][c]) now: the
+  // stores drain while the last row block of the inverse is formed.  L_kk itself is not stored
+  // (MSIM_STORE_LKK=1 restores it): every consumer of the diagonal tile -- the panel tasks and
+  // both triangular sweeps -- uses U_kk.
   double *Uk = U + (size_t)k * TB * TB;
 #pragma unroll 4
   for (int it = 0; it < 16; ++it) {
     const int e = t + it * 256, r = e & 63, c = e >> 6;
+#if MSIM_STORE_LKK
     if (r >= c) __stcg(&L[okk + (size_t)c * nSp + r], A[r * LD + c]);
+#endif
     if (r < 48) __stcg(&Uk[(size_t)c * TB + r], Li[r * LD + c]);
   }
   // last row-block of the inverse (the others were formed during the panels)

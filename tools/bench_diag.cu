@@ -8,6 +8,7 @@
 #include <vector>
 #include <cuda_runtime.h>
 #include "fastmath.cuh"
+#define MSIM_STORE_LKK 1   // the check below reads L_kk back
 
 namespace msim {
 constexpr int TB = 64;
