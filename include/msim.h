@@ -150,7 +150,9 @@ const char *ms_last_error(ms_ctx *ctx);
 ms_status ms_upload_mesh(ms_ctx *ctx, int64_t n_verts, const double *rest_xyz, int64_t n_tets,
                          const int32_t *tets, const double *E, const double *nu,
                          const double *rho);
-/* Dirichlet vertices, pinned at their rest position (Q13: identity rows, g = 0). */
+/* Dirichlet vertices, pinned at their rest position (Q13: identity rows, g = 0).  Must precede
+ * ms_basis_upload (MS_ERR_STATE afterwards): the basis is built for one Dirichlet set and has to
+ * vanish at its vertices, which ms_basis_upload checks (MS_ERR_ARG otherwise). */
 ms_status ms_set_dirichlet(ms_ctx *ctx, int64_t n, const int32_t *verts);
 /* Ground-plane IPC barrier b(d) = -(d-dhat)^2 ln(d/dhat), d = normal.x - offset
  * (P:177); kappa is the barrier stiffness.  kappa <= 0 disables contact. */
@@ -181,7 +183,9 @@ ms_status ms_get_step_state(ms_ctx *ctx, double *x_t, double *xhat, double *x);
 
 /* ---------------------------------------------------------------- the hot path */
 /* One implicit-Euler timestep: begin_step, Newton iterations until converged / cap /
- * line-search failure, end_step (Alg. 1; §3.9). */
+ * line-search failure, end_step (Alg. 1; §3.9).  On a hard error inside the
+ * Newton loop (e.g. MS_ERR_INFEASIBLE, MS_ERR_NOT_SPD) the step is abandoned: x is reset to x^t,
+ * v is unchanged and no step is in progress. */
 ms_status ms_timestep(ms_ctx *ctx, ms_step_stats *out);
 /* xhat = x^t + h v^t + h^2 g, x = x^t (R8). */
 ms_status ms_begin_step(ms_ctx *ctx);

@@ -12,9 +12,13 @@ Test infrastructure only (see oracle/__init__.py).
 """
 from __future__ import annotations
 
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 import scipy.linalg as sla
 import scipy.sparse as sp
+
+from . import fem
 
 
 def lbs_matrix(X, vptr, handle, phi, origins, n_handles):
@@ -48,9 +52,19 @@ def affine_matrix(X, basis):
                       np.asarray(basis.affine_origin, dtype=np.float64)[None, :], 1)
 
 
-def galerkin(U, H):
-    """Dense U^T H U (the 'subspace sandwich matrix', L456)."""
-    return np.asarray((U.T @ (H.tocsr() @ U)).todense())
+def galerkin(U, H, n_blocks=32):
+    """Dense U^T H U (the 'subspace sandwich matrix', L456), formed column block by column
+    block, S[:, J] = U^T (H U[:, J]), on a thread pool (the blocks are independent)."""
+    H = H.tocsr()
+    Ut = U.T.tocsr()
+    Uc = U.tocsc()
+    n = U.shape[1]
+    cuts = np.linspace(0, n, min(n_blocks, n) + 1).astype(int)
+
+    def block(k):
+        return (Ut @ (H @ Uc[:, cuts[k]:cuts[k + 1]])).toarray()
+    with ThreadPoolExecutor(fem.n_threads()) as ex:
+        return np.ascontiguousarray(np.concatenate(list(ex.map(block, range(len(cuts) - 1))), axis=1))
 
 
 def cholesky(S):

@@ -11,6 +11,9 @@ Passages followed:
 """
 from __future__ import annotations
 
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 
 # D_ref maps vertex positions to edge vectors: Ds = X_e @ D_ref, X_e = [x0 x1 x2 x3] (3x4)
@@ -113,7 +116,7 @@ def element_gradient(x, tets, Bm, V, mu, lam):
     """Per-tet 12-vector g_e = V_e G_e^T vec P(F_e) (vertex-major, xyz inner)."""
     F = deformation_gradient(x, tets, Bm)
     G = shape_gradient_matrix(Bm)
-    return V[:, None] * np.einsum("eai,ea->ei", G, vec(first_piola(F, mu, lam)))
+    return V[:, None] * (np.swapaxes(G, -1, -2) @ vec(first_piola(F, mu, lam))[..., None])[..., 0]
 
 
 def element_hessian(x, tets, Bm, V, mu, lam):
@@ -121,20 +124,47 @@ def element_hessian(x, tets, Bm, V, mu, lam):
     F = deformation_gradient(x, tets, Bm)
     G = shape_gradient_matrix(Bm)
     A = d2psi_dF2(F, mu, lam)
-    return V[:, None, None] * np.einsum("eai,eab,ebj->eij", G, A, G)
+    return V[:, None, None] * (np.swapaxes(G, -1, -2) @ A @ G)
 
 
 def psd_project(H):
     """P+(H) = Q max(Lambda, 0) Q^T with H = Q Lambda Q^T (R2; LAPACK syevd via numpy.eigh)."""
     H = 0.5 * (H + np.swapaxes(H, -1, -2))
     w, Q = np.linalg.eigh(H)
-    return np.einsum("...ik,...k,...jk->...ij", Q, np.maximum(w, 0.0), Q)
+    return (Q * np.maximum(w, 0.0)[..., None, :]) @ np.swapaxes(Q, -1, -2)
 
 
-def element_hessian_psd(x, tets, Bm, V, mu, lam, chunk=131072):
-    """P+(H_e) for every tet, evaluated in chunks to bound memory."""
+def n_threads():
+    """Host threads for the element loops (chunks are independent; results do not depend on it)."""
+    return max(1, int(os.environ.get("ORACLE_THREADS", os.cpu_count() or 1)))
+
+
+def map_chunks(fn, n, chunk):
+    """Yields fn(slice) for each chunk of range(n) in chunk order, evaluated on a thread pool
+    (numpy's batched linear algebra releases the GIL) with a bounded number in flight."""
+    sl = [slice(s, min(s + chunk, n)) for s in range(0, n, chunk)]
+    nt = n_threads()
+    if nt == 1 or len(sl) <= 1:
+        for e in sl:
+            yield fn(e)
+        return
+    with ThreadPoolExecutor(nt) as ex:
+        pending = [ex.submit(fn, e) for e in sl[:2 * nt]]
+        nxt = len(pending)
+        while pending:
+            r = pending.pop(0).result()
+            if nxt < len(sl):
+                pending.append(ex.submit(fn, sl[nxt]))
+                nxt += 1
+            yield r
+
+
+def element_hessian_psd(x, tets, Bm, V, mu, lam, chunk=32768):
+    """P+(H_e) for every tet, evaluated in independent chunks to bound memory."""
     out = np.empty((len(tets), 12, 12))
-    for s in range(0, len(tets), chunk):
-        e = slice(s, s + chunk)
+
+    def work(e):
         out[e] = psd_project(element_hessian(x, tets[e], Bm[e], V[e], mu[e], lam[e]))
+    for _ in map_chunks(work, len(tets), chunk):
+        pass
     return out

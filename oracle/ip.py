@@ -168,7 +168,7 @@ def block_pattern(tets, n):
     return A.indptr.astype(np.int64), A.indices.astype(np.int64)
 
 
-def hessian(model, x, xhat, chunk=131072):
+def hessian(model, x, xhat, chunk=32768):
     """H = M + h^2 (sum_e P+(H_e) + kappa b''(d) n n^T), DBC rows/cols -> identity.
 
     Returned as scipy.sparse.bsr_matrix with 3x3 blocks: H_(i,j) = sum over tets e and
@@ -179,17 +179,21 @@ def hessian(model, x, xhat, chunk=131072):
     nnzb = len(indices)
     rows = np.repeat(np.arange(n), np.diff(indptr))
     key = rows * n + indices                   # sorted
-    blocks = np.zeros((nnzb, 3, 3))
-    for s in range(0, len(model.tets), chunk):
-        t = model.tets[s:s + chunk]
-        He = fem.element_hessian_psd(x, t, model.Bm[s:s + chunk], model.V[s:s + chunk],
-                                     model.mu[s:s + chunk], model.lam[s:s + chunk])
-        for a in range(4):
-            for b in range(4):
-                slot = np.searchsorted(key, t[:, a] * n + t[:, b])
-                sub = He[:, 3 * a:3 * a + 3, 3 * b:3 * b + 3].reshape(-1, 9)
-                for q in range(9):
-                    blocks[:, q // 3, q % 3] += np.bincount(slot, weights=sub[:, q], minlength=nnzb)
+    blocks = np.zeros((nnzb, 9))
+
+    def work(e):
+        t = model.tets[e]
+        He = fem.element_hessian_psd(x, t, model.Bm[e], model.V[e], model.mu[e], model.lam[e], chunk=len(t))
+        # the (a,b) 3x3 block of P+(H_e) goes to BSR slot (e[a], e[b])
+        slot = np.searchsorted(key, (t[:, :, None] * n + t[:, None, :]).ravel())      # (c*16,)
+        sub = He.reshape(-1, 4, 3, 4, 3).transpose(0, 1, 3, 2, 4).reshape(-1, 9)  # (c*16, 9)
+        return slot, sub
+
+    for slot, sub in fem.map_chunks(work, len(model.tets), chunk):     # summed in chunk order
+        lo, hi = int(slot.min()), int(slot.max()) + 1
+        for q in range(9):
+            blocks[lo:hi, q] += np.bincount(slot - lo, weights=sub[:, q], minlength=hi - lo)
+    blocks = blocks.reshape(nnzb, 3, 3)
     blocks *= h2
     diag = np.searchsorted(key, np.arange(n) * n + np.arange(n))
     blocks[diag] += model.mass[:, None, None] * np.eye(3)[None]

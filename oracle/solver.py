@@ -91,21 +91,26 @@ def det_poly(A, B):
 
 
 def smallest_positive_root(c):
-    """Smallest real root t > 0 of c0 + c1 t + c2 t^2 + c3 t^3 (inf if none), per element,
-    via numpy.roots (companion-matrix eigenvalues) of the leading-nonzero polynomial."""
-    c0, c1, c2, c3 = c
+    """Smallest real root t > 0 of c0 + c1 t + c2 t^2 + c3 t^3 (inf if none), per element:
+    the eigenvalues of the companion matrix of the leading-nonzero polynomial (what
+    numpy.roots computes), batched over the elements of each degree."""
+    c0, c1, c2, c3 = [np.asarray(ci, dtype=np.float64).ravel() for ci in c]
     out = np.full(c0.shape, np.inf)
-    for e in range(c0.size):
-        coeffs = [c3.flat[e], c2.flat[e], c1.flat[e], c0.flat[e]]
-        while len(coeffs) > 1 and coeffs[0] == 0.0:
-            coeffs = coeffs[1:]
-        if len(coeffs) <= 1:
+    deg = np.where(c3 != 0.0, 3, np.where(c2 != 0.0, 2, np.where(c1 != 0.0, 1, 0)))
+    coef = np.stack([c0, c1, c2, c3], axis=1)
+    for k in (1, 2, 3):
+        sel = np.flatnonzero(deg == k)
+        if len(sel) == 0:
             continue
-        r = np.roots(coeffs)
-        r = r[(np.abs(r.imag) <= 1e-12 * np.maximum(1.0, np.abs(r.real))) & (r.real > 0.0)].real
-        if len(r):
-            out.flat[e] = r.min()
-    return out
+        a = coef[sel, :k] / coef[sel, k:k + 1]          # monic: t^k + a_{k-1} t^{k-1} + ... + a_0
+        comp = np.zeros((len(sel), k, k))
+        comp[:, 0, :] = -a[:, ::-1]                      # numpy.roots' companion layout
+        if k > 1:
+            comp[:, np.arange(1, k), np.arange(k - 1)] = 1.0
+        r = np.linalg.eigvals(comp)
+        ok = (np.abs(r.imag) <= 1e-12 * np.maximum(1.0, np.abs(r.real))) & (r.real > 0.0)
+        out[sel] = np.where(ok, r.real, np.inf).min(axis=1)
+    return out.reshape(np.shape(c[0]))
 
 
 def inversion_alpha(model, x, d):

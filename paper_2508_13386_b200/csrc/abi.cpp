@@ -267,6 +267,10 @@ static ms_status create_common(ms_ctx **out, int device, void *cuda_stream, int 
       ctx->c.part.world = world;
       ms_default_params(&ctx->c.params);
       MS_CUDA(cudaMallocHost((void **)&ctx->c.h_pinned, sizeof(double) * PH_COUNT));
+      // per-device kernel attributes (large shared-memory opt-ins), on this context's device
+      msim::elem_init_attrs(ctx->c);
+      msim::coarse_init_attrs(ctx->c);
+      msim::chol_init_attrs(ctx->c);
       if (world > 1) ctx->c.comm = hub ? msim::make_hub_comm(hub, rank) : msim::make_nccl_comm(nccl_id, rank, world, device);
     });
     return MS_OK;
@@ -410,6 +414,8 @@ ms_status ms_set_dirichlet(ms_ctx *ctx, int64_t n, const int32_t *verts) {
     Ctx &c = ctx->c;
     require_mesh(c);
     MS_REQUIRE(n == 0 || verts, MS_ERR_ARG, "null verts");
+    MS_REQUIRE(c.m == 0, MS_ERR_STATE,
+               "ms_set_dirichlet after ms_basis_upload: the basis was built for another Dirichlet set");
     std::fill(c.h_fixed.begin(), c.h_fixed.end(), 0);
     for (int64_t k = 0; k < n; ++k) {
       MS_REQUIRE(verts[k] >= 0 && verts[k] < c.nv_glob, MS_ERR_ARG, "Dirichlet vertex out of range");
@@ -580,7 +586,16 @@ ms_status ms_timestep(ms_ctx *ctx, ms_step_stats *out) {
     st.status = MS_WARN_NEWTON_CAP;
     for (int it = 0; it < c.params.max_newton; ++it) {
       ms_newton_stats ns{};
-      const ms_status s = newton_step(c, &ns);
+      ms_status s;
+      try {
+        s = newton_step(c, &ns);
+      } catch (...) {
+        // leave a consistent state machine: the step is abandoned at x^t (no half-finished step
+        // for a later ms_newton_step / ms_end_step to continue)
+        cudaMemcpyAsync(c.x, c.xt, sizeof(double) * 3 * (size_t)c.nv, cudaMemcpyDeviceToDevice, c.stream);
+        c.step_begun = false;
+        throw;
+      }
       st.newton_iters++;
       st.pcg_iters += ns.n_cg;
       st.ls_evals += ns.ls_evals;

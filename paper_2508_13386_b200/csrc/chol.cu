@@ -214,42 +214,6 @@ __global__ void __launch_bounds__(256) k_chol_update(int k, const int32_t *__res
 //   U(i,j,k): A_ij -= L_ik L_jk^T (updates of a tile are chained in step order -> deterministic);
 //             upd[i][j] = rank + 1
 // Tile data produced by other CTAs is read through L2 only (cp.async.cg / ld.global.cg).
-#ifdef MSIM_DF_PROF   // diagnostics: global-timer stamps of the critical-path (type-4) tasks
-__device__ unsigned long long g_df_prof[1024][8];
-__device__ unsigned long long g_df_prof2[1024][6];   // [i]: P(i,i-2) claim/start/end, U(i,i-1,i-2) claim/start/end
-#define DF_STAMP2(i, s)                                                             \
-  do {                                                                              \
-    if (threadIdx.x == 0) {                                                         \
-      unsigned long long tt;                                                        \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));                        \
-      g_df_prof2[(i) & 1023][s] = tt;                                               \
-    }                                                                               \
-  } while (0)
-#define DF_STAMP(i, s)                                                              \
-  do {                                                                              \
-    if (threadIdx.x == 0) {                                                         \
-      unsigned long long tt;                                                        \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));                        \
-      g_df_prof[(i) & 1023][s] = tt;                                                \
-    }                                                                               \
-  } while (0)
-// per task: claim, ready (all waits satisfied), end, CTA
-constexpr int kDfTaskMax = 1 << 17;
-__device__ unsigned long long g_df_task[kDfTaskMax][4];
-#define DF_TSTAMP(id, s)                                                            \
-  do {                                                                              \
-    if (threadIdx.x == 0 && (id) < kDfTaskMax) {                                    \
-      unsigned long long tt;                                                        \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));                        \
-      g_df_task[id][s] = tt;                                                        \
-      if ((s) == 0) g_df_task[id][3] = blockIdx.x;                                  \
-    }                                                                               \
-  } while (0)
-#else
-#define DF_TSTAMP(id, s)
-#define DF_STAMP(i, s)
-#define DF_STAMP2(i, s)
-#endif
 
 __device__ __forceinline__ void df_wait(const int *p, int val) {
   if (threadIdx.x == 0) {
@@ -416,23 +380,19 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
     }
     const int4 tk = P.tasks[id];
     const int type = tk.x, i = tk.y, j = tk.z & 0xffff, k = tk.z >> 16, cnt = tk.w;
-    DF_TSTAMP(id, 0);
     if (type == 0) {   // popped from the ready queue: its inputs are done
       (void)cnt;
-      DF_TSTAMP(id, 1);
       diag_factor(k, nSp, L, U, flag, sm);
       df_signal(&dfl[k], 1);
       df_release(P, P.succ_ptr[id], P.succ_ptr[id + 1], &s_keep);
     } else if (type == 4) {
       // critical-path task of step k (i = k+1): P(i,k), U(i,i,k) and D(i) in one CTA.
       // cnt = updates tile (i,k) must have seen; tk.w >> 16 unused; rank of (i,i) is upd order
-      DF_STAMP(i, 0);
       // everything that does not depend on D(k) is fetched before waiting for it: A_ik (its
       // updates are done) and the diagonal tile A_ii (its earlier updates are done)
       double *SA = sm, *SU = sm + TB * TB;
       const size_t oik = tile_off(i, k, nSp), oii = tile_off(i, i, nSp);
       df_wait2(&upd[i * NT + k], cnt & 0xffff, &upd[i * NT + i], cnt >> 16);
-      DF_STAMP(i, 6);
       stage_colmajor(SA, L + oik, nSp);
       asm volatile("cp.async.commit_group;\n" ::);
       double old[16];
@@ -445,8 +405,6 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
       // D(k) is usually this CTA's previous task: its inverse is still in shared memory
       const bool own_d = k == my_d;
       if (!own_d) df_wait(&dfl[k], 1);
-      DF_STAMP(i, 1);
-      DF_TSTAMP(id, 1);
       if (!own_d) stage_colmajor(SU, U + (size_t)k * TB * TB, TB);
       cp_async_commit_wait();
       __syncthreads();
@@ -460,7 +418,6 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
         __stcg(&L[oik + (size_t)c * nSp + r], acc[q]);
       }
       df_signal(&pfl[i * NT + k], 1);             // panel tile published early for the other updates
-      DF_STAMP(i, 2);
       // X = L_ik into k-major smem: SX[c*64 + r] = X[r][c]
       double *SX = sm;
 #pragma unroll
@@ -469,7 +426,6 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
         tile_rc(q, r, c);
         SX[c * TB + r] = acc[q];
       }
-      DF_STAMP(i, 3);
       __syncthreads();
       tile_gemm(SX, SX, acc);
       __syncthreads();   // SX consumed: the updated tile goes straight into D's smem layout
@@ -479,16 +435,12 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
         tile_rc(q, r, c);
         sm[r * LD + c] = r >= c ? old[q] - acc[q] : 0.0;
       }
-      DF_STAMP(i, 4);
       diag_factor(i, nSp, L, U, flag, sm, true);
-      DF_STAMP(i, 7);   // D computed and stored; the signal (barrier, fence, flags) follows
       df_signal2(&dfl[i], 1, &upd[i * NT + i], (cnt >> 16) + 1);
       my_d = i;
-      DF_STAMP(i, 5);
     } else if (type == 1) {
-      if (i == k + 2) DF_STAMP2(i, 0);
-      if (i == k + 2) DF_STAMP2(i, 1);
-      DF_TSTAMP(id, 1);
+
+
       double *SA = sm, *SU = sm + TB * TB;
       const size_t oik = tile_off(i, k, nSp);
       stage_colmajor(SA, L + oik, nSp);
@@ -505,15 +457,12 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
       }
       df_signal(&pfl[i * NT + k], 1);
       df_release(P, P.succ_ptr[id], P.succ_ptr[id + 1], &s_keep);
-      if (i == k + 2) DF_STAMP2(i, 2);
+
     } else {
-      const bool col = (i == k + 2 && j == k + 1);
-      if (col) DF_STAMP2(i, 3);
       double *Si = sm, *Sj = sm + TB * TB;
       stage_colmajor(Si, L + tile_off(i, k, nSp), nSp);
       stage_colmajor(Sj, L + tile_off(j, k, nSp), nSp);
-      if (col) DF_STAMP2(i, 4);
-      DF_TSTAMP(id, 1);
+
       const size_t oij = tile_off(i, j, nSp);
       double old[16];
 #pragma unroll
@@ -534,9 +483,8 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
       }
       df_signal(&upd[i * NT + j], cnt + 1);
       df_release(P, P.succ_ptr[id], P.succ_ptr[id + 1], &s_keep);
-      if (col) DF_STAMP2(i, 5);
+
     }
-    DF_TSTAMP(id, 2);
     __syncthreads();
     if (t == 0 && type != 4) atomicAdd(P.done, 1);   // after this task's pushes (barrier above)
   }
@@ -707,13 +655,23 @@ constexpr size_t kDiagSmem = sizeof(double) * kDiagSmemDoubles;
 constexpr size_t kGemmSmem = sizeof(double) * 2 * TB * TB;
 constexpr size_t kUpdSmem = kDiagSmem > kGemmSmem ? kDiagSmem : kGemmSmem;
 
-void chol_set_attrs() {
-  static bool done = false;
-  if (done) return;
+#ifndef MSIM_DF_PER_SM
+#define MSIM_DF_PER_SM 2   // two queue CTAs per SM, the chain CTA alone on its SM (measured at C4:
+                           // 2.82 -> 2.50 ms; sharing the chain's SM made two per SM slower)
+#endif
+constexpr int kDfCtasPerSm = MSIM_DF_PER_SM;   // CTAs per SM of the dataflow factorisation
+
+// Large-shared-memory opt-ins are per device: set once per context, on its device, right
+// after cudaSetDevice (create_common); the occupancy-derived CTA count is kept in the context.
+void chol_init_attrs(Ctx &c) {
   MS_CUDA(cudaFuncSetAttribute(k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDiagSmem));
   MS_CUDA(cudaFuncSetAttribute(k_chol_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem));
   MS_CUDA(cudaFuncSetAttribute(k_chol_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem));
-  done = true;
+  MS_CUDA(cudaFuncSetAttribute(k_chol_dataflow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem));
+  int per_sm = 0;
+  MS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chol_dataflow, 256, kUpdSmem));
+  const char *e = std::getenv("MSIM_DF_PER_SM");
+  c.df_per_sm = std::max(std::min(per_sm, e ? std::atoi(e) : kDfCtasPerSm), 1);
 }
 
 void launch_scatter_S(Ctx &c);
@@ -723,25 +681,9 @@ static bool step_updates_diag(const Ctx &c, int k) {   // is tile (k+1, k+1) amo
   return !P.empty() && P.front() == k + 1;
 }
 
-#ifndef MSIM_DF_PER_SM
-#define MSIM_DF_PER_SM 2   // two queue CTAs per SM, the chain CTA alone on its SM (measured at C4:
-                           // 2.82 -> 2.50 ms; sharing the chain's SM made two per SM slower)
-#endif
-constexpr int kDfCtasPerSm = MSIM_DF_PER_SM;   // CTAs per SM of the dataflow factorisation
-
-static int dataflow_per_sm() {
-  static int per_sm = -1;
-  if (per_sm < 0) {
-    MS_CUDA(cudaFuncSetAttribute(k_chol_dataflow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem));
-    MS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chol_dataflow, 256, kUpdSmem));
-    const char *e = std::getenv("MSIM_DF_PER_SM");
-    per_sm = std::max(std::min(per_sm, e ? std::atoi(e) : kDfCtasPerSm), 1);
-  }
-  return per_sm;
-}
 
 static int dataflow_grid(const Ctx &c) {
-  const int per_sm = dataflow_per_sm();
+  const int per_sm = c.df_per_sm;
   // the chain CTA, the release helper, at least one CTA per queue
   return (int)std::max<int64_t>(4, (int64_t)per_sm * c.coop_grid);
 }
@@ -784,79 +726,11 @@ void enqueue_chol_factor(Ctx &c) {
     prm.ndep = c.chol_ndep;
     prm.queue = c.chol_queue;
     prm.done = c.chol_queue + 2 * prm.qstride;
-    prm.per_sm = dataflow_per_sm();
+    prm.per_sm = c.df_per_sm;
     prm.chain_sm = c.df_flags + (size_t)2 * NT * NT + NT;   // zeroed with the flags
     void *args[] = {&prm};
     MS_CUDA(cudaLaunchCooperativeKernel((const void *)k_chol_dataflow, dim3(dataflow_grid(c)), dim3(256), args,
                                         kUpdSmem, c.stream));
-#ifdef MSIM_DF_PROF
-    {
-      static unsigned long long h[1024][8];
-      MS_CUDA(cudaStreamSynchronize(c.stream));
-      MS_CUDA(cudaMemcpyFromSymbol(h, g_df_prof, sizeof(h)));
-      double seg[5] = {0, 0, 0, 0, 0}, gap = 0;
-      int n = 0;
-      for (int i = 1; i < NT && i < 1024; ++i) {
-        for (int q = 0; q < 5; ++q) seg[q] += 1e-3 * (double)(h[i][q + 1] - h[i][q]);
-        if (i > 1) gap += 1e-3 * (double)(h[i][1] - h[i - 1][5]);
-        n++;
-      }
-      double wik = 0, wii = 0, wd = 0;
-      for (int i = 2; i < NT && i < 1024; ++i) {
-        const double t5 = (double)h[i - 1][5];
-        wik += 1e-3 * std::max(0.0, (double)h[i][6] - t5);
-        wii += 1e-3 * std::max(0.0, (double)h[i][7] - std::max(t5, (double)h[i][6]));
-        wd += 1e-3 * std::max(0.0, (double)h[i][1] - std::max(t5, (double)h[i][7]));
-      }
-      {
-        static unsigned long long h2[1024][6];
-        MS_CUDA(cudaMemcpyFromSymbol(h2, g_df_prof2, sizeof(h2)));
-        // relative to D(i-2)'s end = critical task i-3's stamp 5 ... use D(k) end with k = i-2: h[i-2][5]
-        double pc = 0, ps = 0, pe = 0, uc = 0, us = 0, ue = 0;
-        int m2 = 0;
-        for (int i = 4; i < NT && i < 1024; ++i) {
-          const double t0 = (double)h[i - 2][5];   // D(i-2) done
-          pc += 1e-3 * ((double)h2[i][0] - t0);
-          ps += 1e-3 * ((double)h2[i][1] - t0);
-          pe += 1e-3 * ((double)h2[i][2] - t0);
-          uc += 1e-3 * ((double)h2[i][3] - t0);
-          us += 1e-3 * ((double)h2[i][4] - t0);
-          ue += 1e-3 * ((double)h2[i][5] - t0);
-          m2++;
-        }
-        {
-          static int dumped = 0;
-          if (++dumped == 4 && ntask <= kDfTaskMax) {   // one launch after warm-up
-            std::vector<unsigned long long> ht((size_t)ntask * 4);
-            std::vector<int32_t> hd((size_t)ntask * 4);
-            MS_CUDA(cudaMemcpyFromSymbol(ht.data(), g_df_task, sizeof(unsigned long long) * ht.size()));
-            MS_CUDA(cudaMemcpy(hd.data(), c.chol_dag.p, sizeof(int32_t) * hd.size(), cudaMemcpyDeviceToHost));
-            if (FILE *fd = std::fopen("gpurun_out/dftask.bin", "wb")) {
-              const int32_t hdr[2] = {ntask, NT};
-              std::fwrite(hdr, sizeof(int32_t), 2, fd);
-              std::fwrite(hd.data(), sizeof(int32_t), hd.size(), fd);
-              std::fwrite(ht.data(), sizeof(unsigned long long), ht.size(), fd);
-              std::fclose(fd);
-            }
-          }
-        }
-        if (FILE *fd = std::fopen("gpurun_out/dfprof_raw.txt", "w")) {
-          for (int i = 0; i < NT && i < 1024; ++i) {
-            std::fprintf(fd, "%d", i);
-            for (int q = 0; q < 8; ++q) std::fprintf(fd, " %llu", h[i][q]);
-            for (int q = 0; q < 6; ++q) std::fprintf(fd, " %llu", h2[i][q]);
-            std::fprintf(fd, "\n");
-          }
-          std::fclose(fd);
-        }
-        fprintf(stderr, "[msim] relative to D(k) done: P(k+2,k) claim %.2f start %.2f end %.2f | U(k+2,k+1,k) claim %.2f start %.2f end %.2f | D(k+1) done %.2f us\n",
-                pc / m2, ps / m2, pe / m2, uc / m2, us / m2, ue / m2, (seg[0] + seg[1] + seg[2] + seg[3] + seg[4]) / n);
-      }
-      fprintf(stderr, "[msim] chol type-4 avg us: wait %.2f  P %.2f  wait-ii %.2f  U %.2f  D %.2f | ready-after-prev-D %.2f (A_ik %.2f, A_ii %.2f, D %.2f) | total %.1f us\n",
-              seg[0] / n, seg[1] / n, seg[2] / n, seg[3] / n, seg[4] / n, gap / n, wik / n, wii / n, wd / n,
-              1e-3 * (double)(h[NT - 1][5] - h[1][0]));
-    }
-#endif
     return;
   }
   k_chol_diag<<<1, 256, kDiagSmem, c.stream>>>(0, nSp, c.Lden, c.Uinv, c.flags + 0);

@@ -301,14 +301,15 @@ void launch_basis_W(Ctx &c) {
 }
 
 // ------------------------------------------------------------------ launchers
+// per context, on its device (create_common): the fused Galerkin kernel's opt-in is raised to the
+// largest row any basis can use (227 KB), never lowered
+void coarse_init_attrs(Ctx &) {
+  MS_CUDA(cudaFuncSetAttribute(k_galerkin_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+}
+
 void launch_coarse_S(Ctx &c) {
   const size_t smem = sizeof(double) * galerkin_smem_doubles(c.gal_max_jup);
-  static size_t smem_set = 0;
-  if (smem > smem_set) {
-    MS_REQUIRE(smem <= 227 * 1024, MS_ERR_ARG, "coarse S row too wide for the fused Galerkin kernel");
-    MS_CUDA(cudaFuncSetAttribute(k_galerkin_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    smem_set = smem;
-  }
+  MS_REQUIRE(smem <= 227 * 1024, MS_ERR_ARG, "coarse S row too wide for the fused Galerkin kernel");
   const GalParams G = galerkin_params(c);
   k_galerkin_fused<<<c.m * G.nparts, kGalThreads, smem, c.stream>>>(G);
   c.launches++;
@@ -337,11 +338,7 @@ void launch_scatter_S(Ctx &c) {
 // Capture a fixed launch sequence once (pointers are fixed per basis) and replay it.
 template <typename F>
 static void run_captured(Ctx &c, cudaGraphExec_t &exec, F enqueue) {
-#ifdef MSIM_DF_PROF
-  const bool graphs = false;   // the profiling read-back synchronises
-#else
   const bool graphs = c.params.use_graphs && !c.dist();
-#endif
   if (!graphs) {
     enqueue(c);
     return;
@@ -370,7 +367,6 @@ void coarse_reset_graphs(Ctx &c) {
 }
 
 void launch_coarse_factor(Ctx &c) {
-  chol_set_attrs();
   run_captured(c, c.factor_graph, enqueue_chol_factor);
   c.launches += chol_factor_kernels(c);
   MS_CUDA(cudaGetLastError());

@@ -195,6 +195,7 @@ struct Ctx {
   DBuf<int32_t> chol_queue0, chol_queue;                   // two ready queues: pristine / live
   int64_t n_crit = 0, n_pool = 0;
   int df_hi_ctas = 64;   // CTAs serving the high-priority queue
+  int df_per_sm = 1;     // dataflow factorisation CTAs per SM (chol_init_attrs)
   int64_t n_dag = 0;
   DBuf<int> df_flags;               // upd[NT*NT], pfl[NT*NT], dfl[NT]
   bool chol_dataflow = true;
@@ -285,7 +286,9 @@ void enqueue_chol_factor(Ctx &c);
 void enqueue_chol_solve(Ctx &c);
 int64_t chol_factor_kernels(const Ctx &c);
 int64_t chol_solve_kernels(const Ctx &c);
-void chol_set_attrs();
+void chol_init_attrs(Ctx &c);
+void coarse_init_attrs(Ctx &c);
+void elem_init_attrs(Ctx &c);
 void coarse_reset_graphs(Ctx &c);
 void launch_lift(Ctx &c, const double *q, double *w, bool accumulate);
 void launch_restrict(Ctx &c, const double *y, double *z);

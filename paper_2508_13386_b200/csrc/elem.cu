@@ -531,14 +531,16 @@ void launch_elem_grad_to(Ctx &c, const double *x, double *Ee) {
 
 void launch_elem_grad(Ctx &c) { launch_elem_grad_to(c, c.x, nullptr); }
 
+constexpr int kHessSmem = sizeof(double) * (kHessScratch > kHessStg ? kHessScratch : kHessStg) * kHessThreads;
+
+// per context, on its device (create_common)
+void elem_init_attrs(Ctx &) {
+  MS_CUDA(cudaFuncSetAttribute(k_elem_hess, cudaFuncAttributeMaxDynamicSharedMemorySize, kHessSmem));
+}
+
 void launch_elem_hess_to(Ctx &c, const double *x) {
   MS_CUDA(cudaMemsetAsync(c.hess_nwork, 0, sizeof(unsigned int), c.stream));
-  constexpr int smem = sizeof(double) * (kHessScratch > kHessStg ? kHessScratch : kHessStg) * kHessThreads;
-  static bool attr = false;
-  if (!attr) {
-    MS_CUDA(cudaFuncSetAttribute(k_elem_hess, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  constexpr int smem = kHessSmem;
   k_elem_hess<<<div_up(c.nt, kHessThreads), kHessThreads, smem, c.stream>>>(
       mesh_view(c), x, c.stage_h, c.hess_work, c.hess_nwork);
   k_elem_hess_eig<<<148 * 2, 128, 0, c.stream>>>(mesh_view(c), x, c.stage_h, c.hess_work, c.hess_nwork);

@@ -323,6 +323,9 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
       MS_REQUIRE(phi[k] > 0.0, MS_ERR_ARG, "phi entries must be > 0");
       sum += phi[k];
     }
+    // pinned vertices never move: every basis column must vanish there
+    MS_REQUIRE(!c.h_fixed[v] || (vptr[v + 1] == vptr[v] && phi_aff[v] == 0.0), MS_ERR_ARG,
+               "basis does not vanish at a Dirichlet vertex (set the Dirichlet set before the basis)");
     // POU: sum phi + phi_DBC = 1 with phi_DBC = 1 - phi_affine; a hole is sum phi = phi_DBC = 0
     MS_REQUIRE(sum > 0.0 || c.h_fixed[v] || phi_aff[v] < 1.0, MS_ERR_COVERAGE,
                "basis coverage hole: no handle covers a free vertex");

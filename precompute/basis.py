@@ -22,12 +22,14 @@ from __future__ import annotations
 
 import dataclasses
 import os
-from collections import deque
 
 import numpy as np
 import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 from scipy.spatial import cKDTree
+
+
+BASIS_VERSION = "v2"   # v2: counter-based kmeans++ draws (splitmix64), exact nearest-centre ties
 
 
 @dataclasses.dataclass
@@ -65,8 +67,20 @@ class Basis:
 # ----------------------------------------------------------------------------- geometry
 
 def tet_volumes(X, tets):
-    D = X[tets[:, 1:]] - X[tets[:, :1]]
-    return np.linalg.det(D) / 6.0
+    """V = det[X1-X0 | X2-X0 | X3-X0] / 6, the determinant written out as a.(b x c) in a fixed
+    order (the native ms_basis_build evaluates the same expression)."""
+    a = X[tets[:, 1]] - X[tets[:, 0]]
+    b = X[tets[:, 2]] - X[tets[:, 0]]
+    c = X[tets[:, 3]] - X[tets[:, 0]]
+    det = (a[:, 0] * (b[:, 1] * c[:, 2] - b[:, 2] * c[:, 1])
+           - a[:, 1] * (b[:, 0] * c[:, 2] - b[:, 2] * c[:, 0])
+           + a[:, 2] * (b[:, 0] * c[:, 1] - b[:, 1] * c[:, 0]))
+    return det / 6.0
+
+
+def tet_barycentres(X, tets):
+    """((X0 + X1) + X2) + X3) / 4."""
+    return (((X[tets[:, 0]] + X[tets[:, 1]]) + X[tets[:, 2]]) + X[tets[:, 3]]) / 4.0
 
 
 def face_adjacency(tets):
@@ -84,24 +98,63 @@ def face_adjacency(tets):
 
 # ----------------------------------------------------------------------------- k-means
 
-def kmeans_pp(P, w, m, rng):
-    n = len(P)
-    first = int(rng.choice(n, p=w / w.sum()))
+def splitmix64_uniform(seed, k):
+    """k-th uniform double in [0, 1) of the counter-based SplitMix64 stream of `seed`:
+    z = seed + (k+1) 0x9E3779B97F4A7C15, two xor-shift-multiply rounds, top 53 bits.
+    The native ms_basis_build draws the same numbers (random draws shared by counter)."""
+    M = (1 << 64) - 1
+    z = (int(seed) + (int(k) + 1) * 0x9E3779B97F4A7C15) & M
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+    z ^= z >> 31
+    return (z >> 11) * (1.0 / 9007199254740992.0)
+
+
+def sq_dist(P, c):
+    """(dx^2 + dy^2) + dz^2 per row (fixed order, no fused multiply-add)."""
+    d = P - c
+    return (d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2]
+
+
+def weighted_pick(p, u):
+    """Index i with cdf[i-1] <= u cdf[n-1] < cdf[i], cdf = sequential prefix sums of p."""
+    cdf = np.cumsum(p)
+    t = u * cdf[-1]
+    return min(int(np.searchsorted(cdf, t, side="right")), len(p) - 1)
+
+
+def kmeans_pp(P, w, m, seed):
+    """kmeans++ seeding ('k-means++'): first centre drawn with probability ~ w, each
+    next with probability ~ w d^2 (d = distance to the nearest chosen centre); draw k uses
+    splitmix64_uniform(seed, k)."""
+    first = weighted_pick(w, splitmix64_uniform(seed, 0))
     C = [P[first]]
-    d2 = np.sum((P - C[0]) ** 2, axis=1)
-    for _ in range(1, m):
-        p = w * d2
-        s = p.sum()
-        idx = int(rng.choice(n, p=p / s)) if s > 0 else int(rng.integers(n))
+    d2 = sq_dist(P, P[first])
+    for k in range(1, m):
+        idx = weighted_pick(w * d2, splitmix64_uniform(seed, k))
         C.append(P[idx])
-        d2 = np.minimum(d2, np.sum((P - P[idx]) ** 2, axis=1))
+        d2 = np.minimum(d2, sq_dist(P, P[idx]))
     return np.array(C)
 
 
+def nearest_centre(P, C, k=4):
+    """Index of the nearest centre per point by exact squared distance (sq_dist), ties -> lowest
+    centre index; cKDTree only proposes the k candidates."""
+    k = min(k, len(C))
+    _, cand = cKDTree(C).query(P, k=k)
+    cand = np.asarray(cand).reshape(len(P), k)
+    d = np.stack([sq_dist(P, C[cand[:, j]]) for j in range(k)], axis=1)
+    best = d.min(axis=1, keepdims=True)
+    idx = np.where(d == best, cand, np.iinfo(np.int64).max).min(axis=1)
+    return idx
+
+
 def lloyd(P, w, C, max_iter=100):
+    """Lloyd iterations: assign to the nearest centre, move centres to the w-weighted means;
+    stop at an assignment fixed point or after max_iter."""
     assign = None
     for _ in range(max_iter):
-        _, a = cKDTree(C).query(P, k=1)
+        a = nearest_centre(P, C)
         if assign is not None and np.array_equal(a, assign):
             break
         assign = a
@@ -251,6 +304,24 @@ def _solve_dbc():
     return out
 
 
+def n_cg_from_radius(r):
+    """N_cg = the closer of 20 and 40 to the mean hop radius (ties -> 20)."""
+    return 20 if abs(r - 20) <= abs(r - 40) else 40
+
+
+def pou_normalise(rows, uraw, u_dbc, n_v):
+    """Clip and normalise (P:338, P:352, P:379-381): phi_i(v) = max(u_i(v), 0) / D(v) and
+    phi_DBC(v) = u_DBC(v) / D(v), D(v) = sum_j max(u_j(v), 0) + u_DBC(v), for basis entries
+    (rows[k] = vertex, uraw[k] = u_i(v)).  Returns (phi per entry, phi_DBC, D); entries of
+    vertices with D = 0 are left 0 (coverage holes, handled by the caller)."""
+    val = np.maximum(uraw, 0.0)
+    denom = np.bincount(rows, weights=val, minlength=n_v) + u_dbc
+    safe = np.where(denom > 0, denom, 1.0)
+    phi = np.where(denom[rows] > 0, val / safe[rows], 0.0)
+    phi_dbc = np.where(denom > 0, u_dbc / safe, 0.0)
+    return phi, phi_dbc, denom
+
+
 def hop_radius(assign, tets, cv, n_v, m):
     """Mean over partitions of the max edge-hop distance from the centroid vertex to the
     partition's vertices, BFS on mesh edges restricted to the partition (Q7)."""
@@ -272,11 +343,11 @@ def build_basis(scene, m=None, seed=None, workers=None, verbose=False) -> Basis:
     X, tets = scene.X, scene.tets.astype(np.int64)
     m = scene.m if m is None else m
     n_v, n_t = len(X), len(tets)
-    rng = scene.rngs()[2] if seed is None else np.random.default_rng(seed)
+    seed = scene.config if seed is None else seed
 
     vol = tet_volumes(X, tets)
-    bary = X[tets].mean(axis=1)
-    C0 = kmeans_pp(bary, vol, m, rng)
+    bary = tet_barycentres(X, tets)
+    C0 = kmeans_pp(bary, vol, m, seed)
     assign = lloyd(bary, vol, C0)
     adj = face_adjacency(tets)
     assign = enforce_connectivity(assign.copy(), tets, adj, m)
@@ -345,8 +416,7 @@ def build_basis(scene, m=None, seed=None, workers=None, verbose=False) -> Basis:
     rows = np.concatenate([r[0] for r in res])
     hid = np.concatenate([np.full(len(r[0]), i, dtype=np.int64) for i, r in enumerate(res)])
     uraw = np.concatenate([r[1] for r in res])
-    val = np.maximum(uraw, 0.0)                      # clip
-    denom = np.bincount(rows, weights=val, minlength=n_v) + u_dbc
+    _, _, denom = pou_normalise(rows, uraw, u_dbc, n_v)
     free = np.ones(n_v, dtype=bool)
     if dbc_mask is not None:
         free &= ~dbc_mask
@@ -362,22 +432,20 @@ def build_basis(scene, m=None, seed=None, workers=None, verbose=False) -> Basis:
         srt = sel[o]
         first = np.ones(len(srt), dtype=bool)
         first[1:] = rows[srt][1:] != rows[srt][:-1]
-        val[srt[first]] = 1.0
-        denom = np.bincount(rows, weights=val, minlength=n_v) + u_dbc
+        uraw = uraw.copy()
+        uraw[srt[first]] = 1.0
         if verbose:
             print(f"  coverage holes repaired: {len(holes)}")
+    phi, phi_dbc, denom = pou_normalise(rows, uraw, u_dbc, n_v)
     if np.any(denom[free] <= 0):
         bad = np.nonzero((denom <= 0) & free)[0]
         raise RuntimeError(f"basis coverage hole at {len(bad)} free vertices, e.g. {bad[:5]}")
-    keep = val > 0
-    rows, hid, val = rows[keep], hid[keep], val[keep]
-    phi = val / denom[rows]
+    keep = phi > 0
+    rows, hid, phi = rows[keep], hid[keep], phi[keep]
     o = np.lexsort((hid, rows))
     rows, hid, phi = rows[o], hid[o], phi[o]
     vptr = np.zeros(n_v + 1, dtype=np.int64)
     np.cumsum(np.bincount(rows, minlength=n_v), out=vptr[1:])
-    with np.errstate(invalid="ignore", divide="ignore"):
-        phi_dbc = np.where(denom > 0, u_dbc / np.where(denom > 0, denom, 1.0), 0.0)
     if dbc_mask is not None:
         phi_dbc[dbc_mask] = 1.0
     phi_aff = 1.0 - phi_dbc
@@ -387,7 +455,7 @@ def build_basis(scene, m=None, seed=None, workers=None, verbose=False) -> Basis:
 
     t2 = time.time()
     hr = hop_radius(assign, tets, cv, n_v, m)
-    n_cg = 20 if abs(hr - 20) <= abs(hr - 40) else 40
+    n_cg = n_cg_from_radius(hr)
     if verbose:
         print(f"  hop radius {hr:.2f} -> n_cg {n_cg} ({time.time()-t2:.1f}s); total {time.time()-t0:.1f}s")
     return Basis(m=m, origins=X[cv].copy(), n_holes=len(holes), vptr=vptr, handle=hid.astype(np.int32), phi=phi,
@@ -399,7 +467,7 @@ def cached_basis(scene, cache_dir=None, **kw) -> Basis:
     """Build or load the basis of a scene (cache keyed by scene name, sizes and m)."""
     cache_dir = cache_dir or os.environ.get("MSIM_CACHE", os.path.join(os.path.dirname(__file__), "..", ".cache"))
     os.makedirs(cache_dir, exist_ok=True)
-    key = f"{scene.name}_{scene.n_verts}_{scene.n_tets}_{scene.m}.npz"
+    key = f"{scene.name}_{scene.n_verts}_{scene.n_tets}_{scene.m}_{BASIS_VERSION}.npz"
     path = os.path.join(cache_dir, key)
     if os.path.exists(path):
         return Basis.load(path)

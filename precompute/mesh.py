@@ -221,6 +221,18 @@ def make_scene(c: int) -> Scene:
     return SCENES[c]()
 
 
+def contact_state(scene: Scene):
+    """Deterministic contact entry state (x, v) for timed / bootstrapped Newton iterations: the
+    rest shape lowered so its bottom layer sits inside the barrier band, 0.6 dhat above the
+    ground, falling at 0.5 m/s (scenes without ground: rest, v = 0)."""
+    x = np.array(scene.X, dtype=np.float64)
+    v = np.zeros_like(x)
+    if scene.ground is not None:
+        x[:, 2] += 0.6 * scene.ground["dhat"] - x[:, 2].min()
+        v[:, 2] = -0.5
+    return x, v
+
+
 def random_state(scene: Scene, amp: float, seed: int):
     """Seeded random perturbation of the rest shape (for element-level parity inputs).
 

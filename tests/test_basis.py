@@ -81,15 +81,21 @@ def test_full_column_rank(c1_scene, c1_basis):
 
 
 def test_ncg_bins_golden():
-    g = GOLD["ncg_bins"]
-    for r, expect in g["cases"]:
-        assert (20 if abs(r - 20) <= abs(r - 40) else 40) == expect
+    """precompute.basis.n_cg_from_radius on SPEC's worked cases (golden, cited in the fixture)."""
+    from precompute.basis import n_cg_from_radius
+    for r, expect in GOLD["ncg_bins"]["cases"]:
+        assert n_cg_from_radius(r) == expect
 
 
 def test_pou_arithmetic_golden():
+    """precompute.basis.pou_normalise on SPEC's pou_normalize examples: the clip and
+    normalisation the basis build uses, called directly."""
+    from precompute.basis import pou_normalise
     g = GOLD["pou_examples"]
-    u = np.array(g["u"])
-    assert np.allclose(u / u.sum(), g["phi"])
-    u2 = np.array(g["u2"])
-    den = u2.sum() + g["u2_dbc"]
-    assert np.allclose(u2 / den, g["phi2"]) and abs(g["u2_dbc"] / den - g["phi2_dbc"]) < 1e-15
+    phi, phi_dbc, _ = pou_normalise(np.array([0, 0]), np.array(g["u"]), np.zeros(1), 1)
+    assert np.allclose(phi, g["phi"], rtol=0, atol=1e-15) and phi_dbc[0] == 0.0
+    phi, phi_dbc, _ = pou_normalise(np.array([0, 0]), np.array(g["u2"]), np.array([g["u2_dbc"]]), 1)
+    assert np.allclose(phi, g["phi2"], rtol=0, atol=1e-15) and abs(phi_dbc[0] - g["phi2_dbc"]) < 1e-15
+    # clipping (P:338): a negative u_i contributes nothing to phi or to the denominator
+    phi, _, den = pou_normalise(np.array([0, 0, 0]), np.array([0.2, -0.3, 0.6]), np.zeros(1), 1)
+    assert np.allclose(phi, [0.25, 0.0, 0.75], rtol=0, atol=1e-15) and abs(den[0] - 0.8) < 1e-15

@@ -86,6 +86,42 @@ def test_pcg_exact_on_tiny_spd():
         assert np.abs(d - ref).max() < 1e-10 * np.abs(ref).max()
 
 
+def test_pcg_jacobi_one_iteration_exact_on_diagonal():
+    """Fixed-count pin of the Jacobi preconditioner: on a diagonal H one PCG iteration with
+    z = D^-1 r is the exact solution; with D instead of D^-1, or without preconditioning, it is
+    not (the diagonal entries differ)."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(5)
+    diag = rng.uniform(0.5, 50.0, 40)
+    H = sp.diags(diag).tocsr()
+    b = rng.standard_normal(40)
+    d = solver.pcg(H, b, 1)
+    assert np.abs(d - b / diag).max() < 1e-13 * np.abs(b / diag).max()
+
+
+def test_pcg_fixed_count_krylov_optimality():
+    """CG optimality (Hestenes-Stiefel): after k iterations from 0, Jacobi-PCG returns the
+    minimiser of the H-norm error over the preconditioned Krylov space
+    K_k = span{z, (D^-1 H) z, ..., (D^-1 H)^{k-1} z}, z = D^-1 b.  The minimiser is formed here by
+    a direct Galerkin solve on that space, independently of the recurrence."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(6)
+    n = 30
+    A = rng.standard_normal((n, n))
+    Hd = A @ A.T + np.diag(rng.uniform(1.0, 100.0, n))
+    H = sp.csr_matrix(Hd)
+    b = rng.standard_normal(n)
+    Dinv = 1.0 / np.diag(Hd)
+    for k in (1, 2, 3, 5):
+        K = [Dinv * b]
+        for _ in range(k - 1):
+            K.append(Dinv * (Hd @ K[-1]))
+        V, _ = np.linalg.qr(np.array(K).T)
+        ref = V @ np.linalg.solve(V.T @ Hd @ V, V.T @ b)
+        d = solver.pcg(H, b, k)
+        assert np.linalg.norm(d - ref) < 1e-9 * np.linalg.norm(ref), k
+
+
 def test_pcg_converges_to_lapack_on_c1(c1_scene):
     m, x, xhat = perturbed_c1(c1_scene)
     H = ip.hessian(m, x, xhat).tocsr()

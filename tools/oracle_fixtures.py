@@ -1,0 +1,97 @@
+"""Oracle fixtures for the full-size GPU parity tests (test infrastructure; calls only oracle/
+and precompute/, never the CUDA path).
+
+    python tools/oracle_fixtures.py newton C      # bootstrapped Newton iterations of config C
+    python tools/oracle_fixtures.py traj C [K]    # free-running timesteps 1..K of config C
+
+newton: from precompute.mesh.contact_state (x^t, v) the oracle runs N_ITER Newton iterations of
+one timestep (Alg. 1, §3.9) and stores, per iteration, the start iterate x,
+d = d_s + d_f, d_s, alpha0 (CCD / inversion filters), alpha, ls_evals, energy and ||d_s||.
+traj: the oracle's own timesteps from the scene's initial state (rest, v = 0): x after every
+step and the Newton iterations it took (SURVEY §8(c) per-timestep tolerance).
+Files go to .cache/fixtures/ (git-ignored; they travel with the repo snapshot to the GPU box).
+"""
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle import solver  # noqa: E402
+from precompute.basis import BASIS_VERSION, cached_basis  # noqa: E402
+from precompute.mesh import contact_state, make_scene  # noqa: E402
+
+N_ITER = 2
+FIX_DIR = os.environ.get("MSIM_FIXTURES", os.path.join(ROOT, ".cache", "fixtures"))
+
+
+def fixture_path(kind, c, k=None):
+    tag = f"_{k}" if k is not None else ""
+    return os.path.join(FIX_DIR, f"{kind}_C{c}{tag}_{BASIS_VERSION}.npz")
+
+
+def newton_fixture(c, n_iter=N_ITER, verbose=True):
+    s = make_scene(c)
+    b = cached_basis(s)
+    sim = solver.OracleSim(s, b)
+    sim.x, sim.v = contact_state(s)
+    x_t = sim.x.copy()
+    v_t = sim.v.copy()
+    sim.begin_step()
+    out = {"x_t": x_t, "v_t": v_t, "xhat": sim.xhat}
+    for it in range(n_iter):
+        x0 = sim.x.copy()
+        t0 = time.time()
+        info = sim.newton_iteration()
+        if verbose:
+            print(f"C{c} iteration {it}: alpha0={info.alpha0:.6g} alpha={info.alpha:.6g} evals={info.ls_evals} "
+                  f"|ds|={info.ds_norm:.6g} ({time.time() - t0:.1f}s)", flush=True)
+        out[f"x{it}"] = x0
+        out[f"d{it}"] = info.d.reshape(-1, 3)
+        out[f"ds{it}"] = info.ds.reshape(-1, 3)
+        out[f"scal{it}"] = np.array([info.alpha0, info.alpha, info.ls_evals, info.ds_norm, info.energy,
+                                     float(info.converged), float(info.ls_failed)])
+        if info.converged or info.ls_failed:
+            break
+    out["n_iter"] = np.array(it + 1)
+    return out
+
+
+def traj_fixture(c, k, verbose=True):
+    s = make_scene(c)
+    b = cached_basis(s)
+    sim = solver.OracleSim(s, b)
+    xs, newton = [], []
+    for step in range(k):
+        t0 = time.time()
+        infos = sim.timestep()
+        xs.append(sim.x.copy())
+        newton.append(len(infos))
+        if verbose:
+            print(f"C{c} step {step + 1}: {len(infos)} Newton iterations, alpha={[round(i.alpha, 4) for i in infos]} "
+                  f"({time.time() - t0:.1f}s)", flush=True)
+    return {"x": np.array(xs), "newton": np.array(newton)}
+
+
+def main():
+    kind, c = sys.argv[1], int(sys.argv[2])
+    os.makedirs(FIX_DIR, exist_ok=True)
+    if kind == "newton":
+        data = newton_fixture(c)
+        path = fixture_path("newton", c)
+    else:
+        k = int(sys.argv[3]) if len(sys.argv) > 3 else make_scene(c).steps
+        data = traj_fixture(c, k)
+        path = fixture_path("traj", c, k)
+    np.savez(path + ".tmp.npz", **data)
+    os.replace(path + ".tmp.npz", path)
+    print("wrote", path, flush=True)
+
+
+if __name__ == "__main__":
+    main()
