@@ -173,6 +173,57 @@ ms_status ms_basis_upload(ms_ctx *ctx, int32_t m, const double *origins, const i
                           const int32_t *handle, const double *phi, const double *phi_affine,
                           const double affine_origin[3], int32_t n_cg);
 
+/* Build the SMS + affine bases natively on the host (C++/OpenMP) from the uploaded mesh,
+ * material (E weights the Laplacian, Q17), Dirichlet set and densities, then upload them as
+ * ms_basis_upload does (SURVEY §8(b) `ms_basis_build`; §3.5 L304-381 SMS basis,
+ * §3.5.1 L364-381 Dirichlet weight, §3.6 L383-419 partitioning, §3.7.2 L492-495 N_cg):
+ *  1. m clusters of the tets: kmeans++ seeding on volume-weighted tet barycentres with draws
+ *     k = 0..m-1 of the counter-based SplitMix64 stream of `seed` (z = seed + (k+1)
+ *     0x9E3779B97F4A7C15, two xor-shift-multiply rounds, u = (z >> 11) 2^-53; the pick is the
+ *     first index whose sequential prefix sum exceeds u * total), Lloyd iterations with exact
+ *     squared distances (ties -> lowest centre) to a fixed point or 100 rounds (Euclidean
+ *     stand-in for the paper's heat geodesics, reading B2);
+ *  2. face-connected clusters (largest component kept, the rest moved to the face-adjacent
+ *     cluster with most shared faces); empty clusters dropped, so info->m may be < m;
+ *  3. centroid vertex per cluster (nearest to the volume-weighted barycentre, Q15); handles
+ *     ordered by (x, y, z) of their centroid vertex;
+ *  4. per handle: K u = 0, K = L_s M^-1 L_s on the cluster + vertex-sharing clusters (R9, Q17),
+ *     u(c_i) = 1, u = 0 at neighbour centroids / internal boundary / Dirichlet vertices, clip;
+ *  5. Dirichlet weight, partition-of-unity normalisation, coverage-hole repair (B1), affine
+ *     handle at the centre of mass with phi_a = 1 - phi_DBC (Q14); N_cg from the hop heuristic.
+ * The same algorithm, draws and tie rules as precompute/basis.py: partition, centroid vertices
+ * and handle lists agree exactly, weights to the rounding of the subdomain solves.
+ * info may be NULL.  Errors: MS_ERR_ARG (m <= 0 or m > n_tets), MS_ERR_NOT_SPD (a subdomain
+ * system is singular), MS_ERR_COVERAGE, MS_ERR_STATE (no mesh). */
+typedef struct ms_basis_info {
+  int32_t m;              /* handles after dropping empty clusters                         */
+  int32_t n_cg;           /* refinement iterations from the hop heuristic                  */
+  int32_t n_holes;        /* free vertices repaired by reading B1                           */
+  int32_t pad_;
+  int64_t nnz_phi;        /* (vertex, handle) entries with phi > 0                          */
+  double hop_radius;      /* mean over partitions of the max hop distance                  */
+  double t_kmeans, t_connect, t_solve, t_total;   /* host seconds per stage                */
+} ms_basis_info;
+ms_status ms_basis_build(ms_ctx *ctx, int32_t m, uint64_t seed, ms_basis_info *info);
+/* Host-only form of the same construction (no GPU, no context): the global mesh as in
+ * ms_upload_mesh (E and rho per tet; nu is not used) and the Dirichlet vertices.  On success *out
+ * owns the result (free with ms_basis_free); read it with ms_basis_copy (sizes from info). */
+typedef struct ms_basis ms_basis;
+ms_status ms_basis_compute(int64_t n_verts, const double *rest_xyz, int64_t n_tets, const int32_t *tets,
+                           const double *E, const double *rho, int64_t n_dbc, const int32_t *dbc, int32_t m,
+                           uint64_t seed, ms_basis **out, ms_basis_info *info);
+ms_status ms_basis_copy(const ms_basis *b, double *origins, int64_t *vptr, int32_t *handle, double *phi,
+                        double *phi_affine, double affine_origin[3], int32_t *cluster,
+                        int32_t *centroid_vertex);
+void ms_basis_free(ms_basis *b);
+/* Copy out the last ms_basis_build result (sizes from ms_basis_info): origins (m x 3),
+ * vptr (n_verts + 1), handle / phi (nnz_phi), phi_affine (n_verts), affine_origin (3),
+ * cluster (n_tets, handle id of each tet), centroid_vertex (m).  NULL pointers are skipped.
+ * MS_ERR_STATE if no basis was built by this context. */
+ms_status ms_basis_export(ms_ctx *ctx, double *origins, int64_t *vptr, int32_t *handle, double *phi,
+                          double *phi_affine, double affine_origin[3], int32_t *cluster,
+                          int32_t *centroid_vertex);
+
 /* ---------------------------------------------------------------- state */
 /* Set / get positions x and velocities v (n_verts x 3). */
 ms_status ms_set_state(ms_ctx *ctx, const double *x, const double *v);

@@ -9,9 +9,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libmsim.so")
-SOURCES = ["elem.cu", "sparse.cu", "coarse.cu", "chol.cu", "ls.cu", "setup.cpp", "dist.cpp", "abi.cpp"]
+SOURCES = ["elem.cu", "sparse.cu", "coarse.cu", "chol.cu", "ls.cu", "setup.cpp", "dist.cpp", "basis.cpp", "abi.cpp"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC,-O2", "-shared"]
+              "-Xcompiler", "-fPIC,-O2,-fopenmp,-ffp-contract=off", "-shared"]
 
 
 def _nvcc():
@@ -35,7 +35,7 @@ def build(force=False, verbose=True):
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     extra = os.environ.get("MSIM_NVCC_EXTRA", "").split()   # e.g. -DMSIM_HESS_MINB=3 (tuning runs)
     cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"),
-           *[os.path.join(CSRC, s) for s in SOURCES], "-lnccl", "-o", LIB + ".tmp"]
+           *[os.path.join(CSRC, s) for s in SOURCES], "-lnccl", "-lgomp", "-o", LIB + ".tmp"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)

@@ -9,6 +9,7 @@
 #include <new>
 
 #include "common.cuh"
+#include "basis.h"
 
 using namespace msim;
 
@@ -358,6 +359,7 @@ ms_status ms_destroy(ms_ctx *ctx) {
   for (auto e : ctx->c.ev_pool) cudaEventDestroy(e);
   if (ctx->c.h_pinned) cudaFreeHost(ctx->c.h_pinned);
   delete ctx->c.comm;
+  delete ctx->c.built_basis;
   delete ctx;
   return MS_OK;
 }
@@ -375,6 +377,10 @@ ms_status ms_upload_mesh(ms_ctx *ctx, int64_t n_verts, const double *rest_xyz, i
     c.m = 0;
     pcg_reset_graph(c);
     c.nv_glob = (int32_t)n_verts;
+    c.h_Eg.assign(E, E + n_tets);
+    c.h_rhog.assign(rho, rho + n_tets);
+    c.h_dbc_glob.clear();
+    if (c.dist()) c.h_Xg.assign(rest_xyz, rest_xyz + 3 * n_verts);
     if (!c.dist()) {
       c.nv = c.nv_own = (int32_t)n_verts;
       c.nt = c.nt_own = (int32_t)n_tets;
@@ -417,6 +423,7 @@ ms_status ms_set_dirichlet(ms_ctx *ctx, int64_t n, const int32_t *verts) {
     MS_REQUIRE(c.m == 0, MS_ERR_STATE,
                "ms_set_dirichlet after ms_basis_upload: the basis was built for another Dirichlet set");
     std::fill(c.h_fixed.begin(), c.h_fixed.end(), 0);
+    c.h_dbc_glob.assign(verts, verts + n);
     for (int64_t k = 0; k < n; ++k) {
       MS_REQUIRE(verts[k] >= 0 && verts[k] < c.nv_glob, MS_ERR_ARG, "Dirichlet vertex out of range");
       const int32_t l = c.dist() ? c.part.g2l[verts[k]] : verts[k];
@@ -468,14 +475,10 @@ ms_status ms_get_params(ms_ctx *ctx, ms_params *p) {
   return MS_OK;
 }
 
-ms_status ms_basis_upload(ms_ctx *ctx, int32_t m, const double *origins, const int64_t *vptr,
-                          const int32_t *handle, const double *phi, const double *phi_affine,
-                          const double affine_origin[3], int32_t n_cg) {
-  if (!ctx) return MS_ERR_ARG;
-  MS_TRY(ctx, {
-    Ctx &c = ctx->c;
-    require_mesh(c);
-    MS_REQUIRE(origins && vptr && handle && phi && phi_affine && affine_origin, MS_ERR_ARG, "null basis array");
+namespace msim {
+static void basis_upload_impl(Ctx &c, int32_t m, const double *origins, const int64_t *vptr, const int32_t *handle,
+                              const double *phi, const double *phi_affine, const double affine_origin[3],
+                              int32_t n_cg) {
     MS_REQUIRE(n_cg > 0, MS_ERR_ARG, "n_cg must be > 0");
     if (!c.dist()) {
       build_basis_structures(c, m, origins, vptr, handle, phi, phi_affine, affine_origin);
@@ -501,6 +504,130 @@ ms_status ms_basis_upload(ms_ctx *ctx, int32_t m, const double *origins, const i
     }
     c.n_cg_basis = n_cg;
     pcg_reset_graph(c);
+}
+}  // namespace msim
+
+ms_status ms_basis_upload(ms_ctx *ctx, int32_t m, const double *origins, const int64_t *vptr,
+                          const int32_t *handle, const double *phi, const double *phi_affine,
+                          const double affine_origin[3], int32_t n_cg) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    require_mesh(c);
+    MS_REQUIRE(origins && vptr && handle && phi && phi_affine && affine_origin, MS_ERR_ARG, "null basis array");
+    basis_upload_impl(c, m, origins, vptr, handle, phi, phi_affine, affine_origin, n_cg);
+  });
+  return MS_OK;
+}
+
+struct ms_basis {
+  msim::BasisOutput b;
+};
+
+static void fill_info(const BasisOutput &b, ms_basis_info *info) {
+  if (!info) return;
+  info->m = b.m;
+  info->n_cg = b.n_cg;
+  info->n_holes = b.n_holes;
+  info->pad_ = 0;
+  info->nnz_phi = (int64_t)b.phi.size();
+  info->hop_radius = b.hop_radius;
+  info->t_kmeans = b.t_kmeans;
+  info->t_connect = b.t_connect;
+  info->t_solve = b.t_solve;
+  info->t_total = b.t_total;
+}
+
+static void copy_basis(const BasisOutput &b, double *origins, int64_t *vptr, int32_t *handle, double *phi,
+                       double *phi_affine, double affine_origin[3], int32_t *cluster, int32_t *centroid_vertex) {
+  if (origins) std::copy(b.origins.begin(), b.origins.end(), origins);
+  if (vptr) std::copy(b.vptr.begin(), b.vptr.end(), vptr);
+  if (handle) std::copy(b.handle.begin(), b.handle.end(), handle);
+  if (phi) std::copy(b.phi.begin(), b.phi.end(), phi);
+  if (phi_affine) std::copy(b.phi_affine.begin(), b.phi_affine.end(), phi_affine);
+  if (affine_origin) std::copy(b.affine_origin, b.affine_origin + 3, affine_origin);
+  if (cluster) std::copy(b.cluster.begin(), b.cluster.end(), cluster);
+  if (centroid_vertex) std::copy(b.centroid_vertex.begin(), b.centroid_vertex.end(), centroid_vertex);
+}
+
+ms_status ms_basis_compute(int64_t n_verts, const double *rest_xyz, int64_t n_tets, const int32_t *tets,
+                           const double *E, const double *rho, int64_t n_dbc, const int32_t *dbc, int32_t m,
+                           uint64_t seed, ms_basis **out, ms_basis_info *info) {
+  if (!out) return MS_ERR_ARG;
+  *out = nullptr;
+  if (n_verts <= 0 || n_tets <= 0 || !rest_xyz || !tets || !E || !rho || (n_dbc > 0 && !dbc)) return MS_ERR_ARG;
+  if (n_verts >= INT32_MAX / 3 || n_tets >= INT32_MAX / 16) return MS_ERR_ARG;
+  for (int64_t i = 0; i < 4 * n_tets; ++i)
+    if (tets[i] < 0 || tets[i] >= n_verts) return MS_ERR_ARG;
+  for (int64_t k = 0; k < n_dbc; ++k)
+    if (dbc[k] < 0 || dbc[k] >= n_verts) return MS_ERR_ARG;
+  ms_basis *h = new (std::nothrow) ms_basis();
+  if (!h) return MS_ERR_OOM;
+  try {
+    BasisInput in;
+    in.nv = (int32_t)n_verts;
+    in.nt = (int32_t)n_tets;
+    in.X = rest_xyz;
+    in.tets = tets;
+    in.E = E;
+    in.rho = rho;
+    in.dbc.assign(dbc, dbc + n_dbc);
+    build_basis_host(in, m, seed, h->b);
+  } catch (const msim::Error &err) {
+    delete h;
+    return err.code;
+  } catch (const std::bad_alloc &) {
+    delete h;
+    return MS_ERR_OOM;
+  } catch (...) {
+    delete h;
+    return MS_ERR_ARG;
+  }
+  fill_info(h->b, info);
+  *out = h;
+  return MS_OK;
+}
+
+ms_status ms_basis_copy(const ms_basis *h, double *origins, int64_t *vptr, int32_t *handle, double *phi,
+                        double *phi_affine, double affine_origin[3], int32_t *cluster, int32_t *centroid_vertex) {
+  if (!h) return MS_ERR_ARG;
+  copy_basis(h->b, origins, vptr, handle, phi, phi_affine, affine_origin, cluster, centroid_vertex);
+  return MS_OK;
+}
+
+void ms_basis_free(ms_basis *h) { delete h; }
+
+ms_status ms_basis_build(ms_ctx *ctx, int32_t m, uint64_t seed, ms_basis_info *info) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    require_mesh(c);
+    BasisInput in;
+    in.nv = c.nv_glob;
+    in.nt = (int32_t)c.h_Eg.size();
+    in.X = c.dist() ? c.h_Xg.data() : c.h_X.data();
+    in.tets = c.dist() ? c.h_tets_glob.data() : c.h_tets.data();
+    in.E = c.h_Eg.data();
+    in.rho = c.h_rhog.data();
+    in.dbc = c.h_dbc_glob;
+    if (!c.built_basis) c.built_basis = new BasisOutput();
+    BasisOutput &b = *c.built_basis;
+    build_basis_host(in, m, seed, b);
+    basis_upload_impl(c, b.m, b.origins.data(), b.vptr.data(), b.handle.data(), b.phi.data(), b.phi_affine.data(),
+                      b.affine_origin, b.n_cg);
+    fill_info(b, info);
+  });
+  return MS_OK;
+}
+
+ms_status ms_basis_export(ms_ctx *ctx, double *origins, int64_t *vptr, int32_t *handle, double *phi,
+                          double *phi_affine, double affine_origin[3], int32_t *cluster,
+                          int32_t *centroid_vertex) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    MS_REQUIRE(c.built_basis != nullptr, MS_ERR_STATE, "ms_basis_export before ms_basis_build");
+    copy_basis(*c.built_basis, origins, vptr, handle, phi, phi_affine, affine_origin, cluster, centroid_vertex);
   });
   return MS_OK;
 }

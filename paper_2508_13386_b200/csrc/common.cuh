@@ -102,6 +102,9 @@ struct Ctx {
   DBuf<double> halo_send, halo_recv;
   bool dist() const { return part.world > 1; }
   std::vector<double> h_X;          // rest positions (host copy)
+  std::vector<double> h_Xg, h_Eg, h_rhog;   // global rest positions (world > 1) / per-tet E, rho
+  std::vector<int32_t> h_dbc_glob;          // global Dirichlet vertex ids (ms_basis_build)
+  struct BasisOutput *built_basis = nullptr;   // last ms_basis_build result (ms_basis_export)
   std::vector<int32_t> h_tets;
   DBuf<double> X;                   // (nv,3)
   DBuf<int32_t> tets;               // (nt,4)

@@ -55,6 +55,12 @@ class CoarseInfo(C.Structure):
                 ("flops_xorder", C.c_double), ("flops_nd", C.c_double), ("galerkin_flops", C.c_double)]
 
 
+class BasisInfo(C.Structure):
+    _fields_ = [("m", C.c_int32), ("n_cg", C.c_int32), ("n_holes", C.c_int32), ("pad_", C.c_int32),
+                ("nnz_phi", C.c_int64), ("hop_radius", C.c_double), ("t_kmeans", C.c_double),
+                ("t_connect", C.c_double), ("t_solve", C.c_double), ("t_total", C.c_double)]
+
+
 class PcgStats(C.Structure):
     _fields_ = [("iters", C.c_int32), ("rz0", C.c_double), ("rz", C.c_double)]
 
@@ -76,6 +82,12 @@ def _load():
         "ms_set_params": ([P, C.POINTER(Params)], C.c_int32),
         "ms_get_params": ([P, C.POINTER(Params)], C.c_int32),
         "ms_basis_upload": ([P, C.c_int32, D, I64, I32, D, D, D, C.c_int32], C.c_int32),
+        "ms_basis_build": ([P, C.c_int32, C.c_uint64, C.POINTER(BasisInfo)], C.c_int32),
+        "ms_basis_export": ([P, D, I64, I32, D, D, D, I32, I32], C.c_int32),
+        "ms_basis_compute": ([C.c_int64, D, C.c_int64, I32, D, D, C.c_int64, I32, C.c_int32, C.c_uint64,
+                              C.POINTER(C.c_void_p), C.POINTER(BasisInfo)], C.c_int32),
+        "ms_basis_copy": ([P, D, I64, I32, D, D, D, I32, I32], C.c_int32),
+        "ms_basis_free": ([P], None),
         "ms_set_state": ([P, D, D], C.c_int32),
         "ms_get_state": ([P, D, D], C.c_int32),
         "ms_set_step_state": ([P, D, D, D], C.c_int32),
@@ -222,6 +234,17 @@ class Context:
         ph, pa, ao = _f64(phi), _f64(phi_affine), _f64(affine_origin)
         self._chk(lib.ms_basis_upload(self.h, int(m), _d(o), _i64(vp), _i32(hd), _d(ph), _d(pa), _d(ao), int(n_cg)))
         self.m = int(m)
+
+    def basis_build(self, m, seed):
+        """ms_basis_build: native basis construction + upload; returns (info dict, arrays dict)."""
+        info = BasisInfo()
+        self._chk(lib.ms_basis_build(self.h, int(m), C.c_uint64(int(seed)), C.byref(info)))
+        self.m = int(info.m)
+        out = _basis_arrays(self.n_verts, self.n_tets, info)
+        self._chk(lib.ms_basis_export(self.h, _d(out["origins"]), _i64(out["vptr"]), _i32(out["handle"]),
+                                      _d(out["phi"]), _d(out["phi_affine"]), _d(out["affine_origin"]),
+                                      _i32(out["cluster"]), _i32(out["centroid_vertex"])))
+        return {k: getattr(info, k) for k, _ in BasisInfo._fields_ if k != "pad_"}, out
 
     # ---------------------------------------------------------------- state
     def set_state(self, x=None, v=None):
@@ -371,6 +394,39 @@ class Context:
         ci = CoarseInfo()
         self._chk(lib.ms_get_coarse_info(self.h, C.byref(ci)))
         return {k: getattr(ci, k) for k, _ in CoarseInfo._fields_ if k != "pad_"}
+
+
+def _basis_arrays(nv, nt, info):
+    mm, nnz = int(info.m), int(info.nnz_phi)
+    return dict(origins=np.empty((mm, 3)), vptr=np.empty(nv + 1, dtype=np.int64),
+                handle=np.empty(nnz, dtype=np.int32), phi=np.empty(nnz), phi_affine=np.empty(nv),
+                affine_origin=np.empty(3), cluster=np.empty(nt, dtype=np.int32),
+                centroid_vertex=np.empty(mm, dtype=np.int32))
+
+
+def basis_compute(X, tets, E, rho, dbc, m, seed):
+    """Host-only ms_basis_compute (no GPU): returns (info dict, arrays dict)."""
+    X = _f64(X, (-1, 3))
+    tets = np.ascontiguousarray(tets, dtype=np.int32).reshape(-1, 4)
+    E, rho = _f64(E), _f64(rho)
+    dbc = np.ascontiguousarray(dbc, dtype=np.int32)
+    h = C.c_void_p()
+    info = BasisInfo()
+    st = lib.ms_basis_compute(len(X), _d(X), len(tets), _i32(tets), _d(E), _d(rho), len(dbc),
+                              _i32(dbc) if len(dbc) else None, int(m), C.c_uint64(int(seed)), C.byref(h),
+                              C.byref(info))
+    if st != 0:
+        raise MsimError(st, "ms_basis_compute failed")
+    try:
+        out = _basis_arrays(len(X), len(tets), info)
+        st = lib.ms_basis_copy(h, _d(out["origins"]), _i64(out["vptr"]), _i32(out["handle"]), _d(out["phi"]),
+                               _d(out["phi_affine"]), _d(out["affine_origin"]), _i32(out["cluster"]),
+                               _i32(out["centroid_vertex"]))
+        if st != 0:
+            raise MsimError(st, "ms_basis_copy failed")
+    finally:
+        lib.ms_basis_free(h)
+    return {k: getattr(info, k) for k, _ in BasisInfo._fields_ if k != "pad_"}, out
 
 
 def nccl_unique_id():

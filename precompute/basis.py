@@ -463,12 +463,16 @@ def build_basis(scene, m=None, seed=None, workers=None, verbose=False) -> Basis:
                  cluster=assign.astype(np.int32), centroid_vertex=cv)
 
 
-def cached_basis(scene, cache_dir=None, **kw) -> Basis:
-    """Build or load the basis of a scene (cache keyed by scene name, sizes and m)."""
+def cached_basis_path(scene, cache_dir=None):
     cache_dir = cache_dir or os.environ.get("MSIM_CACHE", os.path.join(os.path.dirname(__file__), "..", ".cache"))
-    os.makedirs(cache_dir, exist_ok=True)
     key = f"{scene.name}_{scene.n_verts}_{scene.n_tets}_{scene.m}_{BASIS_VERSION}.npz"
-    path = os.path.join(cache_dir, key)
+    return os.path.join(cache_dir, key)
+
+
+def cached_basis(scene, cache_dir=None, **kw) -> Basis:
+    """Build or load the basis of a scene (cache keyed by scene name, sizes, m and version)."""
+    path = cached_basis_path(scene, cache_dir)
+    os.makedirs(os.path.dirname(path), exist_ok=True)
     if os.path.exists(path):
         return Basis.load(path)
     b = build_basis(scene, **kw)

@@ -19,7 +19,7 @@ def declared_symbols():
 
 def test_header_declares_the_boundary():
     syms = declared_symbols()
-    for name in ["ms_create", "ms_destroy", "ms_upload_mesh", "ms_basis_upload", "ms_timestep",
+    for name in ["ms_create", "ms_destroy", "ms_upload_mesh", "ms_basis_upload", "ms_basis_build", "ms_timestep",
                  "ms_newton_step", "ms_pcg_solve", "ms_eval_elements", "ms_spmv", "ms_export_coarse"]:
         assert name in syms
 

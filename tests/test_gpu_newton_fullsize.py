@@ -26,7 +26,8 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-from precompute.basis import cached_basis  # noqa: E402
+from precompute.basis import cached_basis, cached_basis_path  # noqa: E402
+from oracle import ip  # noqa: E402
 from precompute.mesh import make_scene  # noqa: E402
 from tools import oracle_fixtures as fx  # noqa: E402
 
@@ -41,13 +42,17 @@ def _ctx(c):
         pytest.skip("no CUDA device")
     from paper_2508_13386_b200 import msim
     s = make_scene(c)
+    if c == 5 and not os.path.exists(cached_basis_path(s)):
+        pytest.skip("C5 basis not precomputed (python tools/oracle_fixtures.py needs it; ~1 h of CPU)")
     b = cached_basis(s)
     return s, b, msim.context_from_scene(s, b)
 
 
 def _newton_fixture(c):
     path = fx.fixture_path("newton", c)
-    if not os.path.exists(path):          # compute it (slow at C5: minutes of oracle CPU time)
+    if c == 5 and not os.path.exists(path):
+        pytest.skip("C5 oracle fixture not precomputed (tools/oracle_fixtures.py newton 5)")
+    if not os.path.exists(path):          # compute it (C1-C4: a few minutes of oracle CPU time)
         os.makedirs(fx.FIX_DIR, exist_ok=True)
         np.savez(path, **fx.newton_fixture(c, verbose=False))
     return dict(np.load(path))
@@ -55,8 +60,9 @@ def _newton_fixture(c):
 
 @pytest.mark.parametrize("c", [1, 2, 3, 4, 5], ids=["C1", "C2", "C3", "C4", "C5"])
 def test_fullsize_newton_bootstrapped(c):
-    s, b, ctx = _ctx(c)
     f = _newton_fixture(c)
+    s, b, ctx = _ctx(c)
+    model = ip.make_model(s)
     diag = np.linalg.norm(s.X.max(0) - s.X.min(0))
     for it in range(int(f["n_iter"])):
         ctx.set_step_state(f["x_t"], f["xhat"], f[f"x{it}"])
@@ -67,7 +73,8 @@ def test_fullsize_newton_bootstrapped(c):
         assert rel_err(ds + df, f[f"d{it}"]) < 1e-8, (c, it, rel_err(ds + df, f[f"d{it}"]))
         assert abs(st.alpha0 - a0) <= 1e-8 * a0, (c, it, st.alpha0, a0)
         assert abs(st.ds_norm - dsn) <= 1e-8 * dsn
-        assert abs(st.energy - energy) <= 1e-10 * abs(energy)
+        e0 = ip.energy(model, f[f"x{it}"], f["xhat"])        # E(x) at the start of the iteration
+        assert abs(st.energy - e0) <= 1e-10 * abs(e0), (c, it, st.energy, e0)
         assert bool(st.ls_failed) == bool(failed)
         if not failed:
             assert st.ls_evals == int(evals), (c, it, st.ls_evals, evals)
