@@ -74,7 +74,8 @@ def test_fullsize_newton_bootstrapped(c):
         assert abs(st.alpha0 - a0) <= 1e-8 * a0, (c, it, st.alpha0, a0)
         assert abs(st.ds_norm - dsn) <= 1e-8 * dsn
         e0 = ip.energy(model, f[f"x{it}"], f["xhat"])        # E(x) at the start of the iteration
-        assert abs(st.energy - e0) <= 1e-10 * abs(e0), (c, it, st.energy, e0)
+        # E is a sum of terms that cancel to first order near rest (rest-stable Psi): 1e-9
+        assert abs(st.energy - e0) <= 1e-9 * abs(e0), (c, it, st.energy, e0)
         assert bool(st.ls_failed) == bool(failed)
         if not failed:
             assert st.ls_evals == int(evals), (c, it, st.ls_evals, evals)
