@@ -57,7 +57,11 @@ typedef struct ms_params {
   double filter_safety;   /* CCD / inversion filter safety factor                          */
   int32_t ls_batch;       /* candidate step sizes evaluated per fused line-search pass     */
   int32_t use_graphs;     /* capture the fixed-count PCG loop in a CUDA graph              */
+  int32_t debug_flags;    /* parity hooks, 0 in production: MS_DEBUG_HESS_FALLBACK routes
+                             every indefinite element Hessian to the cyclic-Jacobi eigen-clamp
+                             (the fall-back path of the tridiagonal-QL projection)           */
 } ms_params;
+enum { MS_DEBUG_HESS_FALLBACK = 1 };
 
 typedef struct ms_newton_stats {
   double alpha;           /* accepted step (0 if the line search failed)                   */

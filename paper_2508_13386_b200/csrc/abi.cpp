@@ -249,6 +249,7 @@ void ms_default_params(ms_params *p) {
   p->filter_safety = 0.9;
   p->ls_batch = 4;
   p->use_graphs = 1;
+  p->debug_flags = 0;
 }
 
 static ms_status create_common(ms_ctx **out, int device, void *cuda_stream, int rank, int world,
@@ -862,7 +863,7 @@ ms_status ms_export_coarse(ms_ctx *ctx, double *S, double *Sa) {
     Ctx &c = ctx->c;
     require_basis(c);
     MS_REQUIRE(c.assembled, MS_ERR_STATE, "nothing assembled yet");
-    launch_coarse_S(c);
+    launch_coarse_S(c, true);
     if (S) {
       std::vector<double> blk((size_t)144 * c.nnzb_S);
       c.Sblk.download(blk.data(), blk.size(), c.stream);

@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "fastmath.cuh"
+#include "galerkin.cuh"
 
 namespace msim {
 
@@ -264,6 +265,11 @@ struct DfParams {
   int *ndep;                   // counted inputs still missing per task
   int *queue;                  // queue q at q * qstride: [head, tail, task ids (-1: not yet pushed)]
   int *done;                   // queue tasks finished
+  // fused Galerkin rows (c.gal_fused): G(i, part) / R(i) tasks; rw_ptr == nullptr otherwise
+  GalParams gal;
+  const int32_t *perm;         // handle -> position of its 12 rows in the factor
+  int *rdone;                  // [m] R(i) finished (chain CTA waits)
+  const int32_t *rw_ptr, *rw;  // per chain task: the handles whose R(i) it waits for
 };
 
 // successors [b, e) of a finished task: one input fewer each.  A queue task whose last input
@@ -392,6 +398,8 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
       // updates are done) and the diagonal tile A_ii (its earlier updates are done)
       double *SA = sm, *SU = sm + TB * TB;
       const size_t oik = tile_off(i, k, nSp), oii = tile_off(i, i, nSp);
+      if (P.rw_ptr)   // fused Galerkin: the rows of S this task reads unfactored
+        for (int q2 = P.rw_ptr[ccur - 1]; q2 < P.rw_ptr[ccur]; ++q2) df_wait(&P.rdone[P.rw[q2]], 1);
       df_wait2(&upd[i * NT + k], cnt & 0xffff, &upd[i * NT + i], cnt >> 16);
       stage_colmajor(SA, L + oik, nSp);
       asm volatile("cp.async.commit_group;\n" ::);
@@ -438,9 +446,18 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
       diag_factor(i, nSp, L, U, flag, sm, true);
       df_signal2(&dfl[i], 1, &upd[i * NT + i], (cnt >> 16) + 1);
       my_d = i;
+    } else if (type == 5) {
+      // G(i, part): a quarter of handle i's Galerkin row into its partial row (galerkin.cuh)
+      galerkin_row(P.gal, i, j, sm);
+      if (t == 0) __threadfence();   // the partial row before R(i) is released
+      __syncthreads();
+      df_release(P, P.succ_ptr[id], P.succ_ptr[id + 1], &s_keep);
+    } else if (type == 6) {
+      // R(i): the parts summed in a fixed order, scattered into the factor's tiles
+      galerkin_reduce_to_tiles(P.gal, i, P.perm, nSp, L);
+      df_signal(&P.rdone[i], 1);
+      df_release(P, P.succ_ptr[id], P.succ_ptr[id + 1], &s_keep);
     } else if (type == 1) {
-
-
       double *SA = sm, *SU = sm + TB * TB;
       const size_t oik = tile_off(i, k, nSp);
       stage_colmajor(SA, L + oik, nSp);
@@ -667,7 +684,7 @@ void chol_init_attrs(Ctx &c) {
   MS_CUDA(cudaFuncSetAttribute(k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDiagSmem));
   MS_CUDA(cudaFuncSetAttribute(k_chol_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem));
   MS_CUDA(cudaFuncSetAttribute(k_chol_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem));
-  MS_CUDA(cudaFuncSetAttribute(k_chol_dataflow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem));
+  set_max_dyn_smem((const void *)k_chol_dataflow, c.device);
   int per_sm = 0;
   MS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chol_dataflow, 256, kUpdSmem));
   const char *e = std::getenv("MSIM_DF_PER_SM");
@@ -697,7 +714,7 @@ void enqueue_chol_factor(Ctx &c) {
   if (nSp > c.nS) k_pad_identity2<<<div_up(nSp - c.nS, 64), 64, 0, c.stream>>>(c.nS, nSp, c.Lden);
   if (c.chol_dataflow) {
     const int NT = c.ntiles;
-    MS_CUDA(cudaMemsetAsync(c.df_flags, 0, sizeof(int) * ((size_t)2 * NT * NT + NT + 1), c.stream));
+    MS_CUDA(cudaMemsetAsync(c.df_flags, 0, sizeof(int) * c.df_flags.n, c.stream));
     MS_CUDA(cudaMemcpyAsync(c.chol_ndep.p, c.chol_ndep0.p, sizeof(int32_t) * c.chol_ndep0.n,
                             cudaMemcpyDeviceToDevice, c.stream));
     MS_CUDA(cudaMemcpyAsync(c.chol_queue.p, c.chol_queue0.p, sizeof(int32_t) * c.chol_queue0.n,
@@ -728,9 +745,22 @@ void enqueue_chol_factor(Ctx &c) {
     prm.done = c.chol_queue + 2 * prm.qstride;
     prm.per_sm = c.df_per_sm;
     prm.chain_sm = c.df_flags + (size_t)2 * NT * NT + NT;   // zeroed with the flags
+    size_t smem = kUpdSmem;
+    if (c.gal_fused) {
+      prm.gal = galerkin_params(c);
+      prm.perm = c.perm;
+      prm.rdone = c.df_flags + (size_t)2 * NT * NT + NT + 1;
+      prm.rw_ptr = c.chol_rw_ptr;
+      prm.rw = c.chol_rw;
+      smem = std::max(smem, sizeof(double) * galerkin_smem_doubles(c.gal_max_jup));
+    } else {
+      prm.perm = nullptr;
+      prm.rdone = nullptr;
+      prm.rw_ptr = prm.rw = nullptr;
+    }
     void *args[] = {&prm};
     MS_CUDA(cudaLaunchCooperativeKernel((const void *)k_chol_dataflow, dim3(dataflow_grid(c)), dim3(256), args,
-                                        kUpdSmem, c.stream));
+                                        smem, c.stream));
     return;
   }
   k_chol_diag<<<1, 256, kDiagSmem, c.stream>>>(0, nSp, c.Lden, c.Uinv, c.flags + 0);

@@ -193,9 +193,9 @@ __global__ void k_galerkin_Sa_final(int nch, const double *__restrict__ part, do
   Sa[row * 12 + 4 * c + k] = s;
 }
 
-static HView hview(const Ctx &c) { return HView{c.sl_ptr, c.sell_col, c.vals}; }
+HView hview(const Ctx &c) { return HView{c.sl_ptr, c.sell_col, c.vals}; }
 
-static GalParams galerkin_params(const Ctx &c) {
+GalParams galerkin_params(const Ctx &c) {
   GalParams G;
   G.H = hview(c);
   G.gU_ptr = c.gU_ptr;
@@ -210,6 +210,7 @@ static GalParams galerkin_params(const Ctx &c) {
   G.gl_ent = c.gl_ent;
   G.W = c.Wphi;
   G.sT = c.sT;
+  G.scol = c.scol;
   G.S = c.Sblk;
   G.Spart = c.Spart;
   G.nparts = c.gal_parts;
@@ -301,21 +302,26 @@ void launch_basis_W(Ctx &c) {
 }
 
 // ------------------------------------------------------------------ launchers
-// per context, on its device (create_common): the fused Galerkin kernel's opt-in is raised to the
-// largest row any basis can use (227 KB), never lowered
-void coarse_init_attrs(Ctx &) {
-  MS_CUDA(cudaFuncSetAttribute(k_galerkin_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+// per context, on its device (create_common): the Galerkin kernel's opt-in is raised to the
+// device maximum once (never lowered: a launch uses what its basis needs)
+void coarse_init_attrs(Ctx &c) {
+  set_max_dyn_smem((const void *)k_galerkin_fused, c.device);
 }
 
-void launch_coarse_S(Ctx &c) {
-  const size_t smem = sizeof(double) * galerkin_smem_doubles(c.gal_max_jup);
-  MS_REQUIRE(smem <= 227 * 1024, MS_ERR_ARG, "coarse S row too wide for the fused Galerkin kernel");
-  const GalParams G = galerkin_params(c);
-  k_galerkin_fused<<<c.m * G.nparts, kGalThreads, smem, c.stream>>>(G);
-  c.launches++;
-  if (G.nparts > 1) {
-    k_galerkin_reduce<<<c.m, 256, 0, c.stream>>>(G);
+// S = B^T H B into Sblk (full_S, or whenever the Galerkin rows are not fused into the factor
+// launch) and S_a = U_a^T H U_a.  With c.gal_fused the rows of S are formed by the factorisation
+// launch itself (chol.cu: G / R tasks write straight into the factor's tiles).
+void launch_coarse_S(Ctx &c, bool full_S) {
+  if (full_S || !c.gal_fused) {
+    const size_t smem = sizeof(double) * galerkin_smem_doubles(c.gal_max_jup);
+    MS_REQUIRE(smem <= 227 * 1024, MS_ERR_ARG, "coarse S row too wide for the fused Galerkin kernel");
+    const GalParams G = galerkin_params(c);
+    k_galerkin_fused<<<c.m * G.nparts, kGalThreads, smem, c.stream>>>(G);
     c.launches++;
+    if (G.nparts > 1) {
+      k_galerkin_reduce<<<c.m, 256, 0, c.stream>>>(G);
+      c.launches++;
+    }
   }
   const double *o = c.aff_origin;
   k_galerkin_Ra<<<div_up(c.nv, 128), 128, 0, c.stream>>>(c.nv, hview(c), c.phi_aff, c.X, o[0], o[1], o[2], c.Ra);

@@ -77,6 +77,11 @@ struct Reducer {
 // block starts 16-byte aligned (the assembly gathers it with 5 vector loads)
 constexpr int kStageB = 10, kStageH = 10 * kStageB;
 constexpr int kGalChunk = 128;   // vertices of U_i per Galerkin chunk (7-bit local index)
+constexpr int kGalThreads = 2 * kGalChunk;
+// shared memory of one Galerkin row CTA (galerkin.cuh): R chunk, staged entries, S accumulators
+__host__ __device__ constexpr size_t galerkin_smem_doubles(int max_jup) {
+  return (size_t)kGalChunk * 36 + (kGalThreads / 32) * (32 * 4 + 16) + (size_t)max_jup * 144;
+}
 
 struct CholTask {      // one trailing update A_ij -= L_ik L_jk^T (tiles)
   int32_t i, j;
@@ -197,6 +202,9 @@ struct Ctx {
   DBuf<int32_t> chol_ndep0, chol_ndep;                     // inputs per task: pristine / live
   DBuf<int32_t> chol_queue0, chol_queue;                   // two ready queues: pristine / live
   int64_t n_crit = 0, n_pool = 0;
+  bool gal_fused = false;           // Galerkin row tasks inside the factorisation launch (chol.cu)
+  int64_t n_dag_factor = 0;         // factor tasks (the fused Galerkin tasks follow them)
+  DBuf<int32_t> chol_rw_ptr, chol_rw;   // per chain task: handles whose R(i) it waits for
   int df_hi_ctas = 64;   // CTAs serving the high-priority queue
   int df_per_sm = 1;     // dataflow factorisation CTAs per SM (chol_init_attrs)
   int64_t n_dag = 0;
@@ -267,6 +275,16 @@ constexpr int kMaxLS = 16;
 
 inline int div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
+// raise a kernel's dynamic shared-memory opt-in to the device maximum (minus its static shared
+// memory); per device, so called per context on its device (create_common)
+inline void set_max_dyn_smem(const void *func, int device) {
+  int optin = 0;
+  MS_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  cudaFuncAttributes fa;
+  MS_CUDA(cudaFuncGetAttributes(&fa, func));
+  MS_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
+}
+
 // kernels (defined in the .cu files); every launcher increments ctx.launches
 void launch_elem_grad(Ctx &c);
 void launch_elem_hess(Ctx &c);
@@ -276,7 +294,7 @@ void launch_assemble(Ctx &c);
 void launch_spmv(Ctx &c, const double *xin, double *yout, double alpha_minus_b, const double *b);
 void launch_pcg(Ctx &c, const double *rhs, double *sol, int iters);
 void pcg_reset_graph(Ctx &c);
-void launch_coarse_S(Ctx &c);
+void launch_coarse_S(Ctx &c, bool full_S = false);
 // multi-GPU helpers (abi.cpp): no-ops when world == 1
 void dist_sum(Ctx &c, double *dev, int64_t n);
 void dist_min(Ctx &c, double *dev, int64_t n);

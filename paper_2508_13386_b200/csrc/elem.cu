@@ -455,7 +455,7 @@ constexpr int kHessStg = kStageH + 1;
 __global__ void __launch_bounds__(kHessThreads, MSIM_HESS_MINB) k_elem_hess(MeshView M, const double *__restrict__ x,
                                                             double *__restrict__ stage_h,
                                                             int32_t *__restrict__ work,
-                                                            unsigned int *__restrict__ nwork) {
+                                                            unsigned int *__restrict__ nwork, int force_fallback) {
   extern __shared__ double hsm[];   // eig9 scratch [kHessScratch][kHessThreads] / store staging
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, wbase = threadIdx.x & ~31;
@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(kHessThreads, MSIM_HESS_MINB) k_elem_hess(Mesh
 #pragma unroll
       for (int q = 0; q < 45; ++q) p9[q] = a[q];
       store = true;
-    } else if (e9::psd_project<kMaxNeg>(a, p9, hsm + threadIdx.x, kHessThreads) >= 0) {
+    } else if (!force_fallback && e9::psd_project<kMaxNeg>(a, p9, hsm + threadIdx.x, kHessThreads) >= 0) {
       store = true;
     } else {
       work[atomicAdd(nwork, 1u)] = e;
@@ -542,7 +542,7 @@ void launch_elem_hess_to(Ctx &c, const double *x) {
   MS_CUDA(cudaMemsetAsync(c.hess_nwork, 0, sizeof(unsigned int), c.stream));
   constexpr int smem = kHessSmem;
   k_elem_hess<<<div_up(c.nt, kHessThreads), kHessThreads, smem, c.stream>>>(
-      mesh_view(c), x, c.stage_h, c.hess_work, c.hess_nwork);
+      mesh_view(c), x, c.stage_h, c.hess_work, c.hess_nwork, (c.params.debug_flags & MS_DEBUG_HESS_FALLBACK) ? 1 : 0);
   k_elem_hess_eig<<<148 * 2, 128, 0, c.stream>>>(mesh_view(c), x, c.stage_h, c.hess_work, c.hess_nwork);
   c.launches += 2;
   static const bool dbg = std::getenv("MSIM_DEBUG_HESS") != nullptr;   // diagnostics only

@@ -20,17 +20,17 @@ struct GalParams {
   const uint32_t *gl_ent;
   const double *W;
   const int32_t *sT;
+  const int32_t *scol;              // S pattern columns (handle j of block b)
   double *S;                        // [nnzb_S][144] block storage
   double *Spart;                    // [m * nparts][pstride] partial rows (nparts > 1)
   int nparts, pstride;
 };
 
-constexpr int kGalThreads = 2 * kGalChunk;
+
+GalParams galerkin_params(const Ctx &c);
+HView hview(const Ctx &c);
 constexpr int kGalWarps = kGalThreads / 32;
 
-__host__ __device__ constexpr size_t galerkin_smem_doubles(int max_jup) {
-  return (size_t)kGalChunk * 36 + kGalWarps * (32 * 4 + 16) + (size_t)max_jup * 144;
-}
 
 // One CTA per handle i computes the upper block row S_ij (j >= i) with R_i never leaving the
 // SM.  For each chunk of kGalChunk vertices u of U_i:
@@ -228,6 +228,28 @@ __device__ __forceinline__ void galerkin_reduce_row(const GalParams &G, int i) {
     G.S[144 * (size_t)b + row * 12 + 4 * cc + k] = val;
     const int bt = __ldg(&G.sT[b]);
     if (bt != b) G.S[144 * (size_t)bt + (4 * cc + k) * 12 + row] = val;
+  }
+}
+
+// Fused form (chol.cu task R(i)): the parts of handle i's row summed in the same fixed order,
+// scattered straight into the lower triangle of the padded dense factor array L (column-major,
+// handle i at rows 12 perm[i] ..): block S_ij (j >= i) lands at (12 perm[i] + row, 12 perm[j] + col)
+// if that is in the lower triangle, else (its transposed image) at the mirrored position; of the
+// diagonal block only the lower triangle is written (as k_scatter_S does).
+__device__ __forceinline__ void galerkin_reduce_to_tiles(const GalParams &G, int i, const int32_t *__restrict__ perm,
+                                                         int nSp, double *__restrict__ L) {
+  const int j0 = G.gj_ptr[i], nup = G.gj_ptr[i + 1] - j0;
+  const double *src = G.Spart + (size_t)i * G.nparts * G.pstride;
+  const int pi = 12 * perm[i];
+  for (int e = threadIdx.x; e < nup * 144; e += blockDim.x) {
+    double val = __ldcg(&src[e]);
+    for (int p = 1; p < G.nparts; ++p) val += __ldcg(&src[(size_t)p * G.pstride + e]);
+    const int q = e / 144, r = e % 144, k = r / 36, l = r % 36;
+    const int row = l / 3, cc = l % 3;
+    const int j = __ldg(&G.scol[__ldg(&G.gj_blk[j0 + q])]);
+    const int R = pi + row, C = 12 * perm[j] + 4 * cc + k;
+    if (R >= C) L[(size_t)C * nSp + R] = val;
+    else if (j != i) L[(size_t)R * nSp + C] = val;
   }
 }
 

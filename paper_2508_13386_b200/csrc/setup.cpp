@@ -658,8 +658,115 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   // is handed out through one of two ready queues (served by disjoint CTA sets) as soon as its
   // inputs exist
   std::vector<int32_t> crit, succ_ptr, succ_mid, succ, ndep;
-  std::vector<uint8_t> cls(c.n_dag, 0);
   dataflow_graph(dag, NT, succ_ptr, succ_mid, succ, ndep);
+  {
+    const char *e = std::getenv("MSIM_GAL_PARTS");   // tuning / diagnostics
+    c.gal_parts = e ? std::max(1, std::atoi(e)) : 4;
+  }
+  // ---- fused Galerkin (single GPU): the Galerkin rows of S are tasks of the same dataflow
+  // launch, G(i, part) (a quarter of handle i's row, galerkin.cuh) and R(i) (sum of the parts in
+  // a fixed order, scattered into the factor's tiles).  The task that first reads a tile's
+  // unfactored values (the first update / panel / diagonal factor of that tile) waits for every
+  // R(i) that writes into it: counted inputs for queue tasks, flag waits (rwait) for CTA 0's
+  // chain.  G tasks are the only initially ready tasks, queued in handle order, so the rows of
+  // the first tile columns are formed first and the factorisation starts while the rest of S is
+  // still being projected.
+  std::vector<int32_t> rw_ptr(1, 0), rw;
+  {
+    // opt-in (MSIM_GAL_FUSED=1): measured at C4 it does not pay yet -- the Galerkin rows are
+    // throughput-bound (~2.2 ms of the whole GPU), so running them inside the factor launch only
+    // delays the factor's own bulk updates (4.6 -> 4.7 ms for S + factor)
+    const char *e = std::getenv("MSIM_GAL_FUSED");
+    bool has_chain = false;
+    for (int64_t q = 0; q < c.n_dag; ++q) has_chain |= dag[4 * q] == 4;
+    // two CTAs per SM must still fit beside the Galerkin rows' shared memory (chol.cu)
+    const bool fits = sizeof(double) * galerkin_smem_doubles(max_jup) <= 110 * 1024;
+    c.gal_fused = !c.dist() && (e && e[0] == '1') && c.gal_parts > 1 && has_chain && fits;
+  }
+  c.n_dag_factor = c.n_dag;
+  if (c.gal_fused) {
+    const int64_t n0 = c.n_dag, np = c.gal_parts;
+    const int64_t gid0 = n0, rid0 = n0 + (int64_t)m * np;
+    // raw reader of every tile: the task that first reads its unfactored values
+    std::vector<int32_t> raw((size_t)NT * NT, -1);
+    for (int64_t q = 0; q < n0; ++q) {
+      const int ty = dag[4 * q], i = dag[4 * q + 1], j = dag[4 * q + 2] & 0xffff, k = dag[4 * q + 2] >> 16,
+                cnt = dag[4 * q + 3];
+      auto mark_raw = [&](int a, int b) {
+        if (raw[(size_t)a * NT + b] < 0) raw[(size_t)a * NT + b] = (int32_t)q;
+      };
+      if (ty == 0 && cnt == 0) mark_raw(k, k);
+      if (ty == 4) {
+        if ((cnt & 0xffff) == 0) mark_raw(i, k);
+        if ((cnt >> 16) == 0) mark_raw(i, i);
+      }
+      if (ty == 1 && cnt == 0) mark_raw(i, k);
+      if (ty == 2 && cnt == 0) mark_raw(i, j);
+    }
+    // R(i) -> raw readers of the tiles its blocks S_ij (j >= i, both triangles' lower images) hit
+    std::vector<std::vector<int32_t>> rsucc(m);
+    std::vector<std::vector<int32_t>> chain_wait(c.n_dag);   // type-4 raw readers: handles to wait for
+    for (int32_t i = 0; i < m; ++i) {
+      const int pi = 12 * c.h_perm[i];
+      const int ti0 = pi / T, ti1 = (pi + 11) / T;
+      std::vector<int32_t> succ_i;
+      for (int32_t b = gj_ptr[i]; b < gj_ptr[i + 1]; ++b) {
+        const int32_t j = scol[gj_blk[b]];
+        const int pj = 12 * c.h_perm[j];
+        const int tj0 = pj / T, tj1 = (pj + 11) / T;
+        for (int a = ti0; a <= ti1; ++a)
+          for (int bb = tj0; bb <= tj1; ++bb) {
+            const int I = std::max(a, bb), J = std::min(a, bb);
+            const int32_t q = raw[(size_t)I * NT + J];
+            MS_REQUIRE(q >= 0, MS_ERR_STATE, "fused Galerkin: S block outside the symbolic factor");
+            if (dag[4 * q] == 4) chain_wait[q].push_back(i);
+            else succ_i.push_back(q);
+          }
+      }
+      std::sort(succ_i.begin(), succ_i.end());
+      succ_i.erase(std::unique(succ_i.begin(), succ_i.end()), succ_i.end());
+      for (int32_t q : succ_i) ndep[q]++;
+      rsucc[i] = std::move(succ_i);
+    }
+    // append the tasks: G(i, p) = gid0 + i np + p, R(i) = rid0 + i
+    for (int32_t i = 0; i < m; ++i)
+      for (int p = 0; p < np; ++p) {
+        dag.push_back(5);
+        dag.push_back(i);
+        dag.push_back(p);
+        dag.push_back(0);
+      }
+    for (int32_t i = 0; i < m; ++i) {
+      dag.push_back(6);
+      dag.push_back(i);
+      dag.push_back(0);
+      dag.push_back(0);
+    }
+    for (int32_t i = 0; i < m; ++i)
+      for (int p = 0; p < np; ++p) {
+        succ_mid.push_back((int32_t)succ.size());
+        succ.push_back((int32_t)(rid0 + i));
+        succ_ptr.push_back((int32_t)succ.size());
+        ndep.push_back(0);
+      }
+    for (int32_t i = 0; i < m; ++i) {
+      succ_mid.push_back((int32_t)succ.size());
+      succ.insert(succ.end(), rsucc[i].begin(), rsucc[i].end());
+      succ_ptr.push_back((int32_t)succ.size());
+      ndep.push_back((int32_t)np);
+    }
+    (void)gid0;
+    c.n_dag = (int64_t)dag.size() / 4;
+    for (int64_t q = 0; q < n0; ++q)
+      if (dag[4 * q] == 4) {
+        auto &l = chain_wait[q];
+        std::sort(l.begin(), l.end());
+        l.erase(std::unique(l.begin(), l.end()), l.end());
+        rw.insert(rw.end(), l.begin(), l.end());
+        rw_ptr.push_back((int32_t)rw.size());
+      }
+  }
+  std::vector<uint8_t> cls(c.n_dag, 0);
   c.n_pool = 0;
   int hi_dj = 2;   // measured best at C4 (2..4)
   {
@@ -671,7 +778,7 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
     // high: diagonal factors, panel tiles, and the updates of tiles that become panel tiles
     // within hi_dj steps: each band row is a chain P(i,k) -> U(i,k+1,k) -> P(i,k+1) -> ... fed by
     // the update chains of its tiles, which must not queue behind the bulk updates
-    cls[q] = ty == 4 ? 2 : (ty == 0 || ty == 1 || j <= k + hi_dj) ? 1 : 0;
+    cls[q] = ty == 4 ? 2 : ty == 5 ? 0 : ty == 6 ? 1 : (ty == 0 || ty == 1 || j <= k + hi_dj) ? 1 : 0;
     if (ty == 4) crit.push_back((int32_t)q);
     else c.n_pool++;
   }
@@ -731,10 +838,6 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
     c.sT.upload(sT, s);
   }
   c.Sblk.alloc((size_t)144 * c.nnzb_S);
-  {
-    const char *e = std::getenv("MSIM_GAL_PARTS");   // tuning / diagnostics
-    c.gal_parts = e ? std::max(1, std::atoi(e)) : 4;
-  }
   if (c.gal_parts > 1) c.Spart.alloc((size_t)m * c.gal_parts * 144 * (size_t)std::max(c.gal_max_jup, 1));
   c.gU_ptr.upload(Uptr, s);
   c.gU.upload(Uall, s);
@@ -756,6 +859,8 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   c.sym_tiles.upload(sym_tiles, s);
   c.chol_dag.upload(dag, s);
   c.chol_crit.upload(crit, s);
+  c.chol_rw_ptr.upload(rw_ptr, s);
+  c.chol_rw.upload(rw.empty() ? std::vector<int32_t>{0} : rw, s);
   c.chol_cls.upload(cls, s);
   c.chol_succ_ptr.upload(succ_ptr, s);
   c.chol_succ_mid.upload(succ_mid, s);
@@ -768,7 +873,7 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
     const char *e = std::getenv("MSIM_CHOL_DATAFLOW");   // 0: per-step launches (diagnostics)
     c.chol_dataflow = !(e && e[0] == '0');
   }
-  c.df_flags.alloc((size_t)2 * NT * NT + NT + 1);
+  c.df_flags.alloc((size_t)2 * NT * NT + NT + 1 + m);   // upd, pfl, dfl, chain SM, rdone[m]
   c.Uinv.alloc((size_t)NT * T * T);
   {
     int nsm = 0;

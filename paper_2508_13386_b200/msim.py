@@ -28,7 +28,7 @@ class Params(C.Structure):
     _fields_ = [("h", C.c_double), ("gravity", C.c_double * 3), ("eps", C.c_double),
                 ("max_newton", C.c_int32), ("n_cg", C.c_int32), ("ls_shrink", C.c_double),
                 ("ls_min", C.c_double), ("filter_safety", C.c_double), ("ls_batch", C.c_int32),
-                ("use_graphs", C.c_int32)]
+                ("use_graphs", C.c_int32), ("debug_flags", C.c_int32)]
 
 
 class NewtonStats(C.Structure):

@@ -93,6 +93,27 @@ def test_element_parity_large_strain(msim):
     assert per_element_rel(He[ok], H_o) < 1e-10
 
 
+@pytest.mark.parametrize("name,amp", [("drop", 0.08), ("c1", 0.3)])
+def test_element_hessian_fallback_parity(msim, name, amp):
+    """The cyclic-Jacobi fall-back of the PSD projection (k_elem_hess_eig, taken by tets with more
+    than kMaxNeg negative eigenvalues or without QL convergence) forced for every indefinite
+    element (MS_DEBUG_HESS_FALLBACK) and checked against the oracle's eigen-clamp (R2)."""
+    s, b = scene_and_basis(name)
+    ctx = msim.context_from_scene(s, b, debug_flags=1)
+    m = ip.make_model(s)
+    x = perturbed(s, amp, seed=11)
+    E_o = fem.element_energy(x, m.tets, m.Bm, m.V, m.mu, m.lam)
+    ok = np.isfinite(E_o)
+    assert ok.mean() > 0.5
+    _, _, He = ctx.eval_elements(x)
+    H_o = fem.element_hessian_psd(x, m.tets[ok], m.Bm[ok], m.V[ok], m.mu[ok], m.lam[ok])
+    assert per_element_rel(He[ok], H_o) < 1e-10
+    w = np.linalg.eigvalsh(fem.element_hessian(x, m.tets[ok], m.Bm[ok], m.V[ok], m.mu[ok], m.lam[ok]))
+    neg = (w < -1e-8 * np.abs(w).max(axis=1, keepdims=True)).sum(axis=1)
+    assert np.mean(neg > 0) > 0.2          # the fall-back really ran on many elements
+    assert neg.max() >= 3
+
+
 # ----------------------------------------------------------------------------- assembly
 @pytest.mark.parametrize("name", ["c1", "drop", "c2"])
 def test_assembly_spmv_parity(msim, name):
