@@ -49,10 +49,72 @@ def pcg(H, r, n_iter, Dinv=None):
     return d
 
 
-def subspace_direction(H, g, Ua, Us):
-    """Alg. 2 SolveSubspaceDirection with exact coarse solves and rhs -g (R4, R6).
+def block_jacobi_pcg(apply_S, b, blocks, tol, max_iter):
+    """PCG on S q = b from q = 0 with the block-Jacobi preconditioner z = blockdiag(S_ii)^-1 r
+    (12 x 12 blocks, one per handle: P:463-464) until ||r_k||_2 <= tol ||b||_2 ('a relative
+    residual of 1e-4', reading C1 of DESIGN.md: unpreconditioned 2-norm, relative to the initial
+    residual b) or max_iter iterations (NEXT-1).  apply_S(p) = S p (matrix-free,
+    P:457-462); blocks: (n_handles, 12, 12).  Returns (q, iterations, ||r||_2 / ||b||_2)."""
+    b = np.asarray(b, dtype=np.float64).ravel()
+    nb = np.linalg.norm(b)
+    q = np.zeros_like(b)
+    if nb == 0.0:
+        return q, 0, 0.0
+    Linv = [np.linalg.inv(np.linalg.cholesky(B)) for B in blocks]   # S_ii^-1 = L^-T L^-1
 
-    Returns d_s, d_a and the coarse matrices S_a, S."""
+    def precond(r):
+        rr = r.reshape(-1, 12)
+        return np.concatenate([Li.T @ (Li @ rr[k]) for k, Li in enumerate(Linv)])
+
+    r = b.copy()
+    z = precond(r)
+    p = z.copy()
+    rho = r @ z
+    it = 0
+    while it < max_iter and np.linalg.norm(r) > tol * nb:
+        t = apply_S(p)
+        alpha = rho / (p @ t)
+        q = q + alpha * p
+        r = r - alpha * t
+        it += 1
+        if np.linalg.norm(r) <= tol * nb:
+            break
+        z = precond(r)
+        rho_new = r @ z
+        p = z + (rho_new / rho) * p
+        rho = rho_new
+    return q, it, float(np.linalg.norm(r) / nb)
+
+
+def galerkin_diagonal_blocks(U, H):
+    """The 12 x 12 diagonal blocks (U_i^T H U_i) of the sandwich matrix, one per handle i
+    (the block-Jacobi preconditioner of P:463-464), each by its definition."""
+    H = H.tocsr()
+    Uc = U.tocsc()
+    nh = U.shape[1] // 12
+    return np.array([(Uc[:, 12 * i:12 * i + 12].T @ (H @ Uc[:, 12 * i:12 * i + 12])).toarray() for i in range(nh)])
+
+
+def subspace_direction(H, g, Ua, Us, coarse_mode="exact", tol=1e-4, max_iter=None):
+    """Alg. 2 SolveSubspaceDirection with rhs -g (R6).  coarse_mode = "exact": Cholesky solves (R4);
+    "pcg": the paper's solves: block-Jacobi PCG to relative residual tol on
+    the matrix-free sandwich U^T H U p = U^T (H (U p)) (NEXT-1; max_iter caps the iterations,
+    None = no cap).  In "pcg" mode S_a / S are not formed; the returned "matrices" are then the
+    iteration counts (affine, SMS).
+
+    Returns d_s, d_a and the coarse matrices S_a, S (exact) or the iteration counts (pcg)."""
+    if coarse_mode == "pcg":
+        g = g.ravel()
+        H = H.tocsr()
+        cap = np.iinfo(np.int64).max if max_iter is None else max_iter
+        qa, ita, _ = block_jacobi_pcg(lambda p: Ua.T @ (H @ (Ua @ p)), Ua.T @ (-g),
+                                      galerkin_diagonal_blocks(Ua, H), tol, cap)
+        da = Ua @ qa
+        r1 = -g - H @ da
+        qs, its, _ = block_jacobi_pcg(lambda p: Us.T @ (H @ (Us @ p)), Us.T @ r1,
+                                      galerkin_diagonal_blocks(Us, H), tol, cap)
+        ds = da + Us @ qs
+        return ds, da, ita, its
     g = g.ravel()
     Sa = coarse.galerkin(Ua, H)
     qa = coarse.cho_solve(coarse.cholesky(Sa), Ua.T @ (-g))
@@ -147,7 +209,8 @@ class NewtonInfo:
 class OracleSim:
     """Timestep driver: begin_step / newton_iteration / end_step (Alg. 1)."""
 
-    def __init__(self, scene, basis, n_cg=None):
+    def __init__(self, scene, basis, n_cg=None, coarse_mode="exact", coarse_tol=1e-4, coarse_max_iter=None):
+        self.coarse_mode, self.coarse_tol, self.coarse_max_iter = coarse_mode, coarse_tol, coarse_max_iter
         self.scene = scene
         self.model = ip.make_model(scene)
         self.basis = basis
@@ -168,7 +231,8 @@ class OracleSim:
         m = self.model
         g = ip.gradient(m, x, self.xhat)
         H = ip.hessian(m, x, self.xhat).tocsr()
-        ds, da, Sa, S = subspace_direction(H, g, self.Ua, self.Us)
+        ds, da, Sa, S = subspace_direction(H, g, self.Ua, self.Us, self.coarse_mode, self.coarse_tol,
+                                           self.coarse_max_iter)
         r = -g.ravel() - H @ ds
         df = pcg(H, r, self.n_cg)
         return g, H, ds, df, ds + df
