@@ -344,7 +344,7 @@ void launch_scatter_S(Ctx &c) {
 // Capture a fixed launch sequence once (pointers are fixed per basis) and replay it.
 template <typename F>
 static void run_captured(Ctx &c, cudaGraphExec_t &exec, F enqueue) {
-  const bool graphs = c.params.use_graphs && !c.dist();
+  const bool graphs = c.params.use_graphs;   // (no collectives inside: replicated factor / solves)
   if (!graphs) {
     enqueue(c);
     return;

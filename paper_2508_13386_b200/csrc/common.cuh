@@ -260,6 +260,10 @@ enum {
   SC_ALPHA_INV,   // /
   SC_ALPHA0,
   SC_RZ0,
+  SC_CG_G = 16,   // \ multi-GPU single-reduction PCG: gamma = r.z, delta = z.Hz (summed together)
+  SC_CG_D,        // /
+  SC_CG_GOLD,
+  SC_CG_AOLD,
   SC_COUNT = 32
 };
 constexpr int SC_SUM0 = SC_ENERGY_ELEM, SC_SUM_N = SC_INFEAS - SC_ENERGY_ELEM + 1;

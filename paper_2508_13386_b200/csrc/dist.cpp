@@ -22,11 +22,30 @@ void make_partition(int rank, int world, int32_t nv, const double *X, int32_t nt
   P.world = world;
   P.nv_glob = nv;
   P.nt_glob = nt;
-  // owner: slabs of equal vertex count along x (ties by id)
+  // owner: slabs along x (vertices in (x, id) order) balanced by element work: a vertex weighs
+  // the tets it heads (vertex 0 of the tet, the energy owner) plus one, so slabs of a mesh with
+  // density varying along x (the C3 lattice) carry equal numbers of owned tets; cuts never split
+  // vertices of equal x (a cube layer stays on one rank)
   std::vector<int32_t> order(nv), owner(nv);
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return X[3 * a] < X[3 * b]; });
-  for (int32_t k = 0; k < nv; ++k) owner[order[k]] = (int32_t)((int64_t)k * world / nv);
+  {
+    std::vector<int64_t> wgt(nv, 1);
+    for (int32_t e = 0; e < nt; ++e) wgt[tets[4 * (size_t)e]]++;
+    int64_t total = 0;
+    for (int32_t v = 0; v < nv; ++v) total += wgt[v];
+    int64_t acc = 0;
+    int32_t r = 0;
+    for (int32_t k = 0; k < nv; ++k) {
+      const int32_t v = order[k];
+      // advance to the next rank once this rank's share is reached, but only between x values
+      if (r < world - 1 && acc * world >= (int64_t)(r + 1) * total &&
+          (k == 0 || X[3 * order[k - 1]] != X[3 * v]))
+        ++r;
+      owner[v] = r;
+      acc += wgt[v];
+    }
+  }
   // local tets: owned first (vertex 0 owned), then the other tets with an owned vertex
   std::vector<int32_t> own_t, oth_t;
   for (int32_t e = 0; e < nt; ++e) {
@@ -107,6 +126,7 @@ void make_partition(int rank, int world, int32_t nv, const double *X, int32_t nt
 
 struct NcclComm : Comm {
   ncclComm_t comm = nullptr;
+  bool capturable() const override { return true; }
   ~NcclComm() override {
     if (comm) ncclCommDestroy(comm);
   }

@@ -45,6 +45,8 @@ void make_partition(int rank, int world, int32_t nv, const double *X, int32_t nt
 // Collective backend.  All operations are enqueued on / synchronised with `stream`.
 struct Comm {
   virtual ~Comm() = default;
+  // true if the operations can be recorded into a CUDA graph (NCCL; not the host-side hub)
+  virtual bool capturable() const { return false; }
   virtual void allreduce_sum(double *dev, int64_t n, cudaStream_t stream) = 0;
   virtual void allreduce_min(double *dev, int64_t n, cudaStream_t stream) = 0;
   // send[peer] -> recv[peer] for every peer (3 doubles per vertex), buffers on the device

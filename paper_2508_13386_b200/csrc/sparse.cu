@@ -374,8 +374,93 @@ __global__ void k_pcg_scalars(double *__restrict__ scal, int which) {
   }
 }
 
+// ---- multi-GPU: single-reduction PCG (Chronopoulos & Gear 1989), algebraically the same
+// iterates as the recurrence above with ONE rank reduction per iteration (gamma = r.z and
+// delta = z.Hz summed together):
+//   w = H z; [gamma, delta] summed; beta = gamma / gamma_old; alpha = gamma / (delta - beta gamma / alpha_old)
+//   (first iteration: beta = 0, alpha = gamma / delta); p = z + beta p; s = w + beta s;
+//   x += alpha p; r -= alpha s; z = D^-1 r; gamma' partial = r.z (owned); halo(z)
+__global__ void __launch_bounds__(256) k_cg_spmv(SellView H, int nv_own, const double *__restrict__ z,
+                                                 double *__restrict__ w, double *__restrict__ partial,
+                                                 unsigned int *counter, double *__restrict__ scal) {
+  double acc[1] = {0.0};
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row < H.nv) {
+    double o[3];
+    sell_row_product(H, row, z, o);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      w[3 * row + i] = o[i];
+      if (row < nv_own) acc[0] = fma(z[3 * row + i], o[i], acc[0]);
+    }
+  }
+  double res[1];
+  if (grid_reduce<1>(acc, partial, counter, res) && threadIdx.x == 0) scal[SC_CG_D] = res[0];
+}
+
+__global__ void k_cg_scalars(double *__restrict__ scal, int first) {
+  const double g = scal[SC_CG_G], d = scal[SC_CG_D];
+  double alpha, beta;
+  if (first) {
+    beta = 0.0;
+    alpha = (g != 0.0 && d != 0.0) ? g / d : 0.0;
+    scal[SC_RZ0] = g;
+  } else {
+    const double go = scal[SC_CG_GOLD], ao = scal[SC_CG_AOLD];
+    beta = go != 0.0 ? g / go : 0.0;
+    const double den = (ao != 0.0) ? d - beta * g / ao : 0.0;
+    alpha = (g != 0.0 && den != 0.0) ? g / den : 0.0;
+  }
+  scal[SC_ALPHA] = alpha;
+  scal[SC_BETA] = beta;
+  scal[SC_CG_GOLD] = g;
+  scal[SC_CG_AOLD] = alpha;
+}
+
+__global__ void __launch_bounds__(256) k_cg_update(int n3, int n3_own, const double *__restrict__ dinv,
+                                                   const double *__restrict__ w, double *__restrict__ p,
+                                                   double *__restrict__ s, double *__restrict__ x,
+                                                   double *__restrict__ r, double *__restrict__ z,
+                                                   double *__restrict__ partial, unsigned int *counter,
+                                                   double *__restrict__ scal) {
+  const double alpha = scal[SC_ALPHA], beta = scal[SC_BETA];
+  double acc[1] = {0.0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n3; i += gridDim.x * blockDim.x) {
+    const double pn = fma(beta, p[i], z[i]);
+    const double sn = fma(beta, s[i], w[i]);
+    p[i] = pn;
+    s[i] = sn;
+    x[i] = fma(alpha, pn, x[i]);
+    const double ri = fma(-alpha, sn, r[i]);
+    const double zi = dinv[i] * ri;
+    r[i] = ri;
+    z[i] = zi;
+    if (i < n3_own) acc[0] = fma(ri, zi, acc[0]);
+  }
+  double res[1];
+  if (grid_reduce<1>(acc, partial, counter, res) && threadIdx.x == 0) scal[SC_CG_G] = res[0];
+}
+
+static void enqueue_cg_iters_dist(Ctx &c, double *sol, int iters) {
+  const int n3 = 3 * c.nv, n3o = 3 * c.nv_own, bs = 256;
+  for (int it = 0; it < iters; ++it) {
+    k_cg_spmv<<<div_up(c.nv, bs), bs, 0, c.stream>>>(sell_view(c), c.nv_own, c.z, c.tmp, c.partial, c.counters + 3,
+                                                     c.scal);
+    dist_sum(c, c.scal + SC_CG_G, 2);   // the iteration's only reduction
+    k_cg_scalars<<<1, 1, 0, c.stream>>>(c.scal, it == 0 ? 1 : 0);
+    k_cg_update<<<grid_vec(n3), bs, 0, c.stream>>>(n3, n3o, c.dinv, c.tmp, c.p, c.q, sol, c.r, c.z, c.partial,
+                                                   c.counters + 4, c.scal);
+    halo_exchange(c, c.z);
+    c.launches += 3;
+  }
+}
+
 static void enqueue_pcg_iters(Ctx &c, double *sol, int iters) {
   const int n3 = 3 * c.nv, n3o = 3 * c.nv_own, bs = 256, dist = c.dist() ? 1 : 0;
+  if (dist) {
+    enqueue_cg_iters_dist(c, sol, iters);
+    return;
+  }
   for (int it = 0; it < iters; ++it) {
     k_pcg_spmv<<<div_up(c.nv, bs), bs, 0, c.stream>>>(sell_view(c), c.nv_own, dist, c.z, c.p, c.q, c.partial,
                                                       c.counters + 3, c.scal);
@@ -394,6 +479,13 @@ static void enqueue_pcg_iters(Ctx &c, double *sol, int iters) {
   }
 }
 
+// multi-GPU: the final r.z (PCG statistics) summed across ranks -- outside the iterations
+static void pcg_finish_dist(Ctx &c) {
+  if (!c.dist()) return;
+  MS_CUDA(cudaMemcpyAsync(c.scal + SC_RZ, c.scal + SC_CG_G, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+  dist_sum(c, c.scal + SC_RZ, 1);
+}
+
 void pcg_reset_graph(Ctx &c) {
   if (c.pcg_graph) cudaGraphExecDestroy(c.pcg_graph);
   c.pcg_graph = nullptr;
@@ -408,17 +500,22 @@ void launch_pcg(Ctx &c, const double *rhs, double *sol, int iters) {
                                                   c.q, c.partial, c.counters + 2, c.scal);
   c.launches++;
   MS_CUDA(cudaGetLastError());
-  if (c.dist()) {   // rank-summed r.z; ghost entries of z from their owners
-    dist_sum(c, c.scal + SC_RZ, 1);
-    MS_CUDA(cudaMemcpyAsync(c.scal + SC_RZ0, c.scal + SC_RZ, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+  if (c.dist()) {   // r.z stays a partial sum (summed with z.Hz in the first iteration); ghost z
+    MS_CUDA(cudaMemcpyAsync(c.scal + SC_CG_G, c.scal + SC_RZ, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
     halo_exchange(c, c.z);
+    if (iters <= 0) {
+      dist_sum(c, c.scal + SC_RZ, 1);
+      MS_CUDA(cudaMemcpyAsync(c.scal + SC_RZ0, c.scal + SC_RZ, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+    }
   }
   if (iters <= 0) return;
-  const bool graphs = c.params.use_graphs && sol == c.df.p && !c.dist();
+  // NCCL collectives are recorded into the graph too; the in-process hub synchronises on the host
+  const bool graphs = c.params.use_graphs && sol == c.df.p && (!c.dist() || c.comm->capturable());
   if (!graphs) {
     enqueue_pcg_iters(c, sol, iters);
-    c.launches += 2 * (int64_t)iters;
+    if (!c.dist()) c.launches += 2 * (int64_t)iters;
     MS_CUDA(cudaGetLastError());
+    pcg_finish_dist(c);
     return;
   }
   if (c.pcg_graph_iters != iters || !c.pcg_graph) {
@@ -429,17 +526,21 @@ void launch_pcg(Ctx &c, const double *rhs, double *sol, int iters) {
     c.stream = cap;
     cudaGraph_t graph;
     MS_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    const int64_t l0 = c.launches;
     enqueue_pcg_iters(c, sol, iters);
+    const int64_t captured = c.launches - l0;   // dist: counted while enqueueing
+    c.launches = l0;
     MS_CUDA(cudaStreamEndCapture(cap, &graph));
     c.stream = saved;
     MS_CUDA(cudaGraphInstantiate(&c.pcg_graph, graph, 0));
     cudaGraphDestroy(graph);
     cudaStreamDestroy(cap);
     c.pcg_graph_iters = iters;
-    c.pcg_graph_kernels = 2 * (int64_t)iters;
+    c.pcg_graph_kernels = c.dist() ? captured : 2 * (int64_t)iters;
   }
   MS_CUDA(cudaGraphLaunch(c.pcg_graph, c.stream));
   c.launches += c.pcg_graph_kernels;
+  pcg_finish_dist(c);
 }
 
 // ------------------------------------------------------------------ small vector kernels
