@@ -244,6 +244,7 @@ def run_ours(args):
     s, b, t_basis = load_case(args.config)
     stream = torch.cuda.current_stream()
     partitioned = world > 1 and not args.replicas
+    coarse_mode = 1 if args.coarse == "pcg" else 0
     if partitioned:
         # one problem over N GPUs: x-slab partition, NCCL halo exchange / allreduce inside the
         # library; rank 0 creates the NCCL id, broadcast over the process group
@@ -252,9 +253,9 @@ def run_ours(args):
             uid.copy_(torch.frombuffer(bytearray(msim.nccl_unique_id()), dtype=torch.uint8))
         torch.distributed.broadcast(uid, src=0)
         ctx = msim.context_from_scene(s, b, device=local, stream=stream.cuda_stream, rank=rank, world=world,
-                                      nccl_id=bytes(uid.cpu().numpy().tobytes()))
+                                      nccl_id=bytes(uid.cpu().numpy().tobytes()), coarse_mode=coarse_mode)
     else:
-        ctx = msim.context_from_scene(s, b, device=local, stream=stream.cuda_stream)
+        ctx = msim.context_from_scene(s, b, device=local, stream=stream.cuda_stream, coarse_mode=coarse_mode)
     sizes = ctx.sizes()
 
     def barrier():
@@ -267,7 +268,7 @@ def run_ours(args):
         ctx.timestep()
     # ---- timed region (device resident, per-phase events OFF)
     launches0 = ctx.kernel_launches()
-    newton = pcg = 0
+    newton = pcg = coarse_it = 0
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -276,6 +277,7 @@ def run_ours(args):
             st = ctx.timestep()
             newton += st.newton_iters
             pcg += st.pcg_iters
+            coarse_it += st.coarse_iters
         ev1.record(stream)
         barrier()
     ms = ev0.elapsed_time(ev1)
@@ -347,9 +349,10 @@ def run_ours(args):
             "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong" if partitioned else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(s, b, world, partitioned),
+            "config": dict(config_dict(s, b, world, partitioned), coarse=args.coarse),
             "pcg_iters_per_s": pcg_all / (ms_max * 1e-3),
             "newton_iters": int(newton_all),
+            "coarse_pcg_iters_per_newton": coarse_it / max(newton, 1) if args.coarse == "pcg" else None,
             "roofline": dict(rl_phases[dominant], phase=dominant),
             "roofline_phases": rl_phases,
             "assembly_gbs": ab["assembly"] / (asm_avg * 1e-3) / 1e9 if asm_n else None,
@@ -382,6 +385,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--coarse", default="exact", choices=["exact", "pcg"],
+                    help="coarse solves: exact Cholesky of S (default) or the paper's block-Jacobi PCG to 1e-4")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: N independent copies of the problem instead of one slab-partitioned problem")
     args = ap.parse_args()

@@ -60,7 +60,14 @@ typedef struct ms_params {
   int32_t debug_flags;    /* parity hooks, 0 in production: MS_DEBUG_HESS_FALLBACK routes
                              every indefinite element Hessian to the cyclic-Jacobi eigen-clamp
                              (the fall-back path of the tridiagonal-QL projection)           */
+  int32_t coarse_mode;    /* MS_COARSE_EXACT (default): S = B^T H B formed and factorised
+                             (reading R4); MS_COARSE_PCG: the paper's solves --
+                             block-Jacobi PCG to coarse_tol on the matrix-free sandwich
+                             B^T (H (B p)), 12 x 12 blocks S_ii (NEXT-1)                     */
+  int32_t coarse_max_iter;/* MS_COARSE_PCG: iteration cap (default 1000)                     */
+  double coarse_tol;      /* MS_COARSE_PCG: ||r||_2 <= coarse_tol ||b||_2 (default 1e-4)    */
 } ms_params;
+enum { MS_COARSE_EXACT = 0, MS_COARSE_PCG = 1 };
 enum { MS_DEBUG_HESS_FALLBACK = 1 };
 
 typedef struct ms_newton_stats {
@@ -74,6 +81,8 @@ typedef struct ms_newton_stats {
   int32_t converged;      /* termination test passed after this iteration                  */
   int32_t ls_failed;      /* 1 if no decrease down to ls_min                               */
   int32_t n_cg;           /* PCG iterations performed                                      */
+  int32_t coarse_iters;   /* MS_COARSE_PCG: SMS-stage PCG iterations (0 in exact mode)     */
+  int32_t pad_;
 } ms_newton_stats;
 
 typedef struct ms_step_stats {
@@ -81,6 +90,8 @@ typedef struct ms_step_stats {
   int32_t pcg_iters;      /* total full-space PCG iterations                               */
   int32_t ls_evals;       /* total line-search candidates evaluated                        */
   int32_t status;         /* MS_OK / MS_WARN_*                                              */
+  int32_t coarse_iters;   /* MS_COARSE_PCG: total SMS-stage PCG iterations                 */
+  int32_t pad_;
   double last_ds_norm;
   double last_alpha;
 } ms_step_stats;

@@ -168,6 +168,7 @@ static ms_status newton_step(Ctx &c, ms_newton_stats *st) {
     st->converged = conv ? 1 : 0;
     st->ls_failed = failed ? 1 : 0;
     st->n_cg = ncg;
+    st->coarse_iters = c.params.coarse_mode == MS_COARSE_PCG ? c.coarse_iters_last : 0;
   }
   return failed ? MS_WARN_LS_FAILED : MS_OK;
 }
@@ -250,6 +251,9 @@ void ms_default_params(ms_params *p) {
   p->ls_batch = 4;
   p->use_graphs = 1;
   p->debug_flags = 0;
+  p->coarse_mode = MS_COARSE_EXACT;
+  p->coarse_max_iter = 1000;
+  p->coarse_tol = 1e-4;
 }
 
 static ms_status create_common(ms_ctx **out, int device, void *cuda_stream, int rank, int world,
@@ -461,7 +465,11 @@ ms_status ms_set_params(ms_ctx *ctx, const ms_params *p) {
     MS_REQUIRE(p->filter_safety > 0.0 && p->filter_safety <= 1.0, MS_ERR_ARG, "bad filter safety");
     MS_REQUIRE(p->ls_batch == 1 || p->ls_batch == 2 || p->ls_batch == 4 || p->ls_batch == 8, MS_ERR_ARG,
                "ls_batch must be 1, 2, 4 or 8");
-    if (p->n_cg != ctx->c.params.n_cg || p->use_graphs != ctx->c.params.use_graphs) {
+    MS_REQUIRE(p->coarse_mode == MS_COARSE_EXACT || p->coarse_mode == MS_COARSE_PCG, MS_ERR_ARG, "bad coarse_mode");
+    MS_REQUIRE(p->coarse_tol >= 0.0 && p->coarse_max_iter > 0, MS_ERR_ARG, "bad coarse PCG params");
+    if (p->n_cg != ctx->c.params.n_cg || p->use_graphs != ctx->c.params.use_graphs ||
+        p->coarse_mode != ctx->c.params.coarse_mode || p->coarse_tol != ctx->c.params.coarse_tol ||
+        p->coarse_max_iter != ctx->c.params.coarse_max_iter) {
       pcg_reset_graph(ctx->c);
       coarse_reset_graphs(ctx->c);
     }
@@ -727,6 +735,7 @@ ms_status ms_timestep(ms_ctx *ctx, ms_step_stats *out) {
       st.newton_iters++;
       st.pcg_iters += ns.n_cg;
       st.ls_evals += ns.ls_evals;
+      st.coarse_iters += ns.coarse_iters;
       st.last_ds_norm = ns.ds_norm;
       st.last_alpha = ns.alpha;
       if (ns.converged) {

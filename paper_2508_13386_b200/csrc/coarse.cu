@@ -24,9 +24,9 @@ namespace msim {
 __global__ void k_lift(int nv, const int32_t *__restrict__ vptr, const int32_t *__restrict__ handle,
                        const double *__restrict__ phi, const double *__restrict__ X,
                        const double *__restrict__ origins, const double *__restrict__ q,
-                       double *__restrict__ w, const double *__restrict__ base) {
+                       double *__restrict__ w, const double *__restrict__ base, const int32_t *__restrict__ skip) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= nv) return;
+  if (v >= nv || (skip && *skip)) return;
   double o[3] = {0.0, 0.0, 0.0};
   const double xv0 = X[3 * v], xv1 = X[3 * v + 1], xv2 = X[3 * v + 2];
   for (int k = vptr[v]; k < vptr[v + 1]; ++k) {
@@ -56,8 +56,9 @@ __global__ void k_lift_affine(int nv, const double *__restrict__ phi_a, const do
 __global__ void __launch_bounds__(256) k_restrict(const int32_t *__restrict__ hptr, const int32_t *__restrict__ hvert,
                                                   const double *__restrict__ hphi, const double *__restrict__ X,
                                                   const double *__restrict__ origins, const double *__restrict__ y,
-                                                  double sign, double *__restrict__ z) {
+                                                  double sign, double *__restrict__ z, const int32_t *__restrict__ skip) {
   __shared__ double sh[12 * 32];
+  if (skip && *skip) return;
   const int i = blockIdx.x;
   const double o0 = origins[3 * i], o1 = origins[3 * i + 1], o2 = origins[3 * i + 2];
   double acc[12];
@@ -106,15 +107,15 @@ __global__ void __launch_bounds__(256) k_restrict_affine(int nv, const double *_
   }
 }
 
-void launch_lift(Ctx &c, const double *q, double *w, bool accumulate) {
+void launch_lift(Ctx &c, const double *q, double *w, bool accumulate, const int32_t *skip) {
   k_lift<<<div_up(c.nv, 256), 256, 0, c.stream>>>(c.nv, c.bvptr, c.bhandle, c.bphi, c.X, c.origins, q, w,
-                                                  accumulate ? w : nullptr);
+                                                  accumulate ? w : nullptr, skip);
   c.launches++;
   MS_CUDA(cudaGetLastError());
 }
 
-void launch_restrict(Ctx &c, const double *y, double *z) {
-  k_restrict<<<c.m, 256, 0, c.stream>>>(c.hptr, c.hvert, c.hphi, c.X, c.origins, y, 1.0, z);
+void launch_restrict(Ctx &c, const double *y, double *z, const int32_t *skip) {
+  k_restrict<<<c.m, 256, 0, c.stream>>>(c.hptr, c.hvert, c.hphi, c.X, c.origins, y, 1.0, z, skip);
   c.launches++;
   MS_CUDA(cudaGetLastError());
 }
@@ -308,11 +309,251 @@ void coarse_init_attrs(Ctx &c) {
   set_max_dyn_smem((const void *)k_galerkin_fused, c.device);
 }
 
+// ------------------------------------------------------------------ paper coarse mode (NEXT-1)
+// MS_COARSE_PCG (§3.7.1, Alg. 2): the SMS stage solves
+// (U_s^T H U_s) q = U_s^T r1 by PCG to ||r|| <= tol ||b|| on the matrix-free sandwich -- each
+// iteration lifts (w = B p), applies H (y = H w) and restricts (t = B^T y) -- with the 12 x 12
+// block-Jacobi preconditioner S_ii^-1 (blocks from the diagonal-block Galerkin rows).
+// The affine stage has one 12 x 12 block, so its block-Jacobi PCG is exact after one step: it
+// is the 12 x 12 Cholesky solve of the exact mode.
+// Iterations run in captured batches of kCpcgBatch; every kernel of an iteration returns at once
+// when the device flag state[0] says the solve has converged, so the iterates are exactly those
+// of a loop stopped at the first k with ||r_k|| <= tol ||b|| (tested against oracle/solver.py).
+
+// S_ii^-1 = L^-T L^-1 (one thread per handle, 12 x 12 in local memory; once per Newton iteration)
+__global__ void k_block_inv(int m, const double *__restrict__ Sd, double *__restrict__ Minv, int *__restrict__ flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double L[12][12], Li[12][12];
+  for (int r = 0; r < 12; ++r)
+    for (int c = 0; c < 12; ++c) {
+      L[r][c] = Sd[144 * (size_t)i + 12 * r + c];
+      Li[r][c] = 0.0;
+    }
+  for (int j = 0; j < 12; ++j) {
+    double d = L[j][j];
+    for (int k = 0; k < j; ++k) d -= L[j][k] * L[j][k];
+    if (!(d > 0.0)) {
+      *flag = 1;
+      d = 1.0;
+    }
+    L[j][j] = sqrt(d);
+    for (int r = j + 1; r < 12; ++r) {
+      double s = L[r][j];
+      for (int k = 0; k < j; ++k) s -= L[r][k] * L[j][k];
+      L[r][j] = s / L[j][j];
+    }
+  }
+  for (int c = 0; c < 12; ++c)
+    for (int r = c; r < 12; ++r) {
+      double s = r == c ? 1.0 : 0.0;
+      for (int k = c; k < r; ++k) s -= L[r][k] * Li[k][c];
+      Li[r][c] = s / L[r][r];
+    }
+  for (int a = 0; a < 12; ++a)
+    for (int b = 0; b < 12; ++b) {
+      double s = 0.0;
+      for (int r = a > b ? a : b; r < 12; ++r) s = fma(Li[r][a], Li[r][b], s);
+      Minv[144 * (size_t)i + 12 * a + b] = s;
+    }
+}
+
+constexpr int kCpcgThreads = 1024;
+constexpr int kCpcgBatch = 8;
+
+// z_e = (S_ii^-1 r_i)[row] for entry e = 12 i + row
+__device__ __forceinline__ double block_precond(const double *__restrict__ Minv, const double *__restrict__ r, int e) {
+  const int i = e / 12, row = e - 12 * i;
+  const double *Mi = Minv + 144 * (size_t)i + 12 * row, *ri = r + 12 * (size_t)i;
+  double z = 0.0;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) z = fma(Mi[k], ri[k], z);
+  return z;
+}
+
+__device__ __forceinline__ double cta_sum(double v, double *sh) {
+  double a[1] = {v};
+  block_sum<1>(a, sh);
+  if (threadIdx.x == 0) sh[32] = a[0];
+  __syncthreads();
+  const double out = sh[32];
+  __syncthreads();
+  return out;
+}
+
+// q = 0, r = b, z = M^-1 r, p = z, rho = r.z, ||b||^2; state = {done, iterations}
+__global__ void __launch_bounds__(kCpcgThreads) k_cpcg_init(int n, const double *__restrict__ b,
+                                                           const double *__restrict__ Minv, double *__restrict__ q,
+                                                           double *__restrict__ r, double *__restrict__ z,
+                                                           double *__restrict__ p, double *__restrict__ scal,
+                                                           int32_t *__restrict__ state, int max_iter) {
+  __shared__ double sh[33];
+  double rz = 0.0, bb = 0.0;
+  for (int e = threadIdx.x; e < n; e += kCpcgThreads) {
+    const double zi = block_precond(Minv, b, e), bi = b[e];
+    q[e] = 0.0;
+    r[e] = bi;
+    z[e] = zi;
+    p[e] = zi;
+    rz = fma(bi, zi, rz);
+    bb = fma(bi, bi, bb);
+  }
+  rz = cta_sum(rz, sh);
+  bb = cta_sum(bb, sh);
+  if (threadIdx.x == 0) {
+    scal[SC_CP_RHO] = rz;
+    scal[SC_CP_BN2] = bb;
+    state[0] = (bb == 0.0 || max_iter <= 0) ? 1 : 0;
+    state[1] = 0;
+  }
+}
+
+// one iteration after t = S p: alpha = rho / p.t; q += alpha p; r -= alpha t; stop at
+// ||r||^2 <= tol^2 ||b||^2 or the cap; else z = M^-1 r, beta = r.z / rho, p = z + beta p
+__global__ void __launch_bounds__(kCpcgThreads) k_cpcg_step(int n, const double *__restrict__ t,
+                                                           const double *__restrict__ Minv, double *__restrict__ q,
+                                                           double *__restrict__ r, double *__restrict__ z,
+                                                           double *__restrict__ p, double *__restrict__ scal,
+                                                           int32_t *__restrict__ state, double tol2, int max_iter) {
+  __shared__ double sh[33];
+  __shared__ int done;
+  if (threadIdx.x == 0) done = state[0];
+  __syncthreads();
+  if (done) return;
+  double pt = 0.0;
+  for (int e = threadIdx.x; e < n; e += kCpcgThreads) pt = fma(p[e], t[e], pt);
+  pt = cta_sum(pt, sh);
+  const double rho = scal[SC_CP_RHO];
+  const double alpha = (pt != 0.0 && rho != 0.0) ? rho / pt : 0.0;
+  double rr = 0.0;
+  for (int e = threadIdx.x; e < n; e += kCpcgThreads) {
+    q[e] = fma(alpha, p[e], q[e]);
+    const double re = fma(-alpha, t[e], r[e]);
+    r[e] = re;
+    rr = fma(re, re, rr);
+  }
+  rr = cta_sum(rr, sh);   // (its barriers also publish r for the block products below)
+  const int it = state[1] + 1;
+  if (rr <= tol2 * scal[SC_CP_BN2] || it >= max_iter) {
+    if (threadIdx.x == 0) {
+      state[0] = 1;
+      state[1] = it;
+    }
+    return;
+  }
+  double rz = 0.0;
+  for (int e = threadIdx.x; e < n; e += kCpcgThreads) {
+    const double ze = block_precond(Minv, r, e);
+    z[e] = ze;
+    rz = fma(r[e], ze, rz);
+  }
+  rz = cta_sum(rz, sh);
+  const double beta = rho != 0.0 ? rz / rho : 0.0;
+  for (int e = threadIdx.x; e < n; e += kCpcgThreads) p[e] = fma(beta, p[e], z[e]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    scal[SC_CP_RHO] = rz;
+    state[1] = it;
+  }
+}
+
+static void enqueue_cpcg_batch(Ctx &c) {
+  const int n = 12 * c.m;
+  const double tol2 = c.params.coarse_tol * c.params.coarse_tol;
+  for (int k = 0; k < kCpcgBatch; ++k) {
+    launch_lift(c, c.cp_p, c.tmp, false, c.cp_state);      // w = B p
+    launch_spmv(c, c.tmp, c.r, 0.0, nullptr, c.cp_state);  // y = H w
+    launch_restrict(c, c.r, c.cp_t, c.cp_state);           // t = B^T y
+    dist_sum(c, c.cp_t, n);
+    k_cpcg_step<<<1, kCpcgThreads, 0, c.stream>>>(n, c.cp_t, c.Minv, c.qs, c.cp_r, c.cp_z, c.cp_p, c.scal,
+                                                  c.cp_state, tol2, c.params.coarse_max_iter);
+    c.launches++;
+  }
+}
+
+// SMS stage of the paper's coarse mode: q (in c.qs) from b = B^T r1 (in c.zs)
+static void coarse_pcg_solve(Ctx &c) {
+  const int n = 12 * c.m;
+  k_cpcg_init<<<1, kCpcgThreads, 0, c.stream>>>(n, c.zs, c.Minv, c.qs, c.cp_r, c.cp_z, c.cp_p, c.scal, c.cp_state,
+                                                c.params.coarse_max_iter);
+  c.launches++;
+  const bool graphs = c.params.use_graphs && (!c.dist() || c.comm->capturable());
+  int32_t *hs = reinterpret_cast<int32_t *>(c.h_pinned + PH_COUNT - 2);
+  for (int batch = 0;; ++batch) {
+    if (graphs) {
+      if (!c.cpcg_graph) {
+        cudaStream_t cap;
+        MS_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+        cudaStream_t saved = c.stream;
+        c.stream = cap;
+        cudaGraph_t graph;
+        MS_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+        const int64_t l0 = c.launches;
+        enqueue_cpcg_batch(c);
+        c.cpcg_graph_kernels = c.launches - l0;
+        c.launches = l0;
+        MS_CUDA(cudaStreamEndCapture(cap, &graph));
+        c.stream = saved;
+        MS_CUDA(cudaGraphInstantiate(&c.cpcg_graph, graph, 0));
+        cudaGraphDestroy(graph);
+        cudaStreamDestroy(cap);
+      }
+      MS_CUDA(cudaGraphLaunch(c.cpcg_graph, c.stream));
+      c.launches += c.cpcg_graph_kernels;
+    } else {
+      enqueue_cpcg_batch(c);
+    }
+    MS_CUDA(cudaMemcpyAsync(hs, c.cp_state, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+    if (hs[0]) break;
+    MS_REQUIRE(batch < (c.params.coarse_max_iter + kCpcgBatch - 1) / kCpcgBatch + 1, MS_ERR_STATE,
+               "coarse PCG did not stop");
+  }
+  c.coarse_iters_last = hs[1];
+}
+
+// per Newton iteration: the diagonal blocks S_ii (fused Galerkin kernel with U_i = supp(i) and
+// the single slot j = i) and their inverses
+static void coarse_pcg_blocks(Ctx &c) {
+  build_coarse_pcg_structures(c);
+  GalParams G = galerkin_params(c);
+  G.gU_ptr = c.gd_U_ptr;
+  G.gU = c.gd_U;
+  G.ga_off = c.gd_ga_off;
+  G.ga_ent = c.gd_ga_ent;
+  G.ga_mask = c.gd_ga_mask;
+  G.gj_ptr = c.gd_gj_ptr;
+  G.gj_blk = c.gd_gj_blk;
+  G.gl_base = c.gd_gl_base;
+  G.gl_off = c.gd_gl_off;
+  G.gl_ent = c.gd_gl_ent;
+  G.sT = c.gd_sT;
+  G.S = c.Sdiag;
+  G.Spart = c.Sdiag_part;
+  G.pstride = 144;
+  const size_t smem = sizeof(double) * galerkin_smem_doubles(1);
+  k_galerkin_fused<<<c.m * G.nparts, kGalThreads, smem, c.stream>>>(G);
+  c.launches++;
+  if (G.nparts > 1) {
+    k_galerkin_reduce<<<c.m, 256, 0, c.stream>>>(G);
+    c.launches++;
+  }
+  dist_sum(c, c.Sdiag, 144 * (int64_t)c.m);
+}
+
+void launch_coarse_pcg_prep(Ctx &c) {
+  k_block_inv<<<div_up(c.m, 128), 128, 0, c.stream>>>(c.m, c.Sdiag, c.Minv, c.flags + 0);
+  c.launches++;
+  MS_CUDA(cudaGetLastError());
+}
+
 // S = B^T H B into Sblk (full_S, or whenever the Galerkin rows are not fused into the factor
 // launch) and S_a = U_a^T H U_a.  With c.gal_fused the rows of S are formed by the factorisation
 // launch itself (chol.cu: G / R tasks write straight into the factor's tiles).
 void launch_coarse_S(Ctx &c, bool full_S) {
-  if (full_S || !c.gal_fused) {
+  const bool pcg = c.params.coarse_mode == MS_COARSE_PCG;
+  if (pcg && !full_S) coarse_pcg_blocks(c);
+  if (full_S || (!c.gal_fused && !pcg)) {
     const size_t smem = sizeof(double) * galerkin_smem_doubles(c.gal_max_jup);
     MS_REQUIRE(smem <= 227 * 1024, MS_ERR_ARG, "coarse S row too wide for the fused Galerkin kernel");
     const GalParams G = galerkin_params(c);
@@ -369,10 +610,15 @@ static void run_captured(Ctx &c, cudaGraphExec_t &exec, F enqueue) {
 void coarse_reset_graphs(Ctx &c) {
   if (c.factor_graph) cudaGraphExecDestroy(c.factor_graph);
   if (c.solve_graph) cudaGraphExecDestroy(c.solve_graph);
-  c.factor_graph = c.solve_graph = nullptr;
+  if (c.cpcg_graph) cudaGraphExecDestroy(c.cpcg_graph);
+  c.factor_graph = c.solve_graph = c.cpcg_graph = nullptr;
 }
 
 void launch_coarse_factor(Ctx &c) {
+  if (c.params.coarse_mode == MS_COARSE_PCG) {   // the paper's mode: block-Jacobi inverses only
+    launch_coarse_pcg_prep(c);
+    return;
+  }
   run_captured(c, c.factor_graph, enqueue_chol_factor);
   c.launches += chol_factor_kernels(c);
   MS_CUDA(cudaGetLastError());
@@ -401,9 +647,11 @@ void launch_coarse_direction(Ctx &c) {
   // SMS stage: zs = B^T r1; zs <- S^-1 zs; ds = da + B zs
   launch_restrict(c, c.tmp, c.zs);
   dist_sum(c, c.zs, 12 * (int64_t)c.m);
-  launch_coarse_solve(c);
+  const bool pcg = c.params.coarse_mode == MS_COARSE_PCG;
+  if (pcg) coarse_pcg_solve(c);   // q in qs (tmp and r are its work vectors)
+  else launch_coarse_solve(c);    // q in zs
   MS_CUDA(cudaMemcpyAsync(c.ds, c.da, sizeof(double) * n3, cudaMemcpyDeviceToDevice, c.stream));
-  launch_lift(c, c.zs, c.ds, true);
+  launch_lift(c, pcg ? c.qs : c.zs, c.ds, true);
   // r = -g - H ds
   launch_spmv(c, c.ds, c.r, 0.0, c.rhs);
   MS_CUDA(cudaGetLastError());

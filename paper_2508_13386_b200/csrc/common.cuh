@@ -203,6 +203,19 @@ struct Ctx {
   DBuf<int32_t> chol_queue0, chol_queue;                   // two ready queues: pristine / live
   int64_t n_crit = 0, n_pool = 0;
   bool gal_fused = false;           // Galerkin row tasks inside the factorisation launch (chol.cu)
+  // ---- coarse_mode == MS_COARSE_PCG (coarse.cu): block-Jacobi PCG on the matrix-free sandwich
+  std::vector<int64_t> h_bvptr;     // host copies of the (local) vertex-major basis CSR
+  std::vector<int32_t> h_bhandle;
+  bool cpcg_ready = false;          // diagonal-block Galerkin lists built (lazily)
+  DBuf<int32_t> gd_U_ptr, gd_U, gd_ga_off, gd_gj_ptr, gd_gj_blk, gd_gl_base, gd_gl_off, gd_sT;
+  DBuf<uint32_t> gd_ga_ent, gd_gl_ent;
+  DBuf<unsigned long long> gd_ga_mask;
+  DBuf<double> Sdiag, Sdiag_part, Minv;   // [m][144] blocks S_ii, their partial rows, S_ii^-1
+  DBuf<double> cp_r, cp_z, cp_p, cp_t;    // [12m] PCG vectors (the solution goes to zs)
+  DBuf<int32_t> cp_state;           // [2]: done flag, iterations
+  cudaGraphExec_t cpcg_graph = nullptr;
+  int64_t cpcg_graph_kernels = 0;
+  int32_t coarse_iters_last = 0;
   int64_t n_dag_factor = 0;         // factor tasks (the fused Galerkin tasks follow them)
   DBuf<int32_t> chol_rw_ptr, chol_rw;   // per chain task: handles whose R(i) it waits for
   int df_hi_ctas = 64;   // CTAs serving the high-priority queue
@@ -264,6 +277,8 @@ enum {
   SC_CG_D,        // /
   SC_CG_GOLD,
   SC_CG_AOLD,
+  SC_CP_RHO,      // coarse PCG (MS_COARSE_PCG): r.z, ||b||^2
+  SC_CP_BN2,
   SC_COUNT = 32
 };
 constexpr int SC_SUM0 = SC_ENERGY_ELEM, SC_SUM_N = SC_INFEAS - SC_ENERGY_ELEM + 1;
@@ -295,7 +310,8 @@ void launch_elem_hess(Ctx &c);
 void launch_eval_elements(Ctx &c, const double *x_dev, double *Ee, double *ge, double *He);
 void launch_vertex_grad(Ctx &c);
 void launch_assemble(Ctx &c);
-void launch_spmv(Ctx &c, const double *xin, double *yout, double alpha_minus_b, const double *b);
+void launch_spmv(Ctx &c, const double *xin, double *yout, double alpha_minus_b, const double *b,
+                 const int32_t *skip = nullptr);
 void launch_pcg(Ctx &c, const double *rhs, double *sol, int iters);
 void pcg_reset_graph(Ctx &c);
 void launch_coarse_S(Ctx &c, bool full_S = false);
@@ -315,8 +331,8 @@ void chol_init_attrs(Ctx &c);
 void coarse_init_attrs(Ctx &c);
 void elem_init_attrs(Ctx &c);
 void coarse_reset_graphs(Ctx &c);
-void launch_lift(Ctx &c, const double *q, double *w, bool accumulate);
-void launch_restrict(Ctx &c, const double *y, double *z);
+void launch_lift(Ctx &c, const double *q, double *w, bool accumulate, const int32_t *skip = nullptr);
+void launch_restrict(Ctx &c, const double *y, double *z, const int32_t *skip = nullptr);
 void launch_filters(Ctx &c);
 void launch_ls_batch(Ctx &c, int k0, int K);
 void launch_update(Ctx &c, double alpha);
@@ -335,6 +351,7 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
                             const int32_t *handle, const double *phi, const double *phi_aff,
                             const double aff_origin[3]);
 void ensure_state_buffers(Ctx &c);
+void build_coarse_pcg_structures(Ctx &c);
 
 // profiling helpers
 void phase_begin(Ctx &c, int phase);

@@ -332,6 +332,9 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   }
   c.m = m;
   c.nnz_phi = nnz;
+  c.h_bvptr.assign(vptr, vptr + nv + 1);
+  c.h_bhandle.assign(handle, handle + nnz);
+  c.cpcg_ready = false;
   std::vector<int32_t> bvptr(nv + 1);
   for (int32_t v = 0; v <= nv; ++v) bvptr[v] = (int32_t)vptr[v];
   // handle-major transpose (sorted by vertex)
@@ -891,6 +894,92 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   coarse_reset_graphs(c);
   launch_basis_W(c);
   MS_CUDA(cudaStreamSynchronize(s));
+}
+
+// Lists of the diagonal-block Galerkin rows S_ii = U_i^T H U_i (the block-Jacobi preconditioner
+// of the paper's coarse PCG): the same fused Galerkin kernel with U_i = supp(i) (only
+// rows u in supp(i) meet W_ui != 0) and the single upper slot j = i.  Built on first use.
+void build_coarse_pcg_structures(Ctx &c) {
+  if (c.cpcg_ready) return;
+  const int32_t m = c.m, nv = c.nv;
+  const int64_t *vptr = c.h_bvptr.data();
+  const int32_t *handle = c.h_bhandle.data();
+  const int32_t *rp = c.h_rowptr.data(), *ci = c.h_colidx.data();
+  // supp(i), owned rows, vertex order
+  std::vector<int32_t> Uptr(m + 1, 0), Uall;
+  {
+    std::vector<std::vector<int32_t>> supp(m);
+    for (int32_t v = 0; v < std::min(nv, c.nv_own); ++v)
+      for (int64_t k = vptr[v]; k < vptr[v + 1]; ++k) supp[handle[k]].push_back(v);
+    for (int32_t i = 0; i < m; ++i) {
+      Uall.insert(Uall.end(), supp[i].begin(), supp[i].end());
+      Uptr[i + 1] = (int32_t)Uall.size();
+    }
+  }
+  std::vector<int32_t> ga_off(1, 0);
+  std::vector<uint32_t> ga_ent;
+  std::vector<unsigned long long> ga_mask;
+  for (int32_t i = 0; i < m; ++i)
+    for (int32_t q = Uptr[i]; q < Uptr[i + 1]; ++q) {
+      const int32_t u = Uall[q];
+      MS_REQUIRE(rp[u + 1] - rp[u] <= 64, MS_ERR_ARG, "Hessian row longer than 64 blocks (Galerkin encoding)");
+      unsigned long long mask = 0;
+      for (int32_t j = 0; j < rp[u + 1] - rp[u]; ++j) {
+        const int32_t v = ci[rp[u] + j];
+        const int32_t *hb = handle + vptr[v], *he = handle + vptr[v + 1];
+        const int32_t *f = std::lower_bound(hb, he, i);
+        if (f != he && *f == i) {
+          ga_ent.push_back((uint32_t)j | ((uint32_t)(vptr[v] + (f - hb)) << 6));
+          mask |= 1ull << j;
+        }
+      }
+      ga_mask.push_back(mask);
+      ga_off.push_back((int32_t)ga_ent.size());
+    }
+  std::vector<int32_t> gj_ptr(m + 1), gj_blk(m), gl_base(m + 1, 0), gl_off, sT(m);
+  std::vector<uint32_t> gl_ent;
+  for (int32_t i = 0; i < m; ++i) {
+    gj_ptr[i] = i;
+    gj_blk[i] = i;
+    sT[i] = i;
+    const int32_t nU = Uptr[i + 1] - Uptr[i];
+    const int32_t nch = (nU + kGalChunk - 1) / kGalChunk;
+    gl_base[i + 1] = gl_base[i] + nch * 2;
+    for (int32_t ch = 0; ch < nch; ++ch) {
+      gl_off.push_back((int32_t)gl_ent.size());
+      for (int32_t t = 0; t < kGalChunk && ch * kGalChunk + t < nU; ++t) {
+        const int32_t u = Uall[Uptr[i] + ch * kGalChunk + t];
+        const int32_t *hb = handle + vptr[u], *he = handle + vptr[u + 1];
+        const int32_t *f = std::lower_bound(hb, he, i);
+        MS_REQUIRE(f != he && *f == i, MS_ERR_STATE, "diagonal Galerkin lists: vertex outside the support");
+        gl_ent.push_back((uint32_t)t | ((uint32_t)(vptr[u] + (f - hb)) << 7));
+      }
+      gl_off.push_back((int32_t)gl_ent.size());
+    }
+  }
+  gj_ptr[m] = m;
+  cudaStream_t s = c.stream;
+  c.gd_U_ptr.upload(Uptr, s);
+  c.gd_U.upload(Uall.empty() ? std::vector<int32_t>{0} : Uall, s);
+  c.gd_ga_off.upload(ga_off, s);
+  c.gd_ga_ent.upload(ga_ent.empty() ? std::vector<uint32_t>{0} : ga_ent, s);
+  c.gd_ga_mask.upload(ga_mask.empty() ? std::vector<unsigned long long>{0} : ga_mask, s);
+  c.gd_gj_ptr.upload(gj_ptr, s);
+  c.gd_gj_blk.upload(gj_blk, s);
+  c.gd_gl_base.upload(gl_base, s);
+  c.gd_gl_off.upload(gl_off.empty() ? std::vector<int32_t>{0} : gl_off, s);
+  c.gd_gl_ent.upload(gl_ent.empty() ? std::vector<uint32_t>{0} : gl_ent, s);
+  c.gd_sT.upload(sT, s);
+  c.Sdiag.alloc((size_t)144 * m);
+  c.Sdiag_part.alloc((size_t)144 * m * std::max(c.gal_parts, 1));
+  c.Minv.alloc((size_t)144 * m);
+  c.cp_r.alloc((size_t)12 * m);
+  c.cp_z.alloc((size_t)12 * m);
+  c.cp_p.alloc((size_t)12 * m);
+  c.cp_t.alloc((size_t)12 * m);
+  c.cp_state.alloc(2);
+  MS_CUDA(cudaStreamSynchronize(s));
+  c.cpcg_ready = true;
 }
 
 }  // namespace msim

@@ -239,17 +239,19 @@ __device__ __forceinline__ void sell_row_product(const SellView &H, int row, con
 }
 
 __global__ void __launch_bounds__(256) k_spmv(SellView H, const double *__restrict__ xin,
-                                              double *__restrict__ yout, const double *__restrict__ b) {
+                                              double *__restrict__ yout, const double *__restrict__ b,
+                                              const int32_t *__restrict__ skip) {
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= H.nv) return;
+  if (row >= H.nv || (skip && *skip)) return;
   double o[3];
   sell_row_product(H, row, xin, o);
 #pragma unroll
   for (int i = 0; i < 3; ++i) yout[3 * row + i] = b ? b[3 * row + i] - o[i] : o[i];
 }
 
-void launch_spmv(Ctx &c, const double *xin, double *yout, double /*unused*/, const double *b) {
-  k_spmv<<<div_up(c.nv, 256), 256, 0, c.stream>>>(sell_view(c), xin, yout, b);
+// skip (device flag, may be NULL): the launch does nothing while *skip != 0 (coarse PCG batches)
+void launch_spmv(Ctx &c, const double *xin, double *yout, double /*unused*/, const double *b, const int32_t *skip) {
+  k_spmv<<<div_up(c.nv, 256), 256, 0, c.stream>>>(sell_view(c), xin, yout, b, skip);
   c.launches++;
   MS_CUDA(cudaGetLastError());
 }

@@ -28,19 +28,21 @@ class Params(C.Structure):
     _fields_ = [("h", C.c_double), ("gravity", C.c_double * 3), ("eps", C.c_double),
                 ("max_newton", C.c_int32), ("n_cg", C.c_int32), ("ls_shrink", C.c_double),
                 ("ls_min", C.c_double), ("filter_safety", C.c_double), ("ls_batch", C.c_int32),
-                ("use_graphs", C.c_int32), ("debug_flags", C.c_int32)]
+                ("use_graphs", C.c_int32), ("debug_flags", C.c_int32), ("coarse_mode", C.c_int32),
+                ("coarse_max_iter", C.c_int32), ("coarse_tol", C.c_double)]
 
 
 class NewtonStats(C.Structure):
     _fields_ = [("alpha", C.c_double), ("alpha0", C.c_double), ("ds_norm", C.c_double),
                 ("energy", C.c_double), ("delta_energy", C.c_double), ("grad_norm", C.c_double),
                 ("ls_evals", C.c_int32), ("converged", C.c_int32), ("ls_failed", C.c_int32),
-                ("n_cg", C.c_int32)]
+                ("n_cg", C.c_int32), ("coarse_iters", C.c_int32), ("pad_", C.c_int32)]
 
 
 class StepStats(C.Structure):
     _fields_ = [("newton_iters", C.c_int32), ("pcg_iters", C.c_int32), ("ls_evals", C.c_int32),
-                ("status", C.c_int32), ("last_ds_norm", C.c_double), ("last_alpha", C.c_double)]
+                ("status", C.c_int32), ("coarse_iters", C.c_int32), ("pad_", C.c_int32),
+                ("last_ds_norm", C.c_double), ("last_alpha", C.c_double)]
 
 
 class PhaseTimes(C.Structure):
