@@ -33,63 +33,22 @@ __device__ __forceinline__ size_t tile_off(int ti, int tj, int nSp) {
 
 #include "chol_diag.cuh"
 
-__global__ void __launch_bounds__(256) k_chol_diag(int k, int nSp, double *__restrict__ L,
-                                                   double *__restrict__ U, int *__restrict__ flag) {
-  extern __shared__ double sm[];
-  diag_factor(k, nSp, L, U, flag, sm);
-}
-
-// ------------------------------------------------------------------ 64^3 tile GEMM core
-// acc[a][b] = sum_kk S1[kk*64 + tr + a] * S2[kk*64 + tc + b]
-__device__ __forceinline__ void gemm64(const double *S1, const double *S2, double (&acc)[4][4], int tr, int tc) {
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  // thread (tr, tc) = (t & 15, t >> 4) owns rows tr + 16a and columns tc + 16b: for each a the
-  // 16 lanes of a half-warp read 16 consecutive doubles (one conflict-free wavefront) and the
-  // other half-warp the same addresses (broadcast); the column operand is a 2-address broadcast.
-#pragma unroll 4
-  for (int kk = 0; kk < TB; ++kk) {
-    double x[4], y[4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      x[a] = S1[kk * TB + tr + 16 * a];
-      y[a] = S2[kk * TB + tc + 16 * a];
-    }
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = fma(x[a], y[b], acc[a][b]);
-  }
-}
-
 // ------------------------------------------------------------------ tile GEMM of the dataflow kernel
 // acc = S1^T S2 over the 64-long k dimension (S1[kk*64 + r], S2[kk*64 + c]); thread-owned elements
-// idx = 0..15 at (r, c) = tile_rc(idx).  MSIM_TILE_MMA: FP64 tensor cores (mma.sync m8n8k4): warp w
-// owns rows 16 (w & 3) .. +15 and columns 32 (w >> 2) .. +31 as 2 x 4 blocks of 8 x 8; otherwise
-// the DFMA register-blocked gemm64.
-#ifndef MSIM_TILE_MMA
-#define MSIM_TILE_MMA 1
-#endif
+// idx = 0..15 at (r, c) = tile_rc(idx), on the FP64 tensor cores (mma.sync m8n8k4): warp w owns
+// rows 16 (w & 3) .. +15 and columns 32 (w >> 2) .. +31 as 2 x 4 blocks of 8 x 8.
 
 __device__ __forceinline__ void tile_rc(int idx, int &r, int &c) {
-#if MSIM_TILE_MMA
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int j = idx & 1, bj = (idx >> 1) & 3, bi = idx >> 3;
   r = 16 * (w & 3) + 8 * bi + (lane >> 2);
   c = 32 * (w >> 2) + 8 * bj + 2 * (lane & 3) + j;
-#else
-  r = (threadIdx.x & 15) + 16 * (idx >> 2);
-  c = (threadIdx.x >> 4) + 16 * (idx & 3);
-#endif
 }
 
 // LI: the second operand is a row-major inverse diagonal tile Li [64][LD] left in shared memory
 // by diag_factor (S2[kk*64 + c] = U[kk][c] = Li[c][kk]) instead of a staged k-major tile
 template <bool LI = false>
 __device__ __forceinline__ void tile_gemm(const double *S1, const double *S2, double (&acc)[16]) {
-#if MSIM_TILE_MMA
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int r0 = 16 * (w & 3) + (lane >> 2), c0 = 32 * (w >> 2) + (lane >> 2), kl = lane & 3;
 #pragma unroll
@@ -109,12 +68,6 @@ __device__ __forceinline__ void tile_gemm(const double *S1, const double *S2, do
                      : "+d"(acc[(bi * 4 + bj) * 2]), "+d"(acc[(bi * 4 + bj) * 2 + 1])
                      : "d"(bi ? a1 : a0), "d"(b[bj]));
   }
-#else
-  double a4[4][4];
-  gemm64(S1, S2, a4, threadIdx.x & 15, threadIdx.x >> 4);
-#pragma unroll
-  for (int q = 0; q < 16; ++q) acc[q] = a4[q >> 2][q & 3];
-#endif
 }
 
 // stage a column-major global tile (leading dim nSp) into k-major smem S[kk*64 + r] (cp.async)
@@ -134,67 +87,6 @@ __device__ __forceinline__ void stage_colmajor(double *S, const double *__restri
   for (int it = 0; it < (TB * TB / 2) / 256; ++it) {
     const int e2 = threadIdx.x + it * 256, kk = e2 >> 5, r2 = (e2 & 31) * 2;
     cp_async_cg16(&S[kk * TB + r2], &G[(size_t)kk * ld + r2]);
-  }
-}
-
-// ------------------------------------------------------------------ P(k): L_ik = A_ik U_kk
-__global__ void __launch_bounds__(256) k_chol_trsm(int k, const int32_t *__restrict__ panel, int nSp,
-                                                   double *__restrict__ L, const double *__restrict__ U) {
-  extern __shared__ double sm[];
-  double *SA = sm, *SU = sm + TB * TB;   // SA[kk*64 + r] = A_ik[r][kk]; SU[kk*64 + c] = U[kk][c]
-  const int i = panel[blockIdx.x], t = threadIdx.x;
-  const size_t oik = tile_off(i, k, nSp);
-  stage_colmajor(SA, L + oik, nSp);
-  stage_colmajor(SU, U + (size_t)k * TB * TB, TB);   // row-major U == k-major operand
-  __pipeline_commit();
-  __pipeline_wait_prior(0);
-  __syncthreads();
-  const int tr = t & 15, tc = t >> 4;
-  double acc[4][4];
-  gemm64(SA, SU, acc, tr, tc);
-#pragma unroll
-  for (int b = 0; b < 4; ++b)
-#pragma unroll
-    for (int a = 0; a < 4; ++a) L[oik + (size_t)(tc + 16 * b) * nSp + tr + 16 * a] = acc[a][b];
-}
-
-// ------------------------------------------------------------------ U(k): A_ij -= L_ik L_jk^T
-// Look-ahead: the CTA updating tile (la, la) (la = k + 1) -- or an extra CTA if that tile gets no
-// update in this step -- factorises it right away (D(k+1) runs inside U(k)).
-__global__ void __launch_bounds__(256) k_chol_update(int k, const int32_t *__restrict__ tasks, int ntasks,
-                                                     int la, int nSp, double *__restrict__ L,
-                                                     double *__restrict__ U, int *__restrict__ flag) {
-  extern __shared__ double sm[];
-  if ((int)blockIdx.x >= ntasks) {
-    diag_factor(la, nSp, L, U, flag, sm);
-    return;
-  }
-  double *Si = sm, *Sj = sm + TB * TB;
-  const int i = tasks[2 * blockIdx.x], j = tasks[2 * blockIdx.x + 1], t = threadIdx.x;
-  stage_colmajor(Si, L + tile_off(i, k, nSp), nSp);
-  stage_colmajor(Sj, L + tile_off(j, k, nSp), nSp);
-  __pipeline_commit();
-  const int tr = t & 15, tc = t >> 4;
-  const size_t oij = tile_off(i, j, nSp);
-  double old[4][4];
-#pragma unroll
-  for (int b = 0; b < 4; ++b)
-#pragma unroll
-    for (int a = 0; a < 4; ++a) old[a][b] = L[oij + (size_t)(tc + 16 * b) * nSp + tr + 16 * a];
-  __pipeline_wait_prior(0);
-  __syncthreads();
-  double acc[4][4];
-  gemm64(Si, Sj, acc, tr, tc);
-#pragma unroll
-  for (int b = 0; b < 4; ++b)
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int r = tr + 16 * a, c = tc + 16 * b;
-      if (i != j || r >= c) L[oij + (size_t)c * nSp + r] = old[a][b] - acc[a][b];
-    }
-  if (i == la && j == la) {
-    __syncthreads();
-    diag_factor(la, nSp, L, U, flag, sm);
   }
 }
 
@@ -681,9 +573,6 @@ constexpr int kDfCtasPerSm = MSIM_DF_PER_SM;   // CTAs per SM of the dataflow fa
 // Large-shared-memory opt-ins are per device: set once per context, on its device, right
 // after cudaSetDevice (create_common); the occupancy-derived CTA count is kept in the context.
 void chol_init_attrs(Ctx &c) {
-  MS_CUDA(cudaFuncSetAttribute(k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDiagSmem));
-  MS_CUDA(cudaFuncSetAttribute(k_chol_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem));
-  MS_CUDA(cudaFuncSetAttribute(k_chol_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem));
   set_max_dyn_smem((const void *)k_chol_dataflow, c.device);
   int per_sm = 0;
   MS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chol_dataflow, 256, kUpdSmem));
@@ -693,10 +582,6 @@ void chol_init_attrs(Ctx &c) {
 
 void launch_scatter_S(Ctx &c);
 
-static bool step_updates_diag(const Ctx &c, int k) {   // is tile (k+1, k+1) among the tasks of step k?
-  const auto &P = c.h_chol_panel[k];
-  return !P.empty() && P.front() == k + 1;
-}
 
 
 static int dataflow_grid(const Ctx &c) {
@@ -705,22 +590,19 @@ static int dataflow_grid(const Ctx &c) {
   return (int)std::max<int64_t>(4, (int64_t)per_sm * c.coop_grid);
 }
 
-// D(0); then for each k: P(k), U(k) with D(k+1) fused (look-ahead) -- or the single-launch
-// dataflow version (default)
+// the whole factorisation as one cooperative dataflow launch (zeroed tiles + scattered S first)
 void enqueue_chol_factor(Ctx &c) {
   const int nSp = c.nS_pad;
   k_zero_tiles<<<(int)c.n_sym_tiles, 256, 0, c.stream>>>(c.sym_tiles, nSp, c.Lden);
   launch_scatter_S(c);
   if (nSp > c.nS) k_pad_identity2<<<div_up(nSp - c.nS, 64), 64, 0, c.stream>>>(c.nS, nSp, c.Lden);
-  if (c.chol_dataflow) {
+  {
     const int NT = c.ntiles;
     MS_CUDA(cudaMemsetAsync(c.df_flags, 0, sizeof(int) * c.df_flags.n, c.stream));
     MS_CUDA(cudaMemcpyAsync(c.chol_ndep.p, c.chol_ndep0.p, sizeof(int32_t) * c.chol_ndep0.n,
                             cudaMemcpyDeviceToDevice, c.stream));
     MS_CUDA(cudaMemcpyAsync(c.chol_queue.p, c.chol_queue0.p, sizeof(int32_t) * c.chol_queue0.n,
                             cudaMemcpyDeviceToDevice, c.stream));
-    const int ntask = (int)c.n_dag;
-    (void)ntask;
     DfParams prm;
     prm.NT = NT;
     prm.nSp = nSp;
@@ -761,31 +643,10 @@ void enqueue_chol_factor(Ctx &c) {
     void *args[] = {&prm};
     MS_CUDA(cudaLaunchCooperativeKernel((const void *)k_chol_dataflow, dim3(dataflow_grid(c)), dim3(256), args,
                                         smem, c.stream));
-    return;
-  }
-  k_chol_diag<<<1, 256, kDiagSmem, c.stream>>>(0, nSp, c.Lden, c.Uinv, c.flags + 0);
-  for (int k = 0; k < c.ntiles; ++k) {
-    const int np = (int)c.h_chol_panel[k].size();
-    if (np) k_chol_trsm<<<np, 256, kGemmSmem, c.stream>>>(k, c.chol_panel + c.h_chol_panel_off[k], nSp, c.Lden, c.Uinv);
-    const int nt = (int)(c.h_chol_task_off[k + 1] - c.h_chol_task_off[k]);
-    const int la = k + 1 < c.ntiles ? k + 1 : -1;
-    const int extra = (la >= 0 && !step_updates_diag(c, k)) ? 1 : 0;
-    if (nt + extra)
-      k_chol_update<<<nt + extra, 256, kUpdSmem, c.stream>>>(k, c.chol_tasks + 2 * c.h_chol_task_off[k], nt, la,
-                                                             nSp, c.Lden, c.Uinv, c.flags + 0);
   }
 }
 
-int64_t chol_factor_kernels(const Ctx &c) {
-  if (c.chol_dataflow) return 3 + (c.nS_pad > c.nS ? 1 : 0);
-  int64_t n = 3 + (c.nS_pad > c.nS ? 1 : 0);
-  for (int k = 0; k < c.ntiles; ++k) {
-    const int nt = (int)(c.h_chol_task_off[k + 1] - c.h_chol_task_off[k]);
-    const int extra = (k + 1 < c.ntiles && !step_updates_diag(c, k)) ? 1 : 0;
-    n += (c.h_chol_panel[k].empty() ? 0 : 1) + ((nt + extra) ? 1 : 0);
-  }
-  return n;
-}
+int64_t chol_factor_kernels(const Ctx &c) { return 3 + (c.nS_pad > c.nS ? 1 : 0); }
 
 // solve S q = z in place on c.zs (handle order)
 void enqueue_chol_solve(Ctx &c) {

@@ -1,236 +1,24 @@
 // Diagonal-tile factorisation D(k) of the coarse tile Cholesky (chol.cu): L_kk = chol(A_kk) and
 // U_kk = L_kk^-T for one 64 x 64 tile by one 256-thread CTA.  SURVEY §8(a) a6; reading R4.
-// Variants (selected by MSIM_DIAG_VARIANT; timed by tools/bench_diag.cu):
-//   0 diag_factor_rec      2 x 2 recursion on 32 x 32 blocks, single-warp panel work
-//   1 diag_factor_blocked  right-looking, 16-column panels factored by one warp in registers
-// Both take the tile from L (column-major, leading dimension nSp) or preloaded in shared memory,
-// and write L_kk back there
+// Right-looking, 16-column panels factored by one warp in registers while the other warps form
+// the inverse row blocks of the finished panels on the FP64 tensor cores (timed by
+// tools/bench_diag.cu; measured and dropped: a 2 x 2 recursion on 32 x 32 blocks with single-warp
+// panel work, a shuffle-based panel broadcast, a scalar inverse).  Takes the tile from L
+// (column-major, leading dimension nSp) or preloaded in shared memory, and writes L_kk back there
 // and U_kk (row-major 64 x 64) to U + k 64^2; *flag = 1 if a pivot is not positive.
 // Requires TB = 64, LD = 65 and tile_off() from the including file.
 #pragma once
 #ifndef DIAG_TS
 #define DIAG_TS(i)
 #endif
-#ifndef MSIM_DIAG_VARIANT
-#define MSIM_DIAG_VARIANT 1
-#endif
 #ifndef MSIM_STORE_LKK
 #define MSIM_STORE_LKK 0
 #endif
 
-// ---------------------------------------------------------------- variant 0: recursive
-//   F11 (warp 0)              L11 = chol(A11)                    lane r owns row r
-//   TRSM (warp 1) | INV (w 2) L21 = A21 L11^-T   |   Li11 = L11^-1  lane = row of L21 / column of Li11
-//   SYRK (all)                A22 -= L21 L21^T
-//   F22 + INV (warp 0) | T (warps 1-7)   L22, Li22   |   T = L21 Li11
-//   all                       Li21 = -Li22 T
-// Loops are rolled (the D task runs once per tile: straight-line code would be fetched cold).
-// smem: A [64][LD] (row-major: the factor), Li [64][LD] (row-major: the inverse; its upper-right
-// 32 x 32 block holds T), invd [64].
-constexpr int kDiagSmemDoublesRec = 2 * TB * LD + TB + 64;
-constexpr unsigned kFull = 0xffffffffu;
-
-// The three single-warp kernels below keep one row (or column) per lane in registers, rotated
-// so that the current column is always element 0: the loop over columns stays rolled (compact
-// code: a D task runs once per tile, straight-line code would be fetched cold) while every
-// register index is static, and the rotation costs nothing (each FMA writes the next slot).
-// Entries beyond index 31 read rows >= 32 of the 64-row buffers: they only ever feed slots of
-// columns >= 32, which are never used.
-
-// Cholesky of the 32 x 32 block at A (row-major, ld) in place (lower part); invd[r] = 1 / L_rr;
-// col: 64-double warp scratch, col[32..63] = 0.  Returns false if a pivot is not positive.
-__device__ __forceinline__ bool warp_potrf32(double *A, int ld, double *invd, double *col, int lane) {
-  double a[32];
-#pragma unroll
-  for (int c = 0; c < 32; ++c) a[c] = c <= lane ? A[lane * ld + c] : 0.0;
-  bool ok = true;
-#pragma unroll 1
-  for (int j = 0; j < 32; ++j) {
-    double iv = 0.0;
-    if (lane == j) {
-      if (!(a[0] > 0.0)) {
-        ok = false;
-        a[0] = 1.0;
-      }
-      iv = rsqrt_nr2(a[0]);
-      invd[j] = iv;
-    }
-    const double inv = __shfl_sync(kFull, iv, j);
-    const double l = lane >= j ? a[0] * inv : 0.0;   // L_lane,j (L_jj = a_jj / sqrt(a_jj))
-    col[lane] = l;
-    if (lane >= j) A[lane * ld + j] = l;
-    __syncwarp();
-#pragma unroll
-    for (int c = 1; c < 32; ++c) a[c - 1] = fma(-l, col[j + c], a[c]);   // column j + c
-    a[31] = 0.0;
-    __syncwarp();
-  }
-  return __all_sync(kFull, ok);
-}
-
-// Li (32 x 32, row-major ld) = L^-1 for the lower L at A (rows 32.. of A must be finite): lane c
-// forms column c by column-oriented forward substitution.
-__device__ __forceinline__ void warp_trinv32(const double *A, int ld, const double *invd, double *Li, int lane) {
-  double s[32];
-#pragma unroll
-  for (int r = 0; r < 32; ++r) s[r] = r == lane ? 1.0 : 0.0;
-#pragma unroll 1
-  for (int q = 0; q < 32; ++q) {
-    const double x = s[0] * invd[q];   // zero for q < lane
-    Li[q * ld + lane] = x;
-#pragma unroll
-    for (int r = 1; r < 32; ++r) s[r - 1] = fma(-A[(q + r) * ld + q], x, s[r]);   // row q + r
-    s[31] = 0.0;
-  }
-}
-
-// X (32 rows at A21, row-major ld) <- X L^-T for the lower L at A11 (A11 rows continue into
-// A21): lane r solves row r, column-oriented.
-__device__ __forceinline__ void warp_trsm32(const double *A11, double *A21, int ld, const double *invd, int lane) {
-  double x[32];
-#pragma unroll
-  for (int c = 0; c < 32; ++c) x[c] = A21[lane * ld + c];
-#pragma unroll 1
-  for (int c = 0; c < 32; ++c) {
-    const double v = x[0] * invd[c];
-    A21[lane * ld + c] = v;
-#pragma unroll
-    for (int c2 = 1; c2 < 32; ++c2) x[c2 - 1] = fma(-v, A11[(c + c2) * ld + c], x[c2]);
-    x[31] = 0.0;
-  }
-}
-
-__device__ void diag_factor_rec(int k, int nSp, double *__restrict__ L, double *__restrict__ U,
-                                int *__restrict__ flag, double *sm, bool preloaded) {
-  double *A = sm;              // row-major [64][LD]: the factor
-  double *Li = sm + TB * LD;   // row-major [64][LD]: its inverse (+ T in the upper-right block)
-  double *invd = sm + 2 * TB * LD;
-  double *col = invd + TB;     // [64] broadcast buffer of warp 0 (col[32..63] = 0)
-  const int t = threadIdx.x, w = t >> 5, lane = t & 31;
-  const size_t okk = tile_off(k, k, nSp);
-  if (t < 64) col[t] = 0.0;
-#pragma unroll 4
-  for (int it = 0; it < 16; ++it) {
-    const int e = t + it * 256, r = e & 63, c = e >> 6;
-    if (!preloaded) {
-      const double v = __ldcg(&L[okk + (size_t)c * nSp + r]);
-      A[r * LD + c] = r >= c ? v : 0.0;
-    }
-    Li[r * LD + c] = 0.0;
-  }
-  __syncthreads();
-  DIAG_TS(0);
-  bool ok = true;
-  if (w == 0) ok = warp_potrf32(A, LD, invd, col, lane);
-  __syncthreads();
-  DIAG_TS(1);
-  if (w == 1) warp_trsm32(A, A + 32 * LD, LD, invd, lane);
-  else if (w == 2) warp_trinv32(A, LD, invd, Li, lane);
-  __syncthreads();
-  DIAG_TS(2);
-  // A22 -= L21 L21^T (lower): thread (r, cg) = (t >> 3, t & 7) takes columns cg, cg + 8, ... <= r
-  {
-    const int r = t >> 3, cg = t & 7;
-    const double *xr = A + (32 + r) * LD;
-#pragma unroll 1
-    for (int c = cg; c <= r; c += 8) {
-      const double *xc = A + (32 + c) * LD;
-      double s4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-      for (int q = 0; q < 32; ++q) s4[q & 3] = fma(xr[q], xc[q], s4[q & 3]);
-      A[(32 + r) * LD + 32 + c] -= (s4[0] + s4[1]) + (s4[2] + s4[3]);
-    }
-  }
-  __syncthreads();
-  DIAG_TS(3);
-  if (w == 0) {
-    ok = warp_potrf32(A + 32 * LD + 32, LD, invd + 32, col, lane) && ok;
-    __syncwarp();
-    warp_trinv32(A + 32 * LD + 32, LD, invd + 32, Li + 32 * LD + 32, lane);
-  } else {
-    // T = L21 Li11 (32 x 32) into Li[r][32 + c] (r, c < 32): warps 1..7 stride over the entries
-#pragma unroll 1
-    for (int e = t - 32; e < 1024; e += 224) {
-      const int r = e >> 5, c = e & 31;
-      double s4[4] = {0.0, 0.0, 0.0, 0.0};   // Li11 lower: terms q < c vanish
-#pragma unroll
-      for (int q = 0; q < 32; ++q) s4[q & 3] = fma(A[(32 + r) * LD + q], Li[q * LD + c], s4[q & 3]);
-      Li[r * LD + 32 + c] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-    }
-  }
-  __syncthreads();
-  DIAG_TS(4);
-  // Li21 = -Li22 T
-#pragma unroll 1
-  for (int it = 0; it < 4; ++it) {
-    const int e = t + 256 * it, r = e >> 5, c = e & 31;
-    double s4[4] = {0.0, 0.0, 0.0, 0.0};   // Li22 lower: terms q > r vanish
-#pragma unroll
-    for (int q = 0; q < 32; ++q) s4[q & 3] = fma(Li[(32 + r) * LD + 32 + q], Li[q * LD + 32 + c], s4[q & 3]);
-    Li[(32 + r) * LD + c] = -((s4[0] + s4[1]) + (s4[2] + s4[3]));
-  }
-  if (!__syncthreads_and(ok) && t == 0 && flag) *flag = 1;
-  // store L_kk (lower, column-major) and U_kk = Li^T (row-major: U[c][r] at c*64 + r = Li[r][c])
-  double *Uk = U + (size_t)k * TB * TB;
-#pragma unroll 4
-  for (int it = 0; it < 16; ++it) {
-    const int e = t + it * 256, r = e & 63, c = e >> 6;
-    if (r >= c) __stcg(&L[okk + (size_t)c * nSp + r], A[r * LD + c]);
-    __stcg(&Uk[(size_t)c * TB + r], r >= c ? Li[r * LD + c] : 0.0);   // U[c][r] = Li[r][c]
-  }
-  __syncthreads();
-  DIAG_TS(5);
-}
-
-// ---------------------------------------------------------------- variants 1, 2
+// ---------------------------------------------------------------- blocked factor + inverse
 // smem: A [64][LD], Li [64][LD], Tb [3*16*17], invd [64]
 constexpr int kDiagSmemDoublesBlocked = 2 * TB * LD + 3 * 16 * 17 + TB + 16;
 
-// Row-block pb (16 rows) of Li = L^-1 for the first 16 (pb + 1) columns of L final: the diagonal
-// block inverse (threads tt < 16, one column each) and Li_{pb,q} = -Li_{pb,pb} sum_{s=q}^{pb-1}
-// L_{pb,s} Li_{s,q} for q < pb.  Run by nth threads (tt = 0 .. nth-1) with named barrier bar_id.
-__device__ __forceinline__ void inv_rowblock(int pb, const double *A, double *Li, double (*Tb)[16][17],
-                                             const double *invd, int tt, int nth, int bar_id) {
-  const int o = 16 * pb;
-  if (tt < 16) {
-    double x[16];
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      double s = r == tt ? 1.0 : 0.0, s2 = 0.0;
-#pragma unroll
-      for (int q = 0; q < r; q += 2) {
-        s = fma(-A[(o + r) * LD + o + q], x[q], s);
-        if (q + 1 < r) s2 = fma(-A[(o + r) * LD + o + q + 1], x[q + 1], s2);
-      }
-      x[r] = (s + s2) * invd[o + r];
-    }
-#pragma unroll
-    for (int r = 0; r < 16; ++r) Li[(o + r) * LD + o + tt] = x[r];
-  } else {
-    for (int e = tt - 16; e < pb * 256; e += nth - 16) {
-      const int q = e >> 8, r = (e >> 4) & 15, cc = e & 15;
-      double s4[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int m = 16 * q; m < o; m += 4) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) s4[u] = fma(A[(o + r) * LD + m + u], Li[(m + u) * LD + 16 * q + cc], s4[u]);
-      }
-      Tb[q][r][cc] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-    }
-  }
-  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nth) : "memory");
-  for (int e = tt; e < pb * 256; e += nth) {
-    const int q = e >> 8, r = (e >> 4) & 15, cc = e & 15;
-    double s4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int m = 0; m < 16; ++m) s4[m & 3] = fma(Li[(o + r) * LD + o + m], Tb[q][m][cc], s4[m & 3]);
-    Li[(o + r) * LD + 16 * q + cc] = -((s4[0] + s4[1]) + (s4[2] + s4[3]));
-  }
-  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nth) : "memory");
-}
-
-#ifndef MSIM_INV_MMA
-#define MSIM_INV_MMA 1
-#endif
 __device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1)
@@ -326,11 +114,7 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
       // warps 1-3, 5-7: row-block p-1 of the inverse (its columns of L are final) while warp 0
       // factors panel p
       const int tt = (w < 4 ? w - 1 : w - 2) * 32 + lane;
-#if MSIM_INV_MMA
       if (p > 0) inv_rowblock_mma(p - 1, A, Li, reinterpret_cast<double *>(Tb), invd, tt, 192, 1);
-#else
-      if (p > 0) inv_rowblock(p - 1, A, Li, Tb, invd, tt, 192, 1);
-#endif
     } else {
       // panel rows j0 + lane and j0 + 32 + lane, columns j0 .. j0+15
       const int ra = j0 + lane, rb = j0 + 32 + lane;
@@ -341,24 +125,6 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
         a[c] = va ? A[ra * LD + j0 + c] : 0.0;
         b[c] = vb ? A[rb * LD + j0 + c] : 0.0;
       }
-#ifdef MSIM_PANEL_SHFL
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const double d = __shfl_sync(0xffffffffu, a[j], j);
-        if (!(d > 0.0)) bad = true;
-        const double inv = d > 0.0 ? rsqrt_nr2(d) : 1.0;   // 1 / sqrt(d)
-        const double ljj = d > 0.0 ? d * inv : 1.0;
-        if (lane == 0) invd[j0 + j] = inv;
-        a[j] = lane == j ? ljj : (lane > j ? a[j] * inv : a[j]);
-        b[j] *= inv;
-#pragma unroll
-        for (int c = j + 1; c < 16; ++c) {
-          const double lc = __shfl_sync(0xffffffffu, a[j], c);
-          a[c] = fma(-a[j], lc, a[c]);
-          b[c] = fma(-b[j], lc, b[c]);
-        }
-      }
-#else
       // the pivot's lane takes the rsqrt of its own (final) diagonal; the column of L is then
       // broadcast through shared memory (one store, 15 - j broadcast loads)
       // (the next pivot, a_{j+1,j+1} - l_{j+1,j}^2, is formed by its own lane from its own values,
@@ -397,7 +163,6 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
         }
         __syncwarp();
       }
-#endif
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
         if (va && ra >= j0 + c) A[ra * LD + j0 + c] = a[c];
@@ -445,11 +210,7 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
     if (r < 48) __stcg(&Uk[(size_t)c * TB + r], Li[r * LD + c]);
   }
   // last row-block of the inverse (the others were formed during the panels)
-#if MSIM_INV_MMA
   inv_rowblock_mma(3, A, Li, reinterpret_cast<double *>(Tb), invd, t, 256, 1);
-#else
-  inv_rowblock(3, A, Li, Tb, invd, t, 256, 1);
-#endif
   DIAG_TS(9);
 #pragma unroll
   for (int it = 0; it < 4; ++it) {   // rows 48..63 of Li: 16 x 64 entries
@@ -460,16 +221,11 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
 
 
 // ---------------------------------------------------------------- dispatch
-constexpr int kDiagSmemDoubles = kDiagSmemDoublesBlocked > kDiagSmemDoublesRec ? kDiagSmemDoublesBlocked
-                                                                                : kDiagSmemDoublesRec;
+constexpr int kDiagSmemDoubles = kDiagSmemDoublesBlocked;
 
 // preloaded: the caller has already placed the (updated) tile in sm as A [64][LD] row-major,
 // lower part, zeros above the diagonal (skips the global round trip on the critical path).
 __device__ __noinline__ void diag_factor(int k, int nSp, double *__restrict__ L, double *__restrict__ U,
                                          int *__restrict__ flag, double *sm, bool preloaded = false) {
-#if MSIM_DIAG_VARIANT == 0
-  diag_factor_rec(k, nSp, L, U, flag, sm, preloaded);
-#else
   diag_factor_blocked(k, nSp, L, U, flag, sm, preloaded);
-#endif
 }

@@ -249,33 +249,42 @@ __global__ void k_pad_identity(int nS, int nSp, double *__restrict__ L) {
 }
 
 // ------------------------------------------------------------------ 12x12 affine solve
-__global__ void k_solve12(const double *__restrict__ Sa, const double *__restrict__ z, double *__restrict__ q,
-                          int *__restrict__ flag) {
-  if (threadIdx.x != 0) return;
-  double L[12][12];
-  for (int r = 0; r < 12; ++r)
-    for (int c = 0; c < 12; ++c) L[r][c] = Sa[r * 12 + c];
+// q = S_a^-1 z by Cholesky: one CTA of 144 threads, right-looking in shared memory (thread (r, c)
+// updates entry (r, c)), then the two triangular sweeps by one thread (78 FMA each).  (Round 1 ran
+// the whole factorisation in one thread from local memory: 17-19 us per Newton iteration.)
+__global__ void __launch_bounds__(144) k_solve12(const double *__restrict__ Sa, const double *__restrict__ z,
+                                                 double *__restrict__ q, int *__restrict__ flag) {
+  __shared__ double A[12][13];
+  const int t = threadIdx.x, r = t / 12, c = t % 12;
+  A[r][c] = Sa[t];
+  __syncthreads();
   for (int j = 0; j < 12; ++j) {
-    double d = L[j][j];
-    for (int k = 0; k < j; ++k) d -= L[j][k] * L[j][k];
-    if (!(d > 0.0)) { *flag = 1; d = 1.0; }
-    L[j][j] = sqrt(d);
-    for (int r = j + 1; r < 12; ++r) {
-      double s = L[r][j];
-      for (int k = 0; k < j; ++k) s -= L[r][k] * L[j][k];
-      L[r][j] = s / L[j][j];
+    if (t == 0) {
+      double d = A[j][j];
+      if (!(d > 0.0)) {
+        *flag = 1;
+        d = 1.0;
+      }
+      A[j][j] = sqrt(d);
     }
+    __syncthreads();
+    if (t > j && t < 12) A[t][j] /= A[j][j];
+    __syncthreads();
+    if (r > j && c > j && c <= r) A[r][c] = fma(-A[r][j], A[c][j], A[r][c]);
+    __syncthreads();
   }
-  double y[12];
-  for (int r = 0; r < 12; ++r) {
-    double s = z[r];
-    for (int k = 0; k < r; ++k) s -= L[r][k] * y[k];
-    y[r] = s / L[r][r];
-  }
-  for (int r = 11; r >= 0; --r) {
-    double s = y[r];
-    for (int k = r + 1; k < 12; ++k) s -= L[k][r] * q[k];
-    q[r] = s / L[r][r];
+  if (t == 0) {
+    double y[12];
+    for (int i = 0; i < 12; ++i) {
+      double s = z[i];
+      for (int k = 0; k < i; ++k) s = fma(-A[i][k], y[k], s);
+      y[i] = s / A[i][i];
+    }
+    for (int i = 11; i >= 0; --i) {
+      double s = y[i];
+      for (int k = i + 1; k < 12; ++k) s = fma(-A[k][i], q[k], s);
+      q[i] = s / A[i][i];
+    }
   }
 }
 
@@ -639,7 +648,7 @@ void launch_coarse_direction(Ctx &c) {
   k_restrict_affine<<<std::min(div_up(c.nv_own, 256), 592), 256, 0, c.stream>>>(
       c.nv_own, c.phi_aff, c.X, o[0], o[1], o[2], c.rhs, 1.0, c.partial, c.counters + 6, c.za);
   dist_sum(c, c.za, 12);
-  k_solve12<<<1, 32, 0, c.stream>>>(c.Sa, c.za, c.qa, c.flags + 1);
+  k_solve12<<<1, 144, 0, c.stream>>>(c.Sa, c.za, c.qa, c.flags + 1);
   k_lift_affine<<<div_up(c.nv, 256), 256, 0, c.stream>>>(c.nv, c.phi_aff, c.X, o[0], o[1], o[2], c.qa, c.da);
   c.launches += 3;
   // r1 = -g - H da

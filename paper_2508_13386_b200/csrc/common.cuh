@@ -182,8 +182,6 @@ struct Ctx {
   DBuf<double> Lden;                // [nS_pad * nS_pad] column-major lower factor
   int32_t nS_pad = 0;
   std::vector<std::vector<int32_t>> h_chol_panel;      // per k: tile rows i > k in struct
-  DBuf<int32_t> chol_tasks;         // flattened per-k task lists
-  std::vector<int64_t> h_chol_task_off;
   DBuf<int32_t> chol_panel;
   std::vector<int64_t> h_chol_panel_off;
   std::vector<int32_t> h_perm;      // handle -> position in the nested-dissection order
@@ -222,7 +220,6 @@ struct Ctx {
   int df_per_sm = 1;     // dataflow factorisation CTAs per SM (chol_init_attrs)
   int64_t n_dag = 0;
   DBuf<int> df_flags;               // upd[NT*NT], pfl[NT*NT], dfl[NT]
-  bool chol_dataflow = true;
   int coop_grid = 148;
   cudaGraphExec_t factor_graph = nullptr, solve_graph = nullptr;
   int64_t factor_graph_kernels = 0, solve_graph_kernels = 0;

@@ -240,7 +240,6 @@ __device__ __forceinline__ void cyclic_relabel3(double (&a)[45], double (&v)[81]
     }
 }
 
-#ifndef MSIM_JACOBI_UNROLLED
 __device__ __forceinline__ void jacobi_sweep(double (&a)[45], double (&v)[81]) {
 #pragma unroll 1
   for (int rd = 0; rd < 3; ++rd) {
@@ -250,19 +249,6 @@ __device__ __forceinline__ void jacobi_sweep(double (&a)[45], double (&v)[81]) {
     cyclic_relabel3(a, v);
   }
 }
-#else
-__device__ __forceinline__ void jacobi_sweep(double (&a)[45], double (&v)[81]) {
-  jacobi_round<0>(a, v);
-  jacobi_round<1>(a, v);
-  jacobi_round<2>(a, v);
-  jacobi_round<3>(a, v);
-  jacobi_round<4>(a, v);
-  jacobi_round<5>(a, v);
-  jacobi_round<6>(a, v);
-  jacobi_round<7>(a, v);
-  jacobi_round<8>(a, v);
-}
-#endif
 
 __device__ __forceinline__ double offdiag2(const double (&a)[45]) {
   double s = 0.0;

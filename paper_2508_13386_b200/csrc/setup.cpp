@@ -591,22 +591,15 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
     c.chol_info.lower_tiles = nzt;
   }
   c.h_chol_panel = best.panel;
-  std::vector<int32_t> panel_flat, task_flat, rows_flat, sym_tiles;
+  std::vector<int32_t> panel_flat, rows_flat, sym_tiles;
   std::vector<int32_t> panel_ptr(NT + 1, 0), rows_ptr(NT + 1, 0);
   c.h_chol_panel_off.assign(NT + 1, 0);
-  c.h_chol_task_off.assign(NT + 1, 0);
   c.h_chol_rows_off.assign(NT + 1, 0);
   for (int32_t k = 0; k < NT; ++k) {
     const auto &P = best.panel[k];
-    for (size_t a = 0; a < P.size(); ++a)
-      for (size_t b = 0; b <= a; ++b) {
-        task_flat.push_back(P[a]);
-        task_flat.push_back(P[b]);
-      }
     panel_flat.insert(panel_flat.end(), P.begin(), P.end());
     rows_flat.insert(rows_flat.end(), best.rows[k].begin(), best.rows[k].end());
     c.h_chol_panel_off[k + 1] = (int64_t)panel_flat.size();
-    c.h_chol_task_off[k + 1] = (int64_t)task_flat.size() / 2;
     c.h_chol_rows_off[k + 1] = (int64_t)rows_flat.size();
     panel_ptr[k + 1] = (int32_t)panel_flat.size();
     rows_ptr[k + 1] = (int32_t)rows_flat.size();
@@ -872,10 +865,6 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   c.chol_ndep.alloc(ndep.size());
   c.chol_queue0.upload(queue0, s);
   c.chol_queue.alloc(queue0.size());
-  {
-    const char *e = std::getenv("MSIM_CHOL_DATAFLOW");   // 0: per-step launches (diagnostics)
-    c.chol_dataflow = !(e && e[0] == '0');
-  }
   c.df_flags.alloc((size_t)2 * NT * NT + NT + 1 + m);   // upd, pfl, dfl, chain SM, rdone[m]
   c.Uinv.alloc((size_t)NT * T * T);
   {
@@ -884,7 +873,6 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
     c.coop_grid = std::max(1, nsm);
   }
   c.chol_panel.upload(panel_flat.empty() ? std::vector<int32_t>{0} : panel_flat, s);
-  c.chol_tasks.upload(task_flat.empty() ? std::vector<int32_t>{0, 0} : task_flat, s);
   c.qa.alloc(12);
   c.za.alloc(12);
   c.qs.alloc(c.nS_pad);

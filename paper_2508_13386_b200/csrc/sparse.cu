@@ -222,13 +222,7 @@ __device__ __forceinline__ void sell_row_product(const SellView &H, int row, con
   for (int cc = c0; cc < c1; ++cc) {
     const int col = __ldg(&H.col[(size_t)cc * 32 + lane]);
     const double *v = H.vals + (size_t)cc * 288 + lane;
-#if defined(MSIM_SPMV_NOGATHER)   // diagnostics only (wrong results): streaming cost without the x gather
-    const double x0 = 1.0 + col * 1e-30, x1 = x0, x2 = x0;
-#elif defined(MSIM_SPMV_LDG)
-    const double x0 = __ldg(&xin[3 * col]), x1 = __ldg(&xin[3 * col + 1]), x2 = __ldg(&xin[3 * col + 2]);
-#else
     const double x0 = xin[3 * col], x1 = xin[3 * col + 1], x2 = xin[3 * col + 2];
-#endif
     a0 = fma(ld_stream(v), x0, fma(ld_stream(v + 32), x1, fma(ld_stream(v + 64), x2, a0)));
     a1 = fma(ld_stream(v + 96), x0, fma(ld_stream(v + 128), x1, fma(ld_stream(v + 160), x2, a1)));
     a2 = fma(ld_stream(v + 192), x0, fma(ld_stream(v + 224), x1, fma(ld_stream(v + 256), x2, a2)));

@@ -32,8 +32,7 @@ __global__ void __launch_bounds__(256) kbench(const double *A0, double *L, doubl
     __threadfence_block();
     long long t0 = clock64();
     if (threadIdx.x == 0 && blockIdx.x == 0) g_ts[15] = t0;
-    if (V == 0) diag_factor_rec(0, TB, Lb, Ub, flag, sm, false);
-    else diag_factor_blocked(0, TB, Lb, Ub, flag, sm, false);
+    diag_factor_blocked(0, TB, Lb, Ub, flag, sm, false);
     __syncthreads();
     tot += clock64() - t0;
   }
