@@ -6,6 +6,8 @@ E(x) = 1/2 sum_v m_v |x_v - xhat_v|^2 + h^2 [ sum_e V_e Psi(F_e) + kappa sum_v b
 
 * implicit Euler, alpha = 1 (L182-184); gravity folded into the predictor
   xhat = x^t + h v^t + h^2 g_grav (reading R8 / Q10);
+* BDF2 (L185-189; NEXT-4): alpha = 4/9, xhat = (4x^t - x^{t-1})/3 + (2h/9)(4v^t - v^{t-1}) + alpha h^2 g
+  (gravity is an external potential inside the alpha-scaled term, so it folds in with alpha h^2);
 * lumped mass m_v = sum_{e ni v} rho_e V_e / 4 (reading Q9, SPEC S:50);
 * IPC log barrier against the ground plane, b(d) = -(d - dhat)^2 ln(d/dhat) for
   d < dhat (P:177, P:629, SPEC S:161); E = +inf if any d_v <= 0;
@@ -35,6 +37,7 @@ class Model:
     h: float
     gravity: np.ndarray
     ground: dict | None
+    alpha: float = 1.0        # IP scaling of Eq. 2: 1 (implicit Euler), 4/9 (BDF2)
 
     @property
     def n(self):
@@ -53,9 +56,21 @@ def make_model(scene):
                  np.asarray(scene.gravity, dtype=np.float64), scene.ground)
 
 
+def ah2(model):
+    """alpha h^2, the weight of the potential energies in Eq. 2."""
+    return model.alpha * model.h ** 2
+
+
 def predictor(model, x_t, v_t):
     """xhat = x^t + h v^t + h^2 g_grav (P:183 with gravity folded in, R8)."""
     return x_t + model.h * v_t + model.h ** 2 * model.gravity[None, :]
+
+
+def predictor_bdf2(model, x_t, v_t, x_tm1, v_tm1):
+    """BDF2 predictor: xhat = (4x^t - x^{t-1})/3 + (2h/9)(4v^t - v^{t-1}), plus the folded
+    gravity alpha h^2 g with alpha = 4/9."""
+    h = model.h
+    return (4.0 * x_t - x_tm1) / 3.0 + (2.0 * h / 9.0) * (4.0 * v_t - v_tm1) + (4.0 / 9.0) * h ** 2 * model.gravity[None, :]
 
 
 # ----------------------------------------------------------------------------- barrier
@@ -92,8 +107,8 @@ def ground_distance(model, x):
 # ----------------------------------------------------------------------------- E, g
 
 def energy_terms(model, x, xhat):
-    """(inertia, h^2*elastic, h^2*barrier) with +inf on inversion / penetration."""
-    h2 = model.h ** 2
+    """(inertia, alpha h^2 elastic, alpha h^2 barrier) with +inf on inversion / penetration."""
+    h2 = ah2(model)
     f = model.free
     inertia = 0.5 * np.sum(model.mass[f] * np.sum((x[f] - xhat[f]) ** 2, axis=1))
     elastic = h2 * np.sum(fem.element_energy(x, model.tets, model.Bm, model.V, model.mu, model.lam))
@@ -116,7 +131,7 @@ def energy_difference(model, x, d, alpha, xhat):
     """E(x + alpha d) - E(x), summed term by term (reading Q12: the strict-decrease test of the
     backtracking line search is evaluated on per-element / per-vertex differences so that the
     large constant parts of E cancel exactly instead of at the scale of |E|)."""
-    h2 = model.h ** 2
+    h2 = ah2(model)
     f = model.free
     y = x + alpha * d
     r = x[f] - xhat[f]
@@ -140,8 +155,8 @@ def energy_difference(model, x, d, alpha, xhat):
 
 
 def gradient(model, x, xhat):
-    """g = M (x - xhat) + h^2 [sum_e G_e^T vec P V_e + kappa b'(d) n]; g = 0 at DBC vertices."""
-    h2 = model.h ** 2
+    """g = M (x - xhat) + alpha h^2 [sum_e G_e^T vec P V_e + kappa b'(d) n]; g = 0 at DBC vertices."""
+    h2 = ah2(model)
     ge = fem.element_gradient(x, model.tets, model.Bm, model.V, model.mu, model.lam)
     g = np.zeros_like(x)
     for a in range(4):
@@ -174,7 +189,7 @@ def hessian(model, x, xhat, chunk=32768):
     Returned as scipy.sparse.bsr_matrix with 3x3 blocks: H_(i,j) = sum over tets e and
     local corners (a,b) with e[a]=i, e[b]=j of the (a,b) 3x3 block of P+(H_e)."""
     n = model.n
-    h2 = model.h ** 2
+    h2 = ah2(model)
     indptr, indices = block_pattern(model.tets, n)
     nnzb = len(indices)
     rows = np.repeat(np.arange(n), np.diff(indptr))

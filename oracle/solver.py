@@ -209,8 +209,11 @@ class NewtonInfo:
 class OracleSim:
     """Timestep driver: begin_step / newton_iteration / end_step (Alg. 1)."""
 
-    def __init__(self, scene, basis, n_cg=None, coarse_mode="exact", coarse_tol=1e-4, coarse_max_iter=None):
+    def __init__(self, scene, basis, n_cg=None, coarse_mode="exact", coarse_tol=1e-4, coarse_max_iter=None,
+                 integrator="ie"):
         self.coarse_mode, self.coarse_tol, self.coarse_max_iter = coarse_mode, coarse_tol, coarse_max_iter
+        self.integrator = integrator      # "ie" or "bdf2" (P:182-189; the first step is IE, no history)
+        self.x_prev = self.v_prev = None
         self.scene = scene
         self.model = ip.make_model(scene)
         self.basis = basis
@@ -224,7 +227,13 @@ class OracleSim:
 
     def begin_step(self):
         self.x_t = self.x.copy()
-        self.xhat = ip.predictor(self.model, self.x, self.v)
+        self.v_t = self.v.copy()
+        if self.integrator == "bdf2" and self.x_prev is not None:
+            self.model.alpha = 4.0 / 9.0
+            self.xhat = ip.predictor_bdf2(self.model, self.x, self.v, self.x_prev, self.v_prev)
+        else:
+            self.model.alpha = 1.0
+            self.xhat = ip.predictor(self.model, self.x, self.v)
 
     def direction(self, x):
         """(g, H, d_s, d_f, d) at x: Alg. 1 L229-238."""
@@ -262,7 +271,17 @@ class OracleSim:
                           ip.energy(m, self.x, self.xhat), d, ds, df)
 
     def end_step(self):
-        self.v = (self.x - self.x_t) / self.model.h
+        h = self.model.h
+        if self.model.alpha != 1.0:
+            # BDF2 (reading C2): a = 9/(4h^2)(x - xtilde) with xtilde the predictor without
+            # the folded gravity, v = (4v^t - v^{t-1})/3 + (2h/3) a
+            xtilde = self.xhat - (4.0 / 9.0) * h ** 2 * self.model.gravity[None, :]
+            a = 9.0 / (4.0 * h ** 2) * (self.x - xtilde)
+            v_new = (4.0 * self.v_t - self.v_prev) / 3.0 + (2.0 * h / 3.0) * a
+        else:
+            v_new = (self.x - self.x_t) / h
+        self.x_prev, self.v_prev = self.x_t, self.v_t
+        self.v = v_new
 
     def timestep(self):
         self.begin_step()
