@@ -66,7 +66,14 @@ typedef struct ms_params {
                              B^T (H (B p)), 12 x 12 blocks S_ii (NEXT-1)                     */
   int32_t coarse_max_iter;/* MS_COARSE_PCG: iteration cap (default 1000)                     */
   double coarse_tol;      /* MS_COARSE_PCG: ||r||_2 <= coarse_tol ||b||_2 (default 1e-4)    */
+  int32_t integrator;     /* MS_INTEGRATOR_IE (default) or MS_INTEGRATOR_BDF2 (P:185-189:
+                             alpha = 4/9, xhat = (4x^t - x^{t-1})/3 + (2h/9)(4v^t - v^{t-1}) +
+                             alpha h^2 g, v^{t+1} = (4v^t - v^{t-1})/3 + (2h/3) a^{t+1} with
+                             a^{t+1} = 9/(4h^2)(x^{t+1} - xtilde), reading C2; a step without
+                             history -- the first after ms_set_state -- is implicit Euler)   */
+  int32_t pad_;
 } ms_params;
+enum { MS_INTEGRATOR_IE = 0, MS_INTEGRATOR_BDF2 = 1 };
 enum { MS_COARSE_EXACT = 0, MS_COARSE_PCG = 1 };
 enum { MS_DEBUG_HESS_FALLBACK = 1 };
 

@@ -123,7 +123,7 @@ static ms_status newton_step(Ctx &c, ms_newton_stats *st) {
   MS_REQUIRE(h[SC_INFEAS] == 0.0 && h[SC_INFEAS_V] == 0.0, MS_ERR_INFEASIBLE,
              "infeasible iterate: inverted element or penetrating vertex (E = +inf)");
   MS_REQUIRE(fl[0] == 0 && fl[1] == 0, MS_ERR_NOT_SPD, "coarse matrix not SPD (Cholesky pivot <= 0)");
-  const double h2 = c.params.h * c.params.h;
+  const double h2 = c.ah2();   // alpha h^2 (Eq. 2)
   const double energy = h2 * h[SC_ENERGY_ELEM] + h[SC_ENERGY_VERT];
   double alpha = 0.0, dE = 0.0;
   int evals = 0;
@@ -254,6 +254,8 @@ void ms_default_params(ms_params *p) {
   p->coarse_mode = MS_COARSE_EXACT;
   p->coarse_max_iter = 1000;
   p->coarse_tol = 1e-4;
+  p->integrator = MS_INTEGRATOR_IE;
+  p->pad_ = 0;
 }
 
 static ms_status create_common(ms_ctx **out, int device, void *cuda_stream, int rank, int world,
@@ -382,6 +384,7 @@ ms_status ms_upload_mesh(ms_ctx *ctx, int64_t n_verts, const double *rest_xyz, i
     c.m = 0;
     pcg_reset_graph(c);
     c.nv_glob = (int32_t)n_verts;
+    c.has_history = false;
     c.h_Eg.assign(E, E + n_tets);
     c.h_rhog.assign(rho, rho + n_tets);
     c.h_dbc_glob.clear();
@@ -467,6 +470,8 @@ ms_status ms_set_params(ms_ctx *ctx, const ms_params *p) {
                "ls_batch must be 1, 2, 4 or 8");
     MS_REQUIRE(p->coarse_mode == MS_COARSE_EXACT || p->coarse_mode == MS_COARSE_PCG, MS_ERR_ARG, "bad coarse_mode");
     MS_REQUIRE(p->coarse_tol >= 0.0 && p->coarse_max_iter > 0, MS_ERR_ARG, "bad coarse PCG params");
+    MS_REQUIRE(p->integrator == MS_INTEGRATOR_IE || p->integrator == MS_INTEGRATOR_BDF2, MS_ERR_ARG, "bad integrator");
+    if (p->integrator != ctx->c.params.integrator) ctx->c.has_history = false;
     if (p->n_cg != ctx->c.params.n_cg || p->use_graphs != ctx->c.params.use_graphs ||
         p->coarse_mode != ctx->c.params.coarse_mode || p->coarse_tol != ctx->c.params.coarse_tol ||
         p->coarse_max_iter != ctx->c.params.coarse_max_iter) {
@@ -649,6 +654,7 @@ ms_status ms_set_state(ms_ctx *ctx, const double *x, const double *v) {
     if (x) upload_global(c, c.x, x);
     if (v) upload_global(c, c.v, v);
     c.step_begun = false;
+    c.has_history = false;   // a new trajectory: BDF2 restarts with an implicit-Euler step
     c.assembled = false;
   });
   return MS_OK;
@@ -763,7 +769,7 @@ ms_status ms_assemble(ms_ctx *ctx, double *energy_out) {
     enqueue_assembly(c);
     fetch_scalars(c, 1);
     if (energy_out) {
-      const double h2 = c.params.h * c.params.h;
+      const double h2 = c.ah2();   // alpha h^2 (Eq. 2)
       *energy_out = (c.h_pinned[SC_INFEAS] > 0 || c.h_pinned[SC_INFEAS_V] > 0)
                         ? INFINITY
                         : h2 * c.h_pinned[SC_ENERGY_ELEM] + c.h_pinned[SC_ENERGY_VERT];

@@ -135,6 +135,10 @@ struct Ctx {
 
   // ---- state
   DBuf<double> x, v, xt, xhat;      // (nv,3)
+  DBuf<double> x_prev, v_prev;      // (nv,3) BDF2 history x^{t-1}, v^{t-1}
+  bool has_history = false;         // a previous step exists (BDF2 can be used)
+  double alpha = 1.0;               // IP scaling of the current step: 1 (IE) or 4/9 (BDF2), Eq. 2
+  double ah2() const { return alpha * params.h * params.h; }
   DBuf<double> g, ds, da, df, d, r, rhs;   // 3nv
   DBuf<double> p, q, z, tmp;               // PCG vectors
   DBuf<double> stage_g;             // [nt*12] element gradients (unscaled by h^2)

@@ -292,7 +292,7 @@ void launch_filters(Ctx &c) {
 
 // evaluates candidates k0 .. k0+K-1 into ls_out[0..K) (energy differences) and ls_out[K..2K) (steps)
 void launch_ls_batch(Ctx &c, int k0, int K) {
-  const double h2 = c.params.h * c.params.h;
+  const double h2 = c.ah2();   // alpha h^2 (Eq. 2)
   const int grid = std::min(div_up(std::max(c.nt, c.nv), 256), 148 * 8);
 #define LS_ARGS                                                                                       \
   lsmesh(c), c.nt_own, c.nv_own, c.dist() ? 1 : 0, c.x, c.d, c.xhat, c.mass, c.fixed, c.scal, k0, c.params.ls_shrink, h2, c.gn[0],      \

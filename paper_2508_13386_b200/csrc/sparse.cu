@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(256) k_vertex_grad(
 
 void launch_vertex_grad(Ctx &c) {
   const int bs = 256, nb = std::min(div_up(c.nv, bs), 148 * 8);
-  const double h2 = c.params.h * c.params.h;
+  const double h2 = c.ah2();   // alpha h^2 (Eq. 2)
   k_vertex_grad<<<nb, bs, 0, c.stream>>>(c.nv, c.nv_own, c.vinc_ptr, c.vinc, c.stage_g, c.x, c.xhat, c.mass,
                                          c.fixed, ground_of(c), h2, c.g, c.partial, c.counters + 1,
                                          c.scal + SC_ENERGY_VERT);
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(256) k_assemble(
 
 void launch_assemble(Ctx &c) {
   const int bs = 256;
-  const double h2 = c.params.h * c.params.h;
+  const double h2 = c.ah2();   // alpha h^2 (Eq. 2)
   k_assemble<<<div_up(c.npos, bs), bs, 0, c.stream>>>(c.npos, c.sell_slot, c.sell_col, c.cptr, c.contrib,
                                                       c.stage_h, c.x, c.mass, c.fixed, c.slot_row,
                                                       ground_of(c), h2, c.vals, c.dinv);
@@ -581,10 +581,37 @@ __global__ void k_predictor(int nv, const double *__restrict__ X, const uint8_t 
     xhat[3 * i + k] = xi + h * v[3 * i + k] + h * h * gg[k];
   }
 }
+// BDF2 predictor: xhat = (4x^t - x^{t-1})/3 + (2h/9)(4v^t - v^{t-1}) + (4/9) h^2 g
+__global__ void k_predictor_bdf2(int nv, const double *__restrict__ X, const uint8_t *__restrict__ fixed,
+                                 double *__restrict__ x, const double *__restrict__ v,
+                                 const double *__restrict__ xp, const double *__restrict__ vp,
+                                 double *__restrict__ xt, double *__restrict__ xhat, double h, double g0, double g1,
+                                 double g2) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nv) return;
+  const double gg[3] = {g0, g1, g2};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double xi = x[3 * i + k];
+    if (fixed[i]) xi = X[3 * i + k];
+    x[3 * i + k] = xi;
+    xt[3 * i + k] = xi;
+    xhat[3 * i + k] = (4.0 * xi - xp[3 * i + k]) / 3.0 + (2.0 * h / 9.0) * (4.0 * v[3 * i + k] - vp[3 * i + k]) +
+                      (4.0 / 9.0) * h * h * gg[k];
+  }
+}
+
 void launch_predictor(Ctx &c) {
-  k_predictor<<<div_up(c.nv, 256), 256, 0, c.stream>>>(c.nv, c.X, c.fixed, c.x, c.v, c.xt, c.xhat,
-                                                       c.params.h, c.params.gravity[0],
-                                                       c.params.gravity[1], c.params.gravity[2]);
+  const bool bdf2 = c.params.integrator == MS_INTEGRATOR_BDF2 && c.has_history;
+  c.alpha = bdf2 ? 4.0 / 9.0 : 1.0;
+  if (bdf2)
+    k_predictor_bdf2<<<div_up(c.nv, 256), 256, 0, c.stream>>>(c.nv, c.X, c.fixed, c.x, c.v, c.x_prev, c.v_prev, c.xt,
+                                                              c.xhat, c.params.h, c.params.gravity[0],
+                                                              c.params.gravity[1], c.params.gravity[2]);
+  else
+    k_predictor<<<div_up(c.nv, 256), 256, 0, c.stream>>>(c.nv, c.X, c.fixed, c.x, c.v, c.xt, c.xhat, c.params.h,
+                                                         c.params.gravity[0], c.params.gravity[1],
+                                                         c.params.gravity[2]);
   c.launches++;
   MS_CUDA(cudaGetLastError());
 }
@@ -595,9 +622,42 @@ __global__ void k_velocity(int n3, const double *__restrict__ x, const double *_
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n3) v[i] = (x[i] - xt[i]) * inv_h;
 }
+
+// end of a step with the BDF2 history kept: x^{t-1} <- x^t, v^{t-1} <- v^t and v^{t+1} =
+//   IE step:   (x - x^t) / h
+//   BDF2 step: (4v^t - v^{t-1})/3 + (2h/3) a, a = 9/(4h^2)(x - xtilde), xtilde = xhat - (4/9) h^2 g
+//              (reading C2: the printed 4h^2/9 is not an acceleration)
+__global__ void k_velocity_hist(int n3, int bdf2, const double *__restrict__ x, double *__restrict__ xt,
+                                const double *__restrict__ xhat, double *__restrict__ v, double *__restrict__ xp,
+                                double *__restrict__ vp, double h, double g0, double g1, double g2) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n3) return;
+  const double gk = (i % 3 == 0) ? g0 : (i % 3 == 1 ? g1 : g2);
+  const double vt = v[i], xti = xt[i];
+  double vn;
+  if (bdf2) {
+    const double a = 9.0 / (4.0 * h * h) * (x[i] - (xhat[i] - (4.0 / 9.0) * h * h * gk));
+    vn = (4.0 * vt - vp[i]) / 3.0 + (2.0 * h / 3.0) * a;
+  } else {
+    vn = (x[i] - xti) / h;
+  }
+  xp[i] = xti;
+  vp[i] = vt;
+  v[i] = vn;
+}
+
 void launch_velocity(Ctx &c) {
   const int n3 = 3 * c.nv;
-  k_velocity<<<div_up(n3, 256), 256, 0, c.stream>>>(n3, c.x, c.xt, c.v, 1.0 / c.params.h);
+  if (c.params.integrator == MS_INTEGRATOR_BDF2) {
+    c.x_prev.alloc(n3);
+    c.v_prev.alloc(n3);
+    k_velocity_hist<<<div_up(n3, 256), 256, 0, c.stream>>>(n3, c.alpha != 1.0 ? 1 : 0, c.x, c.xt, c.xhat, c.v,
+                                                           c.x_prev, c.v_prev, c.params.h, c.params.gravity[0],
+                                                           c.params.gravity[1], c.params.gravity[2]);
+    c.has_history = true;
+  } else {
+    k_velocity<<<div_up(n3, 256), 256, 0, c.stream>>>(n3, c.x, c.xt, c.v, 1.0 / c.params.h);
+  }
   c.launches++;
   MS_CUDA(cudaGetLastError());
 }

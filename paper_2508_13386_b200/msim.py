@@ -29,7 +29,8 @@ class Params(C.Structure):
                 ("max_newton", C.c_int32), ("n_cg", C.c_int32), ("ls_shrink", C.c_double),
                 ("ls_min", C.c_double), ("filter_safety", C.c_double), ("ls_batch", C.c_int32),
                 ("use_graphs", C.c_int32), ("debug_flags", C.c_int32), ("coarse_mode", C.c_int32),
-                ("coarse_max_iter", C.c_int32), ("coarse_tol", C.c_double)]
+                ("coarse_max_iter", C.c_int32), ("coarse_tol", C.c_double), ("integrator", C.c_int32),
+                ("pad_", C.c_int32)]
 
 
 class NewtonStats(C.Structure):
