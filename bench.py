@@ -246,6 +246,11 @@ def run_ours(args):
     partitioned = world > 1 and not args.replicas
     coarse_mode = 1 if args.coarse == "pcg" else 0
     integrator = 1 if args.integrator == "bdf2" else 0
+    extra = dict(coarse_mode=coarse_mode, integrator=integrator, use_cubature=int(args.cubature),
+                 lag_hessian=int(args.lag))
+    if args.cubature:
+        from precompute.cubature import cached_cubature
+        extra["cubature"] = cached_cubature(s, b)
     if partitioned:
         # one problem over N GPUs: x-slab partition, NCCL halo exchange / allreduce inside the
         # library; rank 0 creates the NCCL id, broadcast over the process group
@@ -254,11 +259,9 @@ def run_ours(args):
             uid.copy_(torch.frombuffer(bytearray(msim.nccl_unique_id()), dtype=torch.uint8))
         torch.distributed.broadcast(uid, src=0)
         ctx = msim.context_from_scene(s, b, device=local, stream=stream.cuda_stream, rank=rank, world=world,
-                                      nccl_id=bytes(uid.cpu().numpy().tobytes()), coarse_mode=coarse_mode,
-                                      integrator=integrator)
+                                      nccl_id=bytes(uid.cpu().numpy().tobytes()), **extra)
     else:
-        ctx = msim.context_from_scene(s, b, device=local, stream=stream.cuda_stream, coarse_mode=coarse_mode,
-                                      integrator=integrator)
+        ctx = msim.context_from_scene(s, b, device=local, stream=stream.cuda_stream, **extra)
     sizes = ctx.sizes()
 
     def barrier():
@@ -352,7 +355,8 @@ def run_ours(args):
             "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong" if partitioned else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": dict(config_dict(s, b, world, partitioned), coarse=args.coarse, integrator=args.integrator),
+            "config": dict(config_dict(s, b, world, partitioned), coarse=args.coarse, integrator=args.integrator,
+                           cubature=bool(args.cubature), lag_hessian=bool(args.lag)),
             "pcg_iters_per_s": pcg_all / (ms_max * 1e-3),
             "newton_iters": int(newton_all),
             "coarse_pcg_iters_per_newton": coarse_it / max(newton, 1) if args.coarse == "pcg" else None,
@@ -390,6 +394,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--coarse", default="exact", choices=["exact", "pcg"],
                     help="coarse solves: exact Cholesky of S (default) or the paper's block-Jacobi PCG to 1e-4")
+    ap.add_argument("--cubature", action="store_true",
+                    help="NEXT-2: cubature subspace Hessian (precompute/cubature.py, cached under .cache/)")
+    ap.add_argument("--lag", action="store_true", help="NEXT-2: lagged elastic Hessian for the refinement PCG")
     ap.add_argument("--integrator", default="ie", choices=["ie", "bdf2"],
                     help="time integrator: implicit Euler (default, the configs' own) or BDF2 (P:185-189)")
     ap.add_argument("--replicas", action="store_true",

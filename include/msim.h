@@ -66,6 +66,13 @@ typedef struct ms_params {
                              B^T (H (B p)), 12 x 12 blocks S_ii (NEXT-1)                     */
   int32_t coarse_max_iter;/* MS_COARSE_PCG: iteration cap (default 1000)                     */
   double coarse_tol;      /* MS_COARSE_PCG: ||r||_2 <= coarse_tol ||b||_2 (default 1e-4)    */
+  int32_t use_cubature;   /* NEXT-2: the subspace solves use the cubature Hessian
+                             (elastic part over the ms_cubature_upload elements, weight w_e in
+                             place of V_e; inertia and barrier exact); 0 = fully integrated (R3) */
+  int32_t lag_hessian;    /* NEXT-2: the refinement PCG uses a lagged elastic Hessian
+                             (refreshed at the first iteration of every step and when the mean of
+                             the last 3 accepted step sizes < 0.2, at least 5 iterations apart;
+                             inertia and barrier always fresh; reading C4)                    */
   int32_t integrator;     /* MS_INTEGRATOR_IE (default) or MS_INTEGRATOR_BDF2 (P:185-189:
                              alpha = 4/9, xhat = (4x^t - x^{t-1})/3 + (2h/9)(4v^t - v^{t-1}) +
                              alpha h^2 g, v^{t+1} = (4v^t - v^{t-1})/3 + (2h/3) a^{t+1} with
@@ -245,6 +252,13 @@ void ms_basis_free(ms_basis *b);
 ms_status ms_basis_export(ms_ctx *ctx, double *origins, int64_t *vptr, int32_t *handle, double *phi,
                           double *phi_affine, double affine_origin[3], int32_t *cluster,
                           int32_t *centroid_vertex);
+
+/* The cubature of the subspace Hessian (NEXT-2; §3.8, Alg. 3): n elements
+ * (global tet ids, any order, no repeats) with weights w > 0 that replace the element volume in
+ * the elastic-energy integral of the cubature Hessian (precompute/cubature.py fits them by
+ * modal moment fitting).  Used when params.use_cubature = 1.  Errors: MS_ERR_ARG (index range,
+ * w <= 0, repeats), MS_ERR_STATE (no mesh). */
+ms_status ms_cubature_upload(ms_ctx *ctx, int64_t n, const int32_t *elements, const double *weights);
 
 /* ---------------------------------------------------------------- state */
 /* Set / get positions x and velocities v (n_verts x 3). */

@@ -183,11 +183,11 @@ def block_pattern(tets, n):
     return A.indptr.astype(np.int64), A.indices.astype(np.int64)
 
 
-def hessian(model, x, xhat, chunk=32768):
-    """H = M + h^2 (sum_e P+(H_e) + kappa b''(d) n n^T), DBC rows/cols -> identity.
-
-    Returned as scipy.sparse.bsr_matrix with 3x3 blocks: H_(i,j) = sum over tets e and
-    local corners (a,b) with e[a]=i, e[b]=j of the (a,b) 3x3 block of P+(H_e)."""
+def elastic_blocks(model, x, elem_scale=None, chunk=32768):
+    """alpha h^2 sum_e s_e P+(H_e) as 3x3 blocks on the BSR pattern (block_pattern): the (a,b) 3x3
+    block of P+(H_e) goes to slot (e[a], e[b]).  s_e = 1 (full integration) or, for the cubature
+    Hessian of the subspace solves (§3.8, NEXT-2), s_e = w_e / V_e on the cubature elements and 0
+    elsewhere (the weight replaces the element volume)."""
     n = model.n
     h2 = ah2(model)
     indptr, indices = block_pattern(model.tets, n)
@@ -195,21 +195,40 @@ def hessian(model, x, xhat, chunk=32768):
     rows = np.repeat(np.arange(n), np.diff(indptr))
     key = rows * n + indices                   # sorted
     blocks = np.zeros((nnzb, 9))
+    sel = np.arange(len(model.tets)) if elem_scale is None else np.flatnonzero(elem_scale != 0.0)
 
     def work(e):
-        t = model.tets[e]
-        He = fem.element_hessian_psd(x, t, model.Bm[e], model.V[e], model.mu[e], model.lam[e], chunk=len(t))
-        # the (a,b) 3x3 block of P+(H_e) goes to BSR slot (e[a], e[b])
+        t = model.tets[sel[e]]
+        ids = sel[e]
+        He = fem.element_hessian_psd(x, t, model.Bm[ids], model.V[ids], model.mu[ids], model.lam[ids], chunk=len(t))
+        if elem_scale is not None:
+            He = He * elem_scale[ids][:, None, None]
         slot = np.searchsorted(key, (t[:, :, None] * n + t[:, None, :]).ravel())      # (c*16,)
         sub = He.reshape(-1, 4, 3, 4, 3).transpose(0, 1, 3, 2, 4).reshape(-1, 9)  # (c*16, 9)
         return slot, sub
 
-    for slot, sub in fem.map_chunks(work, len(model.tets), chunk):     # summed in chunk order
+    for slot, sub in fem.map_chunks(work, len(sel), chunk):     # summed in chunk order
         lo, hi = int(slot.min()), int(slot.max()) + 1
         for q in range(9):
             blocks[lo:hi, q] += np.bincount(slot - lo, weights=sub[:, q], minlength=hi - lo)
     blocks = blocks.reshape(nnzb, 3, 3)
     blocks *= h2
+    return blocks
+
+
+def hessian(model, x, xhat, chunk=32768, elem_scale=None, elastic=None):
+    """H = M + alpha h^2 (sum_e s_e P+(H_e) + kappa b''(d) n n^T), DBC rows/cols -> identity.
+
+    Returned as scipy.sparse.bsr_matrix with 3x3 blocks: H_(i,j) = sum over tets e and
+    local corners (a,b) with e[a]=i, e[b]=j of the (a,b) 3x3 block of P+(H_e).  elem_scale: see
+    elastic_blocks; elastic: precomputed elastic blocks (the lagged Hessian of the refinement,
+    §3.7.2: elastic part frozen, inertia and barrier always fresh)."""
+    n = model.n
+    h2 = ah2(model)
+    indptr, indices = block_pattern(model.tets, n)
+    rows = np.repeat(np.arange(n), np.diff(indptr))
+    key = rows * n + indices
+    blocks = (elastic_blocks(model, x, elem_scale, chunk) if elastic is None else elastic).copy()
     diag = np.searchsorted(key, np.arange(n) * n + np.arange(n))
     blocks[diag] += model.mass[:, None, None] * np.eye(3)[None]
     if model.ground is not None:

@@ -192,6 +192,19 @@ def inversion_alpha(model, x, d):
     return float(min(1.0, FILTER_SAFETY * np.min(roots)))
 
 
+def hlag_should_update(it, alphas, last_refresh, window=3, threshold=0.2, gap=5):
+    """Refresh of the lagged elastic Hessian (§3.7.2; reading C4): always
+    at the first Newton iteration of a timestep; afterwards when the moving average of the last
+    `window` accepted step sizes drops below `threshold` and at least `gap` iterations passed since
+    the last refresh."""
+    if it == 0:
+        return True
+    if it - last_refresh < gap or not alphas:
+        return False
+    recent = alphas[-window:]
+    return sum(recent) / len(recent) < threshold
+
+
 @dataclasses.dataclass
 class NewtonInfo:
     alpha: float
@@ -210,8 +223,14 @@ class OracleSim:
     """Timestep driver: begin_step / newton_iteration / end_step (Alg. 1)."""
 
     def __init__(self, scene, basis, n_cg=None, coarse_mode="exact", coarse_tol=1e-4, coarse_max_iter=None,
-                 integrator="ie"):
+                 integrator="ie", cubature=None, lag=False):
         self.coarse_mode, self.coarse_tol, self.coarse_max_iter = coarse_mode, coarse_tol, coarse_max_iter
+        # NEXT-2 (§3.8, §3.7.2): cubature Hessian for the subspace solves, lagged Hessian for the
+        # refinement (refresh policy: hlag_should_update)
+        self.cubature, self.lag = cubature, lag
+        self.lag_elastic = None
+        self.lag_refreshes = 0
+        self.step_iter, self.step_alphas, self.last_refresh = 0, [], 0
         self.integrator = integrator      # "ie" or "bdf2" (P:182-189; the first step is IE, no history)
         self.x_prev = self.v_prev = None
         self.scene = scene
@@ -224,8 +243,13 @@ class OracleSim:
         self.max_newton = scene.max_newton
         self.x = self.model.X.copy()
         self.v = np.zeros_like(self.x)
+        self.elem_scale = None
+        if cubature is not None:
+            self.elem_scale = np.zeros(len(self.model.tets))
+            self.elem_scale[cubature.elements] = cubature.weights / self.model.V[cubature.elements]
 
     def begin_step(self):
+        self.step_iter, self.step_alphas, self.last_refresh = 0, [], 0
         self.x_t = self.x.copy()
         self.v_t = self.v.copy()
         if self.integrator == "bdf2" and self.x_prev is not None:
@@ -236,14 +260,26 @@ class OracleSim:
             self.xhat = ip.predictor(self.model, self.x, self.v)
 
     def direction(self, x):
-        """(g, H, d_s, d_f, d) at x: Alg. 1 L229-238."""
+        """(g, H, d_s, d_f, d) at x: Alg. 1 L229-238 -- full-space gradient, the subspace Hessian H
+        (cubature-integrated with NEXT-2, else fully integrated: reading R3), H_lag for the
+        refinement (lagged elastic part with NEXT-2, else H), d_s (Alg. 2), d_f = PCG(H_lag, -g - H d_s)."""
         m = self.model
         g = ip.gradient(m, x, self.xhat)
-        H = ip.hessian(m, x, self.xhat).tocsr()
+        H = ip.hessian(m, x, self.xhat, elem_scale=self.elem_scale).tocsr()
+        if self.lag:
+            if self.lag_elastic is None or hlag_should_update(self.step_iter, self.step_alphas, self.last_refresh):
+                self.lag_elastic = ip.elastic_blocks(m, x)
+                self.last_refresh = self.step_iter
+                self.lag_refreshes += 1
+            H_ref = ip.hessian(m, x, self.xhat, elastic=self.lag_elastic).tocsr()
+        elif self.elem_scale is not None:
+            H_ref = ip.hessian(m, x, self.xhat).tocsr()
+        else:
+            H_ref = H
         ds, da, Sa, S = subspace_direction(H, g, self.Ua, self.Us, self.coarse_mode, self.coarse_tol,
                                            self.coarse_max_iter)
         r = -g.ravel() - H @ ds
-        df = pcg(H, r, self.n_cg)
+        df = pcg(H_ref, r, self.n_cg)
         return g, H, ds, df, ds + df
 
     def newton_iteration(self):
@@ -265,6 +301,8 @@ class OracleSim:
                 break
         if not failed:
             self.x = x + alpha * d3
+        self.step_alphas.append(alpha if not failed else 0.0)
+        self.step_iter += 1
         ds_norm = float(np.linalg.norm(ds))
         conv = ds_norm / (m.h * m.n) < self.eps
         return NewtonInfo(alpha, a0, evals, ds_norm, conv, failed,

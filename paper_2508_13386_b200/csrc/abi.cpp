@@ -59,17 +59,41 @@ static void require_basis(Ctx &c) { MS_REQUIRE(c.m > 0, MS_ERR_STATE, "no basis 
 
 static int n_cg_of(const Ctx &c) { return c.params.n_cg > 0 ? c.params.n_cg : c.n_cg_basis; }
 
+// NEXT-2 refresh policy of the lagged elastic Hessian (reading C4)
+static bool hlag_should_update(const Ctx &c) {
+  if (!c.lag_valid || c.step_iter == 0) return true;
+  if (c.step_iter - c.lag_last_refresh < 5 || c.step_alphas.empty()) return false;
+  const size_t n = std::min<size_t>(3, c.step_alphas.size());
+  double s = 0.0;
+  for (size_t k = c.step_alphas.size() - n; k < c.step_alphas.size(); ++k) s += c.step_alphas[k];
+  return s / (double)n < 0.2;
+}
+
 static void enqueue_assembly(Ctx &c) {
   phase_begin(c, MS_PHASE_GRAD);
   launch_elem_grad(c);
   launch_vertex_grad(c);
   dist_sum(c, c.scal + SC_SUM0, SC_SUM_N);   // energies, |g|^2, infeasibility: over all ranks
   phase_end(c);
+  // H_ref (the refinement Hessian) in vals; with NEXT-2 the subspace Hessian separately in vals_s
+  const bool lag = c.params.lag_hessian != 0, cub = c.params.use_cubature != 0;
+  const bool refresh = !lag || hlag_should_update(c);
   phase_begin(c, MS_PHASE_HESS);
-  launch_elem_hess(c);
+  if (lag && !refresh && cub) launch_elem_hess_list(c);   // only the cubature elements are needed
+  else launch_elem_hess(c);
   phase_end(c);
   phase_begin(c, MS_PHASE_ASSEMBLY);
-  launch_assemble(c);
+  if (refresh) {
+    launch_assemble(c);
+    if (lag) {
+      c.lag_valid = true;
+      c.lag_last_refresh = c.step_iter;
+      c.lag_refreshes++;
+    }
+  } else {
+    launch_lag_diag(c);
+  }
+  if (c.separate_sub()) launch_assemble_sub(c);
   phase_end(c);
   c.assembled = true;
   c.coarse_ready = false;
@@ -155,6 +179,8 @@ static ms_status newton_step(Ctx &c, ms_newton_stats *st) {
   }
   if (!failed) launch_update(c, alpha);
   phase_end(c);
+  c.step_alphas.push_back(failed ? 0.0 : alpha);
+  c.step_iter++;
   const double dsn = std::sqrt(h[SC_DSNORM2]);
   const bool conv = dsn / (c.params.h * c.nv_glob) < c.params.eps;   // R7: all vertices
   if (st) {
@@ -177,6 +203,8 @@ static void begin_step(Ctx &c) {
   require_mesh(c);
   launch_predictor(c);
   c.step_begun = true;
+  c.step_iter = 0;
+  c.step_alphas.clear();
 }
 
 static void end_step(Ctx &c) {
@@ -255,6 +283,8 @@ void ms_default_params(ms_params *p) {
   p->coarse_max_iter = 1000;
   p->coarse_tol = 1e-4;
   p->integrator = MS_INTEGRATOR_IE;
+  p->use_cubature = 0;
+  p->lag_hessian = 0;
   p->pad_ = 0;
 }
 
@@ -472,6 +502,8 @@ ms_status ms_set_params(ms_ctx *ctx, const ms_params *p) {
     MS_REQUIRE(p->coarse_tol >= 0.0 && p->coarse_max_iter > 0, MS_ERR_ARG, "bad coarse PCG params");
     MS_REQUIRE(p->integrator == MS_INTEGRATOR_IE || p->integrator == MS_INTEGRATOR_BDF2, MS_ERR_ARG, "bad integrator");
     if (p->integrator != ctx->c.params.integrator) ctx->c.has_history = false;
+    if (p->lag_hessian != ctx->c.params.lag_hessian || p->use_cubature != ctx->c.params.use_cubature)
+      ctx->c.lag_valid = false;
     if (p->n_cg != ctx->c.params.n_cg || p->use_graphs != ctx->c.params.use_graphs ||
         p->coarse_mode != ctx->c.params.coarse_mode || p->coarse_tol != ctx->c.params.coarse_tol ||
         p->coarse_max_iter != ctx->c.params.coarse_max_iter) {
@@ -642,6 +674,37 @@ ms_status ms_basis_export(ms_ctx *ctx, double *origins, int64_t *vptr, int32_t *
     Ctx &c = ctx->c;
     MS_REQUIRE(c.built_basis != nullptr, MS_ERR_STATE, "ms_basis_export before ms_basis_build");
     copy_basis(*c.built_basis, origins, vptr, handle, phi, phi_affine, affine_origin, cluster, centroid_vertex);
+  });
+  return MS_OK;
+}
+
+ms_status ms_cubature_upload(ms_ctx *ctx, int64_t n, const int32_t *elements, const double *weights) {
+  if (!ctx) return MS_ERR_ARG;
+  MS_TRY(ctx, {
+    Ctx &c = ctx->c;
+    require_mesh(c);
+    MS_REQUIRE(n >= 0 && (n == 0 || (elements && weights)), MS_ERR_ARG, "bad cubature arrays");
+    const int64_t nt_glob = (int64_t)c.h_Eg.size();
+    std::vector<int32_t> g2l;
+    if (c.dist()) {
+      g2l.assign(nt_glob, -1);
+      for (int32_t le = 0; le < c.nt; ++le) g2l[c.part.tet_l2g[le]] = le;
+    }
+    std::vector<char> seen(nt_glob, 0);
+    std::vector<int32_t> loc;
+    std::vector<double> w;
+    for (int64_t k = 0; k < n; ++k) {
+      MS_REQUIRE(elements[k] >= 0 && elements[k] < nt_glob, MS_ERR_ARG, "cubature element out of range");
+      MS_REQUIRE(weights[k] > 0.0, MS_ERR_ARG, "cubature weights must be > 0");
+      MS_REQUIRE(!seen[elements[k]], MS_ERR_ARG, "repeated cubature element");
+      seen[elements[k]] = 1;
+      const int32_t le = c.dist() ? g2l[elements[k]] : elements[k];
+      if (le < 0) continue;   // multi-GPU: not a local tet
+      loc.push_back(le);
+      w.push_back(weights[k]);
+    }
+    build_cubature_structures(c, loc, w);
+    c.lag_valid = false;
   });
   return MS_OK;
 }

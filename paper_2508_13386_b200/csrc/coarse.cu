@@ -194,7 +194,8 @@ __global__ void k_galerkin_Sa_final(int nch, const double *__restrict__ part, do
   Sa[row * 12 + 4 * c + k] = s;
 }
 
-HView hview(const Ctx &c) { return HView{c.sl_ptr, c.sell_col, c.vals}; }
+// the subspace Hessian (NEXT-2: the cubature Hessian; else H itself)
+HView hview(const Ctx &c) { return HView{c.sl_ptr, c.sell_col, c.vals_sub()}; }
 
 GalParams galerkin_params(const Ctx &c) {
   GalParams G;
@@ -471,7 +472,7 @@ static void enqueue_cpcg_batch(Ctx &c) {
   const double tol2 = c.params.coarse_tol * c.params.coarse_tol;
   for (int k = 0; k < kCpcgBatch; ++k) {
     launch_lift(c, c.cp_p, c.tmp, false, c.cp_state);      // w = B p
-    launch_spmv(c, c.tmp, c.r, 0.0, nullptr, c.cp_state);  // y = H w
+    launch_spmv(c, c.tmp, c.r, 0.0, nullptr, c.cp_state, c.vals_sub());  // y = H w
     launch_restrict(c, c.r, c.cp_t, c.cp_state);           // t = B^T y
     dist_sum(c, c.cp_t, n);
     k_cpcg_step<<<1, kCpcgThreads, 0, c.stream>>>(n, c.cp_t, c.Minv, c.qs, c.cp_r, c.cp_z, c.cp_p, c.scal,
@@ -652,7 +653,7 @@ void launch_coarse_direction(Ctx &c) {
   k_lift_affine<<<div_up(c.nv, 256), 256, 0, c.stream>>>(c.nv, c.phi_aff, c.X, o[0], o[1], o[2], c.qa, c.da);
   c.launches += 3;
   // r1 = -g - H da
-  launch_spmv(c, c.da, c.tmp, 0.0, c.rhs);
+  launch_spmv(c, c.da, c.tmp, 0.0, c.rhs, nullptr, c.vals_sub());
   // SMS stage: zs = B^T r1; zs <- S^-1 zs; ds = da + B zs
   launch_restrict(c, c.tmp, c.zs);
   dist_sum(c, c.zs, 12 * (int64_t)c.m);
@@ -662,7 +663,7 @@ void launch_coarse_direction(Ctx &c) {
   MS_CUDA(cudaMemcpyAsync(c.ds, c.da, sizeof(double) * n3, cudaMemcpyDeviceToDevice, c.stream));
   launch_lift(c, pcg ? c.qs : c.zs, c.ds, true);
   // r = -g - H ds
-  launch_spmv(c, c.ds, c.r, 0.0, c.rhs);
+  launch_spmv(c, c.ds, c.r, 0.0, c.rhs, nullptr, c.vals_sub());
   MS_CUDA(cudaGetLastError());
 }
 

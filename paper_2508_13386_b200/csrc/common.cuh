@@ -123,12 +123,25 @@ struct Ctx {
   int64_t nnzb = 0;
   std::vector<int32_t> h_rowptr, h_colidx;
   DBuf<int32_t> rowptr, colidx, diag_slot, slot_row;
+  DBuf<int32_t> diag_pos;           // [nv] SELL position of the diagonal block of each row
   DBuf<int32_t> cptr, contrib;      // slot -> list of (tet*16 + a*4 + b)
   DBuf<double> vals;                // SELL-32 values [npos/32][9][32] (sell.cuh)
   int64_t npos = 0;                 // SELL positions (nnzb + padding)
   DBuf<int32_t> sl_ptr, sell_col, sell_slot;
   std::vector<int64_t> h_sell_pos;  // CSR slot -> SELL position
   DBuf<double> dinv;                // [3 nv] Jacobi D^-1
+  // ---- NEXT-2: cubature subspace Hessian and lagged refinement Hessian
+  DBuf<double> tet_scale;           // [nt] w_e / V_e on cubature elements, 0 elsewhere
+  DBuf<int32_t> cub_tets;           // local ids of the cubature elements
+  int32_t n_cub = 0;
+  DBuf<int32_t> cptr_c, contrib_c;  // per BSR slot: contributions of cubature elements only
+  DBuf<double> vals_s;              // SELL values of the subspace Hessian when it differs from H_ref
+  DBuf<double> lag_diag;            // [nv][9] alpha h^2 elastic part of the lagged diagonal blocks
+  bool lag_valid = false;
+  int32_t step_iter = 0, lag_last_refresh = 0, lag_refreshes = 0;
+  std::vector<double> step_alphas;
+  bool separate_sub() const { return params.use_cubature || params.lag_hessian; }
+  const double *vals_sub() const { return separate_sub() ? vals_s.p : vals.p; }
   // ground
   bool has_ground = false;
   double gn[3] = {0, 0, 1}, goff = 0, dhat = 1e-3, kappa = 0;
@@ -311,8 +324,12 @@ void launch_elem_hess(Ctx &c);
 void launch_eval_elements(Ctx &c, const double *x_dev, double *Ee, double *ge, double *He);
 void launch_vertex_grad(Ctx &c);
 void launch_assemble(Ctx &c);
+void launch_assemble_sub(Ctx &c);      // the subspace Hessian (cubature / fresh) into vals_s
+void launch_lag_diag(Ctx &c);          // H_lag diagonal blocks: frozen elastic part + fresh inertia / barrier
+void launch_elem_hess_list(Ctx &c);    // element Hessians of the cubature elements only
+void build_cubature_structures(Ctx &c, const std::vector<int32_t> &loc_elems, const std::vector<double> &w);
 void launch_spmv(Ctx &c, const double *xin, double *yout, double alpha_minus_b, const double *b,
-                 const int32_t *skip = nullptr);
+                 const int32_t *skip = nullptr, const double *vals = nullptr);
 void launch_pcg(Ctx &c, const double *rhs, double *sol, int iters);
 void pcg_reset_graph(Ctx &c);
 void launch_coarse_S(Ctx &c, bool full_S = false);

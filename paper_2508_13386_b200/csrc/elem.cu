@@ -441,13 +441,17 @@ constexpr int kHessStg = kStageH + 1;
 __global__ void __launch_bounds__(kHessThreads, MSIM_HESS_MINB) k_elem_hess(MeshView M, const double *__restrict__ x,
                                                             double *__restrict__ stage_h,
                                                             int32_t *__restrict__ work,
-                                                            unsigned int *__restrict__ nwork, int force_fallback) {
+                                                            unsigned int *__restrict__ nwork, int force_fallback,
+                                                            const int32_t *__restrict__ list, int nlist) {
   extern __shared__ double hsm[];   // eig9 scratch [kHessScratch][kHessThreads] / store staging
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  // list (NEXT-2 cubature iterations): thread idx handles tet list[idx] instead of tet idx
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n_items = list ? nlist : M.nt;
+  const int e = idx < n_items ? (list ? __ldg(&list[idx]) : idx) : M.nt;
   const int lane = threadIdx.x & 31, wbase = threadIdx.x & ~31;
   bool store = false;
   double p9[45];
-  if (e < M.nt) {
+  if (idx < n_items) {
     TetKin k;
     load_tet_kin(M, x, e, k);
     double a[45];
@@ -470,6 +474,11 @@ __global__ void __launch_bounds__(kHessThreads, MSIM_HESS_MINB) k_elem_hess(Mesh
   double *stg = hsm + (size_t)threadIdx.x * kHessStg;
   if (store) lift_store(p9, stg);
   __syncwarp();
+  if (list) {   // scattered tets: each thread copies its own 100-double row
+    if (store)
+      for (int q = 0; q < kStageH; ++q) stage_h[(size_t)e * kStageH + q] = stg[q];
+    return;
+  }
   const int e0 = blockIdx.x * blockDim.x + wbase;
   const int ntet = min(32, M.nt - e0);
   double *dst = stage_h + (size_t)e0 * kStageH;
@@ -528,7 +537,8 @@ void launch_elem_hess_to(Ctx &c, const double *x) {
   MS_CUDA(cudaMemsetAsync(c.hess_nwork, 0, sizeof(unsigned int), c.stream));
   constexpr int smem = kHessSmem;
   k_elem_hess<<<div_up(c.nt, kHessThreads), kHessThreads, smem, c.stream>>>(
-      mesh_view(c), x, c.stage_h, c.hess_work, c.hess_nwork, (c.params.debug_flags & MS_DEBUG_HESS_FALLBACK) ? 1 : 0);
+      mesh_view(c), x, c.stage_h, c.hess_work, c.hess_nwork, (c.params.debug_flags & MS_DEBUG_HESS_FALLBACK) ? 1 : 0,
+      nullptr, 0);
   k_elem_hess_eig<<<148 * 2, 128, 0, c.stream>>>(mesh_view(c), x, c.stage_h, c.hess_work, c.hess_nwork);
   c.launches += 2;
   static const bool dbg = std::getenv("MSIM_DEBUG_HESS") != nullptr;   // diagnostics only
@@ -542,6 +552,17 @@ void launch_elem_hess_to(Ctx &c, const double *x) {
 }
 
 void launch_elem_hess(Ctx &c) { launch_elem_hess_to(c, c.x); }
+
+// NEXT-2: the element Hessians of the cubature elements only (iterations without an H_lag refresh)
+void launch_elem_hess_list(Ctx &c) {
+  MS_CUDA(cudaMemsetAsync(c.hess_nwork, 0, sizeof(unsigned int), c.stream));
+  k_elem_hess<<<div_up(std::max(c.n_cub, 1), kHessThreads), kHessThreads, kHessSmem, c.stream>>>(
+      mesh_view(c), c.x, c.stage_h, c.hess_work, c.hess_nwork, (c.params.debug_flags & MS_DEBUG_HESS_FALLBACK) ? 1 : 0,
+      c.cub_tets, c.n_cub);
+  k_elem_hess_eig<<<148 * 2, 128, 0, c.stream>>>(mesh_view(c), c.x, c.stage_h, c.hess_work, c.hess_nwork);
+  c.launches += 2;
+  MS_CUDA(cudaGetLastError());
+}
 
 void launch_eval_elements(Ctx &c, const double *x_dev, double *Ee, double *ge, double *He) {
   launch_elem_grad_to(c, x_dev, Ee);

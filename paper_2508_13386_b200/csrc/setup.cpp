@@ -162,6 +162,13 @@ void build_mesh_structures(Ctx &c, const double *X, const int32_t *tets, const d
   c.rowptr.upload(c.h_rowptr, s);
   c.colidx.upload(c.h_colidx, s);
   c.diag_slot.upload(diag, s);
+  {
+    std::vector<int32_t> dpos(nv);
+    for (int32_t v = 0; v < nv; ++v) dpos[v] = (int32_t)c.h_sell_pos[diag[v]];
+    c.diag_pos.upload(dpos, s);
+  }
+  c.n_cub = 0;
+  c.lag_valid = false;
   c.slot_row.upload(slot_row, s);
   c.cptr.upload(cptr, s);
   c.contrib.upload(contrib, s);
@@ -881,6 +888,48 @@ void build_basis_structures(Ctx &c, int32_t m, const double *origins, const int6
   c.xsol.alloc(c.nS_pad);
   coarse_reset_graphs(c);
   launch_basis_W(c);
+  MS_CUDA(cudaStreamSynchronize(s));
+}
+
+// Cubature of the subspace Hessian (NEXT-2): per-tet scale w_e / V_e and, per BSR slot, the
+// contributions (tet*16 + a*4 + b, tet order) of the cubature elements only.
+void build_cubature_structures(Ctx &c, const std::vector<int32_t> &loc_elems, const std::vector<double> &w) {
+  const int32_t nt = c.nt;
+  std::vector<double> scale(nt, 0.0);
+  std::vector<double> vol(nt);
+  c.vol.download(vol.data(), nt, c.stream);
+  MS_CUDA(cudaStreamSynchronize(c.stream));
+  for (size_t k = 0; k < loc_elems.size(); ++k) scale[loc_elems[k]] = w[k] / vol[loc_elems[k]];
+  const int32_t *tets = c.h_tets.data();
+  auto slot_of = [&](int32_t r, int32_t col) {
+    const int32_t *b = c.h_colidx.data() + c.h_rowptr[r], *e = c.h_colidx.data() + c.h_rowptr[r + 1];
+    return (int32_t)(std::lower_bound(b, e, col) - c.h_colidx.data());
+  };
+  std::vector<int32_t> sorted = loc_elems;
+  std::sort(sorted.begin(), sorted.end());
+  std::vector<int32_t> cptr(c.nnzb + 1, 0), cslot((size_t)16 * sorted.size());
+  for (size_t k = 0; k < sorted.size(); ++k) {
+    const int32_t e = sorted[k];
+    for (int a = 0; a < 4; ++a)
+      for (int b = 0; b < 4; ++b) {
+        const int32_t sl = slot_of(tets[4 * (size_t)e + a], tets[4 * (size_t)e + b]);
+        cslot[16 * k + 4 * a + b] = sl;
+        cptr[sl + 1]++;
+      }
+  }
+  for (int64_t sl = 0; sl < c.nnzb; ++sl) cptr[sl + 1] += cptr[sl];
+  std::vector<int32_t> contrib(cslot.size());
+  {
+    std::vector<int32_t> fill(cptr.begin(), cptr.end() - 1);
+    for (size_t k = 0; k < sorted.size(); ++k)
+      for (int q = 0; q < 16; ++q) contrib[fill[cslot[16 * k + q]]++] = 16 * sorted[k] + q;
+  }
+  cudaStream_t s = c.stream;
+  c.tet_scale.upload(scale, s);
+  c.cub_tets.upload(sorted.empty() ? std::vector<int32_t>{0} : sorted, s);
+  c.cptr_c.upload(cptr, s);
+  c.contrib_c.upload(contrib.empty() ? std::vector<int32_t>{0} : contrib, s);
+  c.n_cub = (int32_t)sorted.size();
   MS_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -118,12 +118,16 @@ __host__ __device__ constexpr int blk4s(int a, int b) { return a * 4 - (a * (a -
 constexpr int kAsmUnroll = MSIM_ASM_UNROLL;
 
 // thread per SELL position (coalesced value writes); slot s = sell_slot[pos] (-1: padding)
+// tet_scale (may be NULL): per-tet factor of the contributions (the cubature weight w_e / V_e);
+// dinv (may be NULL): Jacobi diagonal; diag_el (may be NULL): the alpha h^2 elastic part of the
+// diagonal blocks before inertia and barrier are added (the frozen part of the lagged Hessian)
 __global__ void __launch_bounds__(256) k_assemble(
     int64_t npos, const int32_t *__restrict__ sell_slot, const int32_t *__restrict__ sell_col,
     const int32_t *__restrict__ cptr, const int32_t *__restrict__ contrib,
     const double *__restrict__ stage_h, const double *__restrict__ x, const double *__restrict__ mass,
     const uint8_t *__restrict__ fixed, const int32_t *__restrict__ slot_row, Ground G, double h2,
-    double *__restrict__ vals, double *__restrict__ dinv) {
+    double *__restrict__ vals, double *__restrict__ dinv, const double *__restrict__ tet_scale,
+    double *__restrict__ diag_el) {
   const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (pos >= npos) return;
   const int cidx = (int)(pos >> 5), lane = (int)(pos & 31);
@@ -147,12 +151,17 @@ __global__ void __launch_bounds__(256) k_assemble(
         v[2 * h] = t2.x;
         v[2 * h + 1] = t2.y;
       }
+      const double sc = tet_scale ? __ldg(&tet_scale[e]) : 1.0;
 #pragma unroll
-      for (int q = 0; q < 9; ++q) acc[q] += up ? v[q] : v[(q % 3) * 3 + q / 3];
+      for (int q = 0; q < 9; ++q) acc[q] += sc * (up ? v[q] : v[(q % 3) * 3 + q / 3]);
     }
     const int row = slot_row[s], col = sell_col[pos];
 #pragma unroll
     for (int q = 0; q < 9; ++q) acc[q] *= h2;
+    if (row == col && diag_el) {
+#pragma unroll
+      for (int q = 0; q < 9; ++q) diag_el[9 * (size_t)row + q] = acc[q];
+    }
     if (row == col) {
       const double m = mass[row];
       acc[0] += m;
@@ -170,7 +179,7 @@ __global__ void __launch_bounds__(256) k_assemble(
 #pragma unroll
       for (int q = 0; q < 9; ++q) acc[q] = (row == col && (q % 4 == 0)) ? 1.0 : 0.0;
     }
-    if (row == col) {
+    if (row == col && dinv) {
       dinv[3 * row + 0] = 1.0 / acc[0];
       dinv[3 * row + 1] = 1.0 / acc[4];
       dinv[3 * row + 2] = 1.0 / acc[8];
@@ -180,12 +189,72 @@ __global__ void __launch_bounds__(256) k_assemble(
   for (int q = 0; q < 9; ++q) vals[sell_val_index(cidx, q, lane)] = acc[q];
 }
 
+// the refinement Hessian (H, or H_lag at a refresh) into vals + dinv
 void launch_assemble(Ctx &c) {
   const int bs = 256;
   const double h2 = c.ah2();   // alpha h^2 (Eq. 2)
+  if (c.params.lag_hessian) c.lag_diag.alloc(9 * (size_t)c.nv);
   k_assemble<<<div_up(c.npos, bs), bs, 0, c.stream>>>(c.npos, c.sell_slot, c.sell_col, c.cptr, c.contrib,
                                                       c.stage_h, c.x, c.mass, c.fixed, c.slot_row,
-                                                      ground_of(c), h2, c.vals, c.dinv);
+                                                      ground_of(c), h2, c.vals, c.dinv, nullptr,
+                                                      c.params.lag_hessian ? c.lag_diag.p : nullptr);
+  c.launches++;
+  MS_CUDA(cudaGetLastError());
+}
+
+// the subspace Hessian into vals_s: the cubature Hessian (contributions of the cubature elements,
+// weighted w_e / V_e; NEXT-2) or, with only lagging on, the fresh fully integrated H
+void launch_assemble_sub(Ctx &c) {
+  const int bs = 256;
+  const double h2 = c.ah2();
+  c.vals_s.alloc(c.vals.n);
+  const bool cub = c.params.use_cubature;
+  MS_REQUIRE(!cub || c.n_cub > 0, MS_ERR_STATE, "use_cubature without ms_cubature_upload");
+  k_assemble<<<div_up(c.npos, bs), bs, 0, c.stream>>>(c.npos, c.sell_slot, c.sell_col, cub ? c.cptr_c : c.cptr,
+                                                      cub ? c.contrib_c : c.contrib, c.stage_h, c.x, c.mass,
+                                                      c.fixed, c.slot_row, ground_of(c), h2, c.vals_s, nullptr,
+                                                      cub ? c.tet_scale.p : nullptr, nullptr);
+  c.launches++;
+  MS_CUDA(cudaGetLastError());
+}
+
+// H_lag between refreshes: the off-diagonal blocks keep their frozen elastic values; every
+// diagonal block is rebuilt as frozen elastic part + fresh inertia + fresh barrier (DBC identity)
+__global__ void k_lag_diag(int nv, const int32_t *__restrict__ diag_pos, const double *__restrict__ diag_el,
+                           const double *__restrict__ x, const double *__restrict__ mass,
+                           const uint8_t *__restrict__ fixed, Ground G, double h2, double *__restrict__ vals,
+                           double *__restrict__ dinv) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= nv) return;
+  double acc[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) acc[q] = diag_el[9 * (size_t)row + q];
+  const double m = mass[row];
+  acc[0] += m;
+  acc[4] += m;
+  acc[8] += m;
+  if (G.on) {
+    const double d = G.n0 * x[3 * row] + G.n1 * x[3 * row + 1] + G.n2 * x[3 * row + 2] - G.off;
+    const double kb = h2 * G.kappa * bar_d2(d, G.dhat);
+    const double n[3] = {G.n0, G.n1, G.n2};
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc[q] += kb * n[q / 3] * n[q % 3];
+  }
+  if (fixed[row]) {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc[q] = (q % 4 == 0) ? 1.0 : 0.0;
+  }
+  dinv[3 * row + 0] = 1.0 / acc[0];
+  dinv[3 * row + 1] = 1.0 / acc[4];
+  dinv[3 * row + 2] = 1.0 / acc[8];
+  const int pos = diag_pos[row];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) vals[sell_val_index(pos >> 5, q, pos & 31)] = acc[q];
+}
+
+void launch_lag_diag(Ctx &c) {
+  k_lag_diag<<<div_up(c.nv, 256), 256, 0, c.stream>>>(c.nv, c.diag_pos, c.lag_diag, c.x, c.mass, c.fixed,
+                                                      ground_of(c), c.ah2(), c.vals, c.dinv);
   c.launches++;
   MS_CUDA(cudaGetLastError());
 }
@@ -244,8 +313,11 @@ __global__ void __launch_bounds__(256) k_spmv(SellView H, const double *__restri
 }
 
 // skip (device flag, may be NULL): the launch does nothing while *skip != 0 (coarse PCG batches)
-void launch_spmv(Ctx &c, const double *xin, double *yout, double /*unused*/, const double *b, const int32_t *skip) {
-  k_spmv<<<div_up(c.nv, 256), 256, 0, c.stream>>>(sell_view(c), xin, yout, b, skip);
+void launch_spmv(Ctx &c, const double *xin, double *yout, double /*unused*/, const double *b, const int32_t *skip,
+                 const double *vals) {
+  SellView H = sell_view(c);
+  if (vals) H.vals = vals;
+  k_spmv<<<div_up(c.nv, 256), 256, 0, c.stream>>>(H, xin, yout, b, skip);
   c.launches++;
   MS_CUDA(cudaGetLastError());
 }

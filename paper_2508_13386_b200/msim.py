@@ -29,8 +29,8 @@ class Params(C.Structure):
                 ("max_newton", C.c_int32), ("n_cg", C.c_int32), ("ls_shrink", C.c_double),
                 ("ls_min", C.c_double), ("filter_safety", C.c_double), ("ls_batch", C.c_int32),
                 ("use_graphs", C.c_int32), ("debug_flags", C.c_int32), ("coarse_mode", C.c_int32),
-                ("coarse_max_iter", C.c_int32), ("coarse_tol", C.c_double), ("integrator", C.c_int32),
-                ("pad_", C.c_int32)]
+                ("coarse_max_iter", C.c_int32), ("coarse_tol", C.c_double), ("use_cubature", C.c_int32),
+                ("lag_hessian", C.c_int32), ("integrator", C.c_int32), ("pad_", C.c_int32)]
 
 
 class NewtonStats(C.Structure):
@@ -91,6 +91,7 @@ def _load():
                               C.POINTER(C.c_void_p), C.POINTER(BasisInfo)], C.c_int32),
         "ms_basis_copy": ([P, D, I64, I32, D, D, D, I32, I32], C.c_int32),
         "ms_basis_free": ([P], None),
+        "ms_cubature_upload": ([P, C.c_int64, I32, D], C.c_int32),
         "ms_set_state": ([P, D, D], C.c_int32),
         "ms_get_state": ([P, D, D], C.c_int32),
         "ms_set_step_state": ([P, D, D, D], C.c_int32),
@@ -248,6 +249,11 @@ class Context:
                                       _d(out["phi"]), _d(out["phi_affine"]), _d(out["affine_origin"]),
                                       _i32(out["cluster"]), _i32(out["centroid_vertex"])))
         return {k: getattr(info, k) for k, _ in BasisInfo._fields_ if k != "pad_"}, out
+
+    def cubature_upload(self, elements, weights):
+        e = np.ascontiguousarray(elements, dtype=np.int32)
+        w = _f64(weights)
+        self._chk(lib.ms_cubature_upload(self.h, len(e), _i32(e), _d(w)))
 
     # ---------------------------------------------------------------- state
     def set_state(self, x=None, v=None):
@@ -491,8 +497,10 @@ class Hub:
             pass
 
 
-def context_from_scene(scene, basis, device=0, stream=None, rank=0, world=1, nccl_id=None, hub=None, **params):
-    """Create a context and upload a precompute.mesh.Scene + precompute.basis.Basis."""
+def context_from_scene(scene, basis, device=0, stream=None, rank=0, world=1, nccl_id=None, hub=None, cubature=None,
+                       **params):
+    """Create a context and upload a precompute.mesh.Scene + precompute.basis.Basis (+ optionally a
+    precompute.cubature.Cubature for use_cubature)."""
     ctx = Context(device, stream, rank=rank, world=world, nccl_id=nccl_id, hub=hub)
     ctx.upload_mesh(scene.X, scene.tets, scene.E, scene.nu, scene.rho)
     if len(scene.dbc):
@@ -505,4 +513,6 @@ def context_from_scene(scene, basis, device=0, stream=None, rank=0, world=1, ncc
     ctx.set_params(**kw)
     ctx.basis_upload(basis.m, basis.origins, basis.vptr, basis.handle, basis.phi, basis.phi_affine,
                      basis.affine_origin, basis.n_cg)
+    if cubature is not None:
+        ctx.cubature_upload(cubature.elements, cubature.weights)
     return ctx
