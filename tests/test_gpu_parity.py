@@ -280,6 +280,31 @@ def test_infeasible_state_rejected(msim):
     with pytest.raises(msim.MsimError) as e:
         ctx.timestep()
     assert e.value.code == -7
+    # the failed step is abandoned cleanly: x is back at x^t, no step is in progress, and the
+    # context runs again from a feasible state
+    xr, _ = ctx.get_state()
+    assert np.array_equal(xr, x)
+    with pytest.raises(msim.MsimError) as e:
+        ctx.end_step()
+    assert e.value.code == -8
+    ctx.set_state(s.X, np.zeros_like(s.X))
+    assert ctx.timestep().newton_iters >= 1
+
+
+def test_dirichlet_after_basis_rejected(msim):
+    """The basis is built for one Dirichlet set: changing it afterwards is a state error, and a
+    basis that does not vanish at a Dirichlet vertex is rejected at upload."""
+    s, b = scene_and_basis("c1")
+    ctx = msim.context_from_scene(s, b)
+    with pytest.raises(msim.MsimError) as e:
+        ctx.set_dirichlet(s.dbc)
+    assert e.value.code == -8
+    ctx2 = msim.Context(0)
+    ctx2.upload_mesh(s.X, s.tets, s.E, s.nu, s.rho)
+    ctx2.set_dirichlet(np.arange(20))          # more vertices than the basis was built for
+    with pytest.raises(msim.MsimError) as e:
+        ctx2.basis_upload(b.m, b.origins, b.vptr, b.handle, b.phi, b.phi_affine, b.affine_origin, b.n_cg)
+    assert e.value.code == -1
 
 
 def test_invalid_mesh_rejected(msim):
