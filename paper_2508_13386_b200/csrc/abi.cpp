@@ -201,6 +201,8 @@ static ms_status newton_step(Ctx &c, ms_newton_stats *st) {
 
 static void begin_step(Ctx &c) {
   require_mesh(c);
+  // error flags (pivot <= 0, infeasibility) describe one iteration: clear what an abandoned step left
+  MS_CUDA(cudaMemsetAsync(c.flags, 0, sizeof(int32_t) * c.flags.n, c.stream));
   launch_predictor(c);
   c.step_begun = true;
   c.step_iter = 0;
@@ -743,6 +745,7 @@ ms_status ms_set_step_state(ms_ctx *ctx, const double *x_t, const double *xhat, 
     upload_global(c, c.xt, x_t);
     upload_global(c, c.xhat, xhat);
     upload_global(c, c.x, x);
+    MS_CUDA(cudaMemsetAsync(c.flags, 0, sizeof(int32_t) * c.flags.n, c.stream));
     c.step_begun = true;
     c.assembled = false;
   });
