@@ -104,7 +104,7 @@ def load_traffic():
     return json.load(open(p)) if os.path.exists(p) else {}
 
 
-def phase_rooflines(phases, ab, ci, n_cg, hbm, peak_src, fp64_peak, fp64_src, traffic):
+def phase_rooflines(phases, ab, ci, n_cg, hbm, peak_src, fp64_peak, fp64_src, traffic, jacobi=True):
     """Roofline of every phase with a defined algorithmic work unit: HBM bytes
     for the PCG iteration and the assembly, FP64 flops for the coarse factorisation and the
     Galerkin projection.  achieved = work per launch / measured average launch time."""
@@ -121,7 +121,7 @@ def phase_rooflines(phases, ab, ci, n_cg, hbm, peak_src, fp64_peak, fp64_src, tr
 
     newton = max(phases["pcg"][1], 1)
     ms, n = phases["pcg"]
-    if n:
+    if n and jacobi:   # (the two-level iteration adds restrict / triangular sweeps / lift: no HBM unit)
         put("pcg", "hbm", ab["pcg_iter"], "GB/s", hbm, peak_src, "k_pcg_spmv+k_pcg_update",
             ms / (n * n_cg), n_cg, newton)
     ms, n = phases["assembly"]
@@ -247,7 +247,7 @@ def run_ours(args):
     coarse_mode = 1 if args.coarse == "pcg" else 0
     integrator = 1 if args.integrator == "bdf2" else 0
     extra = dict(coarse_mode=coarse_mode, integrator=integrator, use_cubature=int(args.cubature),
-                 lag_hessian=int(args.lag))
+                 lag_hessian=int(args.lag), refine_mode=1 if args.refine == "two_level" else 0)
     if args.cubature:
         from precompute.cubature import cached_cubature
         extra["cubature"] = cached_cubature(s, b)
@@ -291,8 +291,11 @@ def run_ours(args):
     # ---- second pass (not part of `value`): per-phase CUDA events for the breakdown/rooflines
     ctx.set_profiling(True)
     prof_newton = 0
+    prof_pcg = 0
     for _ in range(min(args.steps, 10)):
-        prof_newton += ctx.timestep().newton_iters
+        st = ctx.timestep()
+        prof_newton += st.newton_iters
+        prof_pcg += st.pcg_iters
     phases = ctx.phase_times()
     ctx.set_profiling(False)
     ms_t = torch.tensor([ms], device="cuda")
@@ -347,7 +350,8 @@ def run_ours(args):
         ci = ctx.coarse_info()
         fp64_peak, fp64_src = load_fp64_peak()
         traffic = load_traffic()
-        rl_phases = phase_rooflines(phases, ab, ci, b.n_cg, hbm, peak_src, fp64_peak, fp64_src, traffic)
+        rl_phases = phase_rooflines(phases, ab, ci, b.n_cg, hbm, peak_src, fp64_peak, fp64_src, traffic,
+                                    jacobi=args.refine == "jacobi")
         dominant = max(rl_phases, key=lambda k: rl_phases[k]["ms_per_newton"] if rl_phases[k]["ms_per_newton"] else 0)
         line = {
             "metric": METRIC, "value": newton_all / (ms_max * 1e-3), "unit": "Newton steps/s",
@@ -356,9 +360,10 @@ def run_ours(args):
             "scaling": "strong" if partitioned else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": dict(config_dict(s, b, world, partitioned), coarse=args.coarse, integrator=args.integrator,
-                           cubature=bool(args.cubature), lag_hessian=bool(args.lag)),
+                           cubature=bool(args.cubature), lag_hessian=bool(args.lag), refine=args.refine),
             "pcg_iters_per_s": pcg_all / (ms_max * 1e-3),
             "newton_iters": int(newton_all),
+            "pcg_iters_per_newton": pcg_all / max(newton_all, 1),
             "coarse_pcg_iters_per_newton": coarse_it / max(newton, 1) if args.coarse == "pcg" else None,
             "roofline": dict(rl_phases[dominant], phase=dominant),
             "roofline_phases": rl_phases,
@@ -399,6 +404,9 @@ def main():
     ap.add_argument("--lag", action="store_true", help="NEXT-2: lagged elastic Hessian for the refinement PCG")
     ap.add_argument("--integrator", default="ie", choices=["ie", "bdf2"],
                     help="time integrator: implicit Euler (default, the configs' own) or BDF2 (P:185-189)")
+    ap.add_argument("--refine", default="jacobi", choices=["jacobi", "two_level"],
+                    help="refinement PCG: N_cg Jacobi iterations (default, the paper's) or NEXT-4's two-level "
+                         "PCG (Jacobi + SMS coarse correction every iteration) to 1e-4 ||g||")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: N independent copies of the problem instead of one slab-partitioned problem")
     args = ap.parse_args()

@@ -78,9 +78,18 @@ typedef struct ms_params {
                              alpha h^2 g, v^{t+1} = (4v^t - v^{t-1})/3 + (2h/3) a^{t+1} with
                              a^{t+1} = 9/(4h^2)(x^{t+1} - xtilde), reading C2; a step without
                              history -- the first after ms_set_state -- is implicit Euler)   */
-  int32_t pad_;
+  int32_t refine_mode;    /* full-space refinement d_f (Alg. 1): MS_REFINE_JACOBI
+                             (default, reading R5: exactly n_cg Jacobi-PCG iterations) or
+                             MS_REFINE_TWO_LEVEL (NEXT-4, not in the paper; reading C5): PCG with
+                             y = D^-1 r, z = y + U_s S^-1 U_s^T (r - H y) (the factorised SMS
+                             matrix of the Newton iteration) until ||r_k||_2 <= refine_tol ||g||_2 or
+                             refine_max_iter iterations; needs MS_COARSE_EXACT                */
+  int32_t refine_max_iter;/* MS_REFINE_TWO_LEVEL: iteration cap (default 100)                */
+  double refine_tol;      /* MS_REFINE_TWO_LEVEL: relative residual (default 1e-2, an inexact-
+                             Newton forcing term; 1e-4 needs ~100 iterations at C4)           */
 } ms_params;
 enum { MS_INTEGRATOR_IE = 0, MS_INTEGRATOR_BDF2 = 1 };
+enum { MS_REFINE_JACOBI = 0, MS_REFINE_TWO_LEVEL = 1 };
 enum { MS_COARSE_EXACT = 0, MS_COARSE_PCG = 1 };
 enum { MS_DEBUG_HESS_FALLBACK = 1 };
 
@@ -94,7 +103,8 @@ typedef struct ms_newton_stats {
   int32_t ls_evals;       /* number of candidate steps evaluated                           */
   int32_t converged;      /* termination test passed after this iteration                  */
   int32_t ls_failed;      /* 1 if no decrease down to ls_min                               */
-  int32_t n_cg;           /* PCG iterations performed                                      */
+  int32_t n_cg;           /* refinement PCG iterations performed (n_cg; MS_REFINE_TWO_LEVEL:
+                             the iterations to refine_tol)                                    */
   int32_t coarse_iters;   /* MS_COARSE_PCG: SMS-stage PCG iterations (0 in exact mode)     */
   int32_t pad_;
 } ms_newton_stats;

@@ -7,7 +7,8 @@ Passages followed:
   full-space correction, d = d_s + d_f, filtered backtracking line search, termination
   ||d_s|| / (h |V|) < eps.
 * Alg. 2 L427-450 with readings R4 (exact coarse solves), R6 (right-hand side -g).
-* §3.7.2: fixed-count Jacobi-PCG refinement from d_f = 0 (reading R5).
+* §3.7.2: fixed-count Jacobi-PCG refinement from d_f = 0 (reading R5); NEXT-4 option:
+  two-level PCG (Jacobi + SMS coarse correction) to a tolerance (reading C5, not in the paper).
 * L616 and SPEC S:170-184: CCD (ground plane) and inversion filters with safety 0.9,
   backtracking by halving with strict decrease, alpha_min = 1e-8 (reading Q12).
 * R3: one freshly assembled, fully integrated H for every stage (no cubature / lagging).
@@ -47,6 +48,44 @@ def pcg(H, r, n_iter, Dinv=None):
         p = z + (rho_new / rho) * p
         rho = rho_new
     return d
+
+
+def two_level_pcg(H, r, Us, S_chol, tol, ref_norm, max_iter, Dinv=None):
+    """NEXT-4 (not in the paper -- reading C5 of DESIGN.md): PCG on H d = r from d = 0
+    with the two-level preconditioner
+        y = D^-1 v,   z = y + U_s S^-1 U_s^T (v - H y)
+    (the Jacobi smoother of P:484, then the SMS coarse correction of Alg. 2 on the smoothed
+    residual; S = U_s^T H U_s factorised once per Newton iteration; "A-DEF2" of Tang, Nabben, Vuik &
+    Erlangga 2009, which equals the symmetric balancing preconditioner on residuals with
+    U_s^T r = 0 -- what the SMS stage leaves: r1 = -g - H d_s), stopped at the first k with
+    ||r_k||_2 <= tol ref_norm (ref_norm = ||g||_2) or k = max_iter.  Returns (d, iterations)."""
+    r = np.array(r, dtype=np.float64).ravel()
+    if Dinv is None:
+        Dinv = 1.0 / H.diagonal()
+
+    def precond(v):
+        y = Dinv * v
+        return y + Us @ coarse.cho_solve(S_chol, Us.T @ (v - H @ y))
+
+    d = np.zeros_like(r)
+    k = 0
+    if np.linalg.norm(r) <= tol * ref_norm or max_iter <= 0:
+        return d, 0
+    z = precond(r)
+    p = z.copy()
+    rho = r @ z
+    while True:
+        q = H @ p
+        alpha = rho / (p @ q)
+        d = d + alpha * p
+        r = r - alpha * q
+        k += 1
+        if np.linalg.norm(r) <= tol * ref_norm or k >= max_iter:
+            return d, k
+        z = precond(r)
+        rho_new = r @ z
+        p = z + (rho_new / rho) * p
+        rho = rho_new
 
 
 def block_jacobi_pcg(apply_S, b, blocks, tol, max_iter):
@@ -217,14 +256,20 @@ class NewtonInfo:
     d: np.ndarray
     ds: np.ndarray
     df: np.ndarray
+    cg_iters: int = 0
 
 
 class OracleSim:
     """Timestep driver: begin_step / newton_iteration / end_step (Alg. 1)."""
 
     def __init__(self, scene, basis, n_cg=None, coarse_mode="exact", coarse_tol=1e-4, coarse_max_iter=None,
-                 integrator="ie", cubature=None, lag=False):
+                 integrator="ie", cubature=None, lag=False, refine="jacobi", refine_tol=1e-2, refine_max_iter=100):
         self.coarse_mode, self.coarse_tol, self.coarse_max_iter = coarse_mode, coarse_tol, coarse_max_iter
+        # NEXT-4: refinement PCG = fixed-count Jacobi (R5, default) or two-level to tolerance
+        if refine == "two_level" and coarse_mode != "exact":
+            raise ValueError("the two-level refinement needs the factorised coarse matrix (coarse_mode='exact')")
+        self.refine, self.refine_tol, self.refine_max_iter = refine, refine_tol, refine_max_iter
+        self.last_cg_iters = 0
         # NEXT-2 (§3.8, §3.7.2): cubature Hessian for the subspace solves, lagged Hessian for the
         # refinement (refresh policy: hlag_should_update)
         self.cubature, self.lag = cubature, lag
@@ -279,7 +324,11 @@ class OracleSim:
         ds, da, Sa, S = subspace_direction(H, g, self.Ua, self.Us, self.coarse_mode, self.coarse_tol,
                                            self.coarse_max_iter)
         r = -g.ravel() - H @ ds
-        df = pcg(H_ref, r, self.n_cg)
+        if self.refine == "two_level":
+            df, self.last_cg_iters = two_level_pcg(H_ref, r, self.Us, coarse.cholesky(S), self.refine_tol,
+                                                   float(np.linalg.norm(g)), self.refine_max_iter)
+        else:
+            df, self.last_cg_iters = pcg(H_ref, r, self.n_cg), self.n_cg
         return g, H, ds, df, ds + df
 
     def newton_iteration(self):
@@ -306,7 +355,7 @@ class OracleSim:
         ds_norm = float(np.linalg.norm(ds))
         conv = ds_norm / (m.h * m.n) < self.eps
         return NewtonInfo(alpha, a0, evals, ds_norm, conv, failed,
-                          ip.energy(m, self.x, self.xhat), d, ds, df)
+                          ip.energy(m, self.x, self.xhat), d, ds, df, self.last_cg_iters)
 
     def end_step(self):
         h = self.model.h

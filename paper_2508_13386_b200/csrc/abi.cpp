@@ -130,8 +130,13 @@ static ms_status newton_step(Ctx &c, ms_newton_stats *st) {
   enqueue_assembly(c);
   enqueue_coarse(c);
   phase_begin(c, MS_PHASE_PCG);
-  const int ncg = n_cg_of(c);
-  launch_pcg(c, c.r, c.df, ncg);
+  int ncg;
+  if (c.params.refine_mode == MS_REFINE_TWO_LEVEL) {
+    ncg = launch_refine_two_level(c, c.r, c.df);   // NEXT-4: to refine_tol (host-checked batches)
+  } else {
+    ncg = n_cg_of(c);
+    launch_pcg(c, c.r, c.df, ncg);
+  }
   phase_end(c);
   phase_begin(c, MS_PHASE_LINESEARCH);
   MS_CUDA(cudaMemcpyAsync(c.d, c.ds, sizeof(double) * n3, cudaMemcpyDeviceToDevice, c.stream));
@@ -287,7 +292,9 @@ void ms_default_params(ms_params *p) {
   p->integrator = MS_INTEGRATOR_IE;
   p->use_cubature = 0;
   p->lag_hessian = 0;
-  p->pad_ = 0;
+  p->refine_mode = MS_REFINE_JACOBI;
+  p->refine_max_iter = 100;
+  p->refine_tol = 1e-2;
 }
 
 static ms_status create_common(ms_ctx **out, int device, void *cuda_stream, int rank, int world,
@@ -503,12 +510,18 @@ ms_status ms_set_params(ms_ctx *ctx, const ms_params *p) {
     MS_REQUIRE(p->coarse_mode == MS_COARSE_EXACT || p->coarse_mode == MS_COARSE_PCG, MS_ERR_ARG, "bad coarse_mode");
     MS_REQUIRE(p->coarse_tol >= 0.0 && p->coarse_max_iter > 0, MS_ERR_ARG, "bad coarse PCG params");
     MS_REQUIRE(p->integrator == MS_INTEGRATOR_IE || p->integrator == MS_INTEGRATOR_BDF2, MS_ERR_ARG, "bad integrator");
+    MS_REQUIRE(p->refine_mode == MS_REFINE_JACOBI || p->refine_mode == MS_REFINE_TWO_LEVEL, MS_ERR_ARG,
+               "bad refine_mode");
+    MS_REQUIRE(p->refine_mode == MS_REFINE_JACOBI || p->coarse_mode == MS_COARSE_EXACT, MS_ERR_ARG,
+               "the two-level refinement needs the factorised coarse matrix (MS_COARSE_EXACT)");
+    MS_REQUIRE(p->refine_tol >= 0.0 && p->refine_max_iter >= 0, MS_ERR_ARG, "bad refinement PCG params");
     if (p->integrator != ctx->c.params.integrator) ctx->c.has_history = false;
     if (p->lag_hessian != ctx->c.params.lag_hessian || p->use_cubature != ctx->c.params.use_cubature)
       ctx->c.lag_valid = false;
     if (p->n_cg != ctx->c.params.n_cg || p->use_graphs != ctx->c.params.use_graphs ||
         p->coarse_mode != ctx->c.params.coarse_mode || p->coarse_tol != ctx->c.params.coarse_tol ||
-        p->coarse_max_iter != ctx->c.params.coarse_max_iter) {
+        p->coarse_max_iter != ctx->c.params.coarse_max_iter || p->refine_mode != ctx->c.params.refine_mode ||
+        p->refine_tol != ctx->c.params.refine_tol || p->refine_max_iter != ctx->c.params.refine_max_iter) {
       pcg_reset_graph(ctx->c);
       coarse_reset_graphs(ctx->c);
     }

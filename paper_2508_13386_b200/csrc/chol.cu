@@ -416,12 +416,25 @@ __global__ void k_pad_identity2(int nS, int nSp, double *__restrict__ L) {
 
 // z_perm[12 perm[i] + r] = z[12 i + r]  (dir = 0);  z[12 i + r] = z_perm[12 perm[i] + r]  (dir = 1)
 __global__ void k_permute2(int m, const int32_t *__restrict__ perm, const double *__restrict__ src,
-                           double *__restrict__ dst, int dir) {
+                           double *__restrict__ dst, int dir, const int32_t *__restrict__ skip) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= 12 * m) return;
+  if (t >= 12 * m || (skip && *skip)) return;
   const int i = t / 12, r = t % 12;
   if (dir == 0) dst[12 * perm[i] + r] = src[t];
   else dst[t] = src[12 * perm[i] + r];
+}
+
+// solve set-up: b = permuted z (padding rows 0), y and x filled with the "not ready" pattern
+__global__ void k_solve_prep(int m, int nSp, const int32_t *__restrict__ perm, const double *__restrict__ z,
+                             double *__restrict__ b, double *__restrict__ y, double *__restrict__ x,
+                             const int32_t *__restrict__ skip) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nSp || (skip && *skip)) return;
+  const double nr = __longlong_as_double(-1ll);
+  y[t] = nr;
+  x[t] = nr;
+  if (t < 12 * m) b[12 * perm[t / 12] + t % 12] = z[t];
+  else b[t] = 0.0;
 }
 
 // ------------------------------------------------------------------ cooperative solves
@@ -460,7 +473,9 @@ __device__ __forceinline__ double poll_ready(const double *p) {
 __global__ void __launch_bounds__(256) k_chol_fwd(int NT, const int32_t *__restrict__ rows_ptr,
                                                   const int32_t *__restrict__ rows, int nSp,
                                                   const double *__restrict__ L, const double *__restrict__ U,
-                                                  const double *__restrict__ b, double *__restrict__ y) {
+                                                  const double *__restrict__ b, double *__restrict__ y,
+                                                  const int32_t *__restrict__ skip) {
+  if (skip && *skip) return;   // uniform over the grid (two-level PCG after convergence)
   __shared__ double yj[TB];
   __shared__ double part[4][TB];
   const int t = threadIdx.x, r = t & 63, q = t >> 6;
@@ -507,7 +522,9 @@ __global__ void __launch_bounds__(256) k_chol_fwd(int NT, const int32_t *__restr
 __global__ void __launch_bounds__(256) k_chol_bwd(int NT, const int32_t *__restrict__ pan_ptr,
                                                   const int32_t *__restrict__ panel, int nSp,
                                                   const double *__restrict__ L, const double *__restrict__ U,
-                                                  const double *__restrict__ y, double *__restrict__ x) {
+                                                  const double *__restrict__ y, double *__restrict__ x,
+                                                  const int32_t *__restrict__ skip) {
+  if (skip && *skip) return;
   __shared__ double xi[TB];
   __shared__ double part[4][TB];
   __shared__ double red[TB][TB + 1];
@@ -648,32 +665,30 @@ void enqueue_chol_factor(Ctx &c) {
 
 int64_t chol_factor_kernels(const Ctx &c) { return 3 + (c.nS_pad > c.nS ? 1 : 0); }
 
-// solve S q = z in place on c.zs (handle order)
-void enqueue_chol_solve(Ctx &c) {
+// solve S q = z in place on c.zs (handle order); skip (device flag, may be NULL): every launch
+// does nothing while *skip != 0
+void enqueue_chol_solve(Ctx &c, const int32_t *skip) {
   const int nSp = c.nS_pad, NT = c.ntiles;
   double *b = c.qs, *y = c.yp, *xs = c.xsol;
-  MS_CUDA(cudaMemsetAsync(b, 0, sizeof(double) * nSp, c.stream));
-  MS_CUDA(cudaMemsetAsync(y, 0xff, sizeof(double) * nSp, c.stream));    // "not ready" pattern
-  MS_CUDA(cudaMemsetAsync(xs, 0xff, sizeof(double) * nSp, c.stream));
-  k_permute2<<<div_up(12 * c.m, 256), 256, 0, c.stream>>>(c.m, c.perm, c.zs, b, 0);
+  k_solve_prep<<<div_up(nSp, 256), 256, 0, c.stream>>>(c.m, nSp, c.perm, c.zs, b, y, xs, skip);
   const int G = std::min(NT, c.coop_grid);
   {
     int NTv = NT, nSpv = nSp;
-    const int32_t *rp = c.chol_rows_ptr, *rw = c.chol_rows;
+    const int32_t *rp = c.chol_rows_ptr, *rw = c.chol_rows, *sk = skip;
     const double *Lp = c.Lden, *Up = c.Uinv, *bp = b;
     double *yv = y;
-    void *args[] = {&NTv, &rp, &rw, &nSpv, &Lp, &Up, &bp, &yv};
+    void *args[] = {&NTv, &rp, &rw, &nSpv, &Lp, &Up, &bp, &yv, &sk};
     MS_CUDA(cudaLaunchCooperativeKernel((const void *)k_chol_fwd, dim3(G), dim3(256), args, 0, c.stream));
   }
   {
     int NTv = NT, nSpv = nSp;
-    const int32_t *pp = c.chol_panel_ptr, *pw = c.chol_panel;
+    const int32_t *pp = c.chol_panel_ptr, *pw = c.chol_panel, *sk = skip;
     const double *Lp = c.Lden, *Up = c.Uinv, *yp = y;
     double *xv = xs;
-    void *args[] = {&NTv, &pp, &pw, &nSpv, &Lp, &Up, &yp, &xv};
+    void *args[] = {&NTv, &pp, &pw, &nSpv, &Lp, &Up, &yp, &xv, &sk};
     MS_CUDA(cudaLaunchCooperativeKernel((const void *)k_chol_bwd, dim3(G), dim3(256), args, 0, c.stream));
   }
-  k_permute2<<<div_up(12 * c.m, 256), 256, 0, c.stream>>>(c.m, c.perm, xs, c.zs, 1);
+  k_permute2<<<div_up(12 * c.m, 256), 256, 0, c.stream>>>(c.m, c.perm, xs, c.zs, 1, skip);
 }
 
 int64_t chol_solve_kernels(const Ctx &) { return 4; }

@@ -621,7 +621,8 @@ void coarse_reset_graphs(Ctx &c) {
   if (c.factor_graph) cudaGraphExecDestroy(c.factor_graph);
   if (c.solve_graph) cudaGraphExecDestroy(c.solve_graph);
   if (c.cpcg_graph) cudaGraphExecDestroy(c.cpcg_graph);
-  c.factor_graph = c.solve_graph = c.cpcg_graph = nullptr;
+  if (c.tl_graph) cudaGraphExecDestroy(c.tl_graph);
+  c.factor_graph = c.solve_graph = c.cpcg_graph = c.tl_graph = nullptr;
 }
 
 void launch_coarse_factor(Ctx &c) {
@@ -635,7 +636,7 @@ void launch_coarse_factor(Ctx &c) {
 }
 
 void launch_coarse_solve(Ctx &c) {
-  run_captured(c, c.solve_graph, enqueue_chol_solve);
+  run_captured(c, c.solve_graph, [](Ctx &cc) { enqueue_chol_solve(cc); });
   c.launches += chol_solve_kernels(c);
   MS_CUDA(cudaGetLastError());
 }
@@ -665,6 +666,146 @@ void launch_coarse_direction(Ctx &c) {
   // r = -g - H ds
   launch_spmv(c, c.ds, c.r, 0.0, c.rhs, nullptr, c.vals_sub());
   MS_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ NEXT-4: two-level refinement
+// PCG on H d_f = r1 from d_f = 0 with y = D^-1 r, z = y + U_s S^-1 U_s^T (r - H y) (the SMS factor of
+// this Newton iteration: SpMV, restrict, the two cooperative triangular sweeps, lift; "A-DEF2",
+// equal to the balancing preconditioner since U_s^T r1 = 0 after the SMS stage), stopped at the first k with
+// ||r_k||^2 <= tol^2 ||g||^2 or k = refine_max_iter (reading C5; oracle/solver.py two_level_pcg).
+// Host-driven batches of kTlBatch iterations, one CUDA graph; once the device flag tl_state[0] is
+// set every launch of a batch returns at once, so the iterates are exactly those of a loop that
+// stopped at k.  Scalars: rho = SC_RZ, beta = SC_BETA, alpha = SC_ALPHA (k_pcg_spmv's slots).
+constexpr int kTlBatch = 4;
+
+// x += alpha p; r -= alpha q; z = D^-1 r (the Jacobi part of the preconditioner)
+__global__ void __launch_bounds__(256) k_tl_update(int n3, const double *__restrict__ dinv,
+                                                   const double *__restrict__ p, const double *__restrict__ q,
+                                                   double *__restrict__ x, double *__restrict__ r,
+                                                   double *__restrict__ z, const double *__restrict__ scal,
+                                                   const int32_t *__restrict__ skip) {
+  if (*skip) return;
+  const double alpha = scal[SC_ALPHA];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n3; i += gridDim.x * blockDim.x) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, q[i], r[i]);
+    r[i] = ri;
+    z[i] = dinv[i] * ri;
+  }
+}
+
+// [r.z, r.r] over the owned entries -> scal[SC_TL_RZ], scal[SC_TL_RR] (deterministic grid sum)
+__global__ void __launch_bounds__(256) k_tl_dots(int n3_own, const double *__restrict__ r,
+                                                 const double *__restrict__ z, double *__restrict__ partial,
+                                                 unsigned int *counter, double *__restrict__ scal,
+                                                 const int32_t *__restrict__ skip) {
+  if (*skip) return;
+  double acc[2] = {0.0, 0.0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n3_own; i += gridDim.x * blockDim.x) {
+    acc[0] = fma(r[i], z[i], acc[0]);
+    acc[1] = fma(r[i], r[i], acc[1]);
+  }
+  grid_reduce<2>(acc, partial, counter, scal + SC_TL_RZ);
+}
+
+// stopping rule and beta (init: the check of r_0, rho = r_0.z_0, beta = 0)
+__global__ void k_tl_decide(double *__restrict__ scal, int32_t *__restrict__ state, double tol2, int max_iter,
+                            int init) {
+  if (state[0]) return;
+  const double rz = scal[SC_TL_RZ], rr = scal[SC_TL_RR], gg = scal[SC_GNORM2];
+  if (init) {
+    if (rr <= tol2 * gg || max_iter <= 0) {
+      state[0] = 1;
+      state[1] = 0;
+      return;
+    }
+    scal[SC_RZ] = rz;
+    scal[SC_RZ0] = rz;
+    scal[SC_BETA] = 0.0;
+    state[1] = 0;
+    return;
+  }
+  const int it = state[1] + 1;
+  state[1] = it;
+  if (rr <= tol2 * gg || it >= max_iter) {
+    state[0] = 1;
+    return;
+  }
+  const double rho = scal[SC_RZ];
+  scal[SC_BETA] = rho != 0.0 ? rz / rho : 0.0;
+  scal[SC_RZ] = rz;
+}
+
+static int tl_grid(int64_t n) { return (int)std::min<int64_t>(div_up(n, 256), 148 * 8); }
+
+// z = y + U_s S^-1 U_s^T (r - H y) with y = D^-1 r already in z, then r.z, r.r and the decision
+static void enqueue_tl_precond_decide(Ctx &c, int init) {
+  const int32_t *skip = c.tl_state;
+  if (c.dist()) halo_exchange(c, c.z);                 // y at the ghost vertices (SpMV input)
+  launch_spmv(c, c.z, c.tmp, 0.0, c.r, skip, nullptr);  // t = r - H_ref y (owned rows exact)
+  launch_restrict(c, c.tmp, c.zs, skip);
+  dist_sum(c, c.zs, 12 * (int64_t)c.m);
+  enqueue_chol_solve(c, skip);
+  c.launches += chol_solve_kernels(c);
+  launch_lift(c, c.zs, c.z, true, skip);               // replicated coarse vector: ghosts exact too
+  k_tl_dots<<<tl_grid(3 * (int64_t)c.nv_own), 256, 0, c.stream>>>(3 * c.nv_own, c.r, c.z, c.partial,
+                                                                  c.counters + 10, c.scal, skip);
+  dist_sum(c, c.scal + SC_TL_RZ, 2);
+  const double tol2 = c.params.refine_tol * c.params.refine_tol;
+  k_tl_decide<<<1, 1, 0, c.stream>>>(c.scal, c.tl_state, tol2, c.params.refine_max_iter, init);
+  c.launches += 2;
+}
+
+static void enqueue_tl_batch(Ctx &c, double *sol) {
+  const int n3 = 3 * c.nv;
+  for (int k = 0; k < kTlBatch; ++k) {
+    launch_pcg_spmv(c, c.tl_state);   // p = z + beta p, q = H p, alpha
+    k_tl_update<<<tl_grid(n3), 256, 0, c.stream>>>(n3, c.dinv, c.p, c.q, sol, c.r, c.z, c.scal, c.tl_state);
+    c.launches++;
+    enqueue_tl_precond_decide(c, 0);
+  }
+}
+
+int launch_refine_two_level(Ctx &c, const double *rhs, double *sol) {
+  MS_REQUIRE(c.params.coarse_mode == MS_COARSE_EXACT, MS_ERR_STATE, "two-level refinement needs the coarse factor");
+  if (c.tl_state.n == 0) c.tl_state.alloc(2);
+  MS_CUDA(cudaMemsetAsync(c.tl_state, 0, 2 * sizeof(int32_t), c.stream));
+  launch_pcg_init(c, rhs, sol);   // x = 0, r = rhs, z = D^-1 r, p = q = 0
+  enqueue_tl_precond_decide(c, 1);
+  const bool graphs = c.params.use_graphs && sol == c.df.p && (!c.dist() || c.comm->capturable());
+  int32_t *hs = reinterpret_cast<int32_t *>(c.h_pinned + PH_COUNT - 2);
+  for (int batch = 0;; ++batch) {
+    if (graphs) {
+      if (!c.tl_graph) {
+        cudaStream_t cap;
+        MS_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+        cudaStream_t saved = c.stream;
+        c.stream = cap;
+        cudaGraph_t graph;
+        MS_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+        const int64_t l0 = c.launches;
+        enqueue_tl_batch(c, sol);
+        c.tl_graph_kernels = c.launches - l0;
+        c.launches = l0;
+        MS_CUDA(cudaStreamEndCapture(cap, &graph));
+        c.stream = saved;
+        MS_CUDA(cudaGraphInstantiate(&c.tl_graph, graph, 0));
+        cudaGraphDestroy(graph);
+        cudaStreamDestroy(cap);
+      }
+      MS_CUDA(cudaGraphLaunch(c.tl_graph, c.stream));
+      c.launches += c.tl_graph_kernels;
+    } else {
+      enqueue_tl_batch(c, sol);
+    }
+    MS_CUDA(cudaMemcpyAsync(hs, c.tl_state, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+    MS_CUDA(cudaStreamSynchronize(c.stream));
+    if (hs[0]) break;
+    MS_REQUIRE(batch < c.params.refine_max_iter / kTlBatch + 1, MS_ERR_STATE, "two-level PCG did not stop");
+  }
+  MS_CUDA(cudaGetLastError());
+  c.refine_iters_last = hs[1];
+  return hs[1];
 }
 
 // standalone solve used by the parity hook ms_subspace_direction (same code path)

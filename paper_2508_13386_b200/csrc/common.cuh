@@ -231,6 +231,11 @@ struct Ctx {
   cudaGraphExec_t cpcg_graph = nullptr;
   int64_t cpcg_graph_kernels = 0;
   int32_t coarse_iters_last = 0;
+  // ---- refine_mode == MS_REFINE_TWO_LEVEL (coarse.cu): PCG with the two-level preconditioner
+  DBuf<int32_t> tl_state;           // [2]: done flag, iterations
+  cudaGraphExec_t tl_graph = nullptr;
+  int64_t tl_graph_kernels = 0;
+  int32_t refine_iters_last = 0;
   int64_t n_dag_factor = 0;         // factor tasks (the fused Galerkin tasks follow them)
   DBuf<int32_t> chol_rw_ptr, chol_rw;   // per chain task: handles whose R(i) it waits for
   int df_hi_ctas = 64;   // CTAs serving the high-priority queue
@@ -293,6 +298,8 @@ enum {
   SC_CG_AOLD,
   SC_CP_RHO,      // coarse PCG (MS_COARSE_PCG): r.z, ||b||^2
   SC_CP_BN2,
+  SC_TL_RZ,       // two-level refinement PCG (NEXT-4): r.z, r.r (summed together)
+  SC_TL_RR,
   SC_COUNT = 32
 };
 constexpr int SC_SUM0 = SC_ENERGY_ELEM, SC_SUM_N = SC_INFEAS - SC_ENERGY_ELEM + 1;
@@ -331,6 +338,9 @@ void build_cubature_structures(Ctx &c, const std::vector<int32_t> &loc_elems, co
 void launch_spmv(Ctx &c, const double *xin, double *yout, double alpha_minus_b, const double *b,
                  const int32_t *skip = nullptr, const double *vals = nullptr);
 void launch_pcg(Ctx &c, const double *rhs, double *sol, int iters);
+int launch_refine_two_level(Ctx &c, const double *rhs, double *sol);   // NEXT-4; returns iterations
+void launch_pcg_spmv(Ctx &c, const int32_t *skip);
+void launch_pcg_init(Ctx &c, const double *rhs, double *sol);   // x = 0, r = rhs, z = D^-1 r, p = q = 0   // one fused p / q update + p.q -> alpha
 void pcg_reset_graph(Ctx &c);
 void launch_coarse_S(Ctx &c, bool full_S = false);
 // multi-GPU helpers (abi.cpp): no-ops when world == 1
@@ -342,7 +352,7 @@ void launch_coarse_direction(Ctx &c);
 void launch_coarse_solve(Ctx &c);
 void launch_basis_W(Ctx &c);
 void enqueue_chol_factor(Ctx &c);
-void enqueue_chol_solve(Ctx &c);
+void enqueue_chol_solve(Ctx &c, const int32_t *skip = nullptr);
 int64_t chol_factor_kernels(const Ctx &c);
 int64_t chol_solve_kernels(const Ctx &c);
 void chol_init_attrs(Ctx &c);

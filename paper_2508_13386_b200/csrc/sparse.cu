@@ -361,7 +361,8 @@ __global__ void __launch_bounds__(256) k_pcg_init(int n3, int n3_own, int dist, 
 __global__ void __launch_bounds__(256) k_pcg_spmv(SellView H, int nv_own, int dist, const double *__restrict__ z,
                                                   double *__restrict__ p, double *__restrict__ q,
                                                   double *__restrict__ partial, unsigned int *counter,
-                                                  double *__restrict__ scal) {
+                                                  double *__restrict__ scal, const int32_t *__restrict__ skip) {
+  if (skip && *skip) return;   // uniform over the grid: no block reaches the grid reduction
   const double beta = scal[SC_BETA];
   double acc[1] = {0.0};
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
@@ -531,7 +532,7 @@ static void enqueue_pcg_iters(Ctx &c, double *sol, int iters) {
   }
   for (int it = 0; it < iters; ++it) {
     k_pcg_spmv<<<div_up(c.nv, bs), bs, 0, c.stream>>>(sell_view(c), c.nv_own, dist, c.z, c.p, c.q, c.partial,
-                                                      c.counters + 3, c.scal);
+                                                      c.counters + 3, c.scal, nullptr);
     if (dist) {
       dist_sum(c, c.scal + SC_PQ, 1);
       k_pcg_scalars<<<1, 1, 0, c.stream>>>(c.scal, 0);
@@ -544,6 +545,26 @@ static void enqueue_pcg_iters(Ctx &c, double *sol, int iters) {
       halo_exchange(c, c.z);
       c.launches += 2;
     }
+  }
+}
+
+void launch_pcg_init(Ctx &c, const double *rhs, double *sol) {
+  const int n3 = 3 * c.nv;
+  k_pcg_init<<<grid_vec(n3), 256, 0, c.stream>>>(n3, 3 * c.nv_own, c.dist() ? 1 : 0, rhs, c.dinv, sol, c.r, c.z, c.p,
+                                                 c.q, c.partial, c.counters + 2, c.scal);
+  c.launches++;
+}
+
+// p = z + beta p; q = H z + beta q; alpha = rho / p.q (rank-summed p.q on several GPUs)
+void launch_pcg_spmv(Ctx &c, const int32_t *skip) {
+  const int dist = c.dist() ? 1 : 0;
+  k_pcg_spmv<<<div_up(c.nv, 256), 256, 0, c.stream>>>(sell_view(c), c.nv_own, dist, c.z, c.p, c.q, c.partial,
+                                                      c.counters + 3, c.scal, skip);
+  c.launches++;
+  if (dist) {
+    dist_sum(c, c.scal + SC_PQ, 1);
+    k_pcg_scalars<<<1, 1, 0, c.stream>>>(c.scal, 0);
+    c.launches++;
   }
 }
 

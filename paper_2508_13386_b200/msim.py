@@ -30,7 +30,8 @@ class Params(C.Structure):
                 ("ls_min", C.c_double), ("filter_safety", C.c_double), ("ls_batch", C.c_int32),
                 ("use_graphs", C.c_int32), ("debug_flags", C.c_int32), ("coarse_mode", C.c_int32),
                 ("coarse_max_iter", C.c_int32), ("coarse_tol", C.c_double), ("use_cubature", C.c_int32),
-                ("lag_hessian", C.c_int32), ("integrator", C.c_int32), ("pad_", C.c_int32)]
+                ("lag_hessian", C.c_int32), ("integrator", C.c_int32), ("refine_mode", C.c_int32),
+                ("refine_max_iter", C.c_int32), ("refine_tol", C.c_double)]
 
 
 class NewtonStats(C.Structure):

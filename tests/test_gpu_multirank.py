@@ -25,11 +25,11 @@ def msim():
     return m
 
 
-def run_ranks(msim, s, b, world, steps):
+def run_ranks(msim, s, b, world, steps, **params):
     import torch
     hub = msim.Hub(world)
     streams = [torch.cuda.Stream() for _ in range(world)]
-    ctxs = [msim.context_from_scene(s, b, stream=streams[r].cuda_stream, rank=r, world=world, hub=hub)
+    ctxs = [msim.context_from_scene(s, b, stream=streams[r].cuda_stream, rank=r, world=world, hub=hub, **params)
             for r in range(world)]
     stats = [[] for _ in range(world)]
     errors = []
@@ -77,3 +77,17 @@ def test_partitioned_timesteps_match_single(msim, name, world, steps):
     assert its_p == its
     assert np.abs(x - x_ref).max() <= 1e-9 * diag
     assert np.abs(v - v_ref).max() <= 1e-9 * diag / s.h
+
+
+def test_partitioned_two_level_refinement_matches_single(msim):
+    """NEXT-4 two-level refinement on 2 ranks: restrict sums across ranks, the replicated factor
+    solves, the lift and the z halo give the single-context iterates (same PCG counts)."""
+    s = scene_small_drop(n=(10, 4, 3), m=6, drop=0.002)
+    b = build_basis(s, workers=1)
+    ref = msim.context_from_scene(s, b, refine_mode=1)
+    its = [ref.timestep().newton_iters for _ in range(4)]
+    x_ref, _ = ref.get_state()
+    x, _, its_p = run_ranks(msim, s, b, 2, 4, refine_mode=1)
+    diag = np.linalg.norm(s.X.max(0) - s.X.min(0))
+    assert its_p == its
+    assert np.abs(x - x_ref).max() <= 1e-9 * diag

@@ -122,6 +122,73 @@ def test_pcg_fixed_count_krylov_optimality():
         assert np.linalg.norm(d - ref) < 1e-9 * np.linalg.norm(ref), k
 
 
+def _two_level_problem(n=36, nc=6, seed=16):
+    """SPD H, a sparse coarse basis U and a right-hand side with U^T b = 0 (the refinement's
+    residual after the SMS stage is Galerkin-orthogonal to the coarse space)."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(seed)
+    A = rng.standard_normal((n, n))
+    Hd = A @ A.T + np.diag(rng.uniform(1.0, 100.0, n))
+    U = rng.standard_normal((n, nc))
+    U[rng.uniform(size=(n, nc)) < 0.5] = 0.0
+    b = rng.standard_normal(n)
+    b -= U @ np.linalg.solve(U.T @ U, U.T @ b)
+    return Hd, sp.csr_matrix(Hd), sp.csr_matrix(U), U, b
+
+
+def test_two_level_pcg_krylov_optimality():
+    """NEXT-4: on U^T b = 0 the two-level PCG iterate after k steps minimises the H-norm error over
+    K_k(P H, P b) with the symmetric balancing preconditioner
+    P = Q + (I - Q H) D^-1 (I - H Q), Q = U (U^T H U)^-1 U^T, formed densely with an explicit
+    inverse -- a Galerkin solve on that space, independent of the recurrence and of the oracle's
+    triangular solves.  Dropping the coarse term, using S instead of S^-1 or correcting v instead
+    of v - H D^-1 v changes the space."""
+    Hd, H, Us, U, b = _two_level_problem()
+    n = len(b)
+    Q = U @ np.linalg.inv(U.T @ Hd @ U) @ U.T
+    Dm = np.diag(1.0 / np.diag(Hd))
+    P = Q + (np.eye(n) - Q @ Hd) @ Dm @ (np.eye(n) - Hd @ Q)
+    L = coarse.cholesky(coarse.galerkin(Us, H))
+    for k in (1, 2, 3, 5):
+        K = [P @ b]
+        for _ in range(k - 1):
+            K.append(P @ (Hd @ K[-1]))
+        V, _ = np.linalg.qr(np.array(K).T)
+        ref = V @ np.linalg.solve(V.T @ Hd @ V, V.T @ b)
+        d, it = solver.two_level_pcg(H, b, Us, L, 0.0, 1.0, k)
+        assert it == k
+        assert np.linalg.norm(d - ref) < 1e-9 * np.linalg.norm(ref), k
+
+
+def test_two_level_pcg_stopping_rule_and_limits():
+    """Stops at the FIRST k with ||b - H d_k|| <= tol ref (checked against the iterates of the
+    fixed-count runs); tol 1 with ref = ||b|| stops at 0 iterations; at a tight tolerance the
+    iterate is the LAPACK solution."""
+    Hd, H, Us, U, b = _two_level_problem()
+    L = coarse.cholesky(coarse.galerkin(Us, H))
+    ref_norm = np.linalg.norm(b)
+    tol = 1e-6
+    d, it = solver.two_level_pcg(H, b, Us, L, tol, ref_norm, 500)
+    assert np.linalg.norm(b - Hd @ d) <= tol * ref_norm
+    d_prev, it_prev = solver.two_level_pcg(H, b, Us, L, 0.0, 1.0, it - 1)
+    assert it_prev == it - 1 and np.linalg.norm(b - Hd @ d_prev) > tol * ref_norm
+    assert solver.two_level_pcg(H, b, Us, L, 1.0, ref_norm, 500)[1] == 0
+    d, _ = solver.two_level_pcg(H, b, Us, L, 1e-14, ref_norm, 500)
+    ref = sla.solve(Hd, b, assume_a="pos")
+    assert np.linalg.norm(d - ref) < 1e-10 * np.linalg.norm(ref)
+
+
+def test_two_level_pcg_empty_coarse_space_is_jacobi():
+    """With no coarse columns the preconditioner reduces to Jacobi: the iterates are those of the
+    (pinned) fixed-count Jacobi-PCG."""
+    import scipy.sparse as sp
+    Hd, H, _, _, b = _two_level_problem()
+    U0 = sp.csr_matrix((len(b), 0))
+    for k in (1, 4):
+        d, _ = solver.two_level_pcg(H, b, U0, np.zeros((0, 0)), 0.0, 1.0, k)
+        assert np.linalg.norm(d - solver.pcg(H, b, k)) < 1e-12 * np.linalg.norm(d)
+
+
 def test_pcg_converges_to_lapack_on_c1(c1_scene):
     m, x, xhat = perturbed_c1(c1_scene)
     H = ip.hessian(m, x, xhat).tocsr()
