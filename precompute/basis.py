@@ -337,7 +337,10 @@ def hop_radius(assign, tets, cv, n_v, m):
     return float(np.mean(radii))
 
 
-def build_basis(scene, m=None, seed=None, workers=None, verbose=False) -> Basis:
+def build_basis(scene, m=None, seed=None, workers=None, verbose=False, partition="euclidean") -> Basis:
+    """partition: "euclidean" (step 1 below; the default of every config) or "heat" (NEXT-3: the
+    paper's stiffness-weighted heat-geodesic k-means with jump penalty and pruning,
+    precompute/partition.py; m is then the initial cluster count)."""
     import time
     t0 = time.time()
     X, tets = scene.X, scene.tets.astype(np.int64)
@@ -347,8 +350,14 @@ def build_basis(scene, m=None, seed=None, workers=None, verbose=False) -> Basis:
 
     vol = tet_volumes(X, tets)
     bary = tet_barycentres(X, tets)
-    C0 = kmeans_pp(bary, vol, m, seed)
-    assign = lloyd(bary, vol, C0)
+    if partition == "heat":
+        from .partition import geodesic_kmeans
+        assign, _ = geodesic_kmeans(scene, m, seed)
+    elif partition == "euclidean":
+        C0 = kmeans_pp(bary, vol, m, seed)
+        assign = lloyd(bary, vol, C0)
+    else:
+        raise ValueError(f"unknown partition {partition!r}")
     adj = face_adjacency(tets)
     assign = enforce_connectivity(assign.copy(), tets, adj, m)
     # drop empty clusters (cannot happen after kmeans++ in practice)
@@ -463,15 +472,17 @@ def build_basis(scene, m=None, seed=None, workers=None, verbose=False) -> Basis:
                  cluster=assign.astype(np.int32), centroid_vertex=cv)
 
 
-def cached_basis_path(scene, cache_dir=None):
+def cached_basis_path(scene, cache_dir=None, partition="euclidean"):
     cache_dir = cache_dir or os.environ.get("MSIM_CACHE", os.path.join(os.path.dirname(__file__), "..", ".cache"))
-    key = f"{scene.name}_{scene.n_verts}_{scene.n_tets}_{scene.m}_{BASIS_VERSION}.npz"
+    tag = "" if partition == "euclidean" else f"_{partition}"
+    key = f"{scene.name}_{scene.n_verts}_{scene.n_tets}_{scene.m}_{BASIS_VERSION}{tag}.npz"
     return os.path.join(cache_dir, key)
 
 
 def cached_basis(scene, cache_dir=None, **kw) -> Basis:
-    """Build or load the basis of a scene (cache keyed by scene name, sizes, m and version)."""
-    path = cached_basis_path(scene, cache_dir)
+    """Build or load the basis of a scene (cache keyed by scene name, sizes, m, version and
+    partitioner)."""
+    path = cached_basis_path(scene, cache_dir, kw.get("partition", "euclidean"))
     os.makedirs(os.path.dirname(path), exist_ok=True)
     if os.path.exists(path):
         return Basis.load(path)
