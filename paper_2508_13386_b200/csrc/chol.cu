@@ -25,7 +25,11 @@
 namespace msim {
 
 constexpr int TB = 64;
-constexpr int LD = TB + 1;
+// shared-memory row strides (doubles) of the diagonal-tile layout and of the k-major staged
+// tiles: 68 = 4 (mod 16), so the 8 x 4 fragments of mma.sync m8n8k4 (lanes: 8 rows x 4 k) hit 16
+// distinct bank pairs per half-warp -- conflict-free (stride 65 / 64: 4-way)
+constexpr int LD = TB + 4;
+constexpr int SLD = TB + 4;
 
 __device__ __forceinline__ size_t tile_off(int ti, int tj, int nSp) {
   return (size_t)(tj * TB) * nSp + (size_t)ti * TB;
@@ -34,7 +38,7 @@ __device__ __forceinline__ size_t tile_off(int ti, int tj, int nSp) {
 #include "chol_diag.cuh"
 
 // ------------------------------------------------------------------ tile GEMM of the dataflow kernel
-// acc = S1^T S2 over the 64-long k dimension (S1[kk*64 + r], S2[kk*64 + c]); thread-owned elements
+// acc = S1^T S2 over the 64-long k dimension (S1[kk*SLD + r], S2[kk*SLD + c]); thread-owned elements
 // idx = 0..15 at (r, c) = tile_rc(idx), on the FP64 tensor cores (mma.sync m8n8k4): warp w owns
 // rows 16 (w & 3) .. +15 and columns 32 (w >> 2) .. +31 as 2 x 4 blocks of 8 x 8.
 
@@ -46,7 +50,7 @@ __device__ __forceinline__ void tile_rc(int idx, int &r, int &c) {
 }
 
 // LI: the second operand is a row-major inverse diagonal tile Li [64][LD] left in shared memory
-// by diag_factor (S2[kk*64 + c] = U[kk][c] = Li[c][kk]) instead of a staged k-major tile
+// by diag_factor (S2[kk*SLD + c] = U[kk][c] = Li[c][kk]) instead of a staged k-major tile
 template <bool LI = false>
 __device__ __forceinline__ void tile_gemm(const double *S1, const double *S2, double (&acc)[16]) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -55,7 +59,7 @@ __device__ __forceinline__ void tile_gemm(const double *S1, const double *S2, do
   for (int q = 0; q < 16; ++q) acc[q] = 0.0;
 #pragma unroll 4
   for (int k0 = 0; k0 < TB; k0 += 4) {
-    const double *s1 = S1 + (k0 + kl) * TB, *s2 = S2 + (k0 + kl) * TB;
+    const double *s1 = S1 + (k0 + kl) * SLD, *s2 = S2 + (k0 + kl) * SLD;
     const double a0 = s1[r0], a1 = s1[r0 + 8];
     double b[4];
 #pragma unroll
@@ -70,7 +74,7 @@ __device__ __forceinline__ void tile_gemm(const double *S1, const double *S2, do
   }
 }
 
-// stage a column-major global tile (leading dim nSp) into k-major smem S[kk*64 + r] (cp.async)
+// stage a column-major global tile (leading dim nSp) into k-major smem S[kk*SLD + r] (cp.async)
 // cp.async.cg: 16-byte global -> shared copy through L2 only (L1 is not coherent across SMs, and
 // the dataflow kernel reads tiles other CTAs wrote during the same launch)
 __device__ __forceinline__ void cp_async_cg16(void *smem, const void *gmem) {
@@ -86,7 +90,7 @@ __device__ __forceinline__ void stage_colmajor(double *S, const double *__restri
 #pragma unroll
   for (int it = 0; it < (TB * TB / 2) / 256; ++it) {
     const int e2 = threadIdx.x + it * 256, kk = e2 >> 5, r2 = (e2 & 31) * 2;
-    cp_async_cg16(&S[kk * TB + r2], &G[(size_t)kk * ld + r2]);
+    cp_async_cg16(&S[kk * SLD + r2], &G[(size_t)kk * ld + r2]);
   }
 }
 
@@ -288,7 +292,7 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
       // cnt = updates tile (i,k) must have seen; tk.w >> 16 unused; rank of (i,i) is upd order
       // everything that does not depend on D(k) is fetched before waiting for it: A_ik (its
       // updates are done) and the diagonal tile A_ii (its earlier updates are done)
-      double *SA = sm, *SU = sm + TB * TB;
+      double *SA = sm, *SU = sm + TB * SLD;
       const size_t oik = tile_off(i, k, nSp), oii = tile_off(i, i, nSp);
       if (P.rw_ptr)   // fused Galerkin: the rows of S this task reads unfactored
         for (int q2 = P.rw_ptr[ccur - 1]; q2 < P.rw_ptr[ccur]; ++q2) df_wait(&P.rdone[P.rw[q2]], 1);
@@ -318,13 +322,13 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
         __stcg(&L[oik + (size_t)c * nSp + r], acc[q]);
       }
       df_signal(&pfl[i * NT + k], 1);             // panel tile published early for the other updates
-      // X = L_ik into k-major smem: SX[c*64 + r] = X[r][c]
+      // X = L_ik into k-major smem: SX[c*SLD + r] = X[r][c]
       double *SX = sm;
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         int r, c;
         tile_rc(q, r, c);
-        SX[c * TB + r] = acc[q];
+        SX[c * SLD + r] = acc[q];
       }
       __syncthreads();
       tile_gemm(SX, SX, acc);
@@ -350,7 +354,7 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
       df_signal(&P.rdone[i], 1);
       df_release(P, P.succ_ptr[id], P.succ_ptr[id + 1], &s_keep);
     } else if (type == 1) {
-      double *SA = sm, *SU = sm + TB * TB;
+      double *SA = sm, *SU = sm + TB * SLD;
       const size_t oik = tile_off(i, k, nSp);
       stage_colmajor(SA, L + oik, nSp);
       stage_colmajor(SU, U + (size_t)k * TB * TB, TB);
@@ -368,7 +372,7 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
       df_release(P, P.succ_ptr[id], P.succ_ptr[id + 1], &s_keep);
 
     } else {
-      double *Si = sm, *Sj = sm + TB * TB;
+      double *Si = sm, *Sj = sm + TB * SLD;
       stage_colmajor(Si, L + tile_off(i, k, nSp), nSp);
       stage_colmajor(Sj, L + tile_off(j, k, nSp), nSp);
 
@@ -578,7 +582,7 @@ __global__ void __launch_bounds__(256) k_chol_bwd(int NT, const int32_t *__restr
 
 // ------------------------------------------------------------------ host side
 constexpr size_t kDiagSmem = sizeof(double) * kDiagSmemDoubles;
-constexpr size_t kGemmSmem = sizeof(double) * 2 * TB * TB;
+constexpr size_t kGemmSmem = sizeof(double) * 2 * TB * SLD;
 constexpr size_t kUpdSmem = kDiagSmem > kGemmSmem ? kDiagSmem : kGemmSmem;
 
 #ifndef MSIM_DF_PER_SM

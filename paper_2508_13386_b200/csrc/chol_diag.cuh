@@ -16,8 +16,9 @@
 #endif
 
 // ---------------------------------------------------------------- blocked factor + inverse
-// smem: A [64][LD], Li [64][LD], Tb [3*16*17], invd [64]
-constexpr int kDiagSmemDoublesBlocked = 2 * TB * LD + 3 * 16 * 17 + TB + 16;
+// smem: A [64][LD], Li [64][LD], T [16][kTS], invd [64], broadcast scratch [16]
+constexpr int kTS = 52;   // T row stride: 52 = 4 (mod 16), conflict-free m8n8k4 fragments
+constexpr int kDiagSmemDoublesBlocked = 2 * TB * LD + 16 * kTS + TB + 16;
 
 __device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -33,7 +34,7 @@ __device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double
 // warps.  Measured on the chain: the scalar version's last row block took ~6 k cycles.
 __device__ __forceinline__ void inv_rowblock_mma(int pb, const double *A, double *Li, double *T,
                                                  const double *invd, int tt, int nth, int bar_id) {
-  constexpr int TS = 49;   // T row stride (16 x 49 <= the 3 x 16 x 17 scratch)
+  constexpr int TS = kTS;
   const int o = 16 * pb, lane = tt & 31, gw = tt >> 5, nw = nth >> 5;
   const int lr = lane >> 2, lk = lane & 3;
   if (tt < 16) {
@@ -81,8 +82,8 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
                                     int *__restrict__ flag, double *sm, bool preloaded) {
   double *A = sm;              // row-major [64][LD]: the factor
   double *Li = sm + TB * LD;   // row-major [64][LD]: its inverse
-  double(*Tb)[16][17] = reinterpret_cast<double(*)[16][17]>(sm + 2 * TB * LD);
-  double *invd = sm + 2 * TB * LD + 3 * 16 * 17;
+  double *Tb = sm + 2 * TB * LD;
+  double *invd = sm + 2 * TB * LD + 16 * kTS;
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
   const size_t okk = tile_off(k, k, nSp);
   if (!preloaded) {
@@ -114,7 +115,7 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
       // warps 1-3, 5-7: row-block p-1 of the inverse (its columns of L are final) while warp 0
       // factors panel p
       const int tt = (w < 4 ? w - 1 : w - 2) * 32 + lane;
-      if (p > 0) inv_rowblock_mma(p - 1, A, Li, reinterpret_cast<double *>(Tb), invd, tt, 192, 1);
+      if (p > 0) inv_rowblock_mma(p - 1, A, Li, Tb, invd, tt, 192, 1);
     } else {
       // panel rows j0 + lane and j0 + 32 + lane, columns j0 .. j0+15
       const int ra = j0 + lane, rb = j0 + 32 + lane;
@@ -210,7 +211,7 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
     if (r < 48) __stcg(&Uk[(size_t)c * TB + r], Li[r * LD + c]);
   }
   // last row-block of the inverse (the others were formed during the panels)
-  inv_rowblock_mma(3, A, Li, reinterpret_cast<double *>(Tb), invd, t, 256, 1);
+  inv_rowblock_mma(3, A, Li, Tb, invd, t, 256, 1);
   DIAG_TS(9);
 #pragma unroll
   for (int it = 0; it < 4; ++it) {   // rows 48..63 of Li: 16 x 64 entries
