@@ -35,6 +35,18 @@ __device__ __forceinline__ size_t tile_off(int ti, int tj, int nSp) {
   return (size_t)(tj * TB) * nSp + (size_t)ti * TB;
 }
 
+#ifdef MSIM_CHAIN_PROF   // sub-phases of D on the chain CTA (diagnostic build only): stamps in
+// shared memory (no global round trip on the panel warp), accumulated at D's end
+__device__ long long g_dts[16];
+__device__ __forceinline__ long long *diag_ts_buf() {
+  __shared__ long long ts[16];
+  return ts;
+}
+#define DIAG_TS(i) do { if (threadIdx.x == 0) diag_ts_buf()[i] = clock64(); } while (0)
+#define DIAG_TS_FLUSH() do { if (blockIdx.x == 0 && threadIdx.x == 0) { const long long *b_ = diag_ts_buf(); \
+    long long last_ = b_[0]; const int ord_[12] = {10, 1, 2, 11, 3, 4, 12, 5, 6, 13, 7, 9}; \
+    for (int q_ = 0; q_ < 12; ++q_) { g_dts[ord_[q_]] += b_[ord_[q_]] - last_; last_ = b_[ord_[q_]]; } } } while (0)
+#endif
 #include "chol_diag.cuh"
 
 // ------------------------------------------------------------------ tile GEMM of the dataflow kernel
@@ -212,8 +224,21 @@ __device__ __forceinline__ int df_pop(int *Q, const int *done, int npool) {
 #ifndef MSIM_DF_MINB
 #define MSIM_DF_MINB 2
 #endif
+// -DMSIM_CHAIN_PROF: CTA 0 accumulates clock64 deltas of the phases of its chain tasks and prints
+// them at the end of the launch (diagnostic build only)
+#ifdef MSIM_CHAIN_PROF
+#define CHAIN_TS(q) do { if (t == 0) { const long long now_ = clock64(); prof[q] += now_ - prof_last; prof_last = now_; } } while (0)
+#else
+#define CHAIN_TS(q)
+#endif
 __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfParams P) {
   extern __shared__ double sm[];
+#ifdef MSIM_CHAIN_PROF
+  long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0}, prof_last = clock64();
+  int prof_n = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (int q = 0; q < 16; ++q) g_dts[q] = 0;
+#endif
   __shared__ int s_id, s_keep;
   const int t = threadIdx.x;
   if (t == 0) s_keep = -1;
@@ -294,9 +319,11 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
       // updates are done) and the diagonal tile A_ii (its earlier updates are done)
       double *SA = sm, *SU = sm + TB * SLD;
       const size_t oik = tile_off(i, k, nSp), oii = tile_off(i, i, nSp);
+      CHAIN_TS(0);   // between chain tasks
       if (P.rw_ptr)   // fused Galerkin: the rows of S this task reads unfactored
         for (int q2 = P.rw_ptr[ccur - 1]; q2 < P.rw_ptr[ccur]; ++q2) df_wait(&P.rdone[P.rw[q2]], 1);
       df_wait2(&upd[i * NT + k], cnt & 0xffff, &upd[i * NT + i], cnt >> 16);
+      CHAIN_TS(1);   // waiting for the inputs' updates
       stage_colmajor(SA, L + oik, nSp);
       asm volatile("cp.async.commit_group;\n" ::);
       double old[16];
@@ -312,6 +339,7 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
       if (!own_d) stage_colmajor(SU, U + (size_t)k * TB * TB, TB);
       cp_async_commit_wait();
       __syncthreads();
+      CHAIN_TS(2);   // staging A_ik, A_ii (and U_kk)
       double acc[16];
       if (own_d) tile_gemm<true>(SA, sm + TB * LD, acc);
       else tile_gemm(SA, SU, acc);
@@ -322,6 +350,7 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
         __stcg(&L[oik + (size_t)c * nSp + r], acc[q]);
       }
       df_signal(&pfl[i * NT + k], 1);             // panel tile published early for the other updates
+      CHAIN_TS(3);   // P(i,k) GEMM + stores
       // X = L_ik into k-major smem: SX[c*SLD + r] = X[r][c]
       double *SX = sm;
 #pragma unroll
@@ -339,9 +368,15 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
         tile_rc(q, r, c);
         sm[r * LD + c] = r >= c ? old[q] - acc[q] : 0.0;
       }
+      CHAIN_TS(4);   // U(i,i,k) GEMM
       diag_factor(i, nSp, L, U, flag, sm, true);
+      CHAIN_TS(5);   // D(i)
       df_signal2(&dfl[i], 1, &upd[i * NT + i], (cnt >> 16) + 1);
       my_d = i;
+      CHAIN_TS(6);
+#ifdef MSIM_CHAIN_PROF
+      ++prof_n;
+#endif
     } else if (type == 5) {
       // G(i, part): a quarter of handle i's Galerkin row into its partial row (galerkin.cuh)
       galerkin_row(P.gal, i, j, sm);
@@ -401,6 +436,17 @@ __global__ void __launch_bounds__(256, MSIM_DF_MINB) k_chol_dataflow(const DfPar
     __syncthreads();
     if (t == 0 && type != 4) atomicAdd(P.done, 1);   // after this task's pushes (barrier above)
   }
+#ifdef MSIM_CHAIN_PROF
+  if (blockIdx.x == 0 && t == 0 && prof_n > 0)
+    printf("chain tasks %d  cycles/task: gap %lld wait %lld stage %lld P %lld U %lld D %lld signal %lld\n", prof_n,
+           prof[0] / prof_n, prof[1] / prof_n, prof[2] / prof_n, prof[3] / prof_n, prof[4] / prof_n, prof[5] / prof_n,
+           prof[6] / prof_n);
+  if (blockIdx.x == 0 && t == 0 && prof_n > 0)
+    printf("D sub-phases: panel0 %lld sync %lld trail0 %lld | panel1 %lld sync %lld trail1 %lld | panel2 %lld sync %lld "
+           "trail2 %lld | panel3 %lld sync %lld last %lld\n", g_dts[10] / prof_n, g_dts[1] / prof_n, g_dts[2] / prof_n,
+           g_dts[11] / prof_n, g_dts[3] / prof_n, g_dts[4] / prof_n, g_dts[12] / prof_n, g_dts[5] / prof_n,
+           g_dts[6] / prof_n, g_dts[13] / prof_n, g_dts[7] / prof_n, g_dts[9] / prof_n);
+#endif
 }
 
 __global__ void __launch_bounds__(256) k_zero_tiles(const int32_t *__restrict__ tiles, int nSp, double *__restrict__ L) {

@@ -11,6 +11,9 @@
 #ifndef DIAG_TS
 #define DIAG_TS(i)
 #endif
+#ifndef DIAG_TS_FLUSH
+#define DIAG_TS_FLUSH()
+#endif
 #ifndef MSIM_STORE_LKK
 #define MSIM_STORE_LKK 0
 #endif
@@ -218,6 +221,7 @@ __device__ void diag_factor_blocked(int k, int nSp, double *__restrict__ L, doub
     const int e = t + it * 256, r = 48 + (e & 15), c = e >> 4;
     __stcg(&Uk[(size_t)c * TB + r], Li[r * LD + c]);
   }
+  DIAG_TS_FLUSH();
 }
 
 
