@@ -211,6 +211,8 @@ GalParams galerkin_params(const Ctx &c) {
   G.gl_off = c.gl_off;
   G.gl_ent = c.gl_ent;
   G.W = c.Wphi;
+  G.ga_w = c.ga_w;
+  G.gl_w = c.gl_w;
   G.sT = c.sT;
   G.scol = c.scol;
   G.S = c.Sblk;
@@ -305,10 +307,28 @@ __global__ void k_basis_W(int nv, const int32_t *__restrict__ vptr, const int32_
   }
 }
 
+// out[e] = W[ent[e] >> shift] (4 doubles per entry)
+__global__ void k_gather_w(int64_t n, const uint32_t *__restrict__ ent, int shift, const double *__restrict__ W,
+                           double *__restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const size_t p = ent[e] >> shift;
+  const double4 w = *reinterpret_cast<const double4 *>(W + 4 * p);
+  *reinterpret_cast<double4 *>(out + 4 * e) = w;
+}
+
 void launch_basis_W(Ctx &c) {
   c.Wphi.alloc(4 * (size_t)c.nnz_phi);
   k_basis_W<<<div_up(c.nv, 256), 256, 0, c.stream>>>(c.nv, c.bvptr, c.bhandle, c.bphi, c.X, c.origins, c.Wphi);
   c.launches++;
+  // the Galerkin lists' weights in list order: phase A reads entry (u, slot) with the H row, phase
+  // B entry (u, j) with its u index, both without the dependent index -> W round trip
+  const int64_t na = (int64_t)c.ga_ent.n, nl = (int64_t)c.gl_ent.n;
+  c.ga_w.alloc(4 * (size_t)na);
+  c.gl_w.alloc(4 * (size_t)nl);
+  k_gather_w<<<(unsigned)div_up(na, 256), 256, 0, c.stream>>>(na, c.ga_ent, 6, c.Wphi, c.ga_w);
+  k_gather_w<<<(unsigned)div_up(nl, 256), 256, 0, c.stream>>>(nl, c.gl_ent, 7, c.Wphi, c.gl_w);
+  c.launches += 2;
   MS_CUDA(cudaGetLastError());
 }
 
@@ -537,6 +557,7 @@ static void coarse_pcg_blocks(Ctx &c) {
   G.gl_base = c.gd_gl_base;
   G.gl_off = c.gd_gl_off;
   G.gl_ent = c.gd_gl_ent;
+  G.ga_w = G.gl_w = nullptr;   // (diagonal-block lists: W gathered through the index)
   G.sT = c.gd_sT;
   G.S = c.Sdiag;
   G.Spart = c.Sdiag_part;

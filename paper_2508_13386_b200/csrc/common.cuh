@@ -179,6 +179,8 @@ struct Ctx {
   DBuf<int32_t> sptr, scol, srow, sT;   // sT[b]: block index of the transposed block
   DBuf<double> Sblk;                // [nnzb_S * 144]
   DBuf<double> Wphi;                // [nnz_phi * 4] phi [1, X - c] per basis entry
+  DBuf<double> ga_w, gl_w;          // [|ga| * 4], [|gl| * 4]: the W rows of the Galerkin list entries,
+                                    // gathered once per basis (no dependent gather in the kernel)
   // fused Galerkin (coarse.cu k_galerkin_fused): U_i lists, upper S slots, chunked entries
   DBuf<int32_t> gU_ptr, gU;         // [m+1], [sum |U_i|]
   DBuf<int32_t> ga_off;             // [sum |U_i| + 1] per (i,u) pair: range in ga_ent

@@ -19,6 +19,7 @@ struct GalParams {
   const int32_t *gj_ptr, *gj_blk, *gl_base, *gl_off;
   const uint32_t *gl_ent;
   const double *W;
+  const double *ga_w, *gl_w;        // W rows per list entry (nullable: gather through the index)
   const int32_t *sT;
   const int32_t *scol;              // S pattern columns (handle j of block b)
   double *S;                        // [nnzb_S][144] block storage
@@ -79,7 +80,11 @@ __device__ __forceinline__ void galerkin_row(const GalParams &G, int i, int part
 #pragma unroll
     for (int k = 0; k < 36; ++k) acc[k] = 0.0;
     const int uq = ch * kGalChunk + ul_a;
+#ifdef MSIM_GAL_SKIP_A   // timing diagnostics only (wrong results): phase B alone
+    if (false) {
+#else
     if (uq < nU) {
+#endif
       // slot-synchronous walk of row u: lanes of a warp (consecutive u of one SELL slice) read
       // the same slot j together (coalesced value planes); the two halves take even / odd slots
       const int q = u0 + uq;
@@ -88,14 +93,16 @@ __device__ __forceinline__ void galerkin_row(const GalParams &G, int i, int part
       const int base = __ldg(&H.sl_ptr[u >> 5]), len = __ldg(&H.sl_ptr[(u >> 5) + 1]) - base;
       const unsigned long long mask = __ldg(&ga_mask[q]);
       const int e0 = __ldg(&ga_off[q]);
+#ifndef MSIM_GAL_SKIP_A
 #pragma unroll 2
+#endif
       for (int j = half; j < len; j += 2) {
         if (!((mask >> j) & 1ull)) continue;
-        const uint32_t en = __ldg(&ga_ent[e0 + __popcll(mask & ((1ull << j) - 1ull))]);
+        const int ea = e0 + __popcll(mask & ((1ull << j) - 1ull));
         const size_t cs = (size_t)base + j;
-        const size_t p = en >> 6;
-        const double2 w01 = __ldg(reinterpret_cast<const double2 *>(W + 4 * p));
-        const double2 w23 = __ldg(reinterpret_cast<const double2 *>(W + 4 * p + 2));
+        const double *wp = G.ga_w ? G.ga_w + 4 * (size_t)ea : W + 4 * (size_t)(__ldg(&ga_ent[ea]) >> 6);
+        const double2 w01 = __ldg(reinterpret_cast<const double2 *>(wp));
+        const double2 w23 = __ldg(reinterpret_cast<const double2 *>(wp + 2));
         const double w[4] = {w01.x, w01.y, w23.x, w23.y};
         // H_vu[c'][c] = H_uv[c][c'] = vals plane 3c + c'
         double Hvu[3][3];
@@ -128,7 +135,11 @@ __device__ __forceinline__ void galerkin_row(const GalParams &G, int i, int part
     // summed in a fixed order at the end of the slot
     const int *o = off + ch * (nup + 1);
     const int grp = lane / 9, g = lane - 9 * grp;   // grp 3: lanes 27..31 idle in the FMA loop
+#ifdef MSIM_GAL_SKIP_B   // timing diagnostics only (wrong results): phase A alone
+    for (int q = nup; q < nup; q += kGalWarps) {
+#else
     for (int q = warp; q < nup; q += kGalWarps) {
+#endif
       double a[4][4];
 #pragma unroll
       for (int r = 0; r < 4; ++r)
@@ -142,9 +153,9 @@ __device__ __forceinline__ void galerkin_row(const GalParams &G, int i, int part
       int eb = __ldg(&o[q]);
       if (eb + lane < e1) {
         en_n = __ldg(&gl_ent[eb + lane]);
-        const size_t p = en_n >> 7;
-        w01_n = __ldg(reinterpret_cast<const double2 *>(W + 4 * p));
-        w23_n = __ldg(reinterpret_cast<const double2 *>(W + 4 * p + 2));
+        const double *wp = G.gl_w ? G.gl_w + 4 * (size_t)(eb + lane) : W + 4 * (size_t)(en_n >> 7);
+        w01_n = __ldg(reinterpret_cast<const double2 *>(wp));
+        w23_n = __ldg(reinterpret_cast<const double2 *>(wp + 2));
       }
       for (; eb < e1; eb += 32) {
         const int n = min(32, e1 - eb);
@@ -157,9 +168,9 @@ __device__ __forceinline__ void galerkin_row(const GalParams &G, int i, int part
         __syncwarp();
         if (eb + 32 + lane < e1) {
           en_n = __ldg(&gl_ent[eb + 32 + lane]);
-          const size_t p = en_n >> 7;
-          w01_n = __ldg(reinterpret_cast<const double2 *>(W + 4 * p));
-          w23_n = __ldg(reinterpret_cast<const double2 *>(W + 4 * p + 2));
+          const double *wp = G.gl_w ? G.gl_w + 4 * (size_t)(eb + 32 + lane) : W + 4 * (size_t)(en_n >> 7);
+          w01_n = __ldg(reinterpret_cast<const double2 *>(wp));
+          w23_n = __ldg(reinterpret_cast<const double2 *>(wp + 2));
         }
         if (grp < 3) {
 #pragma unroll 2
