@@ -93,9 +93,7 @@ __device__ __forceinline__ void galerkin_row(const GalParams &G, int i, int part
       const int base = __ldg(&H.sl_ptr[u >> 5]), len = __ldg(&H.sl_ptr[(u >> 5) + 1]) - base;
       const unsigned long long mask = __ldg(&ga_mask[q]);
       const int e0 = __ldg(&ga_off[q]);
-#ifndef MSIM_GAL_SKIP_A
 #pragma unroll 2
-#endif
       for (int j = half; j < len; j += 2) {
         if (!((mask >> j) & 1ull)) continue;
         const int ea = e0 + __popcll(mask & ((1ull << j) - 1ull));
