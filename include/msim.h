@@ -80,7 +80,7 @@ typedef struct ms_params {
                              history -- the first after ms_set_state -- is implicit Euler)   */
   int32_t refine_mode;    /* full-space refinement d_f (Alg. 1): MS_REFINE_JACOBI
                              (default, reading R5: exactly n_cg Jacobi-PCG iterations) or
-                             MS_REFINE_TWO_LEVEL (NEXT-4, not in the paper; reading C5): PCG with
+                             MS_REFINE_TWO_LEVEL (NEXT-4, not in the paper; reading N4): PCG with
                              y = D^-1 r, z = y + U_s S^-1 U_s^T (r - H y) (the factorised SMS
                              matrix of the Newton iteration) until ||r_k||_2 <= refine_tol ||g||_2 or
                              refine_max_iter iterations; needs MS_COARSE_EXACT                */

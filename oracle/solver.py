@@ -8,7 +8,7 @@ Passages followed:
   ||d_s|| / (h |V|) < eps.
 * Alg. 2 L427-450 with readings R4 (exact coarse solves), R6 (right-hand side -g).
 * §3.7.2: fixed-count Jacobi-PCG refinement from d_f = 0 (reading R5); NEXT-4 option:
-  two-level PCG (Jacobi + SMS coarse correction) to a tolerance (reading C5, not in the paper).
+  two-level PCG (Jacobi + SMS coarse correction) to a tolerance (reading N4, not in the paper).
 * L616 and SPEC S:170-184: CCD (ground plane) and inversion filters with safety 0.9,
   backtracking by halving with strict decrease, alpha_min = 1e-8 (reading Q12).
 * R3: one freshly assembled, fully integrated H for every stage (no cubature / lagging).
@@ -51,7 +51,7 @@ def pcg(H, r, n_iter, Dinv=None):
 
 
 def two_level_pcg(H, r, Us, S_chol, tol, ref_norm, max_iter, Dinv=None):
-    """NEXT-4 (not in the paper -- reading C5 of DESIGN.md): PCG on H d = r from d = 0
+    """NEXT-4 (not in the paper -- reading N4 of DESIGN.md): PCG on H d = r from d = 0
     with the two-level preconditioner
         y = D^-1 v,   z = y + U_s S^-1 U_s^T (v - H y)
     (the Jacobi smoother of P:484, then the SMS coarse correction of Alg. 2 on the smoothed

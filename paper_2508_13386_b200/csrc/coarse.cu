@@ -693,7 +693,7 @@ void launch_coarse_direction(Ctx &c) {
 // PCG on H d_f = r1 from d_f = 0 with y = D^-1 r, z = y + U_s S^-1 U_s^T (r - H y) (the SMS factor of
 // this Newton iteration: SpMV, restrict, the two cooperative triangular sweeps, lift; "A-DEF2",
 // equal to the balancing preconditioner since U_s^T r1 = 0 after the SMS stage), stopped at the first k with
-// ||r_k||^2 <= tol^2 ||g||^2 or k = refine_max_iter (reading C5; oracle/solver.py two_level_pcg).
+// ||r_k||^2 <= tol^2 ||g||^2 or k = refine_max_iter (reading N4; oracle/solver.py two_level_pcg).
 // Host-driven batches of kTlBatch iterations, one CUDA graph; once the device flag tl_state[0] is
 // set every launch of a batch returns at once, so the iterates are exactly those of a loop that
 // stopped at k.  Scalars: rho = SC_RZ, beta = SC_BETA, alpha = SC_ALPHA (k_pcg_spmv's slots).

@@ -1,5 +1,5 @@
 """Parity of the NEXT-4 two-level refinement (MS_REFINE_TWO_LEVEL, not in the paper,
-reading C5 of DESIGN.md): PCG on H d_f = -g - H d_s with y = D^-1 r, z = y + U_s S^-1 U_s^T (r - H y), GPU against
+reading N4 of DESIGN.md): PCG on H d_f = -g - H d_s with y = D^-1 r, z = y + U_s S^-1 U_s^T (r - H y), GPU against
 oracle/solver.py two_level_pcg through OracleSim(refine="two_level").
 
 * fixed iteration counts (tolerance 0, cap k): d_f to 1e-8 (the iterates are unique);
