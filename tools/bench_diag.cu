@@ -1,5 +1,8 @@
-// Micro-benchmark of the diagonal-tile factorisation variants (csrc/chol_diag.cuh): cycles per
-// 64 x 64 Cholesky + inverse by one CTA (clock64 inside the kernel), and a correctness check.
+// Micro-benchmark of the diagonal-tile step (csrc/chol_diag.cuh): cycles per 64 x 64
+// U_kk = L_kk^-T by one CTA (clock64 inside the kernel), and a correctness check
+// (Linv lower triangular with a positive diagonal and Linv A Linv^T = I).  Variant 1 is the
+// library's D; the others (tools/diag_variants.cuh) are the measured alternatives of DESIGN.md §7.
+// -DBD_EVICT=6000 runs ~96 KB of other code between factorisations (cold instruction cache).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include -I paper_2508_13386_b200/csrc \
 //        tools/bench_diag.cu -o /tmp/bench_diag && /tmp/bench_diag
 #include <cstdio>
@@ -8,7 +11,6 @@
 #include <vector>
 #include <cuda_runtime.h>
 #include "fastmath.cuh"
-#define MSIM_STORE_LKK 1   // the check below reads L_kk back
 #ifndef BD_MINB
 #define BD_MINB 1   // -DBD_MINB=2: the register budget of the dataflow kernel (2 CTAs per SM)
 #endif
@@ -17,9 +19,8 @@ namespace msim {
 constexpr int TB = 64;
 constexpr int LD = TB + 4;   // as chol.cu
 __device__ __forceinline__ size_t tile_off(int ti, int tj, int nSp) { return (size_t)(tj * TB) * nSp + (size_t)ti * TB; }
-__device__ long long g_ts[16];
-#define DIAG_TS(i) do { if (threadIdx.x == 0 && blockIdx.x == 0) g_ts[i] = clock64(); } while (0)
 #include "chol_diag.cuh"
+#include "diag_variants.cuh"
 }  // namespace msim
 using namespace msim;
 
@@ -45,8 +46,21 @@ __global__ void __launch_bounds__(256, BD_MINB) kbench(const double *A0, double 
     __syncthreads();
     __threadfence_block();
     long long t0 = clock64();
-    if (threadIdx.x == 0 && blockIdx.x == 0) g_ts[15] = t0;
-    diag_factor_blocked(0, TB, Lb, Ub, flag, sm, false);
+    if (V == 1) diag_factor_blocked(0, TB, Lb, Ub, flag, sm, false);
+    else if (V == 2) diag_v2<true>(0, TB, Lb, Ub, flag, sm);
+    else if (V == 3) diag_v3<false>(0, TB, Lb, Ub, flag, sm);
+    else if (V == 4) diag_v3<true>(0, TB, Lb, Ub, flag, sm);
+    else if (V == 5) diag_v5(0, TB, Lb, Ub, flag, sm);
+    else if (V == 6) diag_v6(0, TB, Lb, Ub, flag, sm);
+    else if (V == 8) diag_v8(0, TB, Lb, Ub, flag, sm);
+    else if (V == 9) diag_v9(0, TB, Lb, Ub, flag, sm);
+    else if (V == 10) diag_v10(0, TB, Lb, Ub, flag, sm);
+    else if (V == 11) diag_v11(0, TB, Lb, Ub, flag, sm);
+    else if (V == 12) diag_v12(0, TB, Lb, Ub, flag, sm);
+    else if (V == 20) diag_v7<0>(0, TB, Lb, Ub, flag, sm);
+    else if (V == 21) diag_v7<1>(0, TB, Lb, Ub, flag, sm);
+    else if (V == 22) diag_v7<2>(0, TB, Lb, Ub, flag, sm);
+    else diag_v7<3>(0, TB, Lb, Ub, flag, sm);
     __syncthreads();
     tot += clock64() - t0;
   }
@@ -71,26 +85,26 @@ void run(const std::vector<double> &A, int nblk) {
   std::vector<double> L(4096), U(4096); cudaMemcpy(L.data(), dL, 8 * 4096, cudaMemcpyDeviceToHost);
   cudaMemcpy(U.data(), dU, 8 * 4096, cudaMemcpyDeviceToHost);
   int flag; cudaMemcpy(&flag, dflag, 4, cudaMemcpyDeviceToHost);
-  if (nblk == 1) {
-    long long ts[16]; cudaMemcpyFromSymbol(ts, g_ts, sizeof(ts));
-    printf("v%d phases", V); printf(" (cycles from start): load %lld |", ts[0] - ts[15]);
-    for (int q = 1; q < 16 - 1; ++q) printf(" %d:%lld", q, ts[q] - ts[15]);
-    printf("\n");
-  }
-  // checks: L L^T = A (lower L column-major), U = L^-T (row-major U[c][r] at c*64 + r)
+  // checks: U = L^-T row-major (U[c][r] at c*64 + r = Linv[r][c]); Linv A Linv^T = I
   double e1n = 0, e2n = 0, an = 0;
   for (int i = 0; i < 64; ++i)
-    for (int j = 0; j <= i; ++j) {
-      double s = 0; for (int q = 0; q <= j; ++q) s += L[q * 64 + i] * L[q * 64 + j];
-      e1n = fmax(e1n, fabs(s - A[j * 64 + i])); an = fmax(an, fabs(A[j * 64 + i]));
-    }
-  for (int i = 0; i < 64; ++i)   // (L^-1)[i][j] = U[j][i]; check L^-1 L = I
     for (int j = 0; j < 64; ++j) {
-      double s = 0; for (int q = 0; q < 64; ++q) s += U[q * 64 + i] * (j <= q ? L[j * 64 + q] : 0.0);
-      e2n = fmax(e2n, fabs(s - (i == j ? 1.0 : 0.0)));
+      an = fmax(an, fabs(A[j * 64 + i]));
+      if (j > i) e2n = fmax(e2n, fabs(U[j * 64 + i]));   // upper part of Linv must be 0
     }
-  printf("variant %d  ctas %4d  cycles/factor %8lld  (%.2f us @1.965GHz)  wall %.1f us/factor-wave  |LL^T-A|/|A| %.1e  |Linv L - I| %.1e flag %d\n",
-         V, nblk, c[0], c[0] / 1965.0, 1e3 * ms / 20, e1n / an, e2n, flag);
+  std::vector<double> T(4096);   // T = Linv A
+  for (int i = 0; i < 64; ++i)
+    for (int j = 0; j < 64; ++j) {
+      double s = 0; for (int q = 0; q < 64; ++q) s += U[q * 64 + i] * A[j * 64 + q];
+      T[i * 64 + j] = s;
+    }
+  for (int i = 0; i < 64; ++i)
+    for (int j = 0; j < 64; ++j) {
+      double s = 0; for (int q = 0; q < 64; ++q) s += T[i * 64 + q] * U[q * 64 + j];
+      e1n = fmax(e1n, fabs(s - (i == j ? 1.0 : 0.0)));
+    }
+  printf("variant %d  ctas %4d  cycles/factor %8lld  (%.2f us @1.965GHz)  wall %.1f us/factor-wave  |Linv A Linv^T - I| %.1e  |upper(Linv)| %.1e  |A| %.1e flag %d\n",
+         V, nblk, c[0], c[0] / 1965.0, 1e3 * ms / 20, e1n, e2n, an, flag);
   cudaFree(dA); cudaFree(dL); cudaFree(dU); cudaFree(dflag); cudaFree(dc);
 }
 
@@ -104,6 +118,11 @@ int main() {
       for (int q = 0; q < 64; ++q) s += M[i * 64 + q] * M[j * 64 + q];
       A[j * 64 + i] = s;
     }
-  for (int nb : {1, 148}) { run<1>(A, nb); }
+  if (getenv("BD_ONE")) { run<10>(A, 1);
+    long long ts[8][8]; cudaMemcpyFromSymbol(ts, g_v10ts, sizeof(ts));
+    for (int w = 0; w < 8; ++w) { printf("w%d:", w); for (int q = 0; q < 7; ++q) printf(" %lld", ts[w][q] - ts[0][0]); printf("\n"); }
+    return 0; }
+  if (getenv("BD_DISSECT")) { run<20>(A, 1); run<21>(A, 1); run<22>(A, 1); run<13>(A, 1); return 0; }
+  for (int nb : {1, 148}) { run<1>(A, nb); run<2>(A, nb); run<3>(A, nb); run<9>(A, nb); run<10>(A, nb); run<12>(A, nb); }
   return 0;
 }
