@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(256, BD_MINB) kbench(const double *A0, double 
     else if (V == 10) diag_v10(0, TB, Lb, Ub, flag, sm);
     else if (V == 11) diag_v11(0, TB, Lb, Ub, flag, sm);
     else if (V == 12) diag_v12(0, TB, Lb, Ub, flag, sm);
+    else if (V == 13) diag_v13(0, TB, Lb, Ub, flag, sm);
     else if (V == 20) diag_v7<0>(0, TB, Lb, Ub, flag, sm);
     else if (V == 21) diag_v7<1>(0, TB, Lb, Ub, flag, sm);
     else if (V == 22) diag_v7<2>(0, TB, Lb, Ub, flag, sm);
@@ -123,6 +124,6 @@ int main() {
     for (int w = 0; w < 8; ++w) { printf("w%d:", w); for (int q = 0; q < 7; ++q) printf(" %lld", ts[w][q] - ts[0][0]); printf("\n"); }
     return 0; }
   if (getenv("BD_DISSECT")) { run<20>(A, 1); run<21>(A, 1); run<22>(A, 1); run<13>(A, 1); return 0; }
-  for (int nb : {1, 148}) { run<1>(A, nb); run<2>(A, nb); run<3>(A, nb); run<9>(A, nb); run<10>(A, nb); run<12>(A, nb); }
+  for (int nb : {1, 148}) { run<1>(A, nb); run<2>(A, nb); run<3>(A, nb); run<9>(A, nb); run<10>(A, nb); run<13>(A, nb); }
   return 0;
 }

@@ -1419,3 +1419,215 @@ __device__ __noinline__ void diag_v12(int k, int nSp, double *__restrict__ L, do
     __stcg(&Uk[(size_t)c * TB + r], Li[r * LD + c]);
   }
 }
+
+// V13: V10 with the pair loops not unrolled (panel index still static): smaller code for the
+// cold instruction cache of the chain CTA.
+namespace v13 {
+using v9::bar_arrive;
+using v9::bar_wait;
+using v10::pinv2;
+
+template <int P>
+__device__ __forceinline__ void produce(double (&M)[8][2], double *R, int l) {
+  const int m = l >> 2, n2 = 2 * (l & 3), i = 8 * P + m;
+#pragma unroll 1
+  for (int S = 0; S < 4; ++S) {
+    const int a = 8 * P + 2 * S, b = a + 1;
+    if ((m >> 1) == S) {   // publish rows a, b
+      const int r = 8 * P + m;
+#pragma unroll
+      for (int tt = 0; tt < 8; ++tt)
+        *reinterpret_cast<double2 *>(&R[r * LD + 8 * tt + n2]) = make_double2(M[tt][0], M[tt][1]);
+    }
+    if (P < 7) bar_arrive(1 + S, 64);
+    __syncwarp();
+    const double paa = R[a * LD + a], pab = R[a * LD + b], pbb = R[b * LD + b];
+    double gaa, gab, gbb;
+    if (S < 3) {
+      double2 ua[8], ub[8];
+#pragma unroll
+      for (int tt = 0; tt < 8; ++tt) {
+        ua[tt] = *reinterpret_cast<const double2 *>(&R[a * LD + 8 * tt + n2]);
+        ub[tt] = *reinterpret_cast<const double2 *>(&R[b * LD + 8 * tt + n2]);
+      }
+      const double sa = R[a * LD + i], sb = R[b * LD + i];
+      pinv2(paa, pab, pbb, gaa, gab, gbb);
+      const bool act = m > 2 * S + 1;
+      const double fa = act ? fma(sa, gaa, sb * gab) : 0.0;
+      const double fb = act ? fma(sa, gab, sb * gbb) : 0.0;
+#pragma unroll
+      for (int tt = 0; tt < 8; ++tt) {
+        if (tt != P) {
+          M[tt][0] = fma(-fa, ua[tt].x, fma(-fb, ub[tt].x, M[tt][0]));
+          M[tt][1] = fma(-fa, ua[tt].y, fma(-fb, ub[tt].y, M[tt][1]));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int cp = n2 + e;
+            const bool use = cp >= m || cp < 2 * S;
+            const double xa = use ? (e ? ua[tt].y : ua[tt].x) : (cp == 2 * S ? 1.0 : 0.0);
+            const double xb = use ? (e ? ub[tt].y : ub[tt].x) : (cp == 2 * S + 1 ? 1.0 : 0.0);
+            M[tt][e] = fma(-fa, xa, fma(-fb, xb, M[tt][e]));
+          }
+        }
+      }
+    } else {
+      pinv2(paa, pab, pbb, gaa, gab, gbb);
+    }
+    if (l == 0) {   // G for the far consumers
+      R[a * LD + TB] = gaa;
+      R[a * LD + TB + 1] = gab;
+      R[a * LD + TB + 2] = gbb;
+    }
+  }
+  if (P <= 5) bar_arrive(9 + (P & 1), 32 * (7 - P));
+}
+
+template <int P>
+__device__ __forceinline__ void near(double (&M)[8][2], const double *R, int l) {
+  const int m = l >> 2, n2 = 2 * (l & 3), i = 8 * (P + 1) + m;
+#pragma unroll 1
+  for (int S = 0; S < 4; ++S) {
+    const int a = 8 * P + 2 * S, b = a + 1;
+    bar_wait(1 + S, 64);
+    const double paa = R[a * LD + a], pab = R[a * LD + b], pbb = R[b * LD + b];
+    const double sa = R[a * LD + i], sb = R[b * LD + i];
+    double2 ua[8], ub[8];
+#pragma unroll
+    for (int tt = 0; tt < 8; ++tt) {
+      ua[tt] = *reinterpret_cast<const double2 *>(&R[a * LD + 8 * tt + n2]);
+      ub[tt] = *reinterpret_cast<const double2 *>(&R[b * LD + 8 * tt + n2]);
+    }
+    double gaa, gab, gbb;
+    pinv2(paa, pab, pbb, gaa, gab, gbb);
+    const double fa = fma(sa, gaa, sb * gab), fb = fma(sa, gab, sb * gbb);
+#pragma unroll
+    for (int tt = 0; tt < 8; ++tt) {
+      if (tt < P || tt > P + 1) {
+        M[tt][0] = fma(-fa, ua[tt].x, fma(-fb, ub[tt].x, M[tt][0]));
+        M[tt][1] = fma(-fa, ua[tt].y, fma(-fb, ub[tt].y, M[tt][1]));
+      } else if (tt == P) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int cp = n2 + e;
+          const bool use = cp < 2 * S;
+          const double xa = use ? (e ? ua[tt].y : ua[tt].x) : (cp == 2 * S ? 1.0 : 0.0);
+          const double xb = use ? (e ? ub[tt].y : ub[tt].x) : (cp == 2 * S + 1 ? 1.0 : 0.0);
+          M[tt][e] = fma(-fa, xa, fma(-fb, xb, M[tt][e]));
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (n2 + e >= m)
+            M[tt][e] = fma(-fa, e ? ua[tt].y : ua[tt].x, fma(-fb, e ? ub[tt].y : ub[tt].x, M[tt][e]));
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void far(double (&M)[8][2], const double *R, int l, int w, int P) {
+  bar_wait(9 + (P & 1), 32 * (7 - P));
+  const int m = l >> 2, n2 = 2 * (l & 3), i = 8 * w + m;
+  double fa[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int kk = 8 * P + 4 * h + (l & 3), a = kk & ~1;   // pair (a, a + 1) holding k
+    const double sa = R[a * LD + i], sb = R[(a + 1) * LD + i];
+    const double gaa = R[a * LD + TB], gab = R[a * LD + TB + 1], gbb = R[a * LD + TB + 2];
+    fa[h] = (kk & 1) ? -fma(sa, gab, sb * gbb) : -fma(sa, gaa, sb * gab);
+  }
+#pragma unroll
+  for (int tt = 0; tt < 8; ++tt) {
+    if (tt > P && tt < w) continue;
+    double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int kk = 8 * P + 4 * h + (l & 3), c = 8 * tt + m;
+      double b = R[kk * LD + c];
+      if (tt == P) b = c < kk ? b : (c == kk ? 1.0 : 0.0);
+      if (tt == w) dmma884v(d0, d1, fa[h], b);
+      else dmma884v(M[tt][0], M[tt][1], fa[h], b);
+    }
+    if (tt == w) {
+      if (8 * tt + n2 >= i) M[tt][0] += d0;
+      if (8 * tt + n2 + 1 >= i) M[tt][1] += d1;
+    }
+  }
+}
+}  // namespace v13
+
+__device__ __noinline__ void diag_v13(int k, int nSp, double *__restrict__ L, double *__restrict__ U,
+                                      int *__restrict__ flag, double *sm, bool preloaded = false) {
+  double *R = sm, *Li = sm + TB * LD;
+  const int t = threadIdx.x, w = t >> 5, l = t & 31, m = l >> 2, n2 = 2 * (l & 3);
+  const int i = 8 * w + m;
+  double M[8][2];
+  if (preloaded) {
+#pragma unroll
+    for (int tt = 0; tt < 8; ++tt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = 8 * tt + n2 + e;
+        M[tt][e] = c >= i ? R[c * LD + i] : 0.0;
+      }
+  } else {
+    const size_t okk = tile_off(k, k, nSp);
+#pragma unroll
+    for (int tt = 0; tt < 8; ++tt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = 8 * tt + n2 + e;
+        M[tt][e] = c >= i ? __ldcg(&L[okk + (size_t)i * nSp + c]) : 0.0;
+      }
+  }
+  __syncthreads();
+  for (int P = 0; P + 2 <= w; ++P) v13::far(M, R, l, w, P);
+  if (w > 0) switch (w) {
+    case 1: v13::near<0>(M, R, l); break;
+    case 2: v13::near<1>(M, R, l); break;
+    case 3: v13::near<2>(M, R, l); break;
+    case 4: v13::near<3>(M, R, l); break;
+    case 5: v13::near<4>(M, R, l); break;
+    case 6: v13::near<5>(M, R, l); break;
+    default: v13::near<6>(M, R, l); break;
+  }
+  switch (w) {
+    case 0: v13::produce<0>(M, R, l); break;
+    case 1: v13::produce<1>(M, R, l); break;
+    case 2: v13::produce<2>(M, R, l); break;
+    case 3: v13::produce<3>(M, R, l); break;
+    case 4: v13::produce<4>(M, R, l); break;
+    case 5: v13::produce<5>(M, R, l); break;
+    case 6: v13::produce<6>(M, R, l); break;
+    default: v13::produce<7>(M, R, l); break;
+  }
+  __syncthreads();
+  {
+    // L^-1 = C^-1 N per 2 x 2 block (rows a = i & ~1, b = a + 1; the partner row is lane l ^ 4)
+    const int a = i & ~1, b = a + 1;
+    const double paa = R[a * LD + a], pab = R[a * LD + b], pbb = R[b * LD + b];
+    const bool ok = paa > 0.0;
+    const double ra = rsqrt_nr(ok ? paa : 1.0);
+    const double mm = ok ? pab * ra * ra : 0.0;
+    const double sc = fma(-mm, pab, pbb);
+    const double rb = rsqrt_nr(sc > 0.0 ? sc : 1.0);
+    const bool is_b = i & 1;
+#pragma unroll
+    for (int tt = 0; tt < 8; ++tt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = 8 * tt + n2 + e;
+        const double own = c < a ? M[tt][e] : (c == i ? 1.0 : 0.0);        // N_ic
+        const double na = __shfl_xor_sync(0xffffffffu, own, 4);              // partner row's N
+        Li[i * LD + c] = is_b ? rb * fma(-mm, na, own) : ra * own;
+      }
+    if ((l & 7) == 0 && flag && !(ok && sc > 0.0)) *flag = 1;
+  }
+  __syncthreads();
+  double *Uk = U + (size_t)k * TB * TB;
+#pragma unroll 4
+  for (int it = 0; it < 16; ++it) {
+    const int e = t + it * 256, r = e & 63, c = e >> 6;
+    __stcg(&Uk[(size_t)c * TB + r], Li[r * LD + c]);
+  }
+}
