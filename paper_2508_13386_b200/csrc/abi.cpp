@@ -403,6 +403,12 @@ ms_status ms_destroy(ms_ctx *ctx) {
   pcg_reset_graph(ctx->c);
   coarse_reset_graphs(ctx->c);
   for (auto e : ctx->c.ev_pool) cudaEventDestroy(e);
+  if (ctx->c.halo_stream) {
+    cudaStreamSynchronize(ctx->c.halo_stream);
+    cudaStreamDestroy(ctx->c.halo_stream);
+    cudaEventDestroy(ctx->c.ev_z);
+    cudaEventDestroy(ctx->c.ev_halo);
+  }
   if (ctx->c.h_pinned) cudaFreeHost(ctx->c.h_pinned);
   delete ctx->c.comm;
   delete ctx->c.built_basis;

@@ -105,6 +105,11 @@ struct Ctx {
   std::vector<int32_t> h_sptr_glob, h_scol_glob;
   DBuf<int32_t> halo_send_idx, halo_recv_idx;
   DBuf<double> halo_send, halo_recv;
+  // interior owned rows [int_lo, int_hi): no ghost column, so their SpMV rows need no halo and
+  // run while the halo of z is in flight on halo_stream (int_lo == int_hi: no overlap)
+  int32_t int_lo = 0, int_hi = 0;
+  cudaStream_t halo_stream = nullptr;
+  cudaEvent_t ev_z = nullptr, ev_halo = nullptr;
   bool dist() const { return part.world > 1; }
   std::vector<double> h_X;          // rest positions (host copy)
   std::vector<double> h_Xg, h_Eg, h_rhog;   // global rest positions (world > 1) / per-tet E, rho
@@ -302,6 +307,7 @@ enum {
   SC_CP_BN2,
   SC_TL_RZ,       // two-level refinement PCG (NEXT-4): r.z, r.r (summed together)
   SC_TL_RR,
+  SC_CG_DI,       // multi-GPU PCG: z.Hz over the interior rows (added by the boundary launch)
   SC_COUNT = 32
 };
 constexpr int SC_SUM0 = SC_ENERGY_ELEM, SC_SUM_N = SC_INFEAS - SC_ENERGY_ELEM + 1;

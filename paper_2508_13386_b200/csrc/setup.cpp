@@ -169,6 +169,27 @@ void build_mesh_structures(Ctx &c, const double *X, const int32_t *tets, const d
   }
   c.n_cub = 0;
   c.lag_valid = false;
+  if (c.dist()) {   // interior owned rows: one contiguous run between the rows that read ghosts
+    const int32_t no = c.nv_own;
+    std::vector<uint8_t> touch(no, 0);
+    for (int32_t r = 0; r < no; ++r)
+      for (int32_t k = c.h_rowptr[r]; k < c.h_rowptr[r + 1]; ++k)
+        if (c.h_colidx[k] >= no) touch[r] = 1;
+    int32_t lo = 0, hi = no;
+    for (int32_t r = 0; r < no / 2; ++r)
+      if (touch[r]) lo = r + 1;
+    for (int32_t r = no - 1; r >= no / 2; --r)
+      if (touch[r]) hi = r;
+    bool ok = lo < hi;
+    for (int32_t r = lo; ok && r < hi; ++r) ok = !touch[r];
+    c.int_lo = ok ? lo : 0;
+    c.int_hi = ok ? hi : 0;
+    if (!c.halo_stream) {   // created here, not lazily inside a graph capture
+      MS_CUDA(cudaStreamCreateWithFlags(&c.halo_stream, cudaStreamNonBlocking));
+      MS_CUDA(cudaEventCreateWithFlags(&c.ev_z, cudaEventDisableTiming));
+      MS_CUDA(cudaEventCreateWithFlags(&c.ev_halo, cudaEventDisableTiming));
+    }
+  }
   c.slot_row.upload(slot_row, s);
   c.cptr.upload(cptr, s);
   c.contrib.upload(contrib, s);

@@ -449,12 +449,16 @@ __global__ void k_pcg_scalars(double *__restrict__ scal, int which) {
 //   w = H z; [gamma, delta] summed; beta = gamma / gamma_old; alpha = gamma / (delta - beta gamma / alpha_old)
 //   (first iteration: beta = 0, alpha = gamma / delta); p = z + beta p; s = w + beta s;
 //   x += alpha p; r -= alpha s; z = D^-1 r; gamma' partial = r.z (owned); halo(z)
-__global__ void __launch_bounds__(256) k_cg_spmv(SellView H, int nv_own, const double *__restrict__ z,
-                                                 double *__restrict__ w, double *__restrict__ partial,
-                                                 unsigned int *counter, double *__restrict__ scal) {
+// rows [r0, r1) then [r2, r3) (one thread each); the dot over the owned ones goes to scal[dst]
+// (+ scal[SC_CG_DI] when add_int: the interior part of a split product)
+__global__ void __launch_bounds__(256) k_cg_spmv(SellView H, int nv_own, int r0, int r1, int r2, int r3,
+                                                 const double *__restrict__ z, double *__restrict__ w,
+                                                 double *__restrict__ partial, unsigned int *counter,
+                                                 double *__restrict__ scal, int dst, int add_int) {
   double acc[1] = {0.0};
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row < H.nv) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x, n1 = r1 - r0;
+  const int row = t < n1 ? r0 + t : r2 + (t - n1);
+  if (row < (t < n1 ? r1 : r3)) {
     double o[3];
     sell_row_product(H, row, z, o);
 #pragma unroll
@@ -464,7 +468,8 @@ __global__ void __launch_bounds__(256) k_cg_spmv(SellView H, int nv_own, const d
     }
   }
   double res[1];
-  if (grid_reduce<1>(acc, partial, counter, res) && threadIdx.x == 0) scal[SC_CG_D] = res[0];
+  if (grid_reduce<1>(acc, partial, counter, res) && threadIdx.x == 0)
+    scal[dst] = add_int ? res[0] + scal[SC_CG_DI] : res[0];
 }
 
 __global__ void k_cg_scalars(double *__restrict__ scal, int first) {
@@ -510,18 +515,33 @@ __global__ void __launch_bounds__(256) k_cg_update(int n3, int n3_own, const dou
   if (grid_reduce<1>(acc, partial, counter, res) && threadIdx.x == 0) scal[SC_CG_G] = res[0];
 }
 
+void halo_exchange_async(Ctx &c, double *vec);
+
 static void enqueue_cg_iters_dist(Ctx &c, double *sol, int iters) {
   const int n3 = 3 * c.nv, n3o = 3 * c.nv_own, bs = 256;
+  const int lo = c.int_lo, hi = c.int_hi, nv = c.nv;
+  const bool split = hi > lo;   // the interior rows overlap the halo of z (previous update)
   for (int it = 0; it < iters; ++it) {
-    k_cg_spmv<<<div_up(c.nv, bs), bs, 0, c.stream>>>(sell_view(c), c.nv_own, c.z, c.tmp, c.partial, c.counters + 3,
-                                                     c.scal);
+    if (split && it > 0) {
+      k_cg_spmv<<<div_up(hi - lo, bs), bs, 0, c.stream>>>(sell_view(c), c.nv_own, lo, hi, nv, nv, c.z, c.tmp,
+                                                         c.partial, c.counters + 3, c.scal, SC_CG_DI, 0);
+      MS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_halo, 0));
+      k_cg_spmv<<<div_up(lo + nv - hi, bs), bs, 0, c.stream>>>(sell_view(c), c.nv_own, 0, lo, hi, nv, c.z, c.tmp,
+                                                              c.partial, c.counters + 3, c.scal, SC_CG_D, 1);
+      c.launches += 1;
+    } else {
+      k_cg_spmv<<<div_up(nv, bs), bs, 0, c.stream>>>(sell_view(c), c.nv_own, 0, nv, nv, nv, c.z, c.tmp, c.partial,
+                                                     c.counters + 3, c.scal, SC_CG_D, 0);
+    }
     dist_sum(c, c.scal + SC_CG_G, 2);   // the iteration's only reduction
     k_cg_scalars<<<1, 1, 0, c.stream>>>(c.scal, it == 0 ? 1 : 0);
     k_cg_update<<<grid_vec(n3), bs, 0, c.stream>>>(n3, n3o, c.dinv, c.tmp, c.p, c.q, sol, c.r, c.z, c.partial,
                                                    c.counters + 4, c.scal);
-    halo_exchange(c, c.z);
+    if (split) halo_exchange_async(c, c.z);
+    else halo_exchange(c, c.z);
     c.launches += 3;
   }
+  if (split && iters > 0) MS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_halo, 0));   // join (graph capture too)
 }
 
 static void enqueue_pcg_iters(Ctx &c, double *sol, int iters) {
@@ -777,6 +797,22 @@ void halo_exchange(Ctx &c, double *vec) {
   if (ns) k_halo_pack<<<div_up(3 * (int64_t)ns, 256), 256, 0, c.stream>>>(ns, c.halo_send_idx, vec, c.halo_send);
   c.comm->exchange(c.part.peers, c.halo_send, c.halo_recv, c.stream);
   if (nr) k_halo_unpack<<<div_up(3 * (int64_t)nr, 256), 256, 0, c.stream>>>(nr, c.halo_recv_idx, c.halo_recv, vec);
+  c.launches += 2;
+  MS_CUDA(cudaGetLastError());
+}
+
+// the same exchange on c.halo_stream, ordered after everything enqueued on c.stream so far; the
+// caller makes c.stream wait on c.ev_halo before it reads ghost entries or writes vec again
+void halo_exchange_async(Ctx &c, double *vec) {
+  if (!c.dist()) return;
+  MS_REQUIRE(c.halo_stream, MS_ERR_STATE, "halo stream not created");
+  MS_CUDA(cudaEventRecord(c.ev_z, c.stream));
+  MS_CUDA(cudaStreamWaitEvent(c.halo_stream, c.ev_z, 0));
+  const int ns = (int)c.part.send_idx.size(), nr = (int)c.part.recv_idx.size();
+  if (ns) k_halo_pack<<<div_up(3 * (int64_t)ns, 256), 256, 0, c.halo_stream>>>(ns, c.halo_send_idx, vec, c.halo_send);
+  c.comm->exchange(c.part.peers, c.halo_send, c.halo_recv, c.halo_stream);
+  if (nr) k_halo_unpack<<<div_up(3 * (int64_t)nr, 256), 256, 0, c.halo_stream>>>(nr, c.halo_recv_idx, c.halo_recv, vec);
+  MS_CUDA(cudaEventRecord(c.ev_halo, c.halo_stream));
   c.launches += 2;
   MS_CUDA(cudaGetLastError());
 }
