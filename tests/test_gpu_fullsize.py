@@ -21,6 +21,8 @@ Tolerances as in tests/test_gpu_parity.py.
 """
 import dataclasses
 
+import os
+
 import numpy as np
 import pytest
 import scipy.sparse as sp
@@ -28,7 +30,7 @@ import scipy.sparse as sp
 pytestmark = pytest.mark.gpu
 
 from oracle import coarse, ip, solver  # noqa: E402
-from precompute.basis import cached_basis  # noqa: E402
+from precompute.basis import cached_basis, cached_basis_path  # noqa: E402
 from precompute.mesh import make_scene, random_state  # noqa: E402
 
 
@@ -40,8 +42,8 @@ def c4(request):
         pytest.skip("no CUDA device")
     from paper_2508_13386_b200 import msim
     s = make_scene(request.param)
-    if request.param == 5:
-        from tools.hat_basis import hat_basis
+    if request.param == 5 and not os.path.exists(cached_basis_path(s)):
+        from tools.hat_basis import hat_basis      # stand-in until the C5 basis is precomputed
         b = hat_basis(s)
     else:
         b = cached_basis(s)
