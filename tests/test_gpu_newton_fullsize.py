@@ -36,32 +36,37 @@ def rel_err(a, b):
     return np.linalg.norm(np.ravel(a) - np.ravel(b)) / max(np.linalg.norm(np.ravel(b)), 1e-300)
 
 
-def _ctx(c):
+def _ctx(c, hat=False):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2508_13386_b200 import msim
     s = make_scene(c)
-    if c == 5 and not os.path.exists(cached_basis_path(s)):
-        pytest.skip("C5 basis not precomputed (python tools/oracle_fixtures.py needs it; ~1 h of CPU)")
-    b = cached_basis(s)
+    if hat:   # C5 on the stand-in basis (tools/hat_basis.py) while the paper's basis is not cached
+        from tools.hat_basis import hat_basis
+        b = hat_basis(s)
+    else:
+        if c == 5 and not os.path.exists(cached_basis_path(s)):
+            pytest.skip("C5 basis not precomputed (hours of CPU: tools/rebuild_cache.sh c5basis)")
+        b = cached_basis(s)
     return s, b, msim.context_from_scene(s, b)
 
 
-def _newton_fixture(c):
-    path = fx.fixture_path("newton", c)
+def _newton_fixture(c, hat=False):
+    path = fx.fixture_path("newton", f"{c}hat" if hat else c)
     if c == 5 and not os.path.exists(path):
-        pytest.skip("C5 oracle fixture not precomputed (tools/oracle_fixtures.py newton 5)")
+        pytest.skip("C5 oracle fixture not precomputed (tools/oracle_fixtures.py newton 5 [--hat])")
     if not os.path.exists(path):          # compute it (C1-C4: a few minutes of oracle CPU time)
         os.makedirs(fx.FIX_DIR, exist_ok=True)
         np.savez(path, **fx.newton_fixture(c, verbose=False))
     return dict(np.load(path))
 
 
-@pytest.mark.parametrize("c", [1, 2, 3, 4, 5], ids=["C1", "C2", "C3", "C4", "C5"])
-def test_fullsize_newton_bootstrapped(c):
-    f = _newton_fixture(c)
-    s, b, ctx = _ctx(c)
+@pytest.mark.parametrize("c,hat", [(1, False), (2, False), (3, False), (4, False), (5, False), (5, True)],
+                         ids=["C1", "C2", "C3", "C4", "C5", "C5-standin-basis"])
+def test_fullsize_newton_bootstrapped(c, hat):
+    f = _newton_fixture(c, hat)
+    s, b, ctx = _ctx(c, hat)
     model = ip.make_model(s)
     diag = np.linalg.norm(s.X.max(0) - s.X.min(0))
     for it in range(int(f["n_iter"])):
@@ -89,19 +94,21 @@ def test_fullsize_newton_bootstrapped(c):
 def _traj_files():
     out = []
     for p in sorted(glob.glob(os.path.join(fx.FIX_DIR, f"traj_C*_{fx.BASIS_VERSION}.npz"))):
-        m = re.search(r"traj_C(\d)_(\d+)_", os.path.basename(p))
-        out.append(pytest.param(int(m.group(1)), p, id=f"C{m.group(1)}x{m.group(2)}"))
-    return out or [pytest.param(1, None, id="C1-missing")]
+        m = re.search(r"traj_C(\d)(hat)?_(\d+)_", os.path.basename(p))
+        hat = m.group(2) is not None
+        out.append(pytest.param(int(m.group(1)), p, hat,
+                                id=f"C{m.group(1)}{'-standin-basis' if hat else ''}x{m.group(3)}"))
+    return out or [pytest.param(1, None, False, id="C1-missing")]
 
 
-@pytest.mark.parametrize("c,path", _traj_files())
-def test_fullsize_timestep_free_running(c, path):
+@pytest.mark.parametrize("c,path,hat", _traj_files())
+def test_fullsize_timestep_free_running(c, path, hat):
     if path is None:                    # C1 is cheap: compute its trajectory here
         k = make_scene(1).steps
         data = fx.traj_fixture(1, k, verbose=False)
     else:
         data = dict(np.load(path))
-    s, b, ctx = _ctx(c)
+    s, b, ctx = _ctx(c, hat)
     diag = np.linalg.norm(s.X.max(0) - s.X.min(0))
     worst = 0.0
     for step in range(len(data["x"])):

@@ -1,6 +1,6 @@
 """Free-running timestep parity log (GPU against the oracle's stored trajectory).
 
-    python tools/freerun_log.py C [out.json]
+    python tools/freerun_log.py C [out.json] [--hat]
 
 Runs the config's timesteps from rest on cuda:0 through the C-ABI (the bench's context) and
 compares, after every step, the positions with the oracle trajectory that
@@ -26,8 +26,11 @@ from tools.oracle_fixtures import FIX_DIR  # noqa: E402
 
 
 def main():
+    hat = "--hat" in sys.argv
+    sys.argv = [a for a in sys.argv if a != "--hat"]
     c = int(sys.argv[1])
-    files = sorted(glob.glob(os.path.join(FIX_DIR, f"traj_C{c}_*_{BASIS_VERSION}.npz")),
+    tag = f"{c}hat" if hat else f"{c}"
+    files = sorted(glob.glob(os.path.join(FIX_DIR, f"traj_C{tag}_*_{BASIS_VERSION}.npz")),
                    key=lambda p: int(re.search(r"_(\d+)_v", p).group(1)))
     if not files:
         raise SystemExit(f"no oracle trajectory for C{c} under {FIX_DIR}")
@@ -36,7 +39,11 @@ def main():
     xs, newton_o = data["x"], data["newton"]
     from paper_2508_13386_b200 import msim
     s = make_scene(c)
-    b = cached_basis(s)
+    if hat:
+        from tools.hat_basis import hat_basis
+        b = hat_basis(s)
+    else:
+        b = cached_basis(s)
     ctx = msim.context_from_scene(s, b)
     diag = float(np.linalg.norm(s.X.max(0) - s.X.min(0)))
     steps = []
@@ -53,7 +60,7 @@ def main():
                       "newton_gpu": int(st.newton_iters), "newton_oracle": int(newton_o[k]),
                       "ls_status": int(st.status)})
         x_prev, xo_prev = x, xs[k]
-    out = {"config": s.name, "n_tets": int(s.n_tets), "n_verts": int(s.n_verts), "m": int(b.m),
+    out = {"config": s.name, "basis": "stand-in (tools/hat_basis.py)" if hat else "paper (precompute/basis.py)", "n_tets": int(s.n_tets), "n_verts": int(s.n_verts), "m": int(b.m),
            "steps_compared": len(xs), "steps_of_config": int(s.steps), "oracle_fixture": os.path.basename(path),
            "tolerance": "max_v |x - x_oracle| / bbox diagonal <= 1e-6 (north_star)",
            "worst_max_dx_over_diag": max(r["max_dx_over_diag"] for r in steps),

@@ -4,8 +4,10 @@ solves, hours of CPU at C5) is not available.  NOT the paper's basis: phi_i = h_
 h_i the trilinear hat of lattice node i (partition of unity, <= 8 handles per vertex; the squares
 break the hats' linear precision, which together with the monomials [1, X - c_i] of Eq. 7 would
 give B a 9-dimensional null space and a singular S), handle origins at the nodes, no DBC.
-Used by tools/c5_probe.py only (memory / index-width / timing probe); parity and bench lines use
-the paper's basis."""
+Used by tools/c5_probe.py (memory / index-width / timing probe) and, while the paper's C5 basis is
+not cached, by the C5 stand-in parity cases (tests/test_gpu_fullsize.py, tests/test_gpu_newton_fullsize.py
+"C5-standin-basis", oracle fixtures from tools/oracle_fixtures.py --hat): the oracle and the CUDA path
+then consume the same stand-in arrays.  Bench lines use the paper's basis."""
 import numpy as np
 
 from precompute.basis import Basis

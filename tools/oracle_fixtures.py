@@ -3,6 +3,7 @@ and precompute/, never the CUDA path).
 
     python tools/oracle_fixtures.py newton C      # bootstrapped Newton iterations of config C
     python tools/oracle_fixtures.py traj C [K]    # free-running timesteps 1..K of config C
+    python tools/oracle_fixtures.py newton 5 --hat   # C5 on the stand-in basis of tools/hat_basis.py
 
 newton: from precompute.mesh.contact_state (x^t, v) the oracle runs N_ITER Newton iterations of
 one timestep (Alg. 1, §3.9) and stores, per iteration, the start iterate x,
@@ -35,9 +36,16 @@ def fixture_path(kind, c, k=None):
     return os.path.join(FIX_DIR, f"{kind}_C{c}{tag}_{BASIS_VERSION}.npz")
 
 
-def newton_fixture(c, n_iter=N_ITER, verbose=True):
+def scene_basis(c, hat=False):
     s = make_scene(c)
-    b = cached_basis(s)
+    if hat:   # stand-in partition of unity (tools/hat_basis.py), NOT the paper's basis
+        from tools.hat_basis import hat_basis
+        return s, hat_basis(s)
+    return s, cached_basis(s)
+
+
+def newton_fixture(c, n_iter=N_ITER, verbose=True, hat=False):
+    s, b = scene_basis(c, hat)
     sim = solver.OracleSim(s, b)
     sim.x, sim.v = contact_state(s)
     x_t = sim.x.copy()
@@ -62,9 +70,8 @@ def newton_fixture(c, n_iter=N_ITER, verbose=True):
     return out
 
 
-def traj_fixture(c, k, verbose=True):
-    s = make_scene(c)
-    b = cached_basis(s)
+def traj_fixture(c, k, verbose=True, hat=False):
+    s, b = scene_basis(c, hat)
     sim = solver.OracleSim(s, b)
     xs, newton = [], []
     for step in range(k):
@@ -79,15 +86,18 @@ def traj_fixture(c, k, verbose=True):
 
 
 def main():
-    kind, c = sys.argv[1], int(sys.argv[2])
+    hat = "--hat" in sys.argv
+    argv = [a for a in sys.argv if a != "--hat"]
+    kind, c = argv[1], int(argv[2])
+    tag = f"{c}hat" if hat else c
     os.makedirs(FIX_DIR, exist_ok=True)
     if kind == "newton":
-        data = newton_fixture(c)
-        path = fixture_path("newton", c)
+        data = newton_fixture(c, hat=hat)
+        path = fixture_path("newton", tag)
     else:
-        k = int(sys.argv[3]) if len(sys.argv) > 3 else make_scene(c).steps
-        data = traj_fixture(c, k)
-        path = fixture_path("traj", c, k)
+        k = int(argv[3]) if len(argv) > 3 else make_scene(c).steps
+        data = traj_fixture(c, k, hat=hat)
+        path = fixture_path("traj", tag, k)
     np.savez(path + ".tmp.npz", **data)
     os.replace(path + ".tmp.npz", path)
     print("wrote", path, flush=True)
