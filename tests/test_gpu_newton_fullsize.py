@@ -28,7 +28,7 @@ pytestmark = pytest.mark.gpu
 
 from precompute.basis import cached_basis, cached_basis_path  # noqa: E402
 from oracle import ip  # noqa: E402
-from precompute.mesh import make_scene  # noqa: E402
+from precompute.mesh import contact_state, make_scene  # noqa: E402
 from tools import oracle_fixtures as fx  # noqa: E402
 
 
@@ -58,8 +58,12 @@ def _newton_fixture(c, hat=False):
         pytest.skip("C5 oracle fixture not precomputed (tools/oracle_fixtures.py newton 5 [--hat])")
     if not os.path.exists(path):          # compute it (C1-C4: a few minutes of oracle CPU time)
         os.makedirs(fx.FIX_DIR, exist_ok=True)
-        np.savez(path, **fx.newton_fixture(c, verbose=False))
-    return dict(np.load(path))
+        s = make_scene(c)
+        np.savez(path, **fx.compact(fx.newton_fixture(c, verbose=False), s.n_verts, "newton"))
+    f = dict(np.load(path))
+    if "stride" not in f:                 # full vectors (fixtures written before the sampled form)
+        f["stride"] = np.array(1)
+    return f
 
 
 @pytest.mark.parametrize("c,hat", [(1, False), (2, False), (3, False), (4, False), (5, False), (5, True)],
@@ -69,13 +73,18 @@ def test_fullsize_newton_bootstrapped(c, hat):
     s, b, ctx = _ctx(c, hat)
     model = ip.make_model(s)
     diag = np.linalg.norm(s.X.max(0) - s.X.min(0))
+    st_ = int(f["stride"])                 # the directions are stored at vertices 0, st_, 2 st_, ...
+    if "x_t" not in f:                    # compact large-config form: the entry state is recomputed
+        x_t, v_t = contact_state(s)
+        f["x_t"], f["xhat"], f["x0"] = x_t, ip.predictor(model, x_t, v_t), x_t
     for it in range(int(f["n_iter"])):
         ctx.set_step_state(f["x_t"], f["xhat"], f[f"x{it}"])
         st = ctx.newton_step()
         ds, df = ctx.get_direction()
+        ds, d = ds.reshape(-1, 3)[::st_], (ds + df).reshape(-1, 3)[::st_]
         a0, alpha, evals, dsn, energy, conv, failed = f[f"scal{it}"]
         assert rel_err(ds, f[f"ds{it}"]) < 1e-8, (c, it, rel_err(ds, f[f"ds{it}"]))
-        assert rel_err(ds + df, f[f"d{it}"]) < 1e-8, (c, it, rel_err(ds + df, f[f"d{it}"]))
+        assert rel_err(d, f[f"d{it}"]) < 1e-8, (c, it, rel_err(d, f[f"d{it}"]))
         assert abs(st.alpha0 - a0) <= 1e-8 * a0, (c, it, st.alpha0, a0)
         assert abs(st.ds_norm - dsn) <= 1e-8 * dsn
         e0 = ip.energy(model, f[f"x{it}"], f["xhat"])        # E(x) at the start of the iteration
@@ -86,8 +95,8 @@ def test_fullsize_newton_bootstrapped(c, hat):
             assert st.ls_evals == int(evals), (c, it, st.ls_evals, evals)
             assert abs(st.alpha - alpha) <= 1e-8 * alpha
             _, _, x_new = ctx.get_step_state()
-            x_o = f[f"x{it}"] + alpha * f[f"d{it}"]
-            assert np.abs(x_new - x_o).max() <= 1e-9 * diag
+            x_o = f[f"x{it}"].reshape(-1, 3)[::st_] + alpha * f[f"d{it}"].reshape(-1, 3)
+            assert np.abs(x_new.reshape(-1, 3)[::st_] - x_o).max() <= 1e-9 * diag
         assert bool(st.converged) == bool(conv)
 
 
@@ -111,10 +120,11 @@ def test_fullsize_timestep_free_running(c, path, hat):
     s, b, ctx = _ctx(c, hat)
     diag = np.linalg.norm(s.X.max(0) - s.X.min(0))
     worst = 0.0
+    stv = int(data.get("stride", 1))      # positions stored at vertices 0, stv, 2 stv, ...
     for step in range(len(data["x"])):
         st = ctx.timestep()
         x, _ = ctx.get_state()
-        err = np.linalg.norm(x - data["x"][step], axis=1).max() / diag
+        err = np.linalg.norm(x[::stv] - data["x"][step], axis=1).max() / diag
         worst = max(worst, err)
         assert err <= 1e-6, (c, step + 1, err)
         assert st.newton_iters == int(data["newton"][step]), (c, step + 1, st.newton_iters, data["newton"][step])
