@@ -140,12 +140,16 @@ def phase_rooflines(phases, ab, ci, n_cg, hbm, peak_src, fp64_peak, fp64_src, tr
 
 
 # ----------------------------------------------------------------------------- scenes
-def load_case(config):
+def load_case(config, standin=False):
     from precompute.basis import cached_basis
     from precompute.mesh import make_scene
     s = make_scene(config)
     t0 = time.time()
-    b = cached_basis(s)
+    if standin:   # tools/hat_basis.py: a partition of unity on a handle lattice, NOT the paper's basis
+        from tools.hat_basis import hat_basis
+        b = hat_basis(s)
+    else:
+        b = cached_basis(s)
     return s, b, time.time() - t0
 
 
@@ -241,7 +245,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     from paper_2508_13386_b200 import msim
-    s, b, t_basis = load_case(args.config)
+    s, b, t_basis = load_case(args.config, args.standin_basis)
     stream = torch.cuda.current_stream()
     partitioned = world > 1 and not args.replicas
     coarse_mode = 1 if args.coarse == "pcg" else 0
@@ -360,6 +364,8 @@ def run_ours(args):
             "scaling": "strong" if partitioned else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": dict(config_dict(s, b, world, partitioned), coarse=args.coarse, integrator=args.integrator,
+                           basis="stand-in trilinear-hat partition of unity (tools/hat_basis.py)"
+                           if args.standin_basis else "paper: k-means partition + bilaplacian weights",
                            cubature=bool(args.cubature), lag_hessian=bool(args.lag), refine=args.refine),
             "pcg_iters_per_s": pcg_all / (ms_max * 1e-3),
             "newton_iters": int(newton_all),
@@ -407,6 +413,8 @@ def main():
     ap.add_argument("--refine", default="jacobi", choices=["jacobi", "two_level"],
                     help="refinement PCG: N_cg Jacobi iterations (default, the paper's) or NEXT-4's two-level "
                          "PCG (Jacobi + SMS coarse correction every iteration) to 1e-4 ||g||")
+    ap.add_argument("--standin-basis", action="store_true",
+                    help="use the stand-in basis of tools/hat_basis.py (C5 while its paper basis is not cached)")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: N independent copies of the problem instead of one slab-partitioned problem")
     args = ap.parse_args()
