@@ -236,8 +236,9 @@ def assemble_subdomain(tets_sub, Kl_sub, vol_sub, verts):
     return L, Mdiag
 
 
-def constrained_bilaplacian(L, Mdiag, one_idx, zero_idx):
-    """Solve K u = 0, K = L M^-1 L, with u = 1 on one_idx and u = 0 on zero_idx."""
+def constrained_system(L, Mdiag, one_idx, zero_idx):
+    """K = L M^-1 L with u = 1 on one_idx and u = 0 on zero_idx: returns (u with the constrained
+    values, free indices, K_ff, rhs = -K_fc u_c) of the system K_ff u_f = rhs."""
     n = L.shape[0]
     K = (L @ sp.diags(1.0 / Mdiag) @ L).tocsr()
     u = np.zeros(n)
@@ -248,10 +249,16 @@ def constrained_bilaplacian(L, Mdiag, one_idx, zero_idx):
     u[zero_idx] = 0.0
     cons[one_idx] = True
     free = np.nonzero(~cons)[0]
+    Kff = K[free][:, free]
+    rhs = -(K[free][:, np.nonzero(cons)[0]] @ u[cons])
+    return u, free, Kff, rhs
+
+
+def constrained_bilaplacian(L, Mdiag, one_idx, zero_idx):
+    """Solve K u = 0, K = L M^-1 L, with u = 1 on one_idx and u = 0 on zero_idx (sparse LU)."""
+    u, free, Kff, rhs = constrained_system(L, Mdiag, one_idx, zero_idx)
     if len(free):
-        Kff = K[free][:, free].tocsc()
-        rhs = -(K[free][:, np.nonzero(cons)[0]] @ u[cons])
-        u[free] = spla.spsolve(Kff, rhs, permc_spec="MMD_AT_PLUS_A")
+        u[free] = spla.spsolve(Kff.tocsc(), rhs, permc_spec="MMD_AT_PLUS_A")
     return u
 
 
@@ -260,7 +267,9 @@ def constrained_bilaplacian(L, Mdiag, one_idx, zero_idx):
 _G = {}
 
 
-def _solve_handle(i):
+def _handle_system(i):
+    """The constrained bilaplacian of handle i on its subdomain: (verts, u, free, K_ff,
+    rhs) -- the system _solve_handle solves with SuperLU."""
     g = _G
     sub_tets_mask = g["in_sub"](i)
     tsub = g["tets"][sub_tets_mask]
@@ -277,8 +286,53 @@ def _solve_handle(i):
         zero.update(np.nonzero(g["dbc_mask"][verts])[0].tolist())
     one = int(np.searchsorted(verts, g["cv"][i]))
     zero.discard(one)
-    u = constrained_bilaplacian(L, Md, [one], sorted(zero))
+    u, free, Kff, rhs = constrained_system(L, Md, [one], sorted(zero))
+    return verts, u, free, Kff, rhs
+
+
+def _solve_handle(i):
+    verts, u, free, Kff, rhs = _handle_system(i)
+    if len(free):
+        u[free] = spla.spsolve(Kff.tocsc(), rhs, permc_spec="MMD_AT_PLUS_A")
     return verts, u
+
+
+def _handle_system_csr(i):
+    verts, u, free, Kff, rhs = _handle_system(i)
+    Kff = Kff.tocsr()
+    return i, verts, u, free, (Kff.indptr, Kff.indices, Kff.data, Kff.shape[0]), rhs
+
+
+def _solve_handles_cuda(m, workers, verbose=False):
+    """The m per-handle systems assembled on CPU worker processes and solved on the GPU by a dense
+    fp64 Cholesky (torch.linalg.cholesky: a library factorisation, like SuperLU on the default path;
+    C5's ~56 k-vertex subdomains factor in ~1.8 s each on a B200 against hours of sparse LU)."""
+    import multiprocessing as mp
+    import time
+    import torch
+    dev = torch.device("cuda")
+    res = [None] * m
+    t0 = time.time()
+    ctx = mp.get_context("fork")
+    with ctx.Pool(workers) as pool:
+        for n_done, (i, verts, u, free, (ip, ix, dv, nf), rhs) in enumerate(
+                pool.imap_unordered(_handle_system_csr, range(m), chunksize=1)):
+            if nf:
+                K = torch.zeros((nf, nf), dtype=torch.float64, device=dev)
+                rows = torch.repeat_interleave(torch.arange(nf, device=dev),
+                                               torch.from_numpy(np.diff(ip)).to(dev))
+                K[rows, torch.from_numpy(ix.astype(np.int64)).to(dev)] = torch.from_numpy(dv).to(dev)
+                Lc, info = torch.linalg.cholesky_ex(K)
+                del K
+                if int(info) != 0:
+                    raise RuntimeError(f"handle {i}: subdomain system not positive definite (info {int(info)})")
+                x = torch.cholesky_solve(torch.from_numpy(rhs).to(dev)[:, None], Lc)
+                del Lc
+                u[free] = x[:, 0].cpu().numpy()
+            res[i] = (verts, u)
+            if verbose and (n_done + 1) % 64 == 0:
+                print(f"    {n_done + 1}/{m} handles ({time.time() - t0:.0f}s)", flush=True)
+    return res
 
 
 def _solve_dbc():
@@ -337,7 +391,41 @@ def hop_radius(assign, tets, cv, n_v, m):
     return float(np.mean(radii))
 
 
-def build_basis(scene, m=None, seed=None, workers=None, verbose=False, partition="euclidean") -> Basis:
+def scene_partition(scene, m, seed, partition, X, tets, vol, bary):
+    """Step 1: the clustering of the tets (k-means or NEXT-3's heat-geodesic
+    partitioner), connectivity enforcement and empty clusters dropped.  Returns (assign, m)."""
+    if partition == "heat":
+        from .partition import geodesic_kmeans
+        assign, _ = geodesic_kmeans(scene, m, seed)
+    elif partition == "euclidean":
+        C0 = kmeans_pp(bary, vol, m, seed)
+        assign = lloyd(bary, vol, C0)
+    else:
+        raise ValueError(f"unknown partition {partition!r}")
+    adj = face_adjacency(tets)
+    assign = enforce_connectivity(assign.copy(), tets, adj, m)
+    used = np.unique(assign)
+    remap = -np.ones(m, dtype=np.int64)
+    remap[used] = np.arange(len(used))
+    return remap[assign], len(used)
+
+
+def cached_partition(scene, cache_dir=None, partition="euclidean"):
+    """scene_partition cached next to the bases (the 30 min of single-threaded k-means at C5)."""
+    path = cached_basis_path(scene, cache_dir, partition)[:-4] + "_partition.npz"
+    if os.path.exists(path):
+        z = np.load(path)
+        return z["assign"].astype(np.int64), int(z["m"])
+    X, tets = scene.X, scene.tets.astype(np.int64)
+    assign, m = scene_partition(scene, scene.m, scene.config, partition, X, tets, tet_volumes(X, tets),
+                                tet_barycentres(X, tets))
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    np.savez_compressed(path, assign=assign.astype(np.int32), m=np.array(m))
+    return assign, m
+
+
+def build_basis(scene, m=None, seed=None, workers=None, verbose=False, partition="euclidean",
+                solver="superlu", partition_data=None) -> Basis:
     """partition: "euclidean" (step 1 below; the default of every config) or "heat" (NEXT-3: the
     paper's stiffness-weighted heat-geodesic k-means with jump penalty and pruning,
     precompute/partition.py; m is then the initial cluster count)."""
@@ -350,22 +438,11 @@ def build_basis(scene, m=None, seed=None, workers=None, verbose=False, partition
 
     vol = tet_volumes(X, tets)
     bary = tet_barycentres(X, tets)
-    if partition == "heat":
-        from .partition import geodesic_kmeans
-        assign, _ = geodesic_kmeans(scene, m, seed)
-    elif partition == "euclidean":
-        C0 = kmeans_pp(bary, vol, m, seed)
-        assign = lloyd(bary, vol, C0)
+    if partition_data is not None:   # (assign, m) from cached_partition
+        assign, m = partition_data
+        assign = np.asarray(assign, dtype=np.int64)
     else:
-        raise ValueError(f"unknown partition {partition!r}")
-    adj = face_adjacency(tets)
-    assign = enforce_connectivity(assign.copy(), tets, adj, m)
-    # drop empty clusters (cannot happen after kmeans++ in practice)
-    used = np.unique(assign)
-    remap = -np.ones(m, dtype=np.int64)
-    remap[used] = np.arange(len(used))
-    assign = remap[assign]
-    m = len(used)
+        assign, m = scene_partition(scene, m, seed, partition, X, tets, vol, bary)
     if verbose:
         print(f"  kmeans+connectivity {time.time()-t0:.1f}s", flush=True)
 
@@ -409,7 +486,9 @@ def build_basis(scene, m=None, seed=None, workers=None, verbose=False, partition
     if workers is None:
         workers = min(os.cpu_count() or 1, 64)
     t1 = time.time()
-    if workers > 1 and m > 8:
+    if solver == "cuda":
+        res = _solve_handles_cuda(m, workers, verbose)
+    elif workers > 1 and m > 8:
         import multiprocessing as mp
         ctx = mp.get_context("fork")
         with ctx.Pool(workers) as pool:
