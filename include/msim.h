@@ -150,7 +150,8 @@ void ms_default_params(ms_params *out);
 /* Create a context on `device`, enqueuing on `cuda_stream` (a cudaStream_t; NULL = legacy
  * default stream).  Multi-GPU: one context per rank and GPU, SPMD; world > 1
  * needs nccl_id, the 128-byte ncclUniqueId that rank 0 obtained with ms_nccl_unique_id and
- * shared with the other ranks (world == 1: nccl_id may be NULL).  Every rank then uploads the
+ * shared with the other ranks (world == 1: nccl_id may be NULL; a non-NULL id makes the single
+ * rank run the partitioned path over a one-rank NCCL communicator).  Every rank then uploads the
  * full mesh and basis and makes the same calls in the same order; the context keeps an x-slab of
  * vertices (equal counts) plus one ghost layer, exchanges ghost values with its neighbours over
  * NCCL and sums energies, dot products, B^T r and S across ranks (dist.h).  State arrays

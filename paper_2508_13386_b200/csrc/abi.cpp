@@ -318,7 +318,8 @@ static ms_status create_common(ms_ctx **out, int device, void *cuda_stream, int 
       msim::elem_init_attrs(ctx->c);
       msim::coarse_init_attrs(ctx->c);
       msim::chol_init_attrs(ctx->c);
-      if (world > 1) ctx->c.comm = hub ? msim::make_hub_comm(hub, rank) : msim::make_nccl_comm(nccl_id, rank, world, device);
+      if (world > 1 || nccl_id)
+        ctx->c.comm = hub ? msim::make_hub_comm(hub, rank) : msim::make_nccl_comm(nccl_id, rank, world, device);
     });
     return MS_OK;
   }();

@@ -123,7 +123,9 @@ struct Ctx {
   int32_t int_lo = 0, int_hi = 0;
   cudaStream_t halo_stream = nullptr;
   cudaEvent_t ev_z = nullptr, ev_halo = nullptr;
-  bool dist() const { return part.world > 1; }
+  // the partitioned code path: world > 1, or world == 1 with an explicit communicator (ms_create with
+  // an nccl_id: one rank owning everything runs the NCCL collectives and their graph captures)
+  bool dist() const { return part.world > 1 || comm != nullptr; }
   std::vector<double> h_X;          // rest positions (host copy)
   std::vector<double> h_Xg, h_Eg, h_rhog;   // global rest positions (world > 1) / per-tet E, rho
   std::vector<int32_t> h_dbc_glob;          // global Dirichlet vertex ids (ms_basis_build)

@@ -574,7 +574,8 @@ static void enqueue_cg_iters_dist(Ctx &c, double *sol, int iters) {
       k_cg_spmv<<<div_up(hi - lo, bs), bs, 0, c.stream>>>(sell_view(c), c.nv_own, lo, hi, nv, nv, c.z, c.tmp,
                                                          c.partial, c.counters + 3, c.scal, SC_CG_DI, 0);
       MS_CUDA(cudaStreamWaitEvent(c.stream, c.ev_halo, 0));
-      k_cg_spmv<<<div_up(lo + nv - hi, bs), bs, 0, c.stream>>>(sell_view(c), c.nv_own, 0, lo, hi, nv, c.z, c.tmp,
+      // (a single slab has no boundary rows: one CTA still adds the interior part into SC_CG_D)
+      k_cg_spmv<<<std::max(1, (int)div_up(lo + nv - hi, bs)), bs, 0, c.stream>>>(sell_view(c), c.nv_own, 0, lo, hi, nv, c.z, c.tmp,
                                                               c.partial, c.counters + 3, c.scal, SC_CG_D, 1);
       c.launches += 1;
     } else {

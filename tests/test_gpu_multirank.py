@@ -91,3 +91,27 @@ def test_partitioned_two_level_refinement_matches_single(msim):
     diag = np.linalg.norm(s.X.max(0) - s.X.min(0))
     assert its_p == its
     assert np.abs(x - x_ref).max() <= 1e-9 * diag
+
+
+@pytest.mark.parametrize("name,steps", [("drop", 6), ("c2", 3)])
+def test_nccl_backend_world1_matches_single(msim, name, steps):
+    """The NCCL backend itself on one GPU: a world-1 context created with an ncclUniqueId takes the
+    partitioned code path (slab plan with one slab, ncclAllReduce of every rank sum, the empty
+    halo group, the graph-captured distributed PCG loop and coarse stages -- the hub is not
+    capturable, so only this test runs those captures).  One rank owns everything, so the sums
+    have a single term and the timesteps must reproduce the plain context."""
+    if name == "drop":
+        s = scene_small_drop(n=(10, 4, 3), m=6, drop=0.002)
+    else:
+        s = make_scene(2)
+    b = build_basis(s, workers=1)
+    ref = msim.context_from_scene(s, b)
+    its = [ref.timestep().newton_iters for _ in range(steps)]
+    x_ref, v_ref = ref.get_state()
+    ctx = msim.context_from_scene(s, b, rank=0, world=1, nccl_id=msim.nccl_unique_id())
+    its_n = [ctx.timestep().newton_iters for _ in range(steps)]
+    x, v = ctx.get_state()
+    diag = np.linalg.norm(s.X.max(0) - s.X.min(0))
+    assert its_n == its
+    assert np.abs(x - x_ref).max() <= 1e-9 * diag
+    assert np.abs(v - v_ref).max() <= 1e-9 * diag / s.h
