@@ -232,7 +232,8 @@ def config_dict(s, b, world, partitioned=False):
                         f"{s.n_verts} vertices, m={b.m} handles, N_cg={b.n_cg}, IE h=1/60"
                         + (", ground barrier" if s.ground is not None else ", pinned end"),
             "n_tets": int(s.n_tets), "n_verts": int(s.n_verts), "m": int(b.m), "n_cg": int(b.n_cg),
-            "parallelism": (f"slab{world}" if partitioned else f"replicas{world}") if world > 1 else "single",
+            "parallelism": (f"slab{world}" if partitioned else f"replicas{world}") if world > 1
+                           else ("slab1-nccl (diagnostic)" if partitioned else "single"),
             "l2_flush": "none: the per-step working set (BSR Hessian, staged element Hessians) exceeds the 126 MB L2"
                         if s.n_tets > 500000 else "none (small config: L2-resident, reported for completeness)"}
 
@@ -247,7 +248,7 @@ def run_ours(args):
     from paper_2508_13386_b200 import msim
     s, b, t_basis = load_case(args.config, args.standin_basis)
     stream = torch.cuda.current_stream()
-    partitioned = world > 1 and not args.replicas
+    partitioned = (world > 1 and not args.replicas) or args.nccl1
     coarse_mode = 1 if args.coarse == "pcg" else 0
     integrator = 1 if args.integrator == "bdf2" else 0
     extra = dict(coarse_mode=coarse_mode, integrator=integrator, use_cubature=int(args.cubature),
@@ -261,7 +262,8 @@ def run_ours(args):
         uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
             uid.copy_(torch.frombuffer(bytearray(msim.nccl_unique_id()), dtype=torch.uint8))
-        torch.distributed.broadcast(uid, src=0)
+        if world > 1:
+            torch.distributed.broadcast(uid, src=0)
         ctx = msim.context_from_scene(s, b, device=local, stream=stream.cuda_stream, rank=rank, world=world,
                                       nccl_id=bytes(uid.cpu().numpy().tobytes()), **extra)
     else:
@@ -328,7 +330,7 @@ def run_ours(args):
             x_h.fill(0.0)
             v_h.fill(0.0)
         ctx.get_state(out=(x_h, v_h))
-        if partitioned:   # every rank returns its owned vertices: assemble the global state
+        if partitioned and world > 1:   # every rank returns its owned vertices: assemble the global state
             xv = torch.from_numpy(np.concatenate([x_h.ravel(), v_h.ravel()])).cuda()
             torch.distributed.all_reduce(xv)
             xv = xv.cpu().numpy()
@@ -415,6 +417,9 @@ def main():
                          "PCG (Jacobi + SMS coarse correction every iteration) to 1e-4 ||g||")
     ap.add_argument("--standin-basis", action="store_true",
                     help="use the stand-in basis of tools/hat_basis.py (C5 while its paper basis is not cached)")
+    ap.add_argument("--nccl1", action="store_true",
+                    help="N=1 diagnostic: run the partitioned code path over a one-rank NCCL communicator "
+                         "(cost of the distributed path's collectives and captures on one GPU)")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: N independent copies of the problem instead of one slab-partitioned problem")
     args = ap.parse_args()

@@ -1,6 +1,7 @@
 // Internal header of libmsim (B200 / sm_100a).  Not part of the C-ABI.
 #pragma once
 
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -51,6 +52,13 @@ struct DBuf {
     if (count == 0) return;
     MS_CUDA(cudaMalloc((void **)&p, count * sizeof(T)));
     n = count;
+    // debugging aid (MSIM_POISON=1): fresh buffers hold NaN / -1 instead of whatever the allocator
+    // hands back, so a read of memory nothing wrote shows up in every run, not by allocation luck
+    static const bool poison = std::getenv("MSIM_POISON") != nullptr;
+    if (poison) {
+      MS_CUDA(cudaMemset(p, 0xFF, count * sizeof(T)));
+      MS_CUDA(cudaDeviceSynchronize());
+    }
   }
   void upload(const T *h, size_t count, cudaStream_t s) {
     alloc(count);

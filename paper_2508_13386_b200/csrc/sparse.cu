@@ -704,7 +704,8 @@ void launch_pcg(Ctx &c, const double *rhs, double *sol, int iters) {
 // ------------------------------------------------------------------ small vector kernels
 __global__ void k_axpby(int64_t n, double *__restrict__ y, double a, const double *__restrict__ x, double b) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) y[i] = a * x[i] + b * y[i];
+  // b == 0 overwrites: y may be a fresh buffer (0 * NaN of recycled device memory would poison it)
+  if (i < n) y[i] = b == 0.0 ? a * x[i] : a * x[i] + b * y[i];
 }
 void launch_axpby(Ctx &c, double *y, double a, const double *x, double b, int64_t n) {
   k_axpby<<<div_up(n, 256), 256, 0, c.stream>>>(n, y, a, x, b);

@@ -93,7 +93,11 @@ def test_coarse_pcg_tolerance_newton(msim, name):
     info = sim.newton_iteration()
     st = ctx.newton_step()
     ds, df = ctx.get_direction()
-    assert st.coarse_iters == its_o, (st.coarse_iters, its_o)
+    # the stopping index is an integer decided by ||r_k|| <= 1e-4 ||b|| in fp64 on both sides; the
+    # iterates differ by summation order (atomic-free GPU sums vs scipy), so a residual that lands
+    # within rounding of the threshold may cross one iteration apart (drop scene: 44 / 45) -- the
+    # rule itself is checked on the GPU's own iterate below, the fixed-count iterates above to 1e-8
+    assert abs(st.coarse_iters - its_o) <= 1, (st.coarse_iters, its_o)
     # validity: the paper's stopping rule holds for the GPU's own iterate
     _, da_o, _, _ = solver.subspace_direction(H, g, sim.Ua, sim.Us, "pcg", tol=1e-4)
     r1 = -g.ravel() - H @ da_o
@@ -113,7 +117,7 @@ def test_coarse_pcg_timesteps_drop(msim):
         st = ctx.timestep()
         infos = sim.timestep()
         x, _ = ctx.get_state()
-        assert st.newton_iters == len(infos)
+        assert st.newton_iters == len(infos), (st.status, st.newton_iters, st.last_alpha, st.last_ds_norm, st.coarse_iters)
         assert np.abs(x - sim.x).max() <= 1e-6 * diag
 
 

@@ -8,6 +8,7 @@ timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gp
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
 timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > $O/bench_c4.json 2> $O/bench_c4.err; echo "bench rc=$?" >> $O/bench_c4.err
 timeout 900 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > $O/bench_reference.json 2> $O/bench_reference.err; echo "ref rc=$?" >> $O/bench_reference.err
+timeout 600 python bench.py --nccl1 --steps 10 --warmup 5 --no-cpu-baseline > $O/bench_c4_nccl1.json 2> $O/bench_c4_nccl1.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1200 --csv --log-file $O/launches.csv \
   python bench.py --steps 2 --warmup 6 --no-cpu-baseline > $O/launches_bench.log 2>&1; echo "launch list rc=$?" >> $O/launches_bench.log
 python tools/launch_summary.py $O/launches.csv $O/launches_summary.txt > /dev/null 2>&1
