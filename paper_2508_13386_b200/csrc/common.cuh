@@ -81,22 +81,9 @@ struct Reducer {
 };
 
 // ---------------------------------------------------------------- tile Cholesky schedule
-// staged element Hessian P+(H_e): 80 doubles (640 B, five 128-byte lines) per tet -- the 6
-// off-diagonal blocks (a < b) in full, row-major, at stage_off(a, b), then the 4 diagonal blocks as
-// their upper triangles (6 doubles, 16-byte aligned) at kStageDiag + 6 a, then 2 doubles of padding:
-// the 78 unique values of the symmetric 12x12 block matrix (SURVEY §8(d)'s 624 B per tet)
-constexpr int kStageH = 80, kStageDiag = 54;
-__host__ __device__ constexpr int stage_off(int a, int b) {   // a < b
-  return 9 * (3 * a - a * (a - 1) / 2 + (b - a - 1));
-}
-__host__ __device__ constexpr int sym3(int i, int j) {       // packed upper triangle of a 3x3
-  return i <= j ? 3 * i - i * (i - 1) / 2 + (j - i) : 3 * j - j * (j - 1) / 2 + (i - j);
-}
-// entry (i, i2) of block (a, b) of a staged tet record
-__host__ __device__ constexpr int stage_idx(int a, int b, int i, int i2) {
-  return a == b ? kStageDiag + 6 * a + sym3(i, i2)
-                : (a < b ? stage_off(a, b) + 3 * i + i2 : stage_off(b, a) + 3 * i2 + i);
-}
+// staged element Hessian: 10 upper 3x3 blocks per tet, each padded to 10 doubles so every
+// block starts 16-byte aligned (the assembly gathers it with 5 vector loads)
+constexpr int kStageB = 10, kStageH = 10 * kStageB;
 constexpr int kGalChunk = 128;   // vertices of U_i per Galerkin chunk (7-bit local index)
 constexpr int kGalThreads = 2 * kGalChunk;
 // shared memory of one Galerkin row CTA (galerkin.cuh): R chunk, staged entries, S accumulators
@@ -183,7 +170,7 @@ struct Ctx {
   DBuf<double> g, ds, da, df, d, r, rhs;   // 3nv
   DBuf<double> p, q, z, tmp;               // PCG vectors
   DBuf<double> stage_g;             // [nt*12] element gradients (unscaled by h^2)
-  DBuf<double> stage_h;             // [nt*kStageH] P+(H_e): 6 off-diagonal + 4 packed diagonal blocks
+  DBuf<double> stage_h;             // [nt*kStageH] 10 upper 3x3 blocks of P+(H_e), kStageB apart
   DBuf<int32_t> hess_work;          // [nt] tets whose reduced Hessian needs the eigen-clamp
   DBuf<unsigned int> hess_nwork;    // [1] their count
   bool step_begun = false;

@@ -151,6 +151,9 @@ __global__ void __launch_bounds__(256) k_elem_grad(MeshView M, int nt_own, const
 __host__ __device__ constexpr int sidx(int i, int j) {
   return i <= j ? i * 9 - (i * (i - 1)) / 2 + (j - i) : j * 9 - (j * (j - 1)) / 2 + (i - j);
 }
+__host__ __device__ constexpr int blk4(int a, int b) {  // a <= b, 10 upper blocks
+  return a * 4 - (a * (a - 1)) / 2 + (b - a);
+}
 // Brent-Luk round-robin for n = 9: round r pairs ((r+k)%9, (r-k+9)%9), k = 1..4
 // r < 0 (r = -1 - sh, sh = 0..2): the circle-method pairs (0,7),(1,6),(2,5),(3,4) shifted by sh;
 // three such rounds are unrolled and the matrix is then relabelled by i -> i+3 (mod 9), so a
@@ -382,8 +385,7 @@ __device__ __forceinline__ bool psd_by_cholesky_inplace(double (&l)[45], double 
   return ok;
 }
 
-// dst[stage_idx(a, a2, i, i2)] = block (a, a2), a <= a2, of H_e = Q P9 Q^T (diagonal blocks: upper
-// triangle only; common.cuh) with
+// dst[blk4(a,a2)*kStageB + 3 i + i2] = block (a, a2), a <= a2, of H_e = Q P9 Q^T with
 // Q4 = 1/2 [[1,1,1],[1,-1,-1],[-1,1,-1],[-1,-1,1]]: for each (i, i2) the 4x4 block over (A, A2)
 // is 1/4 H4 P H4^T, formed with the Hadamard pattern (42 adds)
 __device__ __forceinline__ void lift_store(const double (&p9)[45], double *__restrict__ dst) {
@@ -407,15 +409,12 @@ __device__ __forceinline__ void lift_store(const double (&p9)[45], double *__res
         const double t1 = u[A][1] + u[A][2], t2 = u[A][1] - u[A][2];
         const double w[4] = {u[A][0] + t1, u[A][0] - t1, t2 - u[A][0], -t2 - u[A][0]};
 #pragma unroll
-        for (int A2 = A; A2 < 4; ++A2)
-          if (A < A2 || i <= i2) dst[stage_idx(A, A2, i, i2)] = 0.25 * w[A2];
+        for (int A2 = A; A2 < 4; ++A2) dst[blk4(A, A2) * kStageB + 3 * i + i2] = 0.25 * w[A2];
       }
     }
-  dst[kStageH - 2] = 0.0;   // padding
-  dst[kStageH - 1] = 0.0;
 }
 
-// stage_h[e*kStageH + stage_idx(a, a2, i, i2)] = P+(H_e) block (a, a2), a <= a2 (unscaled by h^2).
+// stage_h[e*kStageH + blk4(a,a2)*kStageB + 3 i + i2] = P+(H_e) block (a, a2), a <= a2 (unscaled by h^2).
 // Pass 1 (every tet): reduced Hessian, P+ by e9::psd_project (tridiagonal QL + inverse iteration
 // on the negative eigenvalues, eig9.cuh).  A tet with more than kMaxNeg negative eigenvalues (or
 // no QL convergence) goes to a work list for pass 2, the cyclic-Jacobi eigen-clamp (the list
@@ -434,9 +433,9 @@ constexpr int kHessScratch = 35 + 9 * kMaxNeg;   // doubles per thread (eig9.cuh
 #ifndef MSIM_HESS_MINB
 #define MSIM_HESS_MINB 2
 #endif
-// The projected blocks leave through shared memory: each warp writes its 32 tets' kStageH doubles
-// (row stride kStageH + 1 against bank conflicts) and copies them to the contiguous stage_h rows of
-// those tets with coalesced stores (a direct per-thread store has a 640-byte stride).
+// The projected blocks leave through shared memory: each warp writes its 32 tets' 90 doubles
+// (row stride 91 against bank conflicts) and copies them to the contiguous stage_h rows of those
+// tets with coalesced stores (a direct per-thread store has a 720-byte stride).
 constexpr int kHessStg = kStageH + 1;
 
 __global__ void __launch_bounds__(kHessThreads, MSIM_HESS_MINB) k_elem_hess(MeshView M, const double *__restrict__ x,
@@ -475,7 +474,7 @@ __global__ void __launch_bounds__(kHessThreads, MSIM_HESS_MINB) k_elem_hess(Mesh
   double *stg = hsm + (size_t)threadIdx.x * kHessStg;
   if (store) lift_store(p9, stg);
   __syncwarp();
-  if (list) {   // scattered tets: each thread copies its own kStageH-double row
+  if (list) {   // scattered tets: each thread copies its own 100-double row
     if (store)
       for (int q = 0; q < kStageH; ++q) stage_h[(size_t)e * kStageH + q] = stg[q];
     return;
@@ -510,7 +509,10 @@ __global__ void k_expand_hess(int nt, const double *__restrict__ stage_h, double
   if (idx >= (int64_t)nt * 144) return;
   const int e = (int)(idx / 144), rc = (int)(idx % 144), r = rc / 12, cc = rc % 12;
   const int a = r / 3, i = r % 3, a2 = cc / 3, i2 = cc % 3;
-  He[idx] = stage_h[(size_t)e * kStageH + stage_idx(a, a2, i, i2)];
+  double v;
+  if (a <= a2) v = stage_h[(size_t)e * kStageH + blk4(a, a2) * kStageB + 3 * i + i2];
+  else v = stage_h[(size_t)e * kStageH + blk4(a2, a) * kStageB + 3 * i2 + i];
+  He[idx] = v;
 }
 
 // ------------------------------------------------------------------ launchers

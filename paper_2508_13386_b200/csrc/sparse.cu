@@ -110,160 +110,112 @@ void launch_vertex_grad(Ctx &c) {
 }
 
 // ------------------------------------------------------------------ assembly (a4)
+__host__ __device__ constexpr int blk4s(int a, int b) { return a * 4 - (a * (a - 1)) / 2 + (b - a); }
 
 #ifndef MSIM_ASM_UNROLL
 #define MSIM_ASM_UNROLL 2   // two contributions' gathers in flight (measured: 0.545 -> 0.526 ms at C4)
 #endif
 constexpr int kAsmUnroll = MSIM_ASM_UNROLL;
 
-// The gathers of one slot's contributions, code = tet*16 + a*4 + b (block (a, b) of tet e; the
-// stage record, common.cuh, holds the upper blocks: a lower one is read transposed), scaled per
-// tet by tet_scale.  Off-diagonal: 9 scalar loads (the blocks sit 72 bytes apart); diagonal: the
-// packed upper triangle, 3 vector loads.
-__device__ __forceinline__ void asm_add_off(int code, const double *__restrict__ stage_h,
-                                            const double *__restrict__ tet_scale, double (&acc)[9]) {
-  const int e = code >> 4, a = (code >> 2) & 3, b = code & 3;
-  const bool up = a < b;
-  const double *src = stage_h + (size_t)e * kStageH + (up ? stage_off(a, b) : stage_off(b, a));
-  double v[9];
-#pragma unroll
-  for (int q = 0; q < 9; ++q) v[q] = __ldg(&src[q]);
-  const double sc = tet_scale ? __ldg(&tet_scale[e]) : 1.0;
-#pragma unroll
-  for (int q = 0; q < 9; ++q) acc[q] += sc * (up ? v[q] : v[(q % 3) * 3 + q / 3]);
-}
-
-__device__ __forceinline__ void asm_add_diag(int code, const double *__restrict__ stage_h,
-                                             const double *__restrict__ tet_scale, double (&acc)[9]) {
-  const int e = code >> 4, a = (code >> 2) & 3;
-  const double2 *src = reinterpret_cast<const double2 *>(stage_h + (size_t)e * kStageH + kStageDiag + 6 * a);
-  double v[6];
-#pragma unroll
-  for (int h = 0; h < 3; ++h) {
-    const double2 t2 = __ldg(&src[h]);
-    v[2 * h] = t2.x;
-    v[2 * h + 1] = t2.y;
-  }
-  const double sc = tet_scale ? __ldg(&tet_scale[e]) : 1.0;
-#pragma unroll
-  for (int q = 0; q < 9; ++q) acc[q] += sc * v[sym3(q / 3, q % 3)];
-}
-
-// Two parts in one launch.  Part 1 (the first ceil(npos/256) CTAs): thread per SELL position
-// (coalesced value writes), the off-diagonal blocks -- at most 6 contributions (the tets around
-// an edge) -- and the zero padding.  Part 2: kDiagLanes lanes per row gather the diagonal block's
-// ~24 contributions (the tets around the vertex) with a fixed-order shuffle reduction, add
-// inertia and barrier, apply the Dirichlet identity and write dinv.  Splitting the diagonal off
-// keeps every part-1 warp at the edge valence instead of the vertex valence (a warp of 32 rows
-// almost always holds a diagonal slot, which set its trip count for all 32 lanes).
+// thread per SELL position (coalesced value writes); slot s = sell_slot[pos] (-1: padding)
 // tet_scale (may be NULL): per-tet factor of the contributions (the cubature weight w_e / V_e);
 // dinv (may be NULL): Jacobi diagonal; diag_el (may be NULL): the alpha h^2 elastic part of the
 // diagonal blocks before inertia and barrier are added (the frozen part of the lagged Hessian)
-constexpr int kDiagLanes = 8;
-
 __global__ void __launch_bounds__(256) k_assemble(
-    int64_t npos, int nv, int nblk_off, const int32_t *__restrict__ sell_slot, const int32_t *__restrict__ sell_col,
-    const int32_t *__restrict__ diag_pos, const int32_t *__restrict__ cptr, const int32_t *__restrict__ contrib,
+    int64_t npos, const int32_t *__restrict__ sell_slot, const int32_t *__restrict__ sell_col,
+    const int32_t *__restrict__ cptr, const int32_t *__restrict__ contrib,
     const double *__restrict__ stage_h, const double *__restrict__ x, const double *__restrict__ mass,
     const uint8_t *__restrict__ fixed, const int32_t *__restrict__ slot_row, Ground G, double h2,
     double *__restrict__ vals, double *__restrict__ dinv, const double *__restrict__ tet_scale,
     double *__restrict__ diag_el) {
+  const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= npos) return;
+  const int cidx = (int)(pos >> 5), lane = (int)(pos & 31);
+  const int s = sell_slot[pos];
   double acc[9];
 #pragma unroll
   for (int q = 0; q < 9; ++q) acc[q] = 0.0;
-  if ((int)blockIdx.x < nblk_off) {   // ---- part 1: off-diagonal blocks and padding
-    const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (pos >= npos) return;
-    const int s = sell_slot[pos];
-    if (s >= 0) {
-      const int row = __ldg(&slot_row[s]), col = sell_col[pos];
-      if (row == col) return;   // part 2 writes the diagonal block
-      const int k1 = __ldg(&cptr[s + 1]);
+  if (s >= 0) {
+    const int k1 = __ldg(&cptr[s + 1]);
 #pragma unroll(kAsmUnroll)
-      for (int k = __ldg(&cptr[s]); k < k1; ++k) asm_add_off(__ldg(&contrib[k]), stage_h, tet_scale, acc);
+    for (int k = __ldg(&cptr[s]); k < k1; ++k) {
+      const int code = __ldg(&contrib[k]);
+      const int e = code >> 4, a = (code >> 2) & 3, b = code & 3;
+      const bool up = a <= b;
+      const double2 *src = reinterpret_cast<const double2 *>(
+          stage_h + (size_t)e * kStageH + (up ? blk4s(a, b) : blk4s(b, a)) * kStageB);
+      double v[10];
 #pragma unroll
-      for (int q = 0; q < 9; ++q) acc[q] *= h2;
-      if (fixed[row] || fixed[col]) {
+      for (int h = 0; h < 5; ++h) {
+        const double2 t2 = __ldg(&src[h]);
+        v[2 * h] = t2.x;
+        v[2 * h + 1] = t2.y;
+      }
+      const double sc = tet_scale ? __ldg(&tet_scale[e]) : 1.0;
 #pragma unroll
-        for (int q = 0; q < 9; ++q) acc[q] = 0.0;
+      for (int q = 0; q < 9; ++q) acc[q] += sc * (up ? v[q] : v[(q % 3) * 3 + q / 3]);
+    }
+    const int row = slot_row[s], col = sell_col[pos];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc[q] *= h2;
+    if (row == col && diag_el) {
+#pragma unroll
+      for (int q = 0; q < 9; ++q) diag_el[9 * (size_t)row + q] = acc[q];
+    }
+    if (row == col) {
+      const double m = mass[row];
+      acc[0] += m;
+      acc[4] += m;
+      acc[8] += m;
+      if (G.on) {
+        const double d = G.n0 * x[3 * row] + G.n1 * x[3 * row + 1] + G.n2 * x[3 * row + 2] - G.off;
+        const double kb = h2 * G.kappa * bar_d2(d, G.dhat);
+        const double n[3] = {G.n0, G.n1, G.n2};
+#pragma unroll
+        for (int q = 0; q < 9; ++q) acc[q] += kb * n[q / 3] * n[q % 3];
       }
     }
-    const int cidx = (int)(pos >> 5), lane = (int)(pos & 31);
+    if (fixed[row] || fixed[col]) {
 #pragma unroll
-    for (int q = 0; q < 9; ++q) vals[sell_val_index(cidx, q, lane)] = acc[q];
-    return;
-  }
-  // ---- part 2: diagonal blocks, kDiagLanes lanes per row (rows never straddle a warp)
-  const int64_t t = (int64_t)(blockIdx.x - nblk_off) * blockDim.x + threadIdx.x;
-  const int row = (int)(t / kDiagLanes), sub = (int)(t % kDiagLanes);
-  const bool live = row < nv;
-  int pos = 0;
-  if (live) {
-    pos = __ldg(&diag_pos[row]);
-    const int s = __ldg(&sell_slot[pos]);
-    const int k1 = __ldg(&cptr[s + 1]);
-    for (int k = __ldg(&cptr[s]) + sub; k < k1; k += kDiagLanes) asm_add_diag(__ldg(&contrib[k]), stage_h, tet_scale, acc);
+      for (int q = 0; q < 9; ++q) acc[q] = (row == col && (q % 4 == 0)) ? 1.0 : 0.0;
+    }
+    if (row == col && dinv) {
+      dinv[3 * row + 0] = 1.0 / acc[0];
+      dinv[3 * row + 1] = 1.0 / acc[4];
+      dinv[3 * row + 2] = 1.0 / acc[8];
+    }
   }
 #pragma unroll
-  for (int off = kDiagLanes / 2; off >= 1; off >>= 1)
-#pragma unroll
-    for (int q = 0; q < 9; ++q) acc[q] += __shfl_down_sync(0xffffffffu, acc[q], off, kDiagLanes);
-  if (!live || sub != 0) return;
-#pragma unroll
-  for (int q = 0; q < 9; ++q) acc[q] *= h2;
-  if (diag_el) {
-#pragma unroll
-    for (int q = 0; q < 9; ++q) diag_el[9 * (size_t)row + q] = acc[q];
-  }
-  const double m = mass[row];
-  acc[0] += m;
-  acc[4] += m;
-  acc[8] += m;
-  if (G.on) {
-    const double d = G.n0 * x[3 * row] + G.n1 * x[3 * row + 1] + G.n2 * x[3 * row + 2] - G.off;
-    const double kb = h2 * G.kappa * bar_d2(d, G.dhat);
-    const double n[3] = {G.n0, G.n1, G.n2};
-#pragma unroll
-    for (int q = 0; q < 9; ++q) acc[q] += kb * n[q / 3] * n[q % 3];
-  }
-  if (fixed[row]) {
-#pragma unroll
-    for (int q = 0; q < 9; ++q) acc[q] = (q % 4 == 0) ? 1.0 : 0.0;
-  }
-  if (dinv) {
-    dinv[3 * row + 0] = 1.0 / acc[0];
-    dinv[3 * row + 1] = 1.0 / acc[4];
-    dinv[3 * row + 2] = 1.0 / acc[8];
-  }
-#pragma unroll
-  for (int q = 0; q < 9; ++q) vals[sell_val_index(pos >> 5, q, pos & 31)] = acc[q];
-}
-
-static void assemble_into(Ctx &c, const int32_t *cptr, const int32_t *contrib, double *vals, double *dinv,
-                          const double *tet_scale, double *diag_el) {
-  const int bs = 256;
-  const int nb1 = (int)div_up(c.npos, bs), nb2 = (int)div_up((int64_t)c.nv * kDiagLanes, bs);
-  k_assemble<<<nb1 + nb2, bs, 0, c.stream>>>(c.npos, c.nv, nb1, c.sell_slot, c.sell_col, c.diag_pos, cptr, contrib,
-                                             c.stage_h, c.x, c.mass, c.fixed, c.slot_row, ground_of(c), c.ah2(),
-                                             vals, dinv, tet_scale, diag_el);
-  c.launches++;
-  MS_CUDA(cudaGetLastError());
+  for (int q = 0; q < 9; ++q) vals[sell_val_index(cidx, q, lane)] = acc[q];
 }
 
 // the refinement Hessian (H, or H_lag at a refresh) into vals + dinv
 void launch_assemble(Ctx &c) {
+  const int bs = 256;
+  const double h2 = c.ah2();   // alpha h^2 (Eq. 2)
   if (c.params.lag_hessian) c.lag_diag.alloc(9 * (size_t)c.nv);
-  assemble_into(c, c.cptr, c.contrib, c.vals, c.dinv, nullptr, c.params.lag_hessian ? c.lag_diag.p : nullptr);
+  k_assemble<<<div_up(c.npos, bs), bs, 0, c.stream>>>(c.npos, c.sell_slot, c.sell_col, c.cptr, c.contrib,
+                                                      c.stage_h, c.x, c.mass, c.fixed, c.slot_row,
+                                                      ground_of(c), h2, c.vals, c.dinv, nullptr,
+                                                      c.params.lag_hessian ? c.lag_diag.p : nullptr);
+  c.launches++;
+  MS_CUDA(cudaGetLastError());
 }
 
 // the subspace Hessian into vals_s: the cubature Hessian (contributions of the cubature elements,
 // weighted w_e / V_e; NEXT-2) or, with only lagging on, the fresh fully integrated H
 void launch_assemble_sub(Ctx &c) {
+  const int bs = 256;
+  const double h2 = c.ah2();
   c.vals_s.alloc(c.vals.n);
   const bool cub = c.params.use_cubature;
   MS_REQUIRE(!cub || c.n_cub > 0, MS_ERR_STATE, "use_cubature without ms_cubature_upload");
-  assemble_into(c, cub ? c.cptr_c : c.cptr, cub ? c.contrib_c : c.contrib, c.vals_s, nullptr,
-                cub ? c.tet_scale.p : nullptr, nullptr);
+  k_assemble<<<div_up(c.npos, bs), bs, 0, c.stream>>>(c.npos, c.sell_slot, c.sell_col, cub ? c.cptr_c : c.cptr,
+                                                      cub ? c.contrib_c : c.contrib, c.stage_h, c.x, c.mass,
+                                                      c.fixed, c.slot_row, ground_of(c), h2, c.vals_s, nullptr,
+                                                      cub ? c.tet_scale.p : nullptr, nullptr);
+  c.launches++;
+  MS_CUDA(cudaGetLastError());
 }
 
 // H_lag between refreshes: the off-diagonal blocks keep their frozen elastic values; every
